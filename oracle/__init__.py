@@ -1,0 +1,114 @@
+"""fp64 CPU oracle for the Householder-product apply path (ctypes over hh_ref.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` legs may import this package.  The product
+package `paper_1811_07624_b200` never imports it.
+
+Inputs may be fp32 or fp64; fp32 values are converted exactly to fp64 (reading
+R5: the same bytes the GPU receives, never renormalised) and all arithmetic is
+strict fp64 in hh_ref.c.  Outputs are fp64 numpy arrays.
+
+Layout: U is (h, n) row-major == n x h column-major; X is (N, n) row-major ==
+n x N column-major.  See hh_ref.c for the paper citations of each function.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hh_ref.c")
+_LIB = os.path.join(_HERE, "libhh_ref.so")
+CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-std=c11", "-Wall", "-Wextra",
+          "-fPIC", "-shared"]
+
+OP_N, OP_T = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile hh_ref.c -> libhh_ref.so (gcc, strict fp64)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        i64, p, i32 = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+        L.hh_ref_apply.argtypes = [i32, i64, i64, p, p, p, i64]
+        L.hh_ref_sym_apply.argtypes = [i64, i64, p, p, p, p, i64]
+        L.hh_ref_mahalanobis.argtypes = [i64, i64, p, p, p, i64, p, p, i64, p]
+        for f in (L.hh_ref_apply, L.hh_ref_sym_apply, L.hh_ref_mahalanobis):
+            f.restype = i32
+        L.hh_ref_num_threads.restype = i32
+        L.hh_ref_set_threads.argtypes = [i32]
+        _lib = L
+    return _lib
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def set_threads(t: int) -> None:
+    lib().hh_ref_set_threads(int(t))
+
+
+def num_threads() -> int:
+    return int(lib().hh_ref_num_threads())
+
+
+def apply(op: int, U, X) -> np.ndarray:
+    """Y = Q X (op 0) or Q^T X (op 1), Q = H_1 ... H_h (hh_ref.c: hh_ref_apply)."""
+    U = _f64(U).reshape(-1, np.shape(X)[-1]) if np.size(U) else np.zeros((0, np.shape(X)[-1]))
+    X = _f64(X)
+    h, n = U.shape
+    N = X.shape[0]
+    Y = np.empty_like(X)
+    rc = lib().hh_ref_apply(int(op), n, h, _ptr(U), _ptr(X), _ptr(Y), N)
+    if rc:
+        raise ValueError(f"hh_ref_apply rc={rc}")
+    return Y
+
+
+def sym_apply(U, lam, X) -> np.ndarray:
+    """Y = Q diag(lam) Q^T X (hh_ref.c: hh_ref_sym_apply)."""
+    X = _f64(X)
+    n = X.shape[-1]
+    U = _f64(U).reshape(-1, n)
+    lam = _f64(lam)
+    Y = np.empty_like(X)
+    rc = lib().hh_ref_sym_apply(n, U.shape[0], _ptr(U), _ptr(lam), _ptr(X), _ptr(Y), X.shape[0])
+    if rc:
+        raise ValueError(f"hh_ref_sym_apply rc={rc}")
+    return Y
+
+
+def mahalanobis(U, d, P, ia, ib) -> np.ndarray:
+    """dist[j] = ||D^1/2 Q^T (P[ia[j]] - P[ib[j]])||^2 (hh_ref.c: hh_ref_mahalanobis)."""
+    P = _f64(P)
+    n = P.shape[-1]
+    U = _f64(U).reshape(-1, n)
+    d = _f64(d)
+    ia = np.ascontiguousarray(ia, dtype=np.int32)
+    ib = np.ascontiguousarray(ib, dtype=np.int32)
+    dist = np.empty(ia.shape[0], dtype=np.float64)
+    rc = lib().hh_ref_mahalanobis(n, U.shape[0], _ptr(U), _ptr(d), _ptr(P), P.shape[0],
+                                  _ptr(ia), _ptr(ib), ia.shape[0], _ptr(dist))
+    if rc:
+        raise ValueError(f"hh_ref_mahalanobis rc={rc}")
+    return dist
