@@ -1,0 +1,448 @@
+#!/usr/bin/env python
+"""Benchmark of the Householder-product apply hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {hh,reference}]
+                    [--workload C2|C1|C3|C4|C5h12|C5h64|C5h256|C5h1024] [--op N|T]
+
+Default workload = BASELINE.json configs[1] (the metric's config): Y = H1...Hh X,
+fp32, n=1024, h=10, N=262144 columns (1 GiB in, 1 GiB out; larger than the 126 MB
+L2, so no flush is needed between steps).  One step = one hh_apply launch over the
+whole batch.  metric = algorithmic GB/s (one read + one write of X per step),
+whole job, max-over-ranks device time.  Rank 0 prints ONE JSON line.
+
+Multi-GPU (torchrun): weak scaling, each rank applies Q to its own full-size batch;
+no collective on the data path (columns are independent).
+`--impl reference`: the fp64 C oracle (oracle/) on the host cores, timed per step on a
+bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from gen import inputs as gi  # noqa: E402
+
+METRIC = "H1…Hh·X GB/s and % of HBM roofline (n=1024,h=10,fp32); vectors/s"
+FALLBACK_HBM = 6650.0
+
+
+def workload_case(name: str, N_override=None):
+    name = name.upper()
+    if name == "C1":
+        return gi.make_config(1, N=N_override)
+    if name == "C2":
+        return gi.make_config(2, N=N_override)
+    if name == "C3":
+        return gi.make_config(3, N=N_override)
+    if name == "C4":
+        return gi.make_config(4, N=N_override)
+    if name.startswith("C5H"):
+        return gi.make_config(5, h=int(name[3:]), N=N_override)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def alg_cost(c, op_count=1):
+    """Algorithmic bytes and flops of one step."""
+    s = 4 if c.dtype == "f32" else 8
+    if c.call == "mahalanobis":
+        P = c.npairs
+        byts = c.N * c.n * s + 2 * P * 4 + P * s          # points once + indices + dist
+        flops = 4 * c.h * c.n * c.N + 3 * c.n * P          # transform-once reading (R11)
+        units = P
+    elif c.call == "sym":
+        byts = 2 * c.N * c.n * s
+        flops = (8 * c.h + 1) * c.n * c.N
+        units = c.N
+    else:
+        byts = 2 * c.N * c.n * s
+        flops = 4 * c.h * c.n * c.N
+        units = c.N
+    return byts, flops, units
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    return FALLBACK_HBM, "fallback (B200_PROFILING.md)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled in the background (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return self
+
+        def rd():
+            for line in self.proc.stdout:
+                self.rows.append((time.time(), line.strip()))
+        self.t = threading.Thread(target=rd, daemon=True)
+        self.t.start()
+        return self
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [r for (t, r) in self.rows if t0 <= t <= t1] or [r for (_, r) in self.rows]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def time_oracle(c, op, target_s=10.0, max_cols=None):
+    """Oracle (as it stands) on a bounded column / pair sample; returns (value GB/s,
+    units/s, seconds, sample description, threads)."""
+    import oracle
+    threads = oracle.num_threads()
+    byts, flops, units = alg_cost(c)
+    per_unit_bytes = byts / units
+
+    def run(k):
+        t0 = time.perf_counter()
+        if c.call == "mahalanobis":
+            oracle.mahalanobis(c.U, c.d, c.X, c.ia[:k], c.ib[:k])
+        elif c.call == "sym":
+            oracle.sym_apply(c.U, c.lam, c.X[:k])
+        else:
+            oracle.apply(op, c.U, c.X[:k])
+        return time.perf_counter() - t0
+
+    total = units
+    k = min(total, 256 if c.call != "mahalanobis" else 2048)
+    dt = run(k)
+    while dt < 0.5 and k < total:
+        k = min(total, k * 4)
+        dt = run(k)
+    k2 = min(total, max(k, int(k * target_s / max(dt, 1e-6))))
+    if max_cols:
+        k2 = min(k2, max_cols)
+    if k2 != k:
+        dt = run(k2)
+        k = k2
+    what = "pairs" if c.call == "mahalanobis" else "columns"
+    return (per_unit_bytes * k / dt / 1e9, k / dt, dt,
+            f"{k} of {total} {what} of {c.name} (fp64 oracle, {threads} threads)", threads)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    c = workload_case(args.workload)
+    op = 0 if args.op == "N" else 1
+    import oracle
+    steps, warm = args.steps, args.warmup
+    budget = 150.0 / max(1, steps + warm)          # whole run within a few minutes
+    _, _, units = alg_cost(c)
+    byts, _, _ = alg_cost(c)
+    # calibrate the sample size for ~budget seconds per step
+    _, ups, _, _, threads = time_oracle(c, op, target_s=min(2.0, budget))
+    k = int(max(1, min(units, ups * budget)))
+    sub = workload_case(args.workload, N_override=None)
+    per_unit_bytes = byts / units
+    times = []
+    for i in range(warm + steps):
+        t0 = time.perf_counter()
+        if c.call == "mahalanobis":
+            oracle.mahalanobis(sub.U, sub.d, sub.X, sub.ia[:k], sub.ib[:k])
+        elif c.call == "sym":
+            oracle.sym_apply(sub.U, sub.lam, sub.X[:k])
+        else:
+            oracle.apply(op, sub.U, sub.X[:k])
+        dt = time.perf_counter() - t0
+        if i >= warm:
+            times.append(dt)
+    tot = sum(times)
+    value = per_unit_bytes * k * steps / tot / 1e9
+    what = "pairs" if c.call == "mahalanobis" else "columns"
+    sample = f"{k} of {units} {what} of {c.name} per step (fp64 oracle, {threads} threads)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": ws, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * tot / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gen/inputs.py, seeded)",
+        "config": config_of(c, args),
+        "vectors_per_s": k * steps / tot,
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(c, args):
+    d = {"workload": f"{c.name}: {c.call} {'Q' if args.op == 'N' else 'Q^T'}·X"
+         if c.call == "apply" else f"{c.name}: {c.call}",
+         "n": c.n, "h": c.h, "N": c.N, "dtype": c.dtype,
+         "l2": "inputs larger than L2 (no flush)" if c.N * c.n * (4 if c.dtype == "f32" else 8)
+         > 256 << 20 else "L2-resident inputs (warm L2, labelled)"}
+    if c.call == "mahalanobis":
+        d["npairs"] = c.npairs
+    if c.call == "apply":
+        d["op"] = args.op
+    return d
+
+
+def run_hh(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1811_07624_b200 as hh
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    c = workload_case(args.workload)
+    op = hh.HH_OP_N if args.op == "N" else hh.HH_OP_T
+    byts, flops, units = alg_cost(c)
+
+    U = torch.from_numpy(c.U).to(dev)
+    X = torch.from_numpy(c.X).to(dev)
+    Y = torch.empty_like(X)
+    stream = torch.cuda.current_stream(dev)
+    extra = {}
+    if c.call == "sym":
+        lam = torch.from_numpy(c.lam).to(dev)
+        step = lambda: hh.hh_sym_apply(U, lam, X, Y, stream=stream)  # noqa: E731
+        launches = 1
+    elif c.call == "mahalanobis":
+        d = torch.from_numpy(c.d).to(dev)
+        ia = torch.from_numpy(c.ia).to(dev)
+        ib = torch.from_numpy(c.ib).to(dev)
+        dist_out = torch.empty(c.npairs, dtype=X.dtype, device=dev)
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, c.n, c.h, c.N, c.npairs, X.dtype)
+        wsp = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        step = lambda: hh.hh_mahalanobis(U, d, X, ia, ib, dist_out, workspace=wsp,  # noqa: E731
+                                         stream=stream)
+        launches = 2
+    else:
+        step = lambda: hh.hh_apply(op, U, X, Y, stream=stream)  # noqa: E731
+        launches = 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    info = hh.last_launch_info()
+
+    # quick sampled parity against the oracle (rank 0; outside the timed region)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        import oracle
+        if c.call == "apply":
+            idx = np.linspace(0, c.N - 1, 256).astype(np.int64)
+            got = Y[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
+            ref = oracle.apply(op, c.U, c.X[idx])
+        elif c.call == "sym":
+            idx = np.linspace(0, c.N - 1, 64).astype(np.int64)
+            got = Y[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
+            ref = oracle.sym_apply(c.U, c.lam, c.X[idx])
+        else:
+            idx = np.linspace(0, c.npairs - 1, 4096).astype(np.int64)
+            got = dist_out[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
+            ref = oracle.mahalanobis(c.U, c.d, c.X, c.ia[idx], c.ib[idx])
+        e = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        parity = {"rel_fro": e, "gate": (1e-12 if c.dtype == "f64" else 2e-5 * math.sqrt(c.h)),
+                  "sampled": int(len(idx)), "pass": bool(e <= (1e-12 if c.dtype == "f64"
+                                                               else 2e-5 * math.sqrt(c.h)))}
+
+    sampler = ClockSampler(dev.index if dev.index is not None else 0).start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.time()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_wall1 = time.time()
+    ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        dist.barrier()
+    # keep the GPU busy for >= 1 s of clock samples if the timed region was short
+    t_obs0 = t_wall0
+    if t_wall1 - t_wall0 < 1.0:
+        t_obs0 = time.time()
+        while time.time() - t_obs0 < 1.0:
+            for _ in range(50):
+                step()
+            torch.cuda.synchronize(dev)
+    t_obs1 = time.time()
+    time.sleep(0.1)
+    sampler.stop()
+    clocks = sampler.summary(t_obs0, t_obs1)
+
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    ms_step = ms_max / args.steps
+    value = ws * byts / (ms_step * 1e-3) / 1e9
+
+    # e2e through the public API with host buffers (hh_apply_host): H2D + compute + D2H
+    e2e = None
+    if c.call == "apply" and not args.no_e2e:
+        Xh = torch.from_numpy(c.X).pin_memory()
+        Yh = torch.empty_like(Xh).pin_memory()
+        Uh = torch.from_numpy(c.U)
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_APPLY_HOST, c.n, c.h, c.N, 0, X.dtype)
+        wsp = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        hh.hh_apply_host(op, Uh, Xh, Yh, workspace=wsp)
+        ke = max(1, min(args.steps, args.e2e_steps))
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            hh.hh_apply_host(op, Uh, Xh, Yh, workspace=wsp)
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        se = float(te.item()) / ke
+        e2e = {"value": ws * byts / se / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size() + Uh.numel() * 4),
+               "d2h_bytes_per_step": int(Yh.numel() * Yh.element_size()),
+               "ms_per_step": 1e3 * se, "steps": ke,
+               "path": "hh_apply_host (pinned host X/Y, 3-slot H2D/compute/D2H ring)"}
+        # the host path runs the same kernel per column: results must be bit-identical
+        sel = torch.linspace(0, c.N - 1, 64).long()
+        e2e["matches_device_path"] = bool(torch.equal(Yh[sel].to(dev), Y[sel.to(dev)]))
+
+    out = None
+    if rank == 0:
+        hbm, hbm_src, _ = peaks()
+        achieved = byts / (ms_step * 1e-3) / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get(c.name + ("" if c.call != "apply" else args.op))
+            except (ValueError, OSError):
+                traffic = None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
+                "frac_of_8TBps": achieved / 8000.0,
+                "kernel": info.get("variant"), "launch": info}
+        cpu = None
+        if not args.no_cpu_baseline and ws == 1:
+            v, ups, secs, sample, thr = time_oracle(c, op, target_s=args.cpu_seconds)
+            cpu = {"value": v, "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": sample,
+                   "seconds": secs, "vectors_per_s": ups, "cpu": cpu_model()}
+        out = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": c.dtype, "data": "synthetic (gen/inputs.py, seeded; BASELINE.json recipe)",
+            "config": config_of(c, args),
+            "vectors_per_s": ws * units / (ms_step * 1e-3),
+            "gflops": ws * flops / (ms_step * 1e-3) / 1e9,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": clocks, "parity": parity,
+            "gpu": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="hh", choices=["hh", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--op", default="N", choices=["N", "T"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_hh(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,183 @@
+/*
+ * hh.h -- C ABI of the B200 (sm_100a) Householder-product apply library (libhh.so).
+ *
+ * The operations are the apply-time computations of
+ *   C. Rusu, "Approximate Eigenvalue Decompositions of Linear Transformations
+ *   with a Few Householder Reflectors", arXiv:1811.07624.
+ * Citations "P:L" are lines of the paper's LaTeX source (/root/reference/PAPER.md,
+ * see SURVEY.md §0 for the equation/line table); the readings of ambiguous
+ * passages are numbered R1..R12 in DESIGN.md.
+ *
+ * ----------------------------------------------------------------------------
+ * Notation (Eq. 1-2; reading R1 fixes the product order):
+ *   u_i = U[:, i]  (i = 1..h), U is n x h COLUMN-MAJOR with ld = n
+ *         (== a row-major / C-contiguous (h, n) array, u_i contiguous)
+ *   H_i = I - 2 u_i u_i^T          (Eq. 2; the stored u_i is used literally:
+ *                                   no renormalisation, u_i = 0 is the identity
+ *                                   slot of P:90)
+ *   Q   = H_1 H_2 ... H_h
+ *   X, Y, P: n x N column-major, ld = n (== C-contiguous (N, n)), column j is
+ *         the contiguous n-vector at X + j*n.
+ *
+ * Pointers
+ *   Every array pointer is a DEVICE pointer owned by the caller, except in
+ *   hh_apply_host() where the data pointers are HOST pointers.  The library never
+ *   allocates device memory for the caller's data, never frees or retains a
+ *   pointer after the call returns, and keeps no mutable global state except a
+ *   thread-safe lazily cached device-attribute table.  Scratch comes from the
+ *   caller: query hh_workspace_bytes(); `workspace` may be NULL when the query
+ *   returns 0.
+ *
+ * dtype
+ *   All floating-point arrays of one call share `dtype` (HH_F32 = float,
+ *   HH_F64 = double).  Index arrays are int32.
+ *
+ * Alignment / size (v1 vector path; HH_ERR_UNSUPPORTED otherwise)
+ *   - every float pointer 16-byte aligned, n * sizeof(dtype) % 16 == 0
+ *     (n % 4 == 0 for f32, n % 2 == 0 for f64);
+ *   - n <= 8192 (f32) / 4096 (f64).
+ *
+ * Semantics
+ *   - Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream); no
+ *     host synchronisation except in hh_apply_host().
+ *   - Y == X (exact alias) is allowed; partial overlap is undefined.
+ *   - h = 0 gives Y = X (sym: Y = lambda .* X; Mahalanobis: plain weighted
+ *     squared distance).  N = 0 / npairs = 0 is a successful no-op.
+ *   - Arguments are validated before any launch; on error nothing is written.
+ *   - Asynchronous device faults surface at the caller's next synchronising call
+ *     (as in cuBLAS); HH_ERR_CUDA reports launch-time errors.
+ *   - No C++ exception crosses this boundary.  All functions are thread-safe.
+ *
+ * Preconditions NOT validated (documented): ||u_i|| = 1 or u_i = 0 for an
+ * orthonormal Q; d_r >= 0; 0 <= ia[j], ib[j] < M; finite inputs.
+ * ----------------------------------------------------------------------------
+ */
+#ifndef HH_H_
+#define HH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef HH_NO_CUDA_TYPES
+#include <cuda_runtime_api.h>
+typedef cudaStream_t hh_stream_t;
+#else
+typedef void *hh_stream_t;
+#endif
+
+typedef enum {
+    HH_OK = 0,
+    HH_ERR_INVALID_VALUE = 1, /* bad size, NULL operand, bad op/dtype/call       */
+    HH_ERR_UNSUPPORTED = 2,   /* misaligned pointer, n*size % 16 != 0, n too big  */
+    HH_ERR_WORKSPACE = 3,     /* workspace_bytes below hh_workspace_bytes()       */
+    HH_ERR_CUDA = 4           /* CUDA runtime error at launch / copy              */
+} hh_status;
+
+typedef enum { HH_F32 = 0, HH_F64 = 1 } hh_dtype;
+
+typedef enum {
+    HH_OP_N = 0, /* Y = Q   X = H_1 (H_2 ( ... (H_h X)))  : u_h applied first        */
+    HH_OP_T = 1  /* Y = Q^T X = H_h ( ... (H_1 X))        : u_1 applied first        */
+} hh_op;
+/* The paper's Eq. 1 (D = I) Ubar = U_h ... U_1 is HH_OP_T on the same
+ * columns; reflector symmetry makes the transpose a reversal. */
+
+typedef enum {
+    HH_CALL_APPLY = 0,
+    HH_CALL_SYM = 1,
+    HH_CALL_MAHALANOBIS = 2,
+    HH_CALL_APPLY_HOST = 3
+} hh_call;
+
+/*
+ * hh_apply -- Y = Q X (op = HH_OP_N) or Y = Q^T X (op = HH_OP_T).
+ *   P:42-54 (Eq. 1-2): "Matrix-vector multiplication with the matrix Ubar ...
+ *   takes 4nh operations" -- each column costs h dot products u_i^T x and h
+ *   rank-1 updates x -= 2 (u_i^T x) u_i, never densifying Q.
+ *   n >= 1, h >= 0, N >= 0; U: n x h (may be NULL iff h == 0); X, Y: n x N.
+ *   workspace: none needed (pass NULL, 0).
+ *   Fused small-h kernel: one HBM read + one HBM write of X (bound: HBM).
+ */
+hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
+                   void *Y, int64_t N, hh_dtype dtype, void *workspace,
+                   size_t workspace_bytes, hh_stream_t stream);
+
+/*
+ * hh_sym_apply -- Y = Q diag(lambda) Q^T X.
+ *   eq:thesbar with D = I (reading R2): "Matrix-vector multiplication
+ *   with S-bar takes (8h+1)n operations" = a Q^T pass (u_1 first), one diagonal
+ *   scale by lambda, and a Q pass (u_h first).
+ *   lambda: n values of dtype (the spectrum s-bar; any sign).
+ *   workspace: none needed.
+ */
+hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda,
+                       const void *X, void *Y, int64_t N, hh_dtype dtype,
+                       void *workspace, size_t workspace_bytes, hh_stream_t stream);
+
+/*
+ * hh_mahalanobis -- dist[j] = || D^{1/2} Q^T (P[:, ia[j]] - P[:, ib[j]]) ||^2
+ *                           = (x_a - x_b)^T Q diag(d) Q^T (x_a - x_b).
+ *   P:600 d_S(x_i, x_j) = ||L (x_i - x_j)||_2^2; "L = sqrt(Lambda) U ...
+ *   perform the transformation x <- L x before running the k-NN" with U == Q^T
+ *   (reading R4); d is the metric diagonal Lambda, d_r >= 0 (reading R3).
+ *   P: n x M column-major points; ia, ib: npairs int32 indices in [0, M);
+ *   dist: npairs values of dtype.
+ *   workspace >= hh_workspace_bytes(HH_CALL_MAHALANOBIS, n, h, M, npairs, dtype):
+ *     transform-once: Z = diag(sqrt d) Q^T P into the workspace, then a
+ *     gather kernel dist[j] = ||Z[:,ia[j]] - Z[:,ib[j]]||^2.
+ *   workspace == NULL: per-pair fused kernel (gather x_a - x_b, Q^T, weighted
+ *     norm) -- no scratch, 4nh + 3n flops per pair.
+ *   A non-NULL workspace smaller than the query -> HH_ERR_WORKSPACE.
+ */
+hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d,
+                         const void *P, int64_t M, const int32_t *ia,
+                         const int32_t *ib, int64_t npairs, void *dist,
+                         hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                         hh_stream_t stream);
+
+/*
+ * hh_apply_host -- hh_apply with HOST U, X, Y (end-to-end path).
+ *   Streams column chunks host -> device, applies Q or Q^T with the same fused
+ *   kernel, and streams them back, overlapping H2D copy, compute and D2H copy on
+ *   internal streams ordered after `stream`.  Synchronous: returns after Y is
+ *   written.  Host buffers should be page-locked for full PCIe bandwidth.
+ *   workspace: DEVICE scratch >= hh_workspace_bytes(HH_CALL_APPLY_HOST, n, h, N, 0,
+ *   dtype) (U plus a ring of column chunks; the ring is <= 3 x 64 MiB).
+ */
+hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host,
+                        const void *X_host, void *Y_host, int64_t N, hh_dtype dtype,
+                        void *workspace, size_t workspace_bytes, hh_stream_t stream);
+
+/*
+ * hh_workspace_bytes -- scratch bytes the call needs (cuBLAS bufferSize style).
+ *   N_or_M: N for apply/sym/apply_host, M for Mahalanobis.  Writes *bytes.
+ *   HH_CALL_APPLY / HH_CALL_SYM: 0.  HH_CALL_MAHALANOBIS: n*M*sizeof(dtype) (the
+ *   transform-once Z).  Errors: HH_ERR_INVALID_VALUE for bad arguments.
+ */
+hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
+                             int64_t npairs, hh_dtype dtype, size_t *bytes);
+
+/* Static string for a status code (never NULL). */
+const char *hh_status_string(hh_status s);
+
+/* Library version as "MAJOR.MINOR.PATCH" (static string). */
+const char *hh_version(void);
+
+/*
+ * hh_last_launch_info -- diagnostics of the calling thread's last launch of the
+ * fused kernel: the kernel variant name (static string), grid, block, dynamic
+ * shared-memory bytes and number of reflector chunks.  Any out pointer may be
+ * NULL.  Returns HH_ERR_INVALID_VALUE if this thread launched nothing yet.
+ */
+hh_status hh_last_launch_info(const char **variant, int *grid, int *block,
+                              int *smem_bytes, int *nchunks);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HH_H_ */

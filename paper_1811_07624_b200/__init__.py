@@ -1,0 +1,12 @@
+"""B200-native (sm_100a) Householder-product apply library for arXiv:1811.07624.
+
+C ABI: include/hh.h, implemented by libhh.so (csrc/).  Python binding: .hh.
+"""
+from .hh import (HH_CALL_APPLY, HH_CALL_APPLY_HOST, HH_CALL_MAHALANOBIS, HH_CALL_SYM, HH_F32,
+                 HH_F64, HH_OP_N, HH_OP_T, HHError, hh_apply, hh_apply_host, hh_mahalanobis,
+                 hh_sym_apply, hh_workspace_bytes, last_launch_info, lib, version)
+
+__all__ = ["hh_apply", "hh_sym_apply", "hh_mahalanobis", "hh_apply_host", "hh_workspace_bytes",
+           "HH_OP_N", "HH_OP_T", "HH_F32", "HH_F64", "HH_CALL_APPLY", "HH_CALL_SYM",
+           "HH_CALL_MAHALANOBIS", "HH_CALL_APPLY_HOST", "HHError", "lib", "version",
+           "last_launch_info"]

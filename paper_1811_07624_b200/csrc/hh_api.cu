@@ -1,0 +1,329 @@
+// hh_api.cu -- the extern "C" boundary of libhh.so (declared in include/hh.h).
+//
+// Validation happens before any launch (nothing is written on error); the
+// library allocates nothing for the caller's data and keeps only a cached
+// device-attribute table.  Every computational step runs in this library's own
+// kernels (hh_fused.cu, hh_gather.cu); there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <mutex>
+
+#include "hh.h"
+#include "hh_internal.h"
+
+namespace hh {
+
+namespace {
+constexpr int kMaxDev = 64;
+DevAttr g_attr[kMaxDev];
+std::once_flag g_once[kMaxDev];
+thread_local LaunchInfo t_last;
+thread_local bool t_has_last = false;
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+size_t elem(hh_dtype dt) { return dt == HH_F32 ? 4 : 8; }
+bool dtype_ok(int dt) { return dt == HH_F32 || dt == HH_F64; }
+size_t round256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+
+hh_status map_err(cudaError_t e) {
+    if (e == cudaSuccess) return HH_OK;
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return HH_ERR_UNSUPPORTED;
+    }
+    return HH_ERR_CUDA;
+}
+
+// shape checks shared by the column calls; returns HH_OK or the error
+hh_status check_common(int64_t n, int64_t h, const void *U, int64_t N, hh_dtype dtype,
+                       bool device_u = true) {
+    if (!dtype_ok(dtype) || n < 1 || h < 0 || N < 0) return HH_ERR_INVALID_VALUE;
+    if (h > 0 && !U) return HH_ERR_INVALID_VALUE;
+    if ((static_cast<size_t>(n) * elem(dtype)) % 16 != 0) return HH_ERR_UNSUPPORTED;
+    if (n > max_n(dtype)) return HH_ERR_UNSUPPORTED;
+    if (device_u && h > 0 && !aligned16(U)) return HH_ERR_UNSUPPORTED;
+    if (h > (int64_t(1) << 30)) return HH_ERR_UNSUPPORTED;
+    return HH_OK;
+}
+
+hh_status run_fused(FusedArgs a, hh_dtype dtype, cudaStream_t stream) {
+    LaunchInfo info;
+    cudaError_t e = launch_fused(a, dtype == HH_F32 ? 0 : 1, stream, &info);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (info.variant) {
+        t_last = info;
+        t_has_last = true;
+    }
+    return map_err(e);
+}
+
+// columns per ring slot of hh_apply_host
+int64_t host_chunk_cols(int64_t n, int64_t N, hh_dtype dtype) {
+    const int64_t colB = n * static_cast<int64_t>(elem(dtype));
+    const int64_t cols = std::max<int64_t>(1, (int64_t(64) << 20) / colB);
+    return std::max<int64_t>(1, std::min(cols, N));
+}
+constexpr int kRing = 3;
+
+}  // namespace
+
+const DevAttr &device_attr() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) dev = 0;
+    std::call_once(g_once[dev], [dev]() {
+        DevAttr a;
+        cudaDeviceGetAttribute(&a.sm_count, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&a.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaDeviceGetAttribute(&a.l2_bytes, cudaDevAttrL2CacheSize, dev);
+        if (a.sm_count <= 0) a.sm_count = 148;
+        if (a.max_smem_optin <= 0) a.max_smem_optin = 227 * 1024;
+        g_attr[dev] = a;
+    });
+    return g_attr[dev];
+}
+
+}  // namespace hh
+
+using namespace hh;
+
+extern "C" {
+
+const char *hh_status_string(hh_status s) {
+    switch (s) {
+        case HH_OK: return "HH_OK";
+        case HH_ERR_INVALID_VALUE: return "HH_ERR_INVALID_VALUE";
+        case HH_ERR_UNSUPPORTED: return "HH_ERR_UNSUPPORTED";
+        case HH_ERR_WORKSPACE: return "HH_ERR_WORKSPACE";
+        case HH_ERR_CUDA: return "HH_ERR_CUDA";
+    }
+    return "HH_ERR_UNKNOWN";
+}
+
+const char *hh_version(void) { return "0.1.0"; }
+
+hh_status hh_last_launch_info(const char **variant, int *grid, int *block, int *smem_bytes,
+                              int *nchunks) {
+    if (!t_has_last) return HH_ERR_INVALID_VALUE;
+    if (variant) *variant = t_last.variant;
+    if (grid) *grid = t_last.grid;
+    if (block) *block = t_last.block;
+    if (smem_bytes) *smem_bytes = t_last.smem;
+    if (nchunks) *nchunks = t_last.nchunks;
+    return HH_OK;
+}
+
+hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M, int64_t npairs,
+                             hh_dtype dtype, size_t *bytes) {
+    if (!bytes || !dtype_ok(dtype) || n < 1 || h < 0 || N_or_M < 0 || npairs < 0)
+        return HH_ERR_INVALID_VALUE;
+    switch (call) {
+        case HH_CALL_APPLY:
+        case HH_CALL_SYM:
+            *bytes = 0;
+            return HH_OK;
+        case HH_CALL_MAHALANOBIS:
+            *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype));
+            return HH_OK;
+        case HH_CALL_APPLY_HOST: {
+            const size_t ub = round256(static_cast<size_t>(n) * static_cast<size_t>(h) * elem(dtype));
+            const int64_t cols = host_chunk_cols(n, std::max<int64_t>(N_or_M, 1), dtype);
+            const size_t slot = round256(static_cast<size_t>(cols) * n * elem(dtype));
+            *bytes = ub + kRing * slot;
+            return HH_OK;
+        }
+    }
+    return HH_ERR_INVALID_VALUE;
+}
+
+hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
+                   int64_t N, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                   hh_stream_t stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
+    hh_status st = check_common(n, h, U, N, dtype);
+    if (st != HH_OK) return st;
+    if (N == 0) return HH_OK;
+    if (!X || !Y) return HH_ERR_INVALID_VALUE;
+    if (!aligned16(X) || !aligned16(Y)) return HH_ERR_UNSUPPORTED;
+    FusedArgs a{};
+    a.U = U;
+    a.X = X;
+    a.Y = Y;
+    a.n = n;
+    a.h = h;
+    a.N = N;
+    a.mode = op == HH_OP_N ? MODE_APPLY_N : MODE_APPLY_T;
+    return run_fused(a, dtype, stream);
+}
+
+hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda, const void *X,
+                       void *Y, int64_t N, hh_dtype dtype, void *workspace,
+                       size_t workspace_bytes, hh_stream_t stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    hh_status st = check_common(n, h, U, N, dtype);
+    if (st != HH_OK) return st;
+    if (N == 0) return HH_OK;
+    if (!X || !Y || !lambda) return HH_ERR_INVALID_VALUE;
+    if (!aligned16(X) || !aligned16(Y) || !aligned16(lambda)) return HH_ERR_UNSUPPORTED;
+    FusedArgs a{};
+    a.U = U;
+    a.X = X;
+    a.Y = Y;
+    a.vec = lambda;
+    a.n = n;
+    a.h = h;
+    a.N = N;
+    a.mode = MODE_SYM;
+    return run_fused(a, dtype, stream);
+}
+
+hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, const void *P,
+                         int64_t M, const int32_t *ia, const int32_t *ib, int64_t npairs,
+                         void *dist, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                         hh_stream_t stream) {
+    if (npairs < 0 || M < 0) return HH_ERR_INVALID_VALUE;
+    if (npairs > 0 && M < 1) return HH_ERR_INVALID_VALUE;
+    hh_status st = check_common(n, h, U, M, dtype);
+    if (st != HH_OK) return st;
+    if (npairs == 0) return HH_OK;
+    if (!d || !P || !ia || !ib || !dist) return HH_ERR_INVALID_VALUE;
+    if (!aligned16(d) || !aligned16(P)) return HH_ERR_UNSUPPORTED;
+    if (reinterpret_cast<uintptr_t>(dist) % elem(dtype) != 0) return HH_ERR_UNSUPPORTED;
+    size_t need = 0;
+    hh_workspace_bytes(HH_CALL_MAHALANOBIS, n, h, M, npairs, dtype, &need);
+    if (workspace) {
+        if (workspace_bytes < need) return HH_ERR_WORKSPACE;
+        if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+        // K3a: Z = diag(sqrt d) Q^T P  (transform each point once)
+        FusedArgs a{};
+        a.U = U;
+        a.X = P;
+        a.Y = workspace;
+        a.vec = d;
+        a.n = n;
+        a.h = h;
+        a.N = M;
+        a.mode = MODE_TRANSFORM;
+        st = run_fused(a, dtype, stream);
+        if (st != HH_OK) return st;
+        // K3b: dist[j] = ||Z[:,ia[j]] - Z[:,ib[j]]||^2
+        LaunchInfo info;
+        cudaError_t e = launch_gather_dist(workspace, n, ia, ib, npairs, dist,
+                                           dtype == HH_F32 ? 0 : 1, stream, &info);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (info.variant) {
+            t_last = info;
+            t_has_last = true;
+        }
+        return map_err(e);
+    }
+    // K3c: per-pair fused, no scratch
+    FusedArgs a{};
+    a.U = U;
+    a.X = P;
+    a.Y = dist;
+    a.vec = d;
+    a.ia = ia;
+    a.ib = ib;
+    a.n = n;
+    a.h = h;
+    a.N = npairs;
+    a.mode = MODE_PAIR;
+    return run_fused(a, dtype, stream);
+}
+
+hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host, const void *X_host,
+                        void *Y_host, int64_t N, hh_dtype dtype, void *workspace,
+                        size_t workspace_bytes, hh_stream_t stream) {
+    if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
+    hh_status st = check_common(n, h, U_host, N, dtype, /*device_u=*/false);
+    if (st != HH_OK) return st;
+    if (N == 0) return HH_OK;
+    if (!X_host || !Y_host || !workspace) return HH_ERR_INVALID_VALUE;
+    size_t need = 0;
+    hh_workspace_bytes(HH_CALL_APPLY_HOST, n, h, N, 0, dtype, &need);
+    if (workspace_bytes < need) return HH_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+
+    const size_t s = elem(dtype);
+    const size_t colB = static_cast<size_t>(n) * s;
+    const size_t ub = round256(static_cast<size_t>(h) * colB);
+    const int64_t cols = host_chunk_cols(n, N, dtype);
+    const size_t slotB = round256(static_cast<size_t>(cols) * colB);
+    char *ws = static_cast<char *>(workspace);
+    char *Ud = ws;
+    char *slots = ws + ub;
+
+    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+    cudaEvent_t start = nullptr, ev_in[kRing] = {}, ev_cp[kRing] = {}, ev_out[kRing] = {};
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t r) {
+        if (e == cudaSuccess && r != cudaSuccess) e = r;
+        return e == cudaSuccess;
+    };
+    chk(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
+    chk(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
+    chk(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+    chk(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    for (int i = 0; i < kRing; ++i) {
+        chk(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+        chk(cudaEventCreateWithFlags(&ev_cp[i], cudaEventDisableTiming));
+        chk(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
+    }
+    hh_status kst = HH_OK;
+    if (e == cudaSuccess) {
+        // order after everything already queued on the caller's stream
+        chk(cudaEventRecord(start, stream));
+        chk(cudaStreamWaitEvent(sh, start, 0));
+        if (h > 0) chk(cudaMemcpyAsync(Ud, U_host, static_cast<size_t>(h) * colB,
+                                       cudaMemcpyHostToDevice, sh));
+        const int64_t nchunks = (N + cols - 1) / cols;
+        for (int64_t i = 0; i < nchunks && e == cudaSuccess && kst == HH_OK; ++i) {
+            const int r = static_cast<int>(i % kRing);
+            const int64_t c0 = i * cols;
+            const int64_t cc = std::min(cols, N - c0);
+            char *slot = slots + static_cast<size_t>(r) * slotB;
+            const size_t bytes = static_cast<size_t>(cc) * colB;
+            if (i >= kRing) chk(cudaStreamWaitEvent(sh, ev_out[r], 0));
+            chk(cudaMemcpyAsync(slot, static_cast<const char *>(X_host) + c0 * colB, bytes,
+                                cudaMemcpyHostToDevice, sh));
+            chk(cudaEventRecord(ev_in[r], sh));
+            chk(cudaStreamWaitEvent(sc, ev_in[r], 0));
+            FusedArgs a{};
+            a.U = Ud;
+            a.X = slot;
+            a.Y = slot;
+            a.n = n;
+            a.h = h;
+            a.N = cc;
+            a.mode = op == HH_OP_N ? MODE_APPLY_N : MODE_APPLY_T;
+            if (e == cudaSuccess) kst = run_fused(a, dtype, sc);
+            chk(cudaEventRecord(ev_cp[r], sc));
+            chk(cudaStreamWaitEvent(sd, ev_cp[r], 0));
+            chk(cudaMemcpyAsync(static_cast<char *>(Y_host) + c0 * colB, slot, bytes,
+                                cudaMemcpyDeviceToHost, sd));
+            chk(cudaEventRecord(ev_out[r], sd));
+        }
+        chk(cudaStreamSynchronize(sh));
+        chk(cudaStreamSynchronize(sc));
+        chk(cudaStreamSynchronize(sd));
+    }
+    for (int i = 0; i < kRing; ++i) {
+        if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+        if (ev_cp[i]) cudaEventDestroy(ev_cp[i]);
+        if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+    }
+    if (start) cudaEventDestroy(start);
+    if (sh) cudaStreamDestroy(sh);
+    if (sc) cudaStreamDestroy(sc);
+    if (sd) cudaStreamDestroy(sd);
+    if (kst != HH_OK) return kst;
+    return e == cudaSuccess ? HH_OK : HH_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// hh_internal.h -- declarations shared by the libhh.so translation units.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hh {
+
+enum Mode : int {
+    MODE_APPLY_N = 0,    // Y = Q X        (u_h first)
+    MODE_APPLY_T = 1,    // Y = Q^T X      (u_1 first)
+    MODE_SYM = 2,        // Y = Q diag(vec) Q^T X
+    MODE_TRANSFORM = 3,  // Y = diag(sqrt(vec)) Q^T X       (Mahalanobis transform-once)
+    MODE_PAIR = 4        // dist[j] = sum_r vec_r (Q^T (X[:,ia_j] - X[:,ib_j]))_r^2
+};
+
+struct FusedArgs {
+    const void *U;      // (h, n) row-major reflectors
+    const void *X;      // (N, n) columns (or points for MODE_PAIR)
+    void *Y;            // (N, n) output columns (or dist[npairs] for MODE_PAIR)
+    const void *vec;    // lambda (SYM) or d (TRANSFORM / PAIR), n values
+    const int32_t *ia;  // MODE_PAIR
+    const int32_t *ib;  // MODE_PAIR
+    int64_t n, h, N;    // N = #columns, or #pairs in MODE_PAIR
+    int mode;
+    int R;              // reflectors per shared-memory U chunk
+    int nchunks;        // ceil(h / R); 1 = U resident for the whole kernel
+    int stage_x;        // 1 = stage column tiles through shared memory (bulk copy)
+    int nbatches;       // batches per unit (uniform over the grid)
+};
+
+struct LaunchInfo {
+    const char *variant = nullptr;
+    int grid = 0, block = 0, smem = 0, nchunks = 0;
+};
+
+// Launch the fused reflector kernel (K1 / K2 / K3a / K3c).  dtype: 0 f32, 1 f64.
+// Returns cudaSuccess or the launch error; cudaErrorNotSupported if n is too big.
+cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info);
+
+// K3b: dist[j] = || Z[:, ia[j]] - Z[:, ib[j]] ||^2.
+cudaError_t launch_gather_dist(const void *Z, int64_t n, const int32_t *ia, const int32_t *ib,
+                               int64_t npairs, void *dist, int dtype, cudaStream_t stream,
+                               LaunchInfo *info);
+
+// Largest n the vector kernels support for this dtype.
+int64_t max_n(int dtype);
+
+// Device attributes (cached per device, thread-safe).
+struct DevAttr {
+    int sm_count = 0;
+    int max_smem_optin = 0;
+    int l2_bytes = 0;
+};
+const DevAttr &device_attr();
+
+}  // namespace hh

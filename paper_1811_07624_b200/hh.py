@@ -1,0 +1,214 @@
+"""Thin ctypes binding over libhh.so (include/hh.h).  Argument marshalling only.
+
+Every computation runs in libhh.so's CUDA kernels.  PyTorch is used only to hold
+device memory and to name the current CUDA stream.  If libhh.so is missing or a
+tensor is not on a CUDA device the call raises -- there is no CPU fallback.
+
+Names mirror the C ABI: hh_apply, hh_sym_apply, hh_mahalanobis, hh_apply_host,
+hh_workspace_bytes.  Layout (hh.h): U is a (h, n) tensor (row i = u_{i+1},
+== n x h column-major), X / Y / P are (N, n) tensors (== n x N column-major).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from typing import Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhh.so")
+HEADER = os.path.join(os.path.dirname(_PKG), "include", "hh.h")
+
+HH_OK, HH_ERR_INVALID_VALUE, HH_ERR_UNSUPPORTED, HH_ERR_WORKSPACE, HH_ERR_CUDA = range(5)
+HH_F32, HH_F64 = 0, 1
+HH_OP_N, HH_OP_T = 0, 1
+HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST = range(4)
+
+_DT = {torch.float32: HH_F32, torch.float64: HH_F64}
+
+
+class HHError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libhh.so (built by paper_1811_07624_b200.build / __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not found: run `python -m paper_1811_07624_b200.build` "
+                               "(the CUDA extension is required; there is no fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, p, i32, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+        L.hh_apply.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
+        L.hh_sym_apply.argtypes = [i64, i64, p, p, p, p, i64, i32, p, sz, p]
+        L.hh_mahalanobis.argtypes = [i64, i64, p, p, p, i64, p, p, i64, p, i32, p, sz, p]
+        L.hh_apply_host.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
+        L.hh_workspace_bytes.argtypes = [i32, i64, i64, i64, i64, i32, ctypes.POINTER(sz)]
+        L.hh_status_string.argtypes = [i32]
+        L.hh_status_string.restype = ctypes.c_char_p
+        L.hh_version.restype = ctypes.c_char_p
+        L.hh_last_launch_info.argtypes = [ctypes.POINTER(ctypes.c_char_p)] + \
+            [ctypes.POINTER(ctypes.c_int)] * 4
+        for f in ("hh_apply", "hh_sym_apply", "hh_mahalanobis", "hh_apply_host",
+                  "hh_workspace_bytes", "hh_last_launch_info"):
+            getattr(L, f).restype = i32
+        _lib = L
+    return _lib
+
+
+def declared_symbols() -> list:
+    """Function names declared in include/hh.h."""
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[A-Za-z_]\w*\s*\*?\s*(hh_\w+)\s*\(", src, re.M)))
+
+
+def status_string(s: int) -> str:
+    return lib().hh_status_string(int(s)).decode()
+
+
+def version() -> str:
+    return lib().hh_version().decode()
+
+
+def last_launch_info() -> dict:
+    v = ctypes.c_char_p()
+    g, b, s, c = (ctypes.c_int() for _ in range(4))
+    st = lib().hh_last_launch_info(ctypes.byref(v), ctypes.byref(g), ctypes.byref(b),
+                                   ctypes.byref(s), ctypes.byref(c))
+    if st != HH_OK:
+        return {}
+    return {"variant": v.value.decode(), "grid": g.value, "block": b.value, "smem": s.value,
+            "nchunks": c.value}
+
+
+def _check(st: int, what: str):
+    if st != HH_OK:
+        raise HHError(st, what)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _dtype(t: torch.Tensor) -> int:
+    if t.dtype not in _DT:
+        raise ValueError(f"unsupported dtype {t.dtype}")
+    return _DT[t.dtype]
+
+
+def hh_workspace_bytes(call: int, n: int, h: int, N_or_M: int, npairs: int, dtype) -> int:
+    dt = _DT[dtype] if isinstance(dtype, torch.dtype) else int(dtype)
+    out = ctypes.c_size_t()
+    _check(lib().hh_workspace_bytes(int(call), n, h, N_or_M, npairs, dt, ctypes.byref(out)),
+           "hh_workspace_bytes")
+    return int(out.value)
+
+
+def hh_apply(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor] = None,
+             stream=None) -> torch.Tensor:
+    """Y = Q X (op = HH_OP_N) or Q^T X (HH_OP_T), Q = H_1 ... H_h (hh.h: hh_apply)."""
+    _dev(X, "X")
+    N, n = X.shape
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    if Y is None:
+        Y = torch.empty_like(X)
+    _dev(Y, "Y")
+    st = lib().hh_apply(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N, _dtype(X),
+                        None, 0, _stream(stream))
+    _check(st, "hh_apply")
+    return Y
+
+
+def hh_sym_apply(U: torch.Tensor, lam: torch.Tensor, X: torch.Tensor,
+                 Y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Y = Q diag(lam) Q^T X (hh.h: hh_sym_apply)."""
+    _dev(X, "X")
+    _dev(lam, "lambda")
+    N, n = X.shape
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    if Y is None:
+        Y = torch.empty_like(X)
+    _dev(Y, "Y")
+    st = lib().hh_sym_apply(n, h, _ptr(U) if h else None, _ptr(lam), _ptr(X), _ptr(Y), N,
+                            _dtype(X), None, 0, _stream(stream))
+    _check(st, "hh_sym_apply")
+    return Y
+
+
+def hh_mahalanobis(U: torch.Tensor, d: torch.Tensor, P: torch.Tensor, ia: torch.Tensor,
+                   ib: torch.Tensor, dist: Optional[torch.Tensor] = None,
+                   workspace: Optional[torch.Tensor] = None, fused: bool = False,
+                   stream=None) -> torch.Tensor:
+    """dist[j] = ||D^1/2 Q^T (P[ia[j]] - P[ib[j]])||^2 (hh.h: hh_mahalanobis).
+
+    By default a workspace is allocated for the transform-once path (K3a + K3b);
+    `fused=True` passes NULL and runs the per-pair fused kernel (K3c)."""
+    _dev(P, "P")
+    _dev(d, "d")
+    _dev(ia, "ia")
+    _dev(ib, "ib")
+    if ia.dtype != torch.int32 or ib.dtype != torch.int32:
+        raise ValueError("ia, ib must be int32")
+    M, n = P.shape
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    npairs = ia.numel()
+    if dist is None:
+        dist = torch.empty(npairs, dtype=P.dtype, device=P.device)
+    _dev(dist, "dist")
+    wsb = 0
+    if not fused:
+        wsb = hh_workspace_bytes(HH_CALL_MAHALANOBIS, n, h, M, npairs, P.dtype)
+        if workspace is None or workspace.numel() < wsb:
+            workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=P.device)
+        else:
+            wsb = workspace.numel()
+    st = lib().hh_mahalanobis(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P), M, _ptr(ia),
+                              _ptr(ib), npairs, _ptr(dist), _dtype(P),
+                              None if fused else _ptr(workspace), wsb, _stream(stream))
+    _check(st, "hh_mahalanobis")
+    return dist
+
+
+def hh_apply_host(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor] = None,
+                  workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """hh_apply on HOST (CPU, ideally pinned) tensors; device workspace (hh.h: hh_apply_host)."""
+    if X.is_cuda or (U.numel() and U.is_cuda):
+        raise ValueError("hh_apply_host takes host tensors")
+    N, n = X.shape
+    h = U.shape[0] if U.numel() else 0
+    if Y is None:
+        Y = torch.empty_like(X, pin_memory=X.is_pinned())
+    wsb = hh_workspace_bytes(HH_CALL_APPLY_HOST, n, h, N, 0, X.dtype)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    st = lib().hh_apply_host(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,
+                             _dtype(X), _ptr(workspace), workspace.numel(), _stream(stream))
+    _check(st, "hh_apply_host")
+    return Y

@@ -1,0 +1,110 @@
+"""CPU-side checks of the C ABI boundary: the library loads, exports every symbol
+include/hh.h declares, and validates arguments before any launch (no GPU needed:
+every call here returns before touching the CUDA runtime)."""
+import ctypes
+import os
+
+import pytest
+
+import paper_1811_07624_b200 as hhpkg
+from paper_1811_07624_b200 import hh
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_declared_symbols():
+    L = hh.lib()
+    syms = hh.declared_symbols()
+    for s in ("hh_apply", "hh_sym_apply", "hh_mahalanobis", "hh_apply_host",
+              "hh_workspace_bytes", "hh_status_string", "hh_version", "hh_last_launch_info"):
+        assert s in syms
+    for s in syms:
+        assert hasattr(L, s), f"libhh.so does not export {s}"
+    assert hh.version().count(".") == 2
+
+
+def test_library_is_sm100a():
+    """libhh.so carries sm_100a SASS (cuobjdump), no PTX-only JIT path."""
+    import shutil
+    import subprocess
+    cu = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cu):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([cu, "--list-elf", hh.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings():
+    for s, name in enumerate(["HH_OK", "HH_ERR_INVALID_VALUE", "HH_ERR_UNSUPPORTED",
+                              "HH_ERR_WORKSPACE", "HH_ERR_CUDA"]):
+        assert hh.status_string(s) == name
+    assert hh.status_string(99) == "HH_ERR_UNKNOWN"
+
+
+def test_workspace_query():
+    assert hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 1024, 10, 262144, 0, 0) == 0
+    assert hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 2048, 32, 131072, 0, 0) == 0
+    assert hhpkg.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, 512, 9, 65536, 1 << 21, 0) == \
+        512 * 65536 * 4
+    b = hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY_HOST, 1024, 10, 262144, 0, 0)
+    assert b >= 3 * (64 << 20) + 10 * 1024 * 4
+    with pytest.raises(hh.HHError):
+        hhpkg.hh_workspace_bytes(7, 16, 1, 1, 0, 0)
+    with pytest.raises(hh.HHError):
+        hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 0, 1, 1, 0, 0)
+
+
+def _apply(op, n, h, U, X, Y, N, dt):
+    return hh.lib().hh_apply(op, n, h, U, X, Y, N, dt, None, 0, None)
+
+
+def test_validation_before_launch():
+    L = hh.lib()
+    A = 1 << 20      # a fake but 16-B aligned address: never dereferenced on these paths
+    # invalid values
+    assert _apply(2, 16, 1, A, A, A, 4, 0) == hh.HH_ERR_INVALID_VALUE           # bad op
+    assert _apply(0, 0, 1, A, A, A, 4, 0) == hh.HH_ERR_INVALID_VALUE            # n < 1
+    assert _apply(0, 16, -1, A, A, A, 4, 0) == hh.HH_ERR_INVALID_VALUE          # h < 0
+    assert _apply(0, 16, 1, A, A, A, -1, 0) == hh.HH_ERR_INVALID_VALUE          # N < 0
+    assert _apply(0, 16, 1, None, A, A, 4, 0) == hh.HH_ERR_INVALID_VALUE        # U NULL
+    assert _apply(0, 16, 1, A, A, A, 4, 5) == hh.HH_ERR_INVALID_VALUE           # bad dtype
+    # unsupported
+    assert _apply(0, 18, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED             # n*4 % 16
+    assert _apply(0, 9, 1, A, A, A, 4, 1) == hh.HH_ERR_UNSUPPORTED              # n*8 % 16
+    assert _apply(0, 16, 1, A + 4, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED         # U misaligned
+    assert _apply(0, 16, 1, A, A + 8, A, 4, 0) == hh.HH_ERR_UNSUPPORTED         # X misaligned
+    assert _apply(0, 8196, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED           # n > max
+    # empty batches are successful no-ops (no launch), h = 0 needs no U
+    assert _apply(0, 16, 1, A, None, None, 0, 0) == hh.HH_OK
+    assert _apply(1, 16, 0, None, None, None, 0, 0) == hh.HH_OK
+    # sym / Mahalanobis
+    assert L.hh_sym_apply(16, 1, A, None, A, A, 4, 0, None, 0, None) == hh.HH_ERR_INVALID_VALUE
+    assert L.hh_sym_apply(16, 1, A, A + 4, A, A, 4, 0, None, 0, None) == hh.HH_ERR_UNSUPPORTED
+    assert L.hh_sym_apply(16, 1, A, A, A, A, 0, 0, None, 0, None) == hh.HH_OK
+    assert L.hh_mahalanobis(16, 1, A, A, A, 0, A, A, 3, A, 0, None, 0, None) == \
+        hh.HH_ERR_INVALID_VALUE                                                  # M = 0, pairs
+    assert L.hh_mahalanobis(16, 1, A, A, A, 5, A, A, 3, A, 0, A, 16, None) == \
+        hh.HH_ERR_WORKSPACE                                                      # ws too small
+    assert L.hh_mahalanobis(16, 1, A, A, A, 5, A, A, 0, A, 0, None, 0, None) == hh.HH_OK
+    assert L.hh_apply_host(0, 16, 1, A, A, A, 4, 0, A, 16, None) == hh.HH_ERR_WORKSPACE
+    assert L.hh_apply_host(0, 16, 1, A + 3, A, A, 0, 0, None, 0, None) == hh.HH_OK
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    with pytest.raises(ValueError):
+        hhpkg.hh_apply(0, torch.zeros(1, 16), torch.zeros(2, 16))
+
+
+def test_product_does_not_touch_oracle():
+    """The product package never imports, links or executes the oracle (or anything CPU)."""
+    pkg = os.path.join(ROOT, "paper_1811_07624_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "oracle" not in src.replace("oracle/", ""), f
+                assert "hh_ref" not in src, f
+    L = hh.lib()
+    assert not hasattr(L, "hh_ref_apply")
+    ctypes.CDLL  # keep import used
