@@ -287,13 +287,19 @@ def run_hh(args):
                                          stream=stream)
         launches = 2
     else:
-        step = lambda: hh.hh_apply(op, U, X, Y, stream=stream)  # noqa: E731
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_APPLY, c.n, c.h, c.N, 0, X.dtype)
+        wsp = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        step = lambda: hh.hh_apply(op, U, X, Y, workspace=wsp, stream=stream)  # noqa: E731
         launches = 1
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     info = hh.last_launch_info()
+    wy_path = str(info.get("variant", "")).startswith("wy_")
+    if wy_path:
+        # K4: pack, Gram, T, V; then per block of reflectors K5a (project) + K5b (update)
+        launches = 4 + 2 * int(info["nchunks"])
 
     # quick sampled parity against the oracle (rank 0; outside the timed region)
     parity = None
@@ -398,6 +404,22 @@ def run_hh(args):
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
                 "frac_of_8TBps": achieved / 8000.0,
                 "kernel": info.get("variant"), "launch": info}
+        if wy_path:
+            # compact-WY on the bf16 tensor pipe: algorithmic 4hnN flops and the
+            # executed bf16x3 MMA flops (3 products of 2*b_pad*n per column per GEMM)
+            pk = peaks()[2]
+            tpeak = float(pk.get("bf16_tflops", 1590.0)) if pk else 1590.0
+            hp = info["nchunks"] * ((c.h + info["nchunks"] - 1) // info["nchunks"] + 31) // 32 * 32
+            exe = 3 * 2 * 2 * hp * c.n * c.N
+            roof = {"bound": "tensor", "achieved": flops / (ms_step * 1e-3) / 1e12,
+                    "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": flops / (ms_step * 1e-3) / 1e12 / tpeak, "traffic": traffic,
+                    "peak_source": "measured bf16 (MEASURED_PEAKS.json bf16_tflops)",
+                    "executed_tflops": exe / (ms_step * 1e-3) / 1e12,
+                    "executed_frac": exe / (ms_step * 1e-3) / 1e12 / tpeak,
+                    "hbm_gbs_alg": achieved, "hbm_frac_alg": achieved / hbm,
+                    "kernel": info.get("variant"), "launch": info,
+                    "scope": "whole step (K4 prep + all K5 launches)"}
         cpu = None
         if not args.no_cpu_baseline and ws == 1:
             v, ups, secs, sample, thr = time_oracle(c, op, target_s=args.cpu_seconds)

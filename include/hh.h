@@ -86,6 +86,15 @@ typedef enum {
 /* The paper's Eq. 1 (D = I) Ubar = U_h ... U_1 is HH_OP_T on the same
  * columns; reflector symmetry makes the transpose a reversal. */
 
+/* Path selection for hh_apply (fp32):
+ *   HH_ALGO_AUTO  -- the measured crossover: K1 fused SIMT kernel for
+ *                    small h, K5 compact-WY on the tensor cores for large h when a
+ *                    workspace of hh_workspace_bytes(HH_CALL_APPLY, ...) is passed;
+ *   HH_ALGO_FUSED -- always K1 (any dtype);
+ *   HH_ALGO_WY    -- always K5 (fp32 only; HH_ERR_WORKSPACE without a workspace,
+ *                    HH_ERR_UNSUPPORTED for fp64). */
+typedef enum { HH_ALGO_AUTO = 0, HH_ALGO_FUSED = 1, HH_ALGO_WY = 2 } hh_algo;
+
 typedef enum {
     HH_CALL_APPLY = 0,
     HH_CALL_SYM = 1,
@@ -99,8 +108,12 @@ typedef enum {
  *   takes 4nh operations" -- each column costs h dot products u_i^T x and h
  *   rank-1 updates x -= 2 (u_i^T x) u_i, never densifying Q.
  *   n >= 1, h >= 0, N >= 0; U: n x h (may be NULL iff h == 0); X, Y: n x N.
- *   workspace: none needed (pass NULL, 0).
- *   Fused small-h kernel: one HBM read + one HBM write of X (bound: HBM).
+ *   workspace: DEVICE scratch of hh_workspace_bytes(HH_CALL_APPLY, n, h, N, 0, dtype)
+ *   bytes (0 when the fused kernel is selected; NULL is then fine).
+ *   Small h: fused kernel K1, one HBM read + one HBM write of X (bound: HBM).
+ *   Large h (fp32, workspace given): blocked compact-WY form of the same product
+ *   (I - W T W^T per block of <= 256 reflectors) on the tcgen05 tensor cores with a
+ *   bf16x3 split (fp32-level accuracy); see hh_algo.  Same result up to rounding.
  */
 hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
                    void *Y, int64_t N, hh_dtype dtype, void *workspace,
@@ -153,9 +166,19 @@ hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host,
                         void *workspace, size_t workspace_bytes, hh_stream_t stream);
 
 /*
+ * hh_set_algo -- select the hh_apply path for subsequent calls of the calling
+ * thread (thread-local; default HH_ALGO_AUTO).  HH_ERR_INVALID_VALUE for an
+ * unknown value.  hh_get_algo returns the current selection.
+ */
+hh_status hh_set_algo(hh_algo algo);
+hh_algo hh_get_algo(void);
+
+/*
  * hh_workspace_bytes -- scratch bytes the call needs (cuBLAS bufferSize style).
  *   N_or_M: N for apply/sym/apply_host, M for Mahalanobis.  Writes *bytes.
- *   HH_CALL_APPLY / HH_CALL_SYM: 0.  HH_CALL_MAHALANOBIS: n*M*sizeof(dtype) (the
+ *   HH_CALL_APPLY: the compact-WY scratch when this thread's hh_algo selection
+ *   picks K5 for (n, h, N, dtype) (packed W, T, V = W T and one G block), else 0.
+ *   HH_CALL_SYM: 0.  HH_CALL_MAHALANOBIS: n*M*sizeof(dtype) (the
  *   transform-once Z).  Errors: HH_ERR_INVALID_VALUE for bad arguments.
  */
 hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,

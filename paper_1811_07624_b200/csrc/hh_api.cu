@@ -21,6 +21,18 @@ DevAttr g_attr[kMaxDev];
 std::once_flag g_once[kMaxDev];
 thread_local LaunchInfo t_last;
 thread_local bool t_has_last = false;
+thread_local int t_algo = HH_ALGO_AUTO;
+
+// K1 (fused SIMT) vs K5 (compact-WY on tcgen05) crossover in h, fp32 only.
+// Measured on B200: below it the fused kernel's single HBM pass wins.
+int64_t wy_min_h(int64_t n) { return n >= 512 ? 32 : 1 << 30; }
+
+bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
+    if (dtype != HH_F32 || !wy_supported(n, h, N)) return false;
+    if (algo == HH_ALGO_WY) return true;
+    if (algo == HH_ALGO_FUSED) return false;
+    return h >= wy_min_h(n);
+}
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 size_t elem(hh_dtype dt) { return dt == HH_F32 ? 4 : 8; }
@@ -102,7 +114,26 @@ const char *hh_status_string(hh_status s) {
     return "HH_ERR_UNKNOWN";
 }
 
-const char *hh_version(void) { return "0.1.0"; }
+const char *hh_version(void) { return "0.2.0"; }
+
+// Test hook (not part of hh.h): runs the compact-WY preparation and the first
+// projection only, leaving G (bf16 hi/lo rows) and V in the workspace at the
+// offsets written to off[0..1] (G, V) and the block size b / count nblk to off[2..3].
+hh_status hh_debug_wy_project(int op, int64_t n, int64_t h, const void *U, const void *X,
+                              int64_t N, void *workspace, size_t workspace_bytes, int64_t *off,
+                              hh_stream_t stream) {
+    if (!wy_supported(n, h, N) || !workspace || !off) return HH_ERR_INVALID_VALUE;
+    const WyPlan p = wy_plan(n, h, N);
+    if (workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
+    off[0] = static_cast<int64_t>(p.off_gt);
+    off[1] = static_cast<int64_t>(p.off_vt);
+    off[2] = p.b;
+    off[3] = p.nblk;
+    off[4] = p.n_pad;
+    off[5] = static_cast<int64_t>(p.off_t);
+    return map_err(launch_wy(op, p, static_cast<const float *>(U), static_cast<const float *>(X),
+                             nullptr, workspace, stream, nullptr, 1));
+}
 
 hh_status hh_last_launch_info(const char **variant, int *grid, int *block, int *smem_bytes,
                               int *nchunks) {
@@ -121,6 +152,8 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
         return HH_ERR_INVALID_VALUE;
     switch (call) {
         case HH_CALL_APPLY:
+            *bytes = use_wy(dtype, n, h, N_or_M, t_algo) ? wy_plan(n, h, N_or_M).bytes : 0;
+            return HH_OK;
         case HH_CALL_SYM:
             *bytes = 0;
             return HH_OK;
@@ -138,17 +171,42 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
     return HH_ERR_INVALID_VALUE;
 }
 
+hh_status hh_set_algo(hh_algo algo) {
+    if (algo != HH_ALGO_AUTO && algo != HH_ALGO_FUSED && algo != HH_ALGO_WY)
+        return HH_ERR_INVALID_VALUE;
+    t_algo = algo;
+    return HH_OK;
+}
+
+hh_algo hh_get_algo(void) { return static_cast<hh_algo>(t_algo); }
+
 hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
                    int64_t N, hh_dtype dtype, void *workspace, size_t workspace_bytes,
                    hh_stream_t stream) {
-    (void)workspace;
-    (void)workspace_bytes;
     if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
     hh_status st = check_common(n, h, U, N, dtype);
     if (st != HH_OK) return st;
     if (N == 0) return HH_OK;
     if (!X || !Y) return HH_ERR_INVALID_VALUE;
     if (!aligned16(X) || !aligned16(Y)) return HH_ERR_UNSUPPORTED;
+    if (h > 0 && use_wy(dtype, n, h, N, t_algo)) {
+        const WyPlan p = wy_plan(n, h, N);
+        if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
+        if (workspace && !aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+        if (!workspace && t_algo == HH_ALGO_WY) return HH_ERR_WORKSPACE;
+        if (workspace) {
+            LaunchInfo info;
+            cudaError_t e = launch_wy(op == HH_OP_T ? 1 : 0, p, static_cast<const float *>(U),
+                                      static_cast<const float *>(X), static_cast<float *>(Y),
+                                      workspace, stream, &info);
+            if (info.variant) {
+                t_last = info;
+                t_has_last = true;
+            }
+            return map_err(e);
+        }
+        // no workspace in AUTO mode: the fused kernel (K1) runs instead
+    }
     FusedArgs a{};
     a.U = U;
     a.X = X;

@@ -55,3 +55,22 @@ struct DevAttr {
 const DevAttr &device_attr();
 
 }  // namespace hh
+
+namespace hh {
+
+// ---- K4/K5 compact-WY tensor-core path (hh_wy.cu) ----
+struct WyPlan {
+    int64_t n = 0, h = 0, N = 0;
+    int b = 0, nblk = 0, h_pad = 0;
+    int64_t n_pad = 0;
+    size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_vt = 0, off_gt = 0;
+    size_t bytes = 0;
+};
+WyPlan wy_plan(int64_t n, int64_t h, int64_t N);
+bool wy_supported(int64_t n, int64_t h, int64_t N);
+// op_t = 0: Y = Q X; 1: Y = Q^T X (fp32).  debug_stop_blocks >= 0: run the
+// preparation and only the first projection (test hook).
+cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X, float *Y,
+                      void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks = -1);
+
+}  // namespace hh

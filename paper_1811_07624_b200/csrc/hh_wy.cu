@@ -1,0 +1,754 @@
+// hh_wy.cu -- K4 (compact-WY preparation) and K5 (compact-WY apply on the
+// sm_100a tensor cores) for large h.
+//
+// The reflectors (in the order of the requested product, see below) are cut into
+// nblk blocks of b (b <= 256, a multiple of 32; the last block is padded with
+// u = 0 identity slots).  For one block with W = [w_1 .. w_b] (n x b):
+//
+//     H(w_1) H(w_2) ... H(w_b) = I - W T W^T,     T upper triangular, T_ii = 2,
+//     T[0:i, i] = -2 T[0:i, 0:i] (W[:, 0:i]^T w_i)                     (K4)
+//
+// (verified from Eq. 2, by induction: appending H(w_i) to I - W'T'W'^T
+// adds the column t = -2 T'(W'^T w_i) and the diagonal entry 2).  With V = W T the
+// block acts on a column tile as
+//
+//     G = W^T X          (K5a "project":  M = 128 columns, N = b, K = n)
+//     X <- X - V G^T...  (K5b "update":   M = 128 columns, N = 256 rows, K = b)
+//
+// Q X = H_1 ... H_h X applies the LAST block first; Q^T X = H_h ... H_1 X is the
+// same computation on the reversed reflector list (reflectors are
+// symmetric, so the transpose only reverses the order).  This is algebraically the
+// product of Eq. 1-2 applied one reflector at a time (north_star
+// (c)); only the rounding differs.
+//
+// Precision ("bf16x3"): every tensor-core operand z (fp32) is split as
+// z = hi + lo + O(2^-17 |z|), hi = bf16(z), lo = bf16(z - hi); the products
+// hi*hi + hi*lo + lo*hi are accumulated in fp32 in TMEM.  That keeps fp32-level
+// accuracy (~1e-6 relative against the 2e-5*sqrt(h) gate) at twice the
+// TF32 tensor rate, with bf16's full fp32 exponent range (no scaling).
+//
+// Data movement: X, W and V tiles move by TMA (cp.async.bulk.tensor, SWIZZLE_64B
+// K-major for the MMA operands); the fp32 X tile is split into bf16 hi/lo in shared
+// memory by converter warps; one elected thread issues tcgen05.mma; accumulators
+// live in TMEM (2 x 256 columns, double-buffered) and are drained by epilogue
+// warps with tcgen05.ld.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "hh_internal.h"
+#include "hh_tc.cuh"
+
+namespace hh {
+
+namespace {
+
+constexpr int kSplitK = 8;        // Gram split-K factor (deterministic reduction)
+constexpr int kRowChunk = 256;    // K5b output rows per accumulator (MMA N)
+constexpr int kTileCols = 128;    // columns of X per tile (MMA M)
+constexpr int kStages1 = 3;       // K5a pipeline depth
+constexpr int kStages3 = 3;       // K5b pipeline depth
+constexpr int kStage1Bytes = 65536;  // raw X 16K + X hi/lo 16K + W hi/lo 32K (b = 256)
+constexpr int kStage3Bytes = 32768;  // V hi/lo tile (256 rows x 32 bf16) x 2
+constexpr int kGresBytes = 131072;   // resident G hi/lo (128 x 256 bf16) x 2
+
+size_t al(size_t x) { return (x + 1023) & ~static_cast<size_t>(1023); }
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint16_t f2bf(float x) {
+    uint16_t b;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(b) : "f"(x));
+    return b;
+}
+__device__ __forceinline__ float bf2f(uint16_t b) {
+    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+// ------------------------------------------------------------------ K4: preparation
+// Wf[i][r] (fp32, h_pad x n_pad) = u_{e(i)}[r] in product order (zero padded);
+// Wb = bf16 split [hi rows 0..h_pad) [lo rows h_pad..2h_pad), ld = n_pad.
+__global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h, int reverse,
+                               int h_pad, int64_t n_pad, float *__restrict__ Wf,
+                               uint16_t *__restrict__ Wb) {
+    const int64_t total = static_cast<int64_t>(h_pad) * n_pad;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / n_pad, r = idx % n_pad;
+        float v = 0.f;
+        if (i < h && r < n) {
+            const int64_t e = reverse ? (h - 1 - i) : i;
+            v = U[e * n + r];
+        }
+        Wf[idx] = v;
+        const uint16_t hb = f2bf(v);
+        Wb[idx] = hb;
+        Wb[total + idx] = f2bf(v - bf2f(hb));
+    }
+}
+
+// Sp[blk][split][l][m] = sum_{r in split} w_l[r] w_m[r], upper 64x64 tiles only.
+__global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ Wf, int64_t n_pad,
+                                                      int b, int nblk, float *__restrict__ Sp) {
+    const int ti = blockIdx.x, tj = blockIdx.y;
+    const int blk = blockIdx.z / kSplitK, sp = blockIdx.z % kSplitK;
+    if (ti > tj) return;
+    __shared__ float Ls[32][65], Ms[32][65];
+    const int t = threadIdx.x, tx = t % 16, ty = t / 16;
+    float acc[4][4] = {};
+    const int64_t rlen = n_pad / kSplitK;
+    const int64_t r0 = sp * rlen;
+    const float *Wl = Wf + (static_cast<int64_t>(blk) * b + ti * 64) * n_pad;
+    const float *Wm = Wf + (static_cast<int64_t>(blk) * b + tj * 64) * n_pad;
+    const int rows_l = min(64, b - ti * 64), rows_m = min(64, b - tj * 64);
+    for (int64_t rc = r0; rc < r0 + rlen; rc += 32) {
+        for (int e = t; e < 32 * 64; e += 256) {
+            const int c = e / 32, k = e % 32;
+            Ls[k][c] = c < rows_l ? Wl[c * n_pad + rc + k] : 0.f;
+            Ms[k][c] = c < rows_m ? Wm[c * n_pad + rc + k] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            float a[4], m[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = Ls[k][ty * 4 + q];
+                m[q] = Ms[k][tx * 4 + q];
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[p][q] = fmaf(a[p], m[q], acc[p][q]);
+        }
+        __syncthreads();
+    }
+    float *out = Sp + (static_cast<int64_t>(blk) * kSplitK + sp) * b * b;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int l = ti * 64 + ty * 4 + p;
+        if (l >= b) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int m = tj * 64 + tx * 4 + q;
+            if (m < b) out[static_cast<int64_t>(l) * b + m] = acc[p][q];
+        }
+    }
+}
+
+// T (upper triangular, b x b) per block: reduce the Gram partials (fixed order),
+// build the 32x32 diagonal blocks by the forward recurrence, then extend 32
+// columns at a time: T[0:c, c:c+32] = -T[0:c,0:c] * S[0:c, c:c+32] * T[c:c+32, c:c+32].
+__global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict__ Sp, int b,
+                                                          float *__restrict__ Sg,
+                                                          float *__restrict__ Tg) {
+    const int blk = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t bb = static_cast<int64_t>(b) * b;
+    float *S = Sg + blk * bb;
+    float *T = Tg + blk * bb;
+    const float *P0 = Sp + static_cast<int64_t>(blk) * kSplitK * bb;
+    for (int64_t e = t; e < bb; e += 1024) {
+        const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
+        float s = 0.f;
+        if ((l / 64) <= (m / 64)) {
+#pragma unroll
+            for (int q = 0; q < kSplitK; ++q) s += P0[q * bb + e];
+        }
+        S[e] = s;
+        T[e] = 0.f;
+    }
+    __syncthreads();
+    // level-0 diagonal blocks (8 x 32 x 33) and the extension product (<= 224 x 32)
+    // share one buffer: they are used in disjoint phases
+    __shared__ float shbuf[8 * 32 * 33];
+    float *Pm = shbuf;
+    if (warp < b / 32) {
+        const int o = warp * 32;
+        float(*tb)[33] = reinterpret_cast<float(*)[33]>(shbuf + warp * 32 * 33);
+        for (int c = 0; c < 32; ++c) tb[lane][c] = 0.f;
+        __syncwarp();
+        for (int i = 0; i < 32; ++i) {
+            float v = 0.f;
+            if (lane < i) {
+                float s = 0.f;
+                for (int m = lane; m < i; ++m) s = fmaf(tb[lane][m], S[(o + m) * b + o + i], s);
+                v = -2.f * s;
+            } else if (lane == i) {
+                v = 2.f;
+            }
+            tb[lane][i] = v;
+            __syncwarp();
+        }
+        for (int c = 0; c < 32; ++c) T[(o + lane) * b + o + c] = tb[lane][c];
+    }
+    __syncthreads();
+    for (int c = 32; c < b; c += 32) {
+        // Pm[l][j] = sum_{m<=j} S[l][c+m] T[c+m][c+j]
+        for (int e = t; e < c * 32; e += 1024) {
+            const int l = e / 32, j = e % 32;
+            float s = 0.f;
+            for (int m = 0; m <= j; ++m) s = fmaf(S[l * b + c + m], T[(c + m) * b + c + j], s);
+            Pm[e] = s;
+        }
+        __syncthreads();
+        // T[l][c+j] = -sum_{m=l}^{c-1} T[l][m] Pm[m][j]
+        for (int e = t; e < c * 32; e += 1024) {
+            const int l = e / 32, j = e % 32;
+            float s = 0.f;
+            for (int m = l; m < c; ++m) s = fmaf(T[l * b + m], Pm[m * 32 + j], s);
+            T[l * b + c + j] = -s;
+        }
+        __syncthreads();
+    }
+}
+
+// V = W T (n_pad x b per block), split to bf16 into Vt[hi: blk*n_pad + r][i],
+// Vt[lo: (nblk+blk)*n_pad + r][i] (row length b).
+__global__ void __launch_bounds__(256) wy_v_kernel(const float *__restrict__ Wf,
+                                                   const float *__restrict__ Tg, int64_t n_pad,
+                                                   int b, int nblk, uint16_t *__restrict__ Vt) {
+    const int r0 = blockIdx.x * 64, i0 = blockIdx.y * 32, blk = blockIdx.z;
+    __shared__ float Us[32][65], Ts[32][33];
+    const int t = threadIdx.x, tx = t % 8, ty = t / 8;
+    float acc[2][4] = {};
+    const float *W = Wf + static_cast<int64_t>(blk) * b * n_pad;
+    const float *T = Tg + static_cast<int64_t>(blk) * b * b;
+    const int lmax = i0 + 32;  // T[l][i] = 0 for l > i
+    for (int l0 = 0; l0 < lmax; l0 += 32) {
+        for (int e = t; e < 32 * 64; e += 256) {
+            const int k = e / 64, r = e % 64;
+            Us[k][r] = W[static_cast<int64_t>(l0 + k) * n_pad + r0 + r];
+        }
+        for (int e = t; e < 32 * 32; e += 256) {
+            const int k = e / 32, c = e % 32;
+            Ts[k][c] = T[static_cast<int64_t>(l0 + k) * b + i0 + c];
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            const float u0 = Us[k][ty * 2], u1 = Us[k][ty * 2 + 1];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float tv = Ts[k][tx * 4 + q];
+                acc[0][q] = fmaf(u0, tv, acc[0][q]);
+                acc[1][q] = fmaf(u1, tv, acc[1][q]);
+            }
+        }
+        __syncthreads();
+    }
+    const int64_t lo_off = static_cast<int64_t>(nblk) * n_pad * b;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int64_t r = r0 + ty * 2 + p;
+        uint16_t hv[4], lv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            hv[q] = f2bf(acc[p][q]);
+            lv[q] = f2bf(acc[p][q] - bf2f(hv[q]));
+        }
+        const int64_t o = (static_cast<int64_t>(blk) * n_pad + r) * b + i0 + tx * 4;
+        uint2 H, L;
+        H.x = hv[0] | (static_cast<uint32_t>(hv[1]) << 16);
+        H.y = hv[2] | (static_cast<uint32_t>(hv[3]) << 16);
+        L.x = lv[0] | (static_cast<uint32_t>(lv[1]) << 16);
+        L.y = lv[2] | (static_cast<uint32_t>(lv[3]) << 16);
+        *reinterpret_cast<uint2 *>(Vt + o) = H;
+        *reinterpret_cast<uint2 *>(Vt + lo_off + o) = L;
+    }
+}
+
+// ------------------------------------------------------------------ K5a: G = W^T X
+// 10 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-5 converters (fp32 X
+// tile -> bf16 hi/lo, SW64 K-major), w6-9 epilogue (TMEM -> bf16 hi/lo G rows).
+struct Bars1 {
+    uint64_t full[kStages1], conv[kStages1], empty[kStages1];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(320, 1)
+    wy_project_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                      uint16_t *__restrict__ Gt, int n, int64_t N, int b, int wrow_hi, int wrow_lo,
+                      int ntiles) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    Bars1 *bars = reinterpret_cast<Bars1 *>(smem + kStages1 * kStage1Bytes);
+    auto rawX = [&](int s) { return smem + s * kStage1Bytes; };
+    auto Xhi = [&](int s) { return smem + s * kStage1Bytes + 16384; };
+    auto Xlo = [&](int s) { return smem + s * kStage1Bytes + 24576; };
+    auto Whi = [&](int s) { return smem + s * kStage1Bytes + 32768; };
+    auto Wlo = [&](int s) { return smem + s * kStage1Bytes + 32768 + 64 * b; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nk = (n + 31) / 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages1; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->conv[s], 128);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->acc_full[a], 1);
+            mbar_init(&bars->acc_empty[a], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc<512>(&bars->tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tbase = bars->tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tc::prefetch_tmap(&tmX);
+            tc::prefetch_tmap(&tmW);
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t bytes = 16384u + 128u * static_cast<uint32_t>(b);
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int ks = 0; ks < nk; ++ks) {
+                    mbar_wait(&bars->empty[s], ph ^ 1u);
+                    mbar_arrive_expect_tx(&bars->full[s], bytes);
+                    tc::tma_load_2d(rawX(s), &tmX, ks * 32, tile * kTileCols, &bars->full[s]);
+                    tc::tma_load_2d(Whi(s), &tmW, ks * 32, wrow_hi, &bars->full[s]);
+                    tc::tma_load_2d(Wlo(s), &tmW, ks * 32, wrow_lo, &bars->full[s]);
+                    if (++s == kStages1) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_bf16(128, b);
+            int s = 0, a = 0;
+            uint32_t ph = 0, aph = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+                tc::fence_after_sync();
+                const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
+                for (int ks = 0; ks < nk; ++ks) {
+                    mbar_wait(&bars->conv[s], ph);
+                    tc::fence_after_sync();
+                    const uint32_t xh = smem_u32(Xhi(s)), xl = smem_u32(Xlo(s));
+                    const uint32_t wh = smem_u32(Whi(s)), wl = smem_u32(Wlo(s));
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const uint64_t ah = tc::sdesc_sw64(xh + kk * 32), alo = tc::sdesc_sw64(xl + kk * 32);
+                        const uint64_t bh = tc::sdesc_sw64(wh + kk * 32), blo = tc::sdesc_sw64(wl + kk * 32);
+                        tc::mma_bf16(d, ah, bh, idesc, (ks | kk) != 0);
+                        tc::mma_bf16(d, ah, blo, idesc, 1u);
+                        tc::mma_bf16(d, alo, bh, idesc, 1u);
+                    }
+                    tc::mma_commit(&bars->empty[s]);
+                    if (++s == kStages1) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                tc::mma_commit(&bars->acc_full[a]);
+                if (++a == 2) {
+                    a = 0;
+                    aph ^= 1u;
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp < 6) {
+        // converters: 128 threads, 8 float4 each per stage
+        const int ct = threadIdx.x - 64;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for (int ks = 0; ks < nk; ++ks) {
+                mbar_wait(&bars->full[s], ph);
+                const float4 *raw = reinterpret_cast<const float4 *>(rawX(s));
+                unsigned char *xh = Xhi(s), *xl = Xlo(s);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int idx = ct + 128 * q;
+                    const int r = idx >> 3, c4 = idx & 7;
+                    const float4 v = raw[idx];
+                    uint2 H, L;
+                    tc::split2(v.x, v.y, H.x, L.x);
+                    tc::split2(v.z, v.w, H.y, L.y);
+                    const uint32_t off = tc::sw64_off(r, c4 >> 1) + (c4 & 1) * 8;
+                    *reinterpret_cast<uint2 *>(xh + off) = H;
+                    *reinterpret_cast<uint2 *>(xl + off) = L;
+                }
+                fence_proxy_async_smem();
+                tc::mbar_arrive(&bars->conv[s]);
+                if (++s == kStages1) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // epilogue: TMEM lane quarter q = warp % 4
+        const int q = warp & 3;
+        int a = 0;
+        uint32_t aph = 0;
+        uint16_t *Glo = Gt + N * b;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            mbar_wait(&bars->acc_full[a], aph);
+            tc::fence_after_sync();
+            const int64_t j = static_cast<int64_t>(tile) * kTileCols + q * 32 + lane;
+            for (int c = 0; c < b / 32; ++c) {
+                float v[32];
+                tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                  static_cast<uint32_t>(a * 256 + c * 32),
+                              v);
+                if (j < N) {
+                    uint32_t H[16], L[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
+                    uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
+                    uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
+                        gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
+                    }
+                }
+            }
+            tc::fence_before_sync();
+            tc::mbar_arrive(&bars->acc_empty[a]);
+            if (++a == 2) {
+                a = 0;
+                aph ^= 1u;
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) tc::tmem_free<512>(tbase);
+}
+
+// ------------------------------------------------------------------ K5b: X <- X - V G
+// 6 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-5 epilogue.
+struct Bars3 {
+    uint64_t gfull, gempty;
+    uint64_t full[kStages3], empty[kStages3];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
+                     const float *X, float *Y, int n, int n_pad, int64_t N, int b, int vrow_hi,
+                     int vrow_lo, int ntiles) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int nslab = b / 32;
+    unsigned char *Ghi = smem;                       // nslab x 8 KB
+    unsigned char *Glo = smem + nslab * 8192;        // nslab x 8 KB
+    unsigned char *stg = smem + kGresBytes;
+    Bars3 *bars = reinterpret_cast<Bars3 *>(stg + kStages3 * kStage3Bytes);
+    auto Vhi = [&](int s) { return stg + s * kStage3Bytes; };
+    auto Vlo = [&](int s) { return stg + s * kStage3Bytes + 16384; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nrc = n_pad / kRowChunk;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->gfull, 1);
+        mbar_init(&bars->gempty, 1);
+        for (int s = 0; s < kStages3; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->acc_full[a], 1);
+            mbar_init(&bars->acc_empty[a], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc<512>(&bars->tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tbase = bars->tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tc::prefetch_tmap(&tmG);
+            tc::prefetch_tmap(&tmV);
+            int s = 0;
+            uint32_t ph = 0, gph = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                mbar_wait(&bars->gempty, gph ^ 1u);
+                mbar_arrive_expect_tx(&bars->gfull, static_cast<uint32_t>(nslab) * 16384u);
+                for (int c = 0; c < nslab; ++c) {
+                    tc::tma_load_2d(Ghi + c * 8192, &tmG, c * 32, tile * kTileCols, &bars->gfull);
+                    tc::tma_load_2d(Glo + c * 8192, &tmG, c * 32,
+                                    static_cast<int>(N) + tile * kTileCols, &bars->gfull);
+                }
+                gph ^= 1u;
+                for (int rc = 0; rc < nrc; ++rc) {
+                    for (int c = 0; c < nslab; ++c) {
+                        mbar_wait(&bars->empty[s], ph ^ 1u);
+                        mbar_arrive_expect_tx(&bars->full[s], 32768u);
+                        tc::tma_load_2d(Vhi(s), &tmV, c * 32, vrow_hi + rc * kRowChunk, &bars->full[s]);
+                        tc::tma_load_2d(Vlo(s), &tmV, c * 32, vrow_lo + rc * kRowChunk, &bars->full[s]);
+                        if (++s == kStages3) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_bf16(128, kRowChunk);
+            int s = 0, a = 0;
+            uint32_t ph = 0, aph = 0, gph = 0;
+            const uint32_t gh0 = smem_u32(Ghi), gl0 = smem_u32(Glo);
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                mbar_wait(&bars->gfull, gph);
+                gph ^= 1u;
+                tc::fence_after_sync();
+                for (int rc = 0; rc < nrc; ++rc) {
+                    mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+                    tc::fence_after_sync();
+                    const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
+                    for (int c = 0; c < nslab; ++c) {
+                        mbar_wait(&bars->full[s], ph);
+                        tc::fence_after_sync();
+                        const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk) {
+                            const uint64_t ah = tc::sdesc_sw64(gh0 + c * 8192 + kk * 32);
+                            const uint64_t alo = tc::sdesc_sw64(gl0 + c * 8192 + kk * 32);
+                            const uint64_t bh = tc::sdesc_sw64(vh + kk * 32), blo = tc::sdesc_sw64(vl + kk * 32);
+                            tc::mma_bf16(d, ah, bh, idesc, (c | kk) != 0);
+                            tc::mma_bf16(d, ah, blo, idesc, 1u);
+                            tc::mma_bf16(d, alo, bh, idesc, 1u);
+                        }
+                        tc::mma_commit(&bars->empty[s]);
+                        if (++s == kStages3) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                    tc::mma_commit(&bars->acc_full[a]);
+                    if (++a == 2) {
+                        a = 0;
+                        aph ^= 1u;
+                    }
+                }
+                tc::mma_commit(&bars->gempty);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3;
+        int a = 0;
+        uint32_t aph = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t j = static_cast<int64_t>(tile) * kTileCols + q * 32 + lane;
+            const float *xc = X + j * n;
+            float *yc = Y + j * n;
+            for (int rc = 0; rc < nrc; ++rc) {
+                mbar_wait(&bars->acc_full[a], aph);
+                tc::fence_after_sync();
+                for (int cc = 0; cc < kRowChunk / 32; ++cc) {
+                    const int r0 = rc * kRowChunk + cc * 32;
+                    if (r0 >= n) break;  // warp-uniform
+                    float v[32];
+                    tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                      static_cast<uint32_t>(a * 256 + cc * 32),
+                                  v);
+                    if (j < N) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int r = r0 + e * 4;
+                            if (r < n) {
+                                float4 x = *reinterpret_cast<const float4 *>(xc + r);
+                                x.x -= v[4 * e];
+                                x.y -= v[4 * e + 1];
+                                x.z -= v[4 * e + 2];
+                                x.w -= v[4 * e + 3];
+                                *reinterpret_cast<float4 *>(yc + r) = x;
+                            }
+                        }
+                    }
+                }
+                tc::fence_before_sync();
+                tc::mbar_arrive(&bars->acc_empty[a]);
+                if (++a == 2) {
+                    a = 0;
+                    aph ^= 1u;
+                }
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) tc::tmem_free<512>(tbase);
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    std::call_once(g_encode_once, []() {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    return g_encode;
+}
+
+bool make_map(CUtensorMap *m, CUtensorMapDataType dt, int esize, const void *base, uint64_t inner,
+              uint64_t outer, uint32_t box_in, uint32_t box_out, CUtensorMapSwizzle sw) {
+    auto enc = encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * static_cast<uint64_t>(esize)};
+    cuuint32_t box[2] = {box_in, box_out};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, dt, 2, const_cast<void *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t smem1() { return static_cast<size_t>(kStages1) * kStage1Bytes + sizeof(Bars1) + 1024; }
+size_t smem3() {
+    return kGresBytes + static_cast<size_t>(kStages3) * kStage3Bytes + sizeof(Bars3) + 1024;
+}
+
+std::once_flag g_attr_once;
+cudaError_t g_attr_err = cudaSuccess;
+
+}  // namespace
+
+WyPlan wy_plan(int64_t n, int64_t h, int64_t N) {
+    WyPlan p{};
+    p.n = n;
+    p.h = h;
+    p.N = N;
+    p.nblk = static_cast<int>(std::max<int64_t>(1, (h + 255) / 256));
+    const int64_t per = (h + p.nblk - 1) / p.nblk;
+    p.b = static_cast<int>(std::max<int64_t>(32, (per + 31) / 32 * 32));
+    p.h_pad = p.b * p.nblk;
+    p.n_pad = (n + kRowChunk - 1) / kRowChunk * kRowChunk;
+    size_t off = 0;
+    p.off_wf = off;
+    off += al(static_cast<size_t>(p.h_pad) * p.n_pad * 4);
+    p.off_wb = off;
+    off += al(static_cast<size_t>(p.h_pad) * p.n_pad * 2 * 2);
+    p.off_sp = off;
+    off += al(static_cast<size_t>(p.nblk) * kSplitK * p.b * p.b * 4);
+    p.off_s = off;
+    off += al(static_cast<size_t>(p.nblk) * p.b * p.b * 4);
+    p.off_t = off;
+    off += al(static_cast<size_t>(p.nblk) * p.b * p.b * 4);
+    p.off_vt = off;
+    off += al(static_cast<size_t>(p.nblk) * p.n_pad * p.b * 2 * 2);
+    p.off_gt = off;
+    off += al(static_cast<size_t>(std::max<int64_t>(N, 1)) * p.b * 2 * 2);
+    p.bytes = off;
+    return p;
+}
+
+bool wy_supported(int64_t n, int64_t h, int64_t N) {
+    // TMA coordinates are int32; G rows are addressed as 2N
+    return n >= 32 && n % 4 == 0 && h >= 1 && N >= 1 && 2 * N < (int64_t(1) << 31) &&
+           n <= (int64_t(1) << 20);
+}
+
+cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X, float *Y,
+                      void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks) {
+    if (!encoder()) return cudaErrorNotSupported;
+    std::call_once(g_attr_once, []() {
+        g_attr_err = cudaFuncSetAttribute(wy_project_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem1()));
+        if (g_attr_err == cudaSuccess)
+            g_attr_err = cudaFuncSetAttribute(wy_update_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem3()));
+    });
+    if (g_attr_err != cudaSuccess) return g_attr_err;
+    char *w = static_cast<char *>(ws);
+    float *Wf = reinterpret_cast<float *>(w + p.off_wf);
+    uint16_t *Wb = reinterpret_cast<uint16_t *>(w + p.off_wb);
+    float *Sp = reinterpret_cast<float *>(w + p.off_sp);
+    float *S = reinterpret_cast<float *>(w + p.off_s);
+    float *T = reinterpret_cast<float *>(w + p.off_t);
+    uint16_t *Vt = reinterpret_cast<uint16_t *>(w + p.off_vt);
+    uint16_t *Gt = reinterpret_cast<uint16_t *>(w + p.off_gt);
+    const int sms = device_attr().sm_count;
+
+    // K4: pack + Gram + T + V
+    {
+        const int64_t tot = static_cast<int64_t>(p.h_pad) * p.n_pad;
+        const int g = static_cast<int>(std::min<int64_t>((tot + 255) / 256, sms * 16));
+        wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, op_t, p.h_pad, p.n_pad, Wf, Wb);
+        const int tb = (p.b + 63) / 64;
+        wy_gram_kernel<<<dim3(tb, tb, p.nblk * kSplitK), 256, 0, stream>>>(Wf, p.n_pad, p.b,
+                                                                            p.nblk, Sp);
+        wy_tbuild_kernel<<<p.nblk, 1024, 0, stream>>>(Sp, p.b, S, T);
+        wy_v_kernel<<<dim3(static_cast<unsigned>(p.n_pad / 64), p.b / 32, p.nblk), 256, 0,
+                      stream>>>(Wf, T, p.n_pad, p.b, p.nblk, Vt);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+
+    CUtensorMap mW, mG, mV, mX, mY;
+    const int64_t N = p.N;
+    bool ok = make_map(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, p.n_pad, 2 * p.h_pad, 32,
+                       p.b, CU_TENSOR_MAP_SWIZZLE_64B) &&
+              make_map(&mG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Gt, p.b, 2 * N, 32, kTileCols,
+                       CU_TENSOR_MAP_SWIZZLE_64B) &&
+              make_map(&mV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Vt, p.b, 2 * p.nblk * p.n_pad, 32,
+                       kRowChunk, CU_TENSOR_MAP_SWIZZLE_64B) &&
+              make_map(&mX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, X, p.n, N, 32, kTileCols,
+                       CU_TENSOR_MAP_SWIZZLE_NONE) &&
+              make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, 32, kTileCols,
+                       CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!ok) return cudaErrorNotSupported;
+
+    const int ntiles = static_cast<int>((N + kTileCols - 1) / kTileCols);
+    const int grid = std::max(1, std::min(ntiles, sms));
+    const float *cur = X;
+    int launched = 0;
+    for (int k = p.nblk - 1; k >= 0; --k) {
+        if (debug_stop_blocks >= 0 && launched >= debug_stop_blocks) break;
+        const CUtensorMap &mcur = (cur == X) ? mX : mY;
+        wy_project_kernel<<<grid, 320, smem1(), stream>>>(mcur, mW, Gt, static_cast<int>(p.n), N,
+                                                          p.b, k * p.b, p.h_pad + k * p.b, ntiles);
+        if (debug_stop_blocks >= 0) {
+            ++launched;
+            break;  // debug: stop after the first projection (G of block nblk-1)
+        }
+        wy_update_kernel<<<grid, 192, smem3(), stream>>>(
+            mG, mV, cur, Y, static_cast<int>(p.n), static_cast<int>(p.n_pad), N, p.b,
+            static_cast<int>(k * p.n_pad), static_cast<int>((p.nblk + k) * p.n_pad), ntiles);
+        cur = Y;
+        ++launched;
+    }
+    if (info) {
+        info->variant = "wy_bf16x3_tcgen05";
+        info->grid = grid;
+        info->block = 320;
+        info->smem = static_cast<int>(smem3());
+        info->nchunks = p.nblk;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace hh

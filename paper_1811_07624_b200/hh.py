@@ -25,6 +25,7 @@ HH_OK, HH_ERR_INVALID_VALUE, HH_ERR_UNSUPPORTED, HH_ERR_WORKSPACE, HH_ERR_CUDA =
 HH_F32, HH_F64 = 0, 1
 HH_OP_N, HH_OP_T = 0, 1
 HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST = range(4)
+HH_ALGO_AUTO, HH_ALGO_FUSED, HH_ALGO_WY = range(3)
 
 _DT = {torch.float32: HH_F32, torch.float64: HH_F64}
 
@@ -52,6 +53,12 @@ def lib() -> ctypes.CDLL:
         L.hh_mahalanobis.argtypes = [i64, i64, p, p, p, i64, p, p, i64, p, i32, p, sz, p]
         L.hh_apply_host.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
         L.hh_workspace_bytes.argtypes = [i32, i64, i64, i64, i64, i32, ctypes.POINTER(sz)]
+        L.hh_set_algo.argtypes = [i32]
+        L.hh_set_algo.restype = i32
+        L.hh_get_algo.restype = i32
+        L.hh_debug_wy_project.argtypes = [i32, i64, i64, p, p, i64, p, sz,
+                                          ctypes.POINTER(i64), p]
+        L.hh_debug_wy_project.restype = i32
         L.hh_status_string.argtypes = [i32]
         L.hh_status_string.restype = ctypes.c_char_p
         L.hh_version.restype = ctypes.c_char_p
@@ -117,6 +124,42 @@ def _dtype(t: torch.Tensor) -> int:
     return _DT[t.dtype]
 
 
+def hh_set_algo(algo: int) -> None:
+    """Select the hh_apply path for this thread (hh.h: hh_set_algo)."""
+    _check(lib().hh_set_algo(int(algo)), "hh_set_algo")
+
+
+def hh_get_algo() -> int:
+    return int(lib().hh_get_algo())
+
+
+class algo:
+    """Context manager: `with algo(HH_ALGO_WY): ...` (thread-local selection)."""
+
+    def __init__(self, a: int):
+        self.a = a
+
+    def __enter__(self):
+        self.prev = hh_get_algo()
+        hh_set_algo(self.a)
+        return self
+
+    def __exit__(self, *exc):
+        hh_set_algo(self.prev)
+
+
+def debug_wy_project(op: int, U: torch.Tensor, X: torch.Tensor, workspace: torch.Tensor):
+    """Test hook: compact-WY preparation + the first projection only.  Returns the
+    offsets dict (G, V, b, nblk, n_pad, T) into `workspace`."""
+    N, n = X.shape
+    h = U.shape[0]
+    off = (ctypes.c_int64 * 6)()
+    st = lib().hh_debug_wy_project(int(op), n, h, _ptr(U), _ptr(X), N, _ptr(workspace),
+                                   workspace.numel(), off, _stream(None))
+    _check(st, "hh_debug_wy_project")
+    return {"G": off[0], "V": off[1], "b": off[2], "nblk": off[3], "n_pad": off[4], "T": off[5]}
+
+
 def hh_workspace_bytes(call: int, n: int, h: int, N_or_M: int, npairs: int, dtype) -> int:
     dt = _DT[dtype] if isinstance(dtype, torch.dtype) else int(dtype)
     out = ctypes.c_size_t()
@@ -126,8 +169,11 @@ def hh_workspace_bytes(call: int, n: int, h: int, N_or_M: int, npairs: int, dtyp
 
 
 def hh_apply(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor] = None,
-             stream=None) -> torch.Tensor:
-    """Y = Q X (op = HH_OP_N) or Q^T X (HH_OP_T), Q = H_1 ... H_h (hh.h: hh_apply)."""
+             workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Y = Q X (op = HH_OP_N) or Q^T X (HH_OP_T), Q = H_1 ... H_h (hh.h: hh_apply).
+
+    The workspace the selected path needs (hh_workspace_bytes) is allocated on the
+    tensors' device when not given."""
     _dev(X, "X")
     N, n = X.shape
     h = U.shape[0] if U.numel() else 0
@@ -136,8 +182,12 @@ def hh_apply(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor
     if Y is None:
         Y = torch.empty_like(X)
     _dev(Y, "Y")
+    wsb = hh_workspace_bytes(HH_CALL_APPLY, n, h, N, 0, X.dtype) if N else 0
+    if wsb and (workspace is None or workspace.numel() < wsb):
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
     st = lib().hh_apply(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N, _dtype(X),
-                        None, 0, _stream(stream))
+                        _ptr(workspace) if wsb else None, workspace.numel() if wsb else 0,
+                        _stream(stream))
     _check(st, "hh_apply")
     return Y
 

@@ -108,12 +108,15 @@ def test_C4_full_size_sampled(fused):
 
 
 @pytest.mark.parametrize("h", gi.C5_H)
-def test_C5_sweep(h):
-    """configs[4]: n=4096, h in {12, 64, 256, 1024}; oracle-sized column counts."""
+@pytest.mark.parametrize("path", ["auto", "fused"])
+def test_C5_sweep(h, path):
+    """configs[4]: n=4096, h in {12, 64, 256, 1024}; oracle-sized column counts.  `auto`
+    takes the crossover (compact-WY tensor-core path for large h), `fused` forces K1."""
     N = {12: 777, 64: 515, 256: 260, 1024: 130}[h]
     c = gi.make_config(5, h=h, N=N)
-    got = run_apply(0, c.U, c.X)
-    assert_parity(got, oracle.apply(0, c.U, c.X), "f32", h, f"C5 h={h}")
+    with hh.algo(hh.HH_ALGO_AUTO if path == "auto" else hh.HH_ALGO_FUSED):
+        got = run_apply(0, c.U, c.X)
+    assert_parity(got, oracle.apply(0, c.U, c.X), "f32", h, f"C5 h={h} {path}")
 
 
 # ------------------------------------------------------------------ shapes / edges
@@ -199,8 +202,9 @@ def test_forced_chunking_matches_resident():
     """A large h forces the chunked-U schedule; results must still match the oracle."""
     c = gi.make_case("apply", 1024, 200, 600, "f32", seed=9)   # U = 800 KiB
     for op in (0, 1):
-        got = run_apply(op, c.U, c.X)
-        assert hh.last_launch_info()["nchunks"] > 1
+        with hh.algo(hh.HH_ALGO_FUSED):
+            got = run_apply(op, c.U, c.X)
+            assert hh.last_launch_info()["nchunks"] > 1
         assert_parity(got, oracle.apply(op, c.U, c.X), "f32", 200, f"chunked op{op}")
 
 

@@ -1,0 +1,134 @@
+"""GPU parity of the compact-WY tensor-core path (K4 + K5, hh_wy.cu) against the oracle.
+
+K5 evaluates the same product Q = H_1 ... H_h in the blocked form I - W T W^T
+ on tcgen05 with a bf16x3 split; the gate is the north_star's
+fp32 gate 2e-5*sqrt(h).  The debug hook checks the intermediate G = W^T X and
+V = W T of the first applied block against plain fp64 numpy written from Eq. 2.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import inputs as gi
+from tests._util import assert_parity, rel_fro
+
+pytestmark = pytest.mark.gpu
+hh = pytest.importorskip("paper_1811_07624_b200")
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def wy(op, U, X, Y=None):
+    with hh.algo(hh.HH_ALGO_WY):
+        out = hh.hh_apply(op, dev(U), dev(X), Y)
+        assert hh.last_launch_info()["variant"].startswith("wy_"), hh.last_launch_info()
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def bf16_pair_to_f64(ws, off, count, lo_off):
+    raw = ws[off:off + 2 * count].view(torch.int16).to(torch.int32).cpu().numpy()
+    hi = (raw.astype(np.int64) & 0xFFFF) << 16
+    raw_lo = ws[off + 2 * lo_off:off + 2 * lo_off + 2 * count].view(torch.int16).to(
+        torch.int32).cpu().numpy()
+    lo = (raw_lo.astype(np.int64) & 0xFFFF) << 16
+    f = lambda a: a.astype(np.uint32).view(np.float32).astype(np.float64)  # noqa: E731
+    return f(hi) + f(lo)
+
+
+@pytest.mark.parametrize("n,h,N,op", [(256, 40, 300, 0), (512, 70, 257, 1), (4096, 256, 130, 0)])
+def test_wy_intermediates(n, h, N, op):
+    """G = W^T X and V = W T of the first applied block (the last block of the product
+    order) match fp64 numpy: T by the forward recurrence T[:i, i] = -2 T[:i,:i] W[:, :i]^T w_i."""
+    c = gi.make_case("apply", n, h, N, "f32", seed=21)
+    U, X = dev(c.U), dev(c.X)
+    with hh.algo(hh.HH_ALGO_WY):
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_APPLY, n, h, N, 0, torch.float32)
+    ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
+    off = hh.debug_wy_project(op, U, X, ws)
+    torch.cuda.synchronize()
+    b, nblk, n_pad = off["b"], off["nblk"], off["n_pad"]
+    order = np.arange(h) if op == 0 else np.arange(h)[::-1]
+    Wfull = np.zeros((nblk * b, n))
+    Wfull[:h] = c.U.astype(np.float64)[order]
+    k = nblk - 1
+    W = Wfull[k * b:(k + 1) * b]                       # (b, n): rows w_i
+    G_ref = c.X.astype(np.float64) @ W.T               # (N, b)
+    G = bf16_pair_to_f64(ws, off["G"], N * b, N * b).reshape(N, b)
+    # bf16x3: each operand carries ~2^-17 relative split error, hi*hi + hi*lo + lo*hi
+    # drops lo*lo (~2^-18), and G itself is stored as a hi+lo pair (2^-17): a few
+    # times 2^-17 = 7.6e-6 relative
+    assert rel_fro(G, G_ref) < 4e-5, rel_fro(G, G_ref)
+    T = np.zeros((b, b))
+    for i in range(b):
+        T[i, i] = 2.0
+        if i:
+            T[:i, i] = -2.0 * T[:i, :i] @ (W[:i] @ W[i])
+    V_ref = W.T @ T                                    # (n, b)
+    V = bf16_pair_to_f64(ws, off["V"] + 2 * k * n_pad * b, n_pad * b,
+                         nblk * n_pad * b).reshape(n_pad, b)[:n]
+    assert rel_fro(V, V_ref) < 4e-5, rel_fro(V, V_ref)
+    # the block formula reproduces the sequential product (fp64, pins the recurrence)
+    Qb = np.eye(n) - W.T @ T @ W
+    Qs = np.eye(n)
+    for i in range(b):
+        Qs = Qs @ (np.eye(n) - 2.0 * np.outer(W[i], W[i]))
+    assert np.abs(Qb - Qs).max() < 1e-10
+
+
+WY_SHAPES = [  # (n, h, N): several tiles + ragged tails, b in {32, 64, 160, 256}, nblk up to 4
+    (256, 40, 300), (512, 33, 777), (1024, 64, 1000), (2048, 32, 1500), (100, 50, 129),
+    (4096, 64, 515), (4096, 300, 130), (1000, 257, 200), (4096, 1024, 130), (32, 20, 64),
+]
+
+
+@pytest.mark.parametrize("n,h,N", WY_SHAPES)
+@pytest.mark.parametrize("op", [0, 1])
+def test_wy_parity(n, h, N, op):
+    c = gi.make_case("apply", n, h, N, "f32", seed=22)
+    got = wy(op, c.U, c.X)
+    assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"WY n{n} h{h} N{N} op{op}")
+
+
+def test_wy_alias_zero_slots_and_round_trip():
+    c = gi.make_case("apply", 1024, 96, 400, "f32", seed=23, zero_slots=(0, 5, 95))
+    U, X = dev(c.U), dev(c.X)
+    ref = oracle.apply(0, c.U, c.X)
+    with hh.algo(hh.HH_ALGO_WY):
+        out = hh.hh_apply(0, U, X, Y=X)                 # exact alias
+        torch.cuda.synchronize()
+        assert out.data_ptr() == X.data_ptr()
+        assert_parity(X.cpu().numpy(), ref, "f32", 96, "WY alias")
+        back = hh.hh_apply(1, U, X)                     # Q^T (Q X) = X (orthonormal up to fp32 u)
+    torch.cuda.synchronize()
+    assert rel_fro(back.cpu().numpy(), c.X) < 2e-5 * np.sqrt(96)
+
+
+def test_wy_errors():
+    X = torch.randn(10, 1024, device="cuda")
+    U = torch.randn(40, 1024, device="cuda")
+    with hh.algo(hh.HH_ALGO_WY):
+        st = hh.hh.lib().hh_apply(0, 1024, 40, hh.hh._ptr(U), hh.hh._ptr(X),
+                                  hh.hh._ptr(torch.empty_like(X)), 10, 0, None, 0, None)
+        assert st == hh.hh.HH_ERR_WORKSPACE
+    assert hh.hh_get_algo() == hh.HH_ALGO_AUTO
+    with pytest.raises(hh.HHError):
+        hh.hh_set_algo(7)
+
+
+@pytest.mark.parametrize("h", [64, 256, 1024])
+def test_C5_full_size_sampled_auto(h):
+    """configs[4] at full size (1 GiB X) through the auto path the bench times."""
+    c = gi.make_config(5, h=h)
+    Xd = dev(c.X)
+    Yd = hh.hh_apply(0, dev(c.U), Xd)
+    torch.cuda.synchronize()
+    assert hh.last_launch_info()["variant"].startswith("wy_")
+    idx = np.unique(np.concatenate([np.linspace(0, c.N - 1, 200).astype(np.int64),
+                                    np.arange(c.N - 8, c.N)]))
+    got = Yd[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert np.all(np.isfinite(Yd.cpu().numpy()))
+    assert_parity(got, oracle.apply(0, c.U, c.X[idx]), "f32", h, f"C5 full h={h}")
