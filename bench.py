@@ -341,7 +341,7 @@ def run_hh(args):
         dist.barrier()
     # keep the GPU busy for >= 1 s of clock samples if the timed region was short
     t_obs0 = t_wall0
-    if t_wall1 - t_wall0 < 1.0:
+    if t_wall1 - t_wall0 < 1.0 and not args.ncu:
         t_obs0 = time.time()
         while time.time() - t_obs0 < 1.0:
             for _ in range(50):
@@ -458,7 +458,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--ncu", action="store_true",
+                    help="profiling run: no parity / cpu baseline / e2e / clock-hold loop")
     args = ap.parse_args()
+    if args.ncu:
+        args.no_parity = args.no_cpu_baseline = args.no_e2e = True
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -47,13 +47,15 @@ namespace hh {
 
 namespace {
 
-constexpr int kSplitK = 8;        // Gram split-K factor (deterministic reduction)
-constexpr int kRowChunk = 256;    // K5b output rows per accumulator (MMA N)
-constexpr int kTileCols = 128;    // columns of X per tile (MMA M)
-constexpr int kStages1 = 3;       // K5a pipeline depth
-constexpr int kStages3 = 3;       // K5b pipeline depth
-constexpr int kStage1Bytes = 65536;  // raw X 16K + X hi/lo 16K + W hi/lo 32K (b = 256)
-constexpr int kStage3Bytes = 32768;  // V hi/lo tile (256 rows x 32 bf16) x 2
+constexpr int kGramRows = 128;   // Gram split-K slice (rows of n_pad per CTA)
+constexpr int kRowChunk = 128;    // K5b rows r per accumulator (MMA M)
+constexpr int kTileCols = 128;    // columns of X per tile (K5a MMA M, K5b MMA N)
+constexpr int kRaw1 = 4;          // K5a raw fp32 X ring depth
+constexpr int kStages1 = 3;       // K5a converted X + W ring depth
+constexpr int kStages3 = 6;       // K5b V ring depth
+constexpr int kRawBytes = 16384;     // fp32 X tile (128 columns x 32 rows)
+constexpr int kConv1Bytes = 49152;   // X hi/lo 16K + W hi/lo 32K (b = 256)
+constexpr int kStage3Bytes = 16384;  // V hi/lo tile (128 rows x 32 bf16) x 2
 constexpr int kGresBytes = 131072;   // resident G hi/lo (128 x 256 bf16) x 2
 
 size_t al(size_t x) { return (x + 1023) & ~static_cast<size_t>(1023); }
@@ -90,21 +92,22 @@ __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h
     }
 }
 
-// Sp[blk][split][l][m] = sum_{r in split} w_l[r] w_m[r], upper 64x64 tiles only.
+// Sp[blk][split][l][m] = sum_{r in split} w_l[r] w_m[r] over 128-row splits of
+// n_pad, upper 64x64 tiles only (the reduction over splits is done in fixed order
+// by wy_gram_reduce_kernel: deterministic).
 __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ Wf, int64_t n_pad,
-                                                      int b, int nblk, float *__restrict__ Sp) {
+                                                      int b, int nsplit, float *__restrict__ Sp) {
     const int ti = blockIdx.x, tj = blockIdx.y;
-    const int blk = blockIdx.z / kSplitK, sp = blockIdx.z % kSplitK;
+    const int blk = blockIdx.z / nsplit, sp = blockIdx.z % nsplit;
     if (ti > tj) return;
     __shared__ float Ls[32][65], Ms[32][65];
     const int t = threadIdx.x, tx = t % 16, ty = t / 16;
     float acc[4][4] = {};
-    const int64_t rlen = n_pad / kSplitK;
-    const int64_t r0 = sp * rlen;
+    const int64_t r0 = static_cast<int64_t>(sp) * kGramRows;
     const float *Wl = Wf + (static_cast<int64_t>(blk) * b + ti * 64) * n_pad;
     const float *Wm = Wf + (static_cast<int64_t>(blk) * b + tj * 64) * n_pad;
     const int rows_l = min(64, b - ti * 64), rows_m = min(64, b - tj * 64);
-    for (int64_t rc = r0; rc < r0 + rlen; rc += 32) {
+    for (int64_t rc = r0; rc < r0 + kGramRows; rc += 32) {
         for (int e = t; e < 32 * 64; e += 256) {
             const int c = e / 32, k = e % 32;
             Ls[k][c] = c < rows_l ? Wl[c * n_pad + rc + k] : 0.f;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
         }
         __syncthreads();
     }
-    float *out = Sp + (static_cast<int64_t>(blk) * kSplitK + sp) * b * b;
+    float *out = Sp + (static_cast<int64_t>(blk) * nsplit + sp) * b * b;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const int l = ti * 64 + ty * 4 + p;
@@ -139,70 +142,94 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
     }
 }
 
-// T (upper triangular, b x b) per block: reduce the Gram partials (fixed order),
-// build the 32x32 diagonal blocks by the forward recurrence, then extend 32
-// columns at a time: T[0:c, c:c+32] = -T[0:c,0:c] * S[0:c, c:c+32] * T[c:c+32, c:c+32].
-__global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict__ Sp, int b,
-                                                          float *__restrict__ Sg,
-                                                          float *__restrict__ Tg) {
-    const int blk = blockIdx.x;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+// S[blk][l][m] = sum over splits (ascending) of the Gram partials, upper tiles.
+__global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int nblk, int nsplit,
+                                      float *__restrict__ S) {
     const int64_t bb = static_cast<int64_t>(b) * b;
-    float *S = Sg + blk * bb;
-    float *T = Tg + blk * bb;
-    const float *P0 = Sp + static_cast<int64_t>(blk) * kSplitK * bb;
-    for (int64_t e = t; e < bb; e += 1024) {
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < nblk * bb;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t blk = idx / bb, e = idx % bb;
         const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
         float s = 0.f;
         if ((l / 64) <= (m / 64)) {
-#pragma unroll
-            for (int q = 0; q < kSplitK; ++q) s += P0[q * bb + e];
+            const float *p = Sp + blk * nsplit * bb + e;
+            for (int q = 0; q < nsplit; ++q) s += p[q * bb];
         }
-        S[e] = s;
-        T[e] = 0.f;
+        S[idx] = s;
     }
-    __syncthreads();
-    // level-0 diagonal blocks (8 x 32 x 33) and the extension product (<= 224 x 32)
-    // share one buffer: they are used in disjoint phases
-    __shared__ float shbuf[8 * 32 * 33];
-    float *Pm = shbuf;
-    if (warp < b / 32) {
+}
+
+// T (upper triangular, b x b) per block, built in shared memory (packed upper
+// rows): the 32x32 diagonal blocks by the forward recurrence
+//   T[l][i] = -2 sum_{m=l}^{i-1} T[l][m] S[m][i],  T[i][i] = 2,
+// then 32 columns at a time (block form of the same product, H-blocks 1 = [0,c),
+// 2 = [c,c+32)):  T[0:c, c:c+32] = -T[0:c,0:c] * (S[0:c, c:c+32] * T[c:c+32, c:c+32]).
+__global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict__ Sg, int b,
+                                                          float *__restrict__ Tg) {
+    extern __shared__ float tsm[];
+    const int blk = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t bb = static_cast<int64_t>(b) * b;
+    const float *S = Sg + blk * bb;
+    float *Tout = Tg + blk * bb;
+    float *Tp = tsm;                                   // packed upper, b(b+1)/2
+    float *Sb = Tp + (b * (b + 1) / 2 + 31) / 32 * 32; // 8 x 32 x 33 / S panel (c x 32)
+    float *Pm = Sb + 8 * 32 * 33;                      // c x 32
+    auto tp = [&](int l, int m) -> float & { return Tp[l * b - (l * (l - 1)) / 2 + (m - l)]; };
+    const int nb = b / 32;
+    // level 0: warp w builds diagonal block w
+    if (warp < nb) {
         const int o = warp * 32;
-        float(*tb)[33] = reinterpret_cast<float(*)[33]>(shbuf + warp * 32 * 33);
-        for (int c = 0; c < 32; ++c) tb[lane][c] = 0.f;
+        float(*sb)[33] = reinterpret_cast<float(*)[33]>(Sb + warp * 32 * 33);
+        for (int r = 0; r < 32; ++r) sb[r][lane] = S[(o + r) * b + o + lane];
         __syncwarp();
         for (int i = 0; i < 32; ++i) {
-            float v = 0.f;
             if (lane < i) {
-                float s = 0.f;
-                for (int m = lane; m < i; ++m) s = fmaf(tb[lane][m], S[(o + m) * b + o + i], s);
-                v = -2.f * s;
+                float s0 = 0.f, s1 = 0.f;
+                int m = lane;
+                for (; m + 1 < i; m += 2) {
+                    s0 = fmaf(tp(o + lane, o + m), sb[m][i], s0);
+                    s1 = fmaf(tp(o + lane, o + m + 1), sb[m + 1][i], s1);
+                }
+                if (m < i) s0 = fmaf(tp(o + lane, o + m), sb[m][i], s0);
+                tp(o + lane, o + i) = -2.f * (s0 + s1);
             } else if (lane == i) {
-                v = 2.f;
+                tp(o + i, o + i) = 2.f;
             }
-            tb[lane][i] = v;
             __syncwarp();
         }
-        for (int c = 0; c < 32; ++c) T[(o + lane) * b + o + c] = tb[lane][c];
     }
     __syncthreads();
     for (int c = 32; c < b; c += 32) {
-        // Pm[l][j] = sum_{m<=j} S[l][c+m] T[c+m][c+j]
+        // S panel S[0:c, c:c+32] -> Sb (c x 32)
+        for (int e = t; e < c * 32; e += 1024) Sb[e] = S[(e / 32) * b + c + (e % 32)];
+        __syncthreads();
         for (int e = t; e < c * 32; e += 1024) {
             const int l = e / 32, j = e % 32;
             float s = 0.f;
-            for (int m = 0; m <= j; ++m) s = fmaf(S[l * b + c + m], T[(c + m) * b + c + j], s);
+            for (int m = 0; m <= j; ++m) s = fmaf(Sb[l * 32 + m], tp(c + m, c + j), s);
             Pm[e] = s;
         }
         __syncthreads();
-        // T[l][c+j] = -sum_{m=l}^{c-1} T[l][m] Pm[m][j]
         for (int e = t; e < c * 32; e += 1024) {
             const int l = e / 32, j = e % 32;
-            float s = 0.f;
-            for (int m = l; m < c; ++m) s = fmaf(T[l * b + m], Pm[m * 32 + j], s);
-            T[l * b + c + j] = -s;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            const float *trow = &tp(l, l);
+            int m = l;
+            for (; m + 3 < c; m += 4) {
+                s0 = fmaf(trow[m - l], Pm[m * 32 + j], s0);
+                s1 = fmaf(trow[m - l + 1], Pm[(m + 1) * 32 + j], s1);
+                s2 = fmaf(trow[m - l + 2], Pm[(m + 2) * 32 + j], s2);
+                s3 = fmaf(trow[m - l + 3], Pm[(m + 3) * 32 + j], s3);
+            }
+            for (; m < c; ++m) s0 = fmaf(trow[m - l], Pm[m * 32 + j], s0);
+            tp(l, c + j) = -((s0 + s1) + (s2 + s3));
         }
         __syncthreads();
+    }
+    for (int64_t e = t; e < bb; e += 1024) {
+        const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
+        Tout[e] = m >= l ? tp(l, m) : 0.f;
     }
 }
 
@@ -262,35 +289,42 @@ __global__ void __launch_bounds__(256) wy_v_kernel(const float *__restrict__ Wf,
 }
 
 // ------------------------------------------------------------------ K5a: G = W^T X
-// 10 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-5 converters (fp32 X
-// tile -> bf16 hi/lo, SW64 K-major), w6-9 epilogue (TMEM -> bf16 hi/lo G rows).
+// 15 warps: w0 TMA producer of the fp32 X tiles (4-deep raw ring), w1 TMA producer
+// of the W hi/lo tiles, w2 MMA issuer (+TMEM owner), w3-10 converters (fp32 X tile
+// -> bf16 hi/lo, SW64 K-major), w11-14 epilogue (TMEM -> bf16 hi/lo rows of G).
 struct Bars1 {
-    uint64_t full[kStages1], conv[kStages1], empty[kStages1];
+    uint64_t rfull[kRaw1], rempty[kRaw1];
+    uint64_t wfull[kStages1], cfull[kStages1], cempty[kStages1];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(480, 1)
     wy_project_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       uint16_t *__restrict__ Gt, int n, int64_t N, int b, int wrow_hi, int wrow_lo,
                       int ntiles) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    Bars1 *bars = reinterpret_cast<Bars1 *>(smem + kStages1 * kStage1Bytes);
-    auto rawX = [&](int s) { return smem + s * kStage1Bytes; };
-    auto Xhi = [&](int s) { return smem + s * kStage1Bytes + 16384; };
-    auto Xlo = [&](int s) { return smem + s * kStage1Bytes + 24576; };
-    auto Whi = [&](int s) { return smem + s * kStage1Bytes + 32768; };
-    auto Wlo = [&](int s) { return smem + s * kStage1Bytes + 32768 + 64 * b; };
+    unsigned char *conv = smem + kRaw1 * kRawBytes;
+    Bars1 *bars = reinterpret_cast<Bars1 *>(conv + kStages1 * kConv1Bytes);
+    auto rawX = [&](int s) { return smem + s * kRawBytes; };
+    auto Xhi = [&](int s) { return conv + s * kConv1Bytes; };
+    auto Xlo = [&](int s) { return conv + s * kConv1Bytes + 8192; };
+    auto Whi = [&](int s) { return conv + s * kConv1Bytes + 16384; };
+    auto Wlo = [&](int s) { return conv + s * kConv1Bytes + 16384 + 64 * b; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (n + 31) / 32;
     if (threadIdx.x == 0) {
+        for (int s = 0; s < kRaw1; ++s) {
+            mbar_init(&bars->rfull[s], 1);
+            mbar_init(&bars->rempty[s], 256);
+        }
         for (int s = 0; s < kStages1; ++s) {
-            mbar_init(&bars->full[s], 1);
-            mbar_init(&bars->conv[s], 128);
-            mbar_init(&bars->empty[s], 1);
+            mbar_init(&bars->wfull[s], 1);
+            mbar_init(&bars->cfull[s], 256);
+            mbar_init(&bars->cempty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->acc_full[a], 1);
@@ -298,7 +332,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         fence_mbar_init();
     }
-    if (warp == 1) tc::tmem_alloc<512>(&bars->tmem);
+    if (warp == 2) tc::tmem_alloc<512>(&bars->tmem);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -307,18 +341,14 @@ __global__ void __launch_bounds__(320, 1)
     if (warp == 0) {
         if (lane == 0) {
             tc::prefetch_tmap(&tmX);
-            tc::prefetch_tmap(&tmW);
             int s = 0;
             uint32_t ph = 0;
-            const uint32_t bytes = 16384u + 128u * static_cast<uint32_t>(b);
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int ks = 0; ks < nk; ++ks) {
-                    mbar_wait(&bars->empty[s], ph ^ 1u);
-                    mbar_arrive_expect_tx(&bars->full[s], bytes);
-                    tc::tma_load_2d(rawX(s), &tmX, ks * 32, tile * kTileCols, &bars->full[s]);
-                    tc::tma_load_2d(Whi(s), &tmW, ks * 32, wrow_hi, &bars->full[s]);
-                    tc::tma_load_2d(Wlo(s), &tmW, ks * 32, wrow_lo, &bars->full[s]);
-                    if (++s == kStages1) {
+                    mbar_wait(&bars->rempty[s], ph ^ 1u);
+                    mbar_arrive_expect_tx(&bars->rfull[s], static_cast<uint32_t>(kRawBytes));
+                    tc::tma_load_2d(rawX(s), &tmX, ks * 32, tile * kTileCols, &bars->rfull[s]);
+                    if (++s == kRaw1) {
                         s = 0;
                         ph ^= 1u;
                     }
@@ -326,6 +356,25 @@ __global__ void __launch_bounds__(320, 1)
             }
         }
     } else if (warp == 1) {
+        if (lane == 0) {
+            tc::prefetch_tmap(&tmW);
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t bytes = 128u * static_cast<uint32_t>(b);
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int ks = 0; ks < nk; ++ks) {
+                    mbar_wait(&bars->cempty[s], ph ^ 1u);
+                    mbar_arrive_expect_tx(&bars->wfull[s], bytes);
+                    tc::tma_load_2d(Whi(s), &tmW, ks * 32, wrow_hi, &bars->wfull[s]);
+                    tc::tma_load_2d(Wlo(s), &tmW, ks * 32, wrow_lo, &bars->wfull[s]);
+                    if (++s == kStages1) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 2) {
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_bf16(128, b);
             int s = 0, a = 0;
@@ -335,7 +384,8 @@ __global__ void __launch_bounds__(320, 1)
                 tc::fence_after_sync();
                 const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
                 for (int ks = 0; ks < nk; ++ks) {
-                    mbar_wait(&bars->conv[s], ph);
+                    mbar_wait(&bars->wfull[s], ph);
+                    mbar_wait(&bars->cfull[s], ph);
                     tc::fence_after_sync();
                     const uint32_t xh = smem_u32(Xhi(s)), xl = smem_u32(Xlo(s));
                     const uint32_t wh = smem_u32(Whi(s)), wl = smem_u32(Wlo(s));
@@ -347,7 +397,7 @@ __global__ void __launch_bounds__(320, 1)
                         tc::mma_bf16(d, ah, blo, idesc, 1u);
                         tc::mma_bf16(d, alo, bh, idesc, 1u);
                     }
-                    tc::mma_commit(&bars->empty[s]);
+                    tc::mma_commit(&bars->cempty[s]);
                     if (++s == kStages1) {
                         s = 0;
                         ph ^= 1u;
@@ -361,33 +411,44 @@ __global__ void __launch_bounds__(320, 1)
             }
         }
         __syncwarp();
-    } else if (warp < 6) {
-        // converters: 128 threads, 8 float4 each per stage
-        const int ct = threadIdx.x - 64;
-        int s = 0;
-        uint32_t ph = 0;
+    } else if (warp < 11) {
+        // converters: 256 threads, 4 float4 each per k-step
+        const int ct = threadIdx.x - 96;
+        int rs = 0, cs = 0;
+        uint32_t rph = 0, cph = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             for (int ks = 0; ks < nk; ++ks) {
-                mbar_wait(&bars->full[s], ph);
-                const float4 *raw = reinterpret_cast<const float4 *>(rawX(s));
-                unsigned char *xh = Xhi(s), *xl = Xlo(s);
+                mbar_wait(&bars->rfull[rs], rph);
+                const float4 *raw = reinterpret_cast<const float4 *>(rawX(rs));
+                float4 v[4];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int idx = ct + 128 * q;
+                for (int q = 0; q < 4; ++q) v[q] = raw[ct + 256 * q];
+                mbar_wait(&bars->cempty[cs], cph ^ 1u);
+                unsigned char *xh = Xhi(cs), *xl = Xlo(cs);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int idx = ct + 256 * q;
                     const int r = idx >> 3, c4 = idx & 7;
-                    const float4 v = raw[idx];
                     uint2 H, L;
-                    tc::split2(v.x, v.y, H.x, L.x);
-                    tc::split2(v.z, v.w, H.y, L.y);
+                    tc::split2(v[q].x, v[q].y, H.x, L.x);
+                    tc::split2(v[q].z, v[q].w, H.y, L.y);
                     const uint32_t off = tc::sw64_off(r, c4 >> 1) + (c4 & 1) * 8;
                     *reinterpret_cast<uint2 *>(xh + off) = H;
                     *reinterpret_cast<uint2 *>(xl + off) = L;
                 }
+                // the raw tile is released only after its values were consumed (the
+                // stores above depend on them) and ordered against the async proxy that
+                // refills it (TMA)
                 fence_proxy_async_smem();
-                tc::mbar_arrive(&bars->conv[s]);
-                if (++s == kStages1) {
-                    s = 0;
-                    ph ^= 1u;
+                tc::mbar_arrive(&bars->rempty[rs]);
+                tc::mbar_arrive(&bars->cfull[cs]);
+                if (++rs == kRaw1) {
+                    rs = 0;
+                    rph ^= 1u;
+                }
+                if (++cs == kStages1) {
+                    cs = 0;
+                    cph ^= 1u;
                 }
             }
         }
@@ -429,11 +490,13 @@ __global__ void __launch_bounds__(320, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 1) tc::tmem_free<512>(tbase);
+    if (warp == 2) tc::tmem_free<512>(tbase);
 }
 
 // ------------------------------------------------------------------ K5b: X <- X - V G
-// 6 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-5 epilogue.
+// D[r][j] = sum_i V[r][i] G[j][i] with TMEM lane = row r, TMEM column = column j, so
+// the epilogue's global loads / stores of X[j][r] are 128-B coalesced per warp.
+// 10 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-9 epilogue.
 struct Bars3 {
     uint64_t gfull, gempty;
     uint64_t full[kStages3], empty[kStages3];
@@ -441,7 +504,7 @@ struct Bars3 {
     uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
                      const float *X, float *Y, int n, int n_pad, int64_t N, int b, int vrow_hi,
                      int vrow_lo, int ntiles) {
@@ -449,12 +512,12 @@ __global__ void __launch_bounds__(192, 1)
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int nslab = b / 32;
-    unsigned char *Ghi = smem;                       // nslab x 8 KB
-    unsigned char *Glo = smem + nslab * 8192;        // nslab x 8 KB
+    unsigned char *Ghi = smem;                       // nslab x 8 KB (128 columns x 32 K)
+    unsigned char *Glo = smem + nslab * 8192;
     unsigned char *stg = smem + kGresBytes;
     Bars3 *bars = reinterpret_cast<Bars3 *>(stg + kStages3 * kStage3Bytes);
     auto Vhi = [&](int s) { return stg + s * kStage3Bytes; };
-    auto Vlo = [&](int s) { return stg + s * kStage3Bytes + 16384; };
+    auto Vlo = [&](int s) { return stg + s * kStage3Bytes + 8192; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nrc = n_pad / kRowChunk;
@@ -467,11 +530,11 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->acc_full[a], 1);
-            mbar_init(&bars->acc_empty[a], 128);
+            mbar_init(&bars->acc_empty[a], 256);
         }
         fence_mbar_init();
     }
-    if (warp == 1) tc::tmem_alloc<512>(&bars->tmem);
+    if (warp == 1) tc::tmem_alloc<256>(&bars->tmem);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -495,7 +558,7 @@ __global__ void __launch_bounds__(192, 1)
                 for (int rc = 0; rc < nrc; ++rc) {
                     for (int c = 0; c < nslab; ++c) {
                         mbar_wait(&bars->empty[s], ph ^ 1u);
-                        mbar_arrive_expect_tx(&bars->full[s], 32768u);
+                        mbar_arrive_expect_tx(&bars->full[s], static_cast<uint32_t>(kStage3Bytes));
                         tc::tma_load_2d(Vhi(s), &tmV, c * 32, vrow_hi + rc * kRowChunk, &bars->full[s]);
                         tc::tma_load_2d(Vlo(s), &tmV, c * 32, vrow_lo + rc * kRowChunk, &bars->full[s]);
                         if (++s == kStages3) {
@@ -508,7 +571,7 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_bf16(128, kRowChunk);
+            const uint32_t idesc = tc::idesc_bf16(kRowChunk, kTileCols);
             int s = 0, a = 0;
             uint32_t ph = 0, aph = 0, gph = 0;
             const uint32_t gh0 = smem_u32(Ghi), gl0 = smem_u32(Glo);
@@ -519,16 +582,16 @@ __global__ void __launch_bounds__(192, 1)
                 for (int rc = 0; rc < nrc; ++rc) {
                     mbar_wait(&bars->acc_empty[a], aph ^ 1u);
                     tc::fence_after_sync();
-                    const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
+                    const uint32_t d = tbase + static_cast<uint32_t>(a * kTileCols);
                     for (int c = 0; c < nslab; ++c) {
                         mbar_wait(&bars->full[s], ph);
                         tc::fence_after_sync();
                         const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk) {
-                            const uint64_t ah = tc::sdesc_sw64(gh0 + c * 8192 + kk * 32);
-                            const uint64_t alo = tc::sdesc_sw64(gl0 + c * 8192 + kk * 32);
-                            const uint64_t bh = tc::sdesc_sw64(vh + kk * 32), blo = tc::sdesc_sw64(vl + kk * 32);
+                            const uint64_t ah = tc::sdesc_sw64(vh + kk * 32), alo = tc::sdesc_sw64(vl + kk * 32);
+                            const uint64_t bh = tc::sdesc_sw64(gh0 + c * 8192 + kk * 32);
+                            const uint64_t blo = tc::sdesc_sw64(gl0 + c * 8192 + kk * 32);
                             tc::mma_bf16(d, ah, bh, idesc, (c | kk) != 0);
                             tc::mma_bf16(d, ah, blo, idesc, 1u);
                             tc::mma_bf16(d, alo, bh, idesc, 1u);
@@ -550,36 +613,41 @@ __global__ void __launch_bounds__(192, 1)
         }
         __syncwarp();
     } else {
-        const int q = warp & 3;
+        // 8 epilogue warps: lane quarter q = warp % 4 (rows), column half hf (64 of the
+        // 128 columns).  The X values of the next r-chunk are loaded before waiting for
+        // its accumulator (they do not depend on the MMA): 64 loads in flight per thread.
+        const int q = warp & 3, hf = (warp - 2) >> 2;
         int a = 0;
         uint32_t aph = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int64_t j = static_cast<int64_t>(tile) * kTileCols + q * 32 + lane;
-            const float *xc = X + j * n;
-            float *yc = Y + j * n;
+            const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + hf * 64;
+            const int ncol = static_cast<int>(N - j0 < 64 ? N - j0 : 64);
+            float xb[64];
+            auto load = [&](int rc) {
+                const int r = rc * kRowChunk + q * 32 + lane;
+                const bool rv = rc < nrc && r < n;
+                const float *src = X + j0 * n + r;
+#pragma unroll
+                for (int e = 0; e < 64; ++e)
+                    if (rv && e < ncol) xb[e] = src[static_cast<int64_t>(e) * n];
+            };
+            load(0);
             for (int rc = 0; rc < nrc; ++rc) {
                 mbar_wait(&bars->acc_full[a], aph);
                 tc::fence_after_sync();
-                for (int cc = 0; cc < kRowChunk / 32; ++cc) {
-                    const int r0 = rc * kRowChunk + cc * 32;
-                    if (r0 >= n) break;  // warp-uniform
+                const int r = rc * kRowChunk + q * 32 + lane;
+                float *dst = Y + j0 * n + r;
+#pragma unroll
+                for (int sc = 0; sc < 2; ++sc) {
                     float v[32];
                     tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                                      static_cast<uint32_t>(a * 256 + cc * 32),
+                                      static_cast<uint32_t>(a * kTileCols + hf * 64 + sc * 32),
                                   v);
-                    if (j < N) {
+                    if (r < n) {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const int r = r0 + e * 4;
-                            if (r < n) {
-                                float4 x = *reinterpret_cast<const float4 *>(xc + r);
-                                x.x -= v[4 * e];
-                                x.y -= v[4 * e + 1];
-                                x.z -= v[4 * e + 2];
-                                x.w -= v[4 * e + 3];
-                                *reinterpret_cast<float4 *>(yc + r) = x;
-                            }
-                        }
+                        for (int e = 0; e < 32; ++e)
+                            if (sc * 32 + e < ncol)
+                                dst[static_cast<int64_t>(sc * 32 + e) * n] = xb[sc * 32 + e] - v[e];
                     }
                 }
                 tc::fence_before_sync();
@@ -588,12 +656,13 @@ __global__ void __launch_bounds__(192, 1)
                     a = 0;
                     aph ^= 1u;
                 }
+                load(rc + 1);
             }
         }
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 1) tc::tmem_free<512>(tbase);
+    if (warp == 1) tc::tmem_free<256>(tbase);
 }
 
 // ------------------------------------------------------------------ host side
@@ -625,7 +694,14 @@ bool make_map(CUtensorMap *m, CUtensorMapDataType dt, int esize, const void *bas
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-size_t smem1() { return static_cast<size_t>(kStages1) * kStage1Bytes + sizeof(Bars1) + 1024; }
+size_t tbuild_smem(int b) {
+    return (static_cast<size_t>((b * (b + 1) / 2 + 31) / 32 * 32) + 8 * 32 * 33 + 224 * 32) * 4;
+}
+
+size_t smem1() {
+    return static_cast<size_t>(kRaw1) * kRawBytes + static_cast<size_t>(kStages1) * kConv1Bytes +
+           sizeof(Bars1) + 1024;
+}
 size_t smem3() {
     return kGresBytes + static_cast<size_t>(kStages3) * kStage3Bytes + sizeof(Bars3) + 1024;
 }
@@ -651,7 +727,7 @@ WyPlan wy_plan(int64_t n, int64_t h, int64_t N) {
     p.off_wb = off;
     off += al(static_cast<size_t>(p.h_pad) * p.n_pad * 2 * 2);
     p.off_sp = off;
-    off += al(static_cast<size_t>(p.nblk) * kSplitK * p.b * p.b * 4);
+    off += al(static_cast<size_t>(p.nblk) * (p.n_pad / kGramRows) * p.b * p.b * 4);
     p.off_s = off;
     off += al(static_cast<size_t>(p.nblk) * p.b * p.b * 4);
     p.off_t = off;
@@ -678,6 +754,10 @@ cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(smem1()));
         if (g_attr_err == cudaSuccess)
+            g_attr_err = cudaFuncSetAttribute(wy_tbuild_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(tbuild_smem(256)));
+        if (g_attr_err == cudaSuccess)
             g_attr_err = cudaFuncSetAttribute(wy_update_kernel,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem3()));
@@ -699,9 +779,13 @@ cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X,
         const int g = static_cast<int>(std::min<int64_t>((tot + 255) / 256, sms * 16));
         wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, op_t, p.h_pad, p.n_pad, Wf, Wb);
         const int tb = (p.b + 63) / 64;
-        wy_gram_kernel<<<dim3(tb, tb, p.nblk * kSplitK), 256, 0, stream>>>(Wf, p.n_pad, p.b,
-                                                                            p.nblk, Sp);
-        wy_tbuild_kernel<<<p.nblk, 1024, 0, stream>>>(Sp, p.b, S, T);
+        const int nsplit = static_cast<int>(p.n_pad / kGramRows);
+        wy_gram_kernel<<<dim3(tb, tb, p.nblk * nsplit), 256, 0, stream>>>(Wf, p.n_pad, p.b,
+                                                                           nsplit, Sp);
+        const int64_t ns = static_cast<int64_t>(p.nblk) * p.b * p.b;
+        wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, sms * 8)),
+                                256, 0, stream>>>(Sp, p.b, p.nblk, nsplit, S);
+        wy_tbuild_kernel<<<p.nblk, 1024, tbuild_smem(p.b), stream>>>(S, p.b, T);
         wy_v_kernel<<<dim3(static_cast<unsigned>(p.n_pad / 64), p.b / 32, p.nblk), 256, 0,
                       stream>>>(Wf, T, p.n_pad, p.b, p.nblk, Vt);
     }
@@ -729,13 +813,13 @@ cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X,
     for (int k = p.nblk - 1; k >= 0; --k) {
         if (debug_stop_blocks >= 0 && launched >= debug_stop_blocks) break;
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
-        wy_project_kernel<<<grid, 320, smem1(), stream>>>(mcur, mW, Gt, static_cast<int>(p.n), N,
+        wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, mW, Gt, static_cast<int>(p.n), N,
                                                           p.b, k * p.b, p.h_pad + k * p.b, ntiles);
         if (debug_stop_blocks >= 0) {
             ++launched;
             break;  // debug: stop after the first projection (G of block nblk-1)
         }
-        wy_update_kernel<<<grid, 192, smem3(), stream>>>(
+        wy_update_kernel<<<grid, 320, smem3(), stream>>>(
             mG, mV, cur, Y, static_cast<int>(p.n), static_cast<int>(p.n_pad), N, p.b,
             static_cast<int>(k * p.n_pad), static_cast<int>((p.nblk + k) * p.n_pad), ntiles);
         cur = Y;
