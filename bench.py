@@ -140,10 +140,8 @@ class ClockSampler:
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    from paper_1811_07624_b200 import dist as hd
+    return hd.env()
 
 
 def cpu_model():
@@ -352,10 +350,8 @@ def run_hh(args):
     sampler.stop()
     clocks = sampler.summary(t_obs0, t_obs1)
 
-    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    ms_max = float(tmax.item())
+    from paper_1811_07624_b200 import dist as hd
+    ms_max = hd.max_over_ranks(ms, device=dev)          # max over ranks
     ms_step = ms_max / args.steps
     value = ws * byts / (ms_step * 1e-3) / 1e9
 
@@ -376,10 +372,7 @@ def run_hh(args):
         for _ in range(ke):
             hh.hh_apply_host(op, Uh, Xh, Yh, workspace=wsp)
         torch.cuda.synchronize(dev)
-        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if ws > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        se = float(te.item()) / ke
+        se = hd.max_over_ranks(time.perf_counter() - t0, device=dev) / ke
         e2e = {"value": ws * byts / se / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size() + Uh.numel() * 4),
                "d2h_bytes_per_step": int(Yh.numel() * Yh.element_size()),
