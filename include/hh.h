@@ -125,7 +125,11 @@ hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
  *   with S-bar takes (8h+1)n operations" = a Q^T pass (u_1 first), one diagonal
  *   scale by lambda, and a Q pass (u_h first).
  *   lambda: n values of dtype (the spectrum s-bar; any sign).
- *   workspace: none needed.
+ *   workspace: DEVICE scratch of hh_workspace_bytes(HH_CALL_SYM, n, h, N, 0, dtype)
+ *   (0 -> fused SIMT kernel).  For fp32 and h >= 16 (hh_algo AUTO) the block program
+ *   runs on the tensor cores: blocks 1..m-1 as Q_k^T, the last block folded with
+ *   diag(lambda) into one project/update pair (Y = Lambda X - [A1 A2][G; G_lambda]),
+ *   then blocks m-1..1 as Q_k.
  */
 hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda,
                        const void *X, void *Y, int64_t N, hh_dtype dtype,
@@ -172,13 +176,15 @@ hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host,
  */
 hh_status hh_set_algo(hh_algo algo);
 hh_algo hh_get_algo(void);
+/* (hh_set_algo applies to hh_apply and hh_sym_apply.) */
 
 /*
  * hh_workspace_bytes -- scratch bytes the call needs (cuBLAS bufferSize style).
  *   N_or_M: N for apply/sym/apply_host, M for Mahalanobis.  Writes *bytes.
  *   HH_CALL_APPLY: the compact-WY scratch when this thread's hh_algo selection
  *   picks K5 for (n, h, N, dtype) (packed W, T, V = W T and one G block), else 0.
- *   HH_CALL_SYM: 0.  HH_CALL_MAHALANOBIS: n*M*sizeof(dtype) (the
+ *   HH_CALL_SYM: the compact-WY scratch when the symmetric call picks the tensor-core
+ *   block program, else 0.  HH_CALL_MAHALANOBIS: n*M*sizeof(dtype) (the
  *   transform-once Z).  Errors: HH_ERR_INVALID_VALUE for bad arguments.
  */
 hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,

@@ -34,6 +34,16 @@ bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
     return h >= wy_min_h(n);
 }
 
+// Symmetric apply: the SIMT kernel is FMA-bound from h ~ 11 (AI (8h+1)/8 flop/B vs the
+// ridge 11.4); the tensor-core block program moves 1.5x the bytes of one fused pass, so
+// it wins from h ~ 16.
+bool use_wy_sym(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
+    if (dtype != HH_F32 || !wy_supported(n, h, N)) return false;
+    if (algo == HH_ALGO_WY) return true;
+    if (algo == HH_ALGO_FUSED) return false;
+    return h >= 16 && n >= 256;
+}
+
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 size_t elem(hh_dtype dt) { return dt == HH_F32 ? 4 : 8; }
 bool dtype_ok(int dt) { return dt == HH_F32 || dt == HH_F64; }
@@ -123,16 +133,16 @@ hh_status hh_debug_wy_project(int op, int64_t n, int64_t h, const void *U, const
                               int64_t N, void *workspace, size_t workspace_bytes, int64_t *off,
                               hh_stream_t stream) {
     if (!wy_supported(n, h, N) || !workspace || !off) return HH_ERR_INVALID_VALUE;
-    const WyPlan p = wy_plan(n, h, N);
+    const WyPlan p = wy_plan(op ? WY_APPLY_T : WY_APPLY_N, n, h, N);
     if (workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
     off[0] = static_cast<int64_t>(p.off_gt);
-    off[1] = static_cast<int64_t>(p.off_vt);
+    off[1] = static_cast<int64_t>(p.off_v);
     off[2] = p.b;
     off[3] = p.nblk;
     off[4] = p.n_pad;
     off[5] = static_cast<int64_t>(p.off_t);
-    return map_err(launch_wy(op, p, static_cast<const float *>(U), static_cast<const float *>(X),
-                             nullptr, workspace, stream, nullptr, 1));
+    return map_err(launch_wy(p, static_cast<const float *>(U), nullptr,
+                             static_cast<const float *>(X), nullptr, workspace, stream, nullptr, 1));
 }
 
 hh_status hh_last_launch_info(const char **variant, int *grid, int *block, int *smem_bytes,
@@ -152,10 +162,12 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
         return HH_ERR_INVALID_VALUE;
     switch (call) {
         case HH_CALL_APPLY:
-            *bytes = use_wy(dtype, n, h, N_or_M, t_algo) ? wy_plan(n, h, N_or_M).bytes : 0;
+            *bytes = use_wy(dtype, n, h, N_or_M, t_algo) ? wy_plan(WY_APPLY_N, n, h, N_or_M).bytes
+                                                        : 0;
             return HH_OK;
         case HH_CALL_SYM:
-            *bytes = 0;
+            *bytes = use_wy_sym(dtype, n, h, N_or_M, t_algo) ? wy_plan(WY_SYM, n, h, N_or_M).bytes
+                                                            : 0;
             return HH_OK;
         case HH_CALL_MAHALANOBIS:
             *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype));
@@ -190,13 +202,13 @@ hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
     if (!X || !Y) return HH_ERR_INVALID_VALUE;
     if (!aligned16(X) || !aligned16(Y)) return HH_ERR_UNSUPPORTED;
     if (h > 0 && use_wy(dtype, n, h, N, t_algo)) {
-        const WyPlan p = wy_plan(n, h, N);
+        const WyPlan p = wy_plan(op == HH_OP_T ? WY_APPLY_T : WY_APPLY_N, n, h, N);
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
         if (workspace && !aligned16(workspace)) return HH_ERR_UNSUPPORTED;
         if (!workspace && t_algo == HH_ALGO_WY) return HH_ERR_WORKSPACE;
         if (workspace) {
             LaunchInfo info;
-            cudaError_t e = launch_wy(op == HH_OP_T ? 1 : 0, p, static_cast<const float *>(U),
+            cudaError_t e = launch_wy(p, static_cast<const float *>(U), nullptr,
                                       static_cast<const float *>(X), static_cast<float *>(Y),
                                       workspace, stream, &info);
             if (info.variant) {
@@ -221,13 +233,29 @@ hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
 hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda, const void *X,
                        void *Y, int64_t N, hh_dtype dtype, void *workspace,
                        size_t workspace_bytes, hh_stream_t stream) {
-    (void)workspace;
-    (void)workspace_bytes;
     hh_status st = check_common(n, h, U, N, dtype);
     if (st != HH_OK) return st;
     if (N == 0) return HH_OK;
     if (!X || !Y || !lambda) return HH_ERR_INVALID_VALUE;
     if (!aligned16(X) || !aligned16(Y) || !aligned16(lambda)) return HH_ERR_UNSUPPORTED;
+    if (h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
+        const WyPlan p = wy_plan(WY_SYM, n, h, N);
+        if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
+        if (workspace && !aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+        if (!workspace && t_algo == HH_ALGO_WY) return HH_ERR_WORKSPACE;
+        if (workspace) {
+            LaunchInfo info;
+            cudaError_t e = launch_wy(p, static_cast<const float *>(U),
+                                      static_cast<const float *>(lambda),
+                                      static_cast<const float *>(X), static_cast<float *>(Y),
+                                      workspace, stream, &info);
+            if (info.variant) {
+                t_last = info;
+                t_has_last = true;
+            }
+            return map_err(e);
+        }
+    }
     FusedArgs a{};
     a.U = U;
     a.X = X;

@@ -59,18 +59,21 @@ const DevAttr &device_attr();
 namespace hh {
 
 // ---- K4/K5 compact-WY tensor-core path (hh_wy.cu) ----
+enum WyKind : int { WY_APPLY_N = 0, WY_APPLY_T = 1, WY_SYM = 2 };
 struct WyPlan {
+    int kind = 0;
     int64_t n = 0, h = 0, N = 0;
-    int b = 0, nblk = 0, h_pad = 0;
+    int b = 0, nblk = 0, h_pad = 0, extra = 0, nsplit = 0;
     int64_t n_pad = 0;
-    size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_vt = 0, off_gt = 0;
+    size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_v = 0, off_v2 = 0,
+           off_asym = 0, off_vf = 0, off_vpf = 0, off_pp = 0, off_p = 0, off_m = 0, off_gt = 0;
     size_t bytes = 0;
 };
-WyPlan wy_plan(int64_t n, int64_t h, int64_t N);
+WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N);
 bool wy_supported(int64_t n, int64_t h, int64_t N);
-// op_t = 0: Y = Q X; 1: Y = Q^T X (fp32).  debug_stop_blocks >= 0: run the
-// preparation and only the first projection (test hook).
-cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X, float *Y,
+// Y = Q X / Q^T X / Q diag(lam) Q^T X by the compact-WY block program (fp32 in/out).
+// debug_stop_blocks >= 0: run the preparation and only the first projection (test hook).
+cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const float *X, float *Y,
                       void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks = -1);
 
 }  // namespace hh

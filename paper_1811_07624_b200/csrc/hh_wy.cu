@@ -71,46 +71,55 @@ __device__ __forceinline__ float bf2f(uint16_t b) {
 }
 
 // ------------------------------------------------------------------ K4: preparation
-// Wf[i][r] (fp32, h_pad x n_pad) = u_{e(i)}[r] in product order (zero padded);
-// Wb = bf16 split [hi rows 0..h_pad) [lo rows h_pad..2h_pad), ld = n_pad.
-__global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h, int reverse,
-                               int h_pad, int64_t n_pad, float *__restrict__ Wf,
-                               uint16_t *__restrict__ Wb) {
-    const int64_t total = static_cast<int64_t>(h_pad) * n_pad;
+// Wf[i][r] (fp32, h_pad x n_pad) = u_i[r] (product order of R1, zero padded).
+// Wb = bf16 split, R = h_pad + extra rows: [hi rows 0..R) [lo rows R..2R), ld = n_pad.
+// With lam != NULL the `extra` rows h_pad.. hold lambda (.) w_i of block `lam_blk`
+// (the Lambda W operand of the symmetric block).
+__global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h, int h_pad,
+                               int64_t n_pad, const float *__restrict__ lam, int lam_blk, int b,
+                               int extra, float *__restrict__ Wf, uint16_t *__restrict__ Wb) {
+    const int64_t R = h_pad + extra;
+    const int64_t total = R * n_pad;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = idx / n_pad, r = idx % n_pad;
         float v = 0.f;
-        if (i < h && r < n) {
-            const int64_t e = reverse ? (h - 1 - i) : i;
-            v = U[e * n + r];
+        if (i < h_pad) {
+            if (i < h && r < n) v = U[i * n + r];
+            Wf[idx] = v;
+        } else {
+            const int64_t src = static_cast<int64_t>(lam_blk) * b + (i - h_pad);
+            if (src < h && r < n) v = lam[r] * U[src * n + r];
         }
-        Wf[idx] = v;
         const uint16_t hb = f2bf(v);
         Wb[idx] = hb;
         Wb[total + idx] = f2bf(v - bf2f(hb));
     }
 }
 
-// Sp[blk][split][l][m] = sum_{r in split} w_l[r] w_m[r] over 128-row splits of
-// n_pad, upper 64x64 tiles only (the reduction over splits is done in fixed order
-// by wy_gram_reduce_kernel: deterministic).
+// Sp[blk][split][l][m] = sum_{r in split} w_l[r] wt[r] w_m[r] over 128-row splits
+// of n_pad (wt = 1 or lambda), blocks blk0.., upper 64x64 tiles only unless `full`
+// (the reduction over splits is done in fixed order by wy_gram_reduce_kernel:
+// deterministic).
 __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ Wf, int64_t n_pad,
-                                                      int b, int nsplit, float *__restrict__ Sp) {
+                                                      int b, int nsplit, int blk0,
+                                                      const float *__restrict__ wt, int full,
+                                                      float *__restrict__ Sp) {
     const int ti = blockIdx.x, tj = blockIdx.y;
     const int blk = blockIdx.z / nsplit, sp = blockIdx.z % nsplit;
-    if (ti > tj) return;
+    if (ti > tj && !full) return;
     __shared__ float Ls[32][65], Ms[32][65];
     const int t = threadIdx.x, tx = t % 16, ty = t / 16;
     float acc[4][4] = {};
     const int64_t r0 = static_cast<int64_t>(sp) * kGramRows;
-    const float *Wl = Wf + (static_cast<int64_t>(blk) * b + ti * 64) * n_pad;
-    const float *Wm = Wf + (static_cast<int64_t>(blk) * b + tj * 64) * n_pad;
+    const float *Wl = Wf + (static_cast<int64_t>(blk0 + blk) * b + ti * 64) * n_pad;
+    const float *Wm = Wf + (static_cast<int64_t>(blk0 + blk) * b + tj * 64) * n_pad;
     const int rows_l = min(64, b - ti * 64), rows_m = min(64, b - tj * 64);
     for (int64_t rc = r0; rc < r0 + kGramRows; rc += 32) {
         for (int e = t; e < 32 * 64; e += 256) {
             const int c = e / 32, k = e % 32;
-            Ls[k][c] = c < rows_l ? Wl[c * n_pad + rc + k] : 0.f;
+            const float w = wt ? wt[rc + k] : 1.f;
+            Ls[k][c] = c < rows_l ? w * Wl[c * n_pad + rc + k] : 0.f;
             Ms[k][c] = c < rows_m ? Wm[c * n_pad + rc + k] : 0.f;
         }
         __syncthreads();
@@ -144,14 +153,14 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
 
 // S[blk][l][m] = sum over splits (ascending) of the Gram partials, upper tiles.
 __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int nblk, int nsplit,
-                                      float *__restrict__ S) {
+                                      int full, float *__restrict__ S) {
     const int64_t bb = static_cast<int64_t>(b) * b;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < nblk * bb;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t blk = idx / bb, e = idx % bb;
         const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
         float s = 0.f;
-        if ((l / 64) <= (m / 64)) {
+        if (full || (l / 64) <= (m / 64)) {
             const float *p = Sp + blk * nsplit * bb + e;
             for (int q = 0; q < nsplit; ++q) s += p[q * bb];
         }
@@ -233,58 +242,83 @@ __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict
     }
 }
 
-// V = W T (n_pad x b per block), split to bf16 into Vt[hi: blk*n_pad + r][i],
-// Vt[lo: (nblk+blk)*n_pad + r][i] (row length b).
-__global__ void __launch_bounds__(256) wy_v_kernel(const float *__restrict__ Wf,
-                                                   const float *__restrict__ Tg, int64_t n_pad,
-                                                   int b, int nblk, uint16_t *__restrict__ Vt) {
-    const int r0 = blockIdx.x * 64, i0 = blockIdx.y * 32, blk = blockIdx.z;
-    __shared__ float Us[32][65], Ts[32][33];
+// Small SIMT GEMM of the preparation (fp32):
+//   out[r][c] = alpha_r * C[r][c] + sgn * sum_{l<K} A(r, l) B(l, c),   r < R, c < Kc
+// A(r, l) = A[l*lda + r] (transA: W stored as rows w_l) or A[r*lda + l];
+// B(l, c) = B[l*ldb + c] or B[c*ldb + l] (transB).  Output as fp32 (Of, ld ldo) and/or
+// bf16 hi/lo (Ob hi at Ob[r*ldo + c], lo at Ob[lo_off + r*ldo + c]).  Grid (R/64, Kc/32).
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) wy_rowgemm_kernel(
+    int64_t R, const float *__restrict__ A, int64_t lda, const float *__restrict__ B, int ldb,
+    int K, const float *__restrict__ C, int64_t ldc, const float *__restrict__ alpha,
+    int64_t alpha_n, float sgn, float *__restrict__ Of, uint16_t *__restrict__ Ob, int64_t ldo,
+    int64_t lo_off) {
+    const int64_t r0 = blockIdx.x * 64;
+    const int c0 = blockIdx.y * 32;
+    __shared__ float As[32][65], Bs[32][33];
     const int t = threadIdx.x, tx = t % 8, ty = t / 8;
     float acc[2][4] = {};
-    const float *W = Wf + static_cast<int64_t>(blk) * b * n_pad;
-    const float *T = Tg + static_cast<int64_t>(blk) * b * b;
-    const int lmax = i0 + 32;  // T[l][i] = 0 for l > i
-    for (int l0 = 0; l0 < lmax; l0 += 32) {
+    for (int l0 = 0; l0 < K; l0 += 32) {
         for (int e = t; e < 32 * 64; e += 256) {
-            const int k = e / 64, r = e % 64;
-            Us[k][r] = W[static_cast<int64_t>(l0 + k) * n_pad + r0 + r];
+            if (TA) {
+                const int k = e / 64, r = e % 64;
+                As[k][r] = (l0 + k < K && r0 + r < R)
+                               ? A[static_cast<int64_t>(l0 + k) * lda + r0 + r] : 0.f;
+            } else {
+                const int r = e / 32, k = e % 32;
+                As[k][r] = (l0 + k < K && r0 + r < R) ? A[(r0 + r) * lda + l0 + k] : 0.f;
+            }
         }
         for (int e = t; e < 32 * 32; e += 256) {
-            const int k = e / 32, c = e % 32;
-            Ts[k][c] = T[static_cast<int64_t>(l0 + k) * b + i0 + c];
+            if (TB) {
+                const int c = e / 32, k = e % 32;
+                Bs[k][c] = l0 + k < K ? B[static_cast<int64_t>(c0 + c) * ldb + l0 + k] : 0.f;
+            } else {
+                const int k = e / 32, c = e % 32;
+                Bs[k][c] = l0 + k < K ? B[static_cast<int64_t>(l0 + k) * ldb + c0 + c] : 0.f;
+            }
         }
         __syncthreads();
 #pragma unroll 8
         for (int k = 0; k < 32; ++k) {
-            const float u0 = Us[k][ty * 2], u1 = Us[k][ty * 2 + 1];
+            const float a0 = As[k][ty * 2], a1 = As[k][ty * 2 + 1];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float tv = Ts[k][tx * 4 + q];
-                acc[0][q] = fmaf(u0, tv, acc[0][q]);
-                acc[1][q] = fmaf(u1, tv, acc[1][q]);
+                const float bv = Bs[k][tx * 4 + q];
+                acc[0][q] = fmaf(a0, bv, acc[0][q]);
+                acc[1][q] = fmaf(a1, bv, acc[1][q]);
             }
         }
         __syncthreads();
     }
-    const int64_t lo_off = static_cast<int64_t>(nblk) * n_pad * b;
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
         const int64_t r = r0 + ty * 2 + p;
-        uint16_t hv[4], lv[4];
+        if (r >= R) continue;
+        float v[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            hv[q] = f2bf(acc[p][q]);
-            lv[q] = f2bf(acc[p][q] - bf2f(hv[q]));
+            const int c = c0 + tx * 4 + q;
+            v[q] = sgn * acc[p][q];
+            if (C) v[q] = fmaf(alpha ? (r < alpha_n ? alpha[r] : 0.f) : 1.f, C[r * ldc + c], v[q]);
         }
-        const int64_t o = (static_cast<int64_t>(blk) * n_pad + r) * b + i0 + tx * 4;
-        uint2 H, L;
-        H.x = hv[0] | (static_cast<uint32_t>(hv[1]) << 16);
-        H.y = hv[2] | (static_cast<uint32_t>(hv[3]) << 16);
-        L.x = lv[0] | (static_cast<uint32_t>(lv[1]) << 16);
-        L.y = lv[2] | (static_cast<uint32_t>(lv[3]) << 16);
-        *reinterpret_cast<uint2 *>(Vt + o) = H;
-        *reinterpret_cast<uint2 *>(Vt + lo_off + o) = L;
+        const int64_t o = r * ldo + c0 + tx * 4;
+        if (Of) *reinterpret_cast<float4 *>(Of + o) = make_float4(v[0], v[1], v[2], v[3]);
+        if (Ob) {
+            uint16_t hv[4], lv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                hv[q] = f2bf(v[q]);
+                lv[q] = f2bf(v[q] - bf2f(hv[q]));
+            }
+            uint2 H, L;
+            H.x = hv[0] | (static_cast<uint32_t>(hv[1]) << 16);
+            H.y = hv[2] | (static_cast<uint32_t>(hv[3]) << 16);
+            L.x = lv[0] | (static_cast<uint32_t>(lv[1]) << 16);
+            L.y = lv[2] | (static_cast<uint32_t>(lv[3]) << 16);
+            *reinterpret_cast<uint2 *>(Ob + o) = H;
+            *reinterpret_cast<uint2 *>(Ob + lo_off + o) = L;
+        }
     }
 }
 
@@ -506,8 +540,8 @@ struct Bars3 {
 
 __global__ void __launch_bounds__(320, 1)
     wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
-                     const float *X, float *Y, int n, int n_pad, int64_t N, int b, int vrow_hi,
-                     int vrow_lo, int ntiles) {
+                     const float *X, float *Y, const float *__restrict__ lam, int n, int n_pad,
+                     int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -637,6 +671,7 @@ __global__ void __launch_bounds__(320, 1)
                 tc::fence_after_sync();
                 const int r = rc * kRowChunk + q * 32 + lane;
                 float *dst = Y + j0 * n + r;
+                const float lr = (lam && r < n) ? lam[r] : 1.f;   // symmetric block: Lambda X
 #pragma unroll
                 for (int sc = 0; sc < 2; ++sc) {
                     float v[32];
@@ -647,7 +682,8 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
                         for (int e = 0; e < 32; ++e)
                             if (sc * 32 + e < ncol)
-                                dst[static_cast<int64_t>(sc * 32 + e) * n] = xb[sc * 32 + e] - v[e];
+                                dst[static_cast<int64_t>(sc * 32 + e) * n] =
+                                    fmaf(lr, xb[sc * 32 + e], -v[e]);
                     }
                 }
                 tc::fence_before_sync();
@@ -711,31 +747,45 @@ cudaError_t g_attr_err = cudaSuccess;
 
 }  // namespace
 
-WyPlan wy_plan(int64_t n, int64_t h, int64_t N) {
+WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     WyPlan p{};
+    p.kind = kind;
     p.n = n;
     p.h = h;
     p.N = N;
-    p.nblk = static_cast<int>(std::max<int64_t>(1, (h + 255) / 256));
+    const int64_t bmax = kind == WY_SYM ? 128 : 256;   // MMA N of the project pass <= 256
+    p.nblk = static_cast<int>(std::max<int64_t>(1, (h + bmax - 1) / bmax));
     const int64_t per = (h + p.nblk - 1) / p.nblk;
     p.b = static_cast<int>(std::max<int64_t>(32, (per + 31) / 32 * 32));
     p.h_pad = p.b * p.nblk;
+    p.extra = kind == WY_SYM ? p.b : 0;
     p.n_pad = (n + kRowChunk - 1) / kRowChunk * kRowChunk;
+    p.nsplit = static_cast<int>(p.n_pad / kGramRows);
+    const size_t bb = static_cast<size_t>(p.b) * p.b * 4;
+    const size_t vblk = static_cast<size_t>(p.n_pad) * p.b * 2 * 2;   // bf16 hi/lo per block
     size_t off = 0;
-    p.off_wf = off;
-    off += al(static_cast<size_t>(p.h_pad) * p.n_pad * 4);
-    p.off_wb = off;
-    off += al(static_cast<size_t>(p.h_pad) * p.n_pad * 2 * 2);
-    p.off_sp = off;
-    off += al(static_cast<size_t>(p.nblk) * (p.n_pad / kGramRows) * p.b * p.b * 4);
-    p.off_s = off;
-    off += al(static_cast<size_t>(p.nblk) * p.b * p.b * 4);
-    p.off_t = off;
-    off += al(static_cast<size_t>(p.nblk) * p.b * p.b * 4);
-    p.off_vt = off;
-    off += al(static_cast<size_t>(p.nblk) * p.n_pad * p.b * 2 * 2);
-    p.off_gt = off;
-    off += al(static_cast<size_t>(std::max<int64_t>(N, 1)) * p.b * 2 * 2);
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += al(bytes);
+        return o;
+    };
+    p.off_wf = take(static_cast<size_t>(p.h_pad) * p.n_pad * 4);
+    p.off_wb = take(static_cast<size_t>(p.h_pad + p.extra) * p.n_pad * 2 * 2);
+    p.off_sp = take(static_cast<size_t>(p.nblk) * p.nsplit * bb);
+    p.off_s = take(p.nblk * bb);
+    p.off_t = take(p.nblk * bb);
+    p.off_v = take(p.nblk * vblk);                                      // Vn (N) or Vt (T)
+    if (kind == WY_SYM) {
+        p.off_v2 = take(p.nblk * vblk);                                 // Vn next to Vt
+        p.off_asym = take(static_cast<size_t>(p.n_pad) * 2 * p.b * 2 * 2);
+        p.off_vf = take(static_cast<size_t>(p.n_pad) * p.b * 4);
+        p.off_vpf = take(static_cast<size_t>(p.n_pad) * p.b * 4);
+        p.off_pp = take(static_cast<size_t>(p.nsplit) * bb);
+        p.off_p = take(bb);
+        p.off_m = take(bb);
+    }
+    const int kmax = kind == WY_SYM ? 2 * p.b : p.b;
+    p.off_gt = take(static_cast<size_t>(std::max<int64_t>(N, 1)) * kmax * 2 * 2);
     p.bytes = off;
     return p;
 }
@@ -746,7 +796,19 @@ bool wy_supported(int64_t n, int64_t h, int64_t N) {
            n <= (int64_t(1) << 20);
 }
 
-cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X, float *Y,
+namespace {
+
+struct Pass {
+    int wrow;            // first W row of the project operand
+    int kw;              // its row count (b, or 2b for the symmetric block)
+    const CUtensorMap *mW, *mG, *mV;
+    int vrow_hi, vrow_lo;
+    bool lam;            // symmetric block: Lambda X in the update epilogue
+};
+
+}  // namespace
+
+cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const float *X, float *Y,
                       void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks) {
     if (!encoder()) return cudaErrorNotSupported;
     std::call_once(g_attr_once, []() {
@@ -763,74 +825,143 @@ cudaError_t launch_wy(int op_t, const WyPlan &p, const float *U, const float *X,
                                               static_cast<int>(smem3()));
     });
     if (g_attr_err != cudaSuccess) return g_attr_err;
+    const bool sym = p.kind == WY_SYM;
+    if (sym && !lam) return cudaErrorInvalidValue;
     char *w = static_cast<char *>(ws);
-    float *Wf = reinterpret_cast<float *>(w + p.off_wf);
-    uint16_t *Wb = reinterpret_cast<uint16_t *>(w + p.off_wb);
-    float *Sp = reinterpret_cast<float *>(w + p.off_sp);
-    float *S = reinterpret_cast<float *>(w + p.off_s);
-    float *T = reinterpret_cast<float *>(w + p.off_t);
-    uint16_t *Vt = reinterpret_cast<uint16_t *>(w + p.off_vt);
-    uint16_t *Gt = reinterpret_cast<uint16_t *>(w + p.off_gt);
+    auto F = [&](size_t o) { return reinterpret_cast<float *>(w + o); };
+    auto H = [&](size_t o) { return reinterpret_cast<uint16_t *>(w + o); };
+    float *Wf = F(p.off_wf), *Sp = F(p.off_sp), *S = F(p.off_s), *T = F(p.off_t);
+    uint16_t *Wb = H(p.off_wb), *Gt = H(p.off_gt);
     const int sms = device_attr().sm_count;
+    const int m = p.nblk, b = p.b;
+    const int64_t n_pad = p.n_pad, R = p.h_pad + p.extra;
+    const int64_t vlo = static_cast<int64_t>(m) * n_pad * b;           // lo offset in a V array
 
-    // K4: pack + Gram + T + V
+    // ---------------- K4: pack + Gram + T + V (and the symmetric block's operands)
     {
-        const int64_t tot = static_cast<int64_t>(p.h_pad) * p.n_pad;
+        const int64_t tot = R * n_pad;
         const int g = static_cast<int>(std::min<int64_t>((tot + 255) / 256, sms * 16));
-        wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, op_t, p.h_pad, p.n_pad, Wf, Wb);
-        const int tb = (p.b + 63) / 64;
-        const int nsplit = static_cast<int>(p.n_pad / kGramRows);
-        wy_gram_kernel<<<dim3(tb, tb, p.nblk * nsplit), 256, 0, stream>>>(Wf, p.n_pad, p.b,
-                                                                           nsplit, Sp);
-        const int64_t ns = static_cast<int64_t>(p.nblk) * p.b * p.b;
+        wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b, p.extra,
+                                              Wf, Wb);
+        const int tb = (b + 63) / 64;
+        wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, 0,
+                                                                       nullptr, 0, Sp);
+        const int64_t ns = static_cast<int64_t>(m) * b * b;
         wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, sms * 8)),
-                                256, 0, stream>>>(Sp, p.b, p.nblk, nsplit, S);
-        wy_tbuild_kernel<<<p.nblk, 1024, tbuild_smem(p.b), stream>>>(S, p.b, T);
-        wy_v_kernel<<<dim3(static_cast<unsigned>(p.n_pad / 64), p.b / 32, p.nblk), 256, 0,
-                      stream>>>(Wf, T, p.n_pad, p.b, p.nblk, Vt);
+                                256, 0, stream>>>(Sp, b, m, p.nsplit, 0, S);
+        if (sym) {   // P = W^T Lambda W of the last block (full)
+            wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit,
+                                                                       m - 1, lam, 1, F(p.off_pp));
+            wy_gram_reduce_kernel<<<std::max(1, (b * b + 255) / 256), 256, 0, stream>>>(
+                F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p));
+        }
+        wy_tbuild_kernel<<<m, 1024, tbuild_smem(b), stream>>>(S, b, T);
+        const dim3 gv(static_cast<unsigned>(n_pad / 64), b / 32);
+        for (int k = 0; k < m; ++k) {
+            const float *Wk = Wf + static_cast<int64_t>(k) * b * n_pad;
+            const float *Tk = T + static_cast<int64_t>(k) * b * b;
+            const bool last_sym = sym && k == m - 1;
+            const bool need_n = p.kind == WY_APPLY_N || (sym && !last_sym);
+            const bool need_t = p.kind == WY_APPLY_T || (sym && !last_sym);
+            // op N:  V = W T ;  op T:  V' = W T^T
+            uint16_t *Vn = H(p.kind == WY_APPLY_N ? p.off_v : p.off_v2);
+            uint16_t *Vt = H(p.off_v);
+            if (need_n)
+                wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                    n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
+                    Vn + static_cast<int64_t>(k) * n_pad * b, b, vlo);
+            if (need_t)
+                wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
+                    n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
+                    Vt + static_cast<int64_t>(k) * n_pad * b, b, vlo);
+            if (last_sym) {
+                // A2 = W T (bf16 into columns [b, 2b) of Asym, fp32 copy Vf); V' = W T^T;
+                // M = P T^T; A1 = Lambda V' - V M (columns [0, b)).  DESIGN.md §4.
+                uint16_t *As = H(p.off_asym);
+                const int64_t alo = n_pad * 2 * b;
+                wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                    n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_vf),
+                    nullptr, b, 0);
+                wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                    n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr, As + b,
+                    2 * b, alo);
+                wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
+                    n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_vpf),
+                    nullptr, b, 0);
+                wy_rowgemm_kernel<false, true><<<dim3((b + 63) / 64, b / 32), 256, 0, stream>>>(
+                    b, F(p.off_p), b, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_m), nullptr,
+                    b, 0);
+                wy_rowgemm_kernel<false, false><<<gv, 256, 0, stream>>>(
+                    n_pad, F(p.off_vf), b, F(p.off_m), b, b, F(p.off_vpf), b, lam, p.n, -1.f,
+                    nullptr, As, 2 * b, alo);
+            }
+        }
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
 
-    CUtensorMap mW, mG, mV, mX, mY;
+    // ---------------- tensor maps
     const int64_t N = p.N;
-    bool ok = make_map(&mW, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, p.n_pad, 2 * p.h_pad, 32,
-                       p.b, CU_TENSOR_MAP_SWIZZLE_64B) &&
-              make_map(&mG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Gt, p.b, 2 * N, 32, kTileCols,
+    CUtensorMap mWb, mW2b, mGb, mG2b, mV, mV2, mAs, mX, mY;
+    bool ok = make_map(&mWb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, n_pad, 2 * R, 32, b,
                        CU_TENSOR_MAP_SWIZZLE_64B) &&
-              make_map(&mV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Vt, p.b, 2 * p.nblk * p.n_pad, 32,
+              make_map(&mGb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Gt, b, 2 * N, 32, kTileCols,
+                       CU_TENSOR_MAP_SWIZZLE_64B) &&
+              make_map(&mV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, H(p.off_v), b, 2 * m * n_pad, 32,
                        kRowChunk, CU_TENSOR_MAP_SWIZZLE_64B) &&
               make_map(&mX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, X, p.n, N, 32, kTileCols,
                        CU_TENSOR_MAP_SWIZZLE_NONE) &&
-              make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, 32, kTileCols,
-                       CU_TENSOR_MAP_SWIZZLE_NONE);
+              (!Y || make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, 32, kTileCols,
+                              CU_TENSOR_MAP_SWIZZLE_NONE));
+    if (ok && sym)
+        ok = make_map(&mW2b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, n_pad, 2 * R, 32, 2 * b,
+                      CU_TENSOR_MAP_SWIZZLE_64B) &&
+             make_map(&mG2b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Gt, 2 * b, 2 * N, 32, kTileCols,
+                      CU_TENSOR_MAP_SWIZZLE_64B) &&
+             make_map(&mV2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, H(p.off_v2), b, 2 * m * n_pad,
+                      32, kRowChunk, CU_TENSOR_MAP_SWIZZLE_64B) &&
+             make_map(&mAs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, H(p.off_asym), 2 * b, 2 * n_pad,
+                      32, kRowChunk, CU_TENSOR_MAP_SWIZZLE_64B);
     if (!ok) return cudaErrorNotSupported;
+
+    // ---------------- the block program
+    Pass prog[2 * 64];
+    int np = 0;
+    auto blockpass = [&](int k, const CUtensorMap *mv) {
+        prog[np++] = Pass{k * b, b, &mWb, &mGb, mv, static_cast<int>(k * n_pad),
+                          static_cast<int>((m + k) * n_pad), false};
+    };
+    if (p.kind == WY_APPLY_N) {
+        for (int k = m - 1; k >= 0; --k) blockpass(k, &mV);          // Q X: last block first
+    } else if (p.kind == WY_APPLY_T) {
+        for (int k = 0; k < m; ++k) blockpass(k, &mV);               // Q^T X: first block first
+    } else {
+        for (int k = 0; k < m - 1; ++k) blockpass(k, &mV);           // Q_k^T, k < m-1
+        prog[np++] = Pass{(m - 1) * b, 2 * b, &mW2b, &mG2b, &mAs, 0, static_cast<int>(n_pad), true};
+        for (int k = m - 2; k >= 0; --k) blockpass(k, &mV2);         // Q_k, k < m-1
+    }
 
     const int ntiles = static_cast<int>((N + kTileCols - 1) / kTileCols);
     const int grid = std::max(1, std::min(ntiles, sms));
     const float *cur = X;
-    int launched = 0;
-    for (int k = p.nblk - 1; k >= 0; --k) {
-        if (debug_stop_blocks >= 0 && launched >= debug_stop_blocks) break;
+    for (int q = 0; q < np; ++q) {
+        const Pass &ps = prog[q];
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
-        wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, mW, Gt, static_cast<int>(p.n), N,
-                                                          p.b, k * p.b, p.h_pad + k * p.b, ntiles);
-        if (debug_stop_blocks >= 0) {
-            ++launched;
-            break;  // debug: stop after the first projection (G of block nblk-1)
-        }
+        wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, *ps.mW, Gt, static_cast<int>(p.n),
+                                                          N, ps.kw, ps.wrow,
+                                                          static_cast<int>(R) + ps.wrow, ntiles);
+        if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
         wy_update_kernel<<<grid, 320, smem3(), stream>>>(
-            mG, mV, cur, Y, static_cast<int>(p.n), static_cast<int>(p.n_pad), N, p.b,
-            static_cast<int>(k * p.n_pad), static_cast<int>((p.nblk + k) * p.n_pad), ntiles);
+            *ps.mG, *ps.mV, cur, Y, ps.lam ? lam : nullptr, static_cast<int>(p.n),
+            static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles);
         cur = Y;
-        ++launched;
     }
     if (info) {
-        info->variant = "wy_bf16x3_tcgen05";
+        info->variant = sym ? "wy_sym_bf16x3_tcgen05" : "wy_bf16x3_tcgen05";
         info->grid = grid;
-        info->block = 320;
-        info->smem = static_cast<int>(smem3());
-        info->nchunks = p.nblk;
+        info->block = 480;
+        info->smem = static_cast<int>(smem1());
+        info->nchunks = np;
     }
     return cudaGetLastError();
 }

@@ -193,8 +193,10 @@ def hh_apply(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor
 
 
 def hh_sym_apply(U: torch.Tensor, lam: torch.Tensor, X: torch.Tensor,
-                 Y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """Y = Q diag(lam) Q^T X (hh.h: hh_sym_apply)."""
+                 Y: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+    """Y = Q diag(lam) Q^T X (hh.h: hh_sym_apply); allocates the workspace the selected
+    path needs when not given."""
     _dev(X, "X")
     _dev(lam, "lambda")
     N, n = X.shape
@@ -204,8 +206,12 @@ def hh_sym_apply(U: torch.Tensor, lam: torch.Tensor, X: torch.Tensor,
     if Y is None:
         Y = torch.empty_like(X)
     _dev(Y, "Y")
+    wsb = hh_workspace_bytes(HH_CALL_SYM, n, h, N, 0, X.dtype) if N else 0
+    if wsb and (workspace is None or workspace.numel() < wsb):
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
     st = lib().hh_sym_apply(n, h, _ptr(U) if h else None, _ptr(lam), _ptr(X), _ptr(Y), N,
-                            _dtype(X), None, 0, _stream(stream))
+                            _dtype(X), _ptr(workspace) if wsb else None,
+                            workspace.numel() if wsb else 0, _stream(stream))
     _check(st, "hh_sym_apply")
     return Y
 

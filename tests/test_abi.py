@@ -42,8 +42,17 @@ def test_status_strings():
 
 
 def test_workspace_query():
+    # small h: the fused kernel, no scratch; large h / the symmetric C3 shape (fp32): the
+    # compact-WY block program's scratch, well below the 1 GiB operands; fp64: always 0
     assert hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 1024, 10, 262144, 0, 0) == 0
-    assert hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 2048, 32, 131072, 0, 0) == 0
+    big = hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 4096, 1024, 65536, 0, 0)
+    assert 0 < big < 256 << 20
+    sym = hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 2048, 32, 131072, 0, 0)
+    assert 0 < sym < 64 << 20
+    assert hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 2048, 32, 131072, 0, 1) == 0
+    with hhpkg.algo(hhpkg.HH_ALGO_FUSED):
+        assert hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 4096, 1024, 65536, 0, 0) == 0
+        assert hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 2048, 32, 131072, 0, 0) == 0
     assert hhpkg.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, 512, 9, 65536, 1 << 21, 0) == \
         512 * 65536 * 4
     b = hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY_HOST, 1024, 10, 262144, 0, 0)

@@ -39,10 +39,12 @@ def bf16_pair_to_f64(ws, off, count, lo_off):
     return f(hi) + f(lo)
 
 
-@pytest.mark.parametrize("n,h,N,op", [(256, 40, 300, 0), (512, 70, 257, 1), (4096, 256, 130, 0)])
+@pytest.mark.parametrize("n,h,N,op", [(256, 40, 300, 0), (512, 70, 257, 1), (4096, 256, 130, 0),
+                                      (1024, 300, 129, 1)])
 def test_wy_intermediates(n, h, N, op):
-    """G = W^T X and V = W T of the first applied block (the last block of the product
-    order) match fp64 numpy: T by the forward recurrence T[:i, i] = -2 T[:i,:i] W[:, :i]^T w_i."""
+    """G = W^T X and V of the first applied block match fp64 numpy.  Blocks are cut in
+    product order; Q X applies the last block with V = W T, Q^T X the first block with
+    V' = W T^T, T by the forward recurrence T[:i, i] = -2 T[:i,:i] W[:, :i]^T w_i."""
     c = gi.make_case("apply", n, h, N, "f32", seed=21)
     U, X = dev(c.U), dev(c.X)
     with hh.algo(hh.HH_ALGO_WY):
@@ -51,10 +53,9 @@ def test_wy_intermediates(n, h, N, op):
     off = hh.debug_wy_project(op, U, X, ws)
     torch.cuda.synchronize()
     b, nblk, n_pad = off["b"], off["nblk"], off["n_pad"]
-    order = np.arange(h) if op == 0 else np.arange(h)[::-1]
     Wfull = np.zeros((nblk * b, n))
-    Wfull[:h] = c.U.astype(np.float64)[order]
-    k = nblk - 1
+    Wfull[:h] = c.U.astype(np.float64)
+    k = nblk - 1 if op == 0 else 0
     W = Wfull[k * b:(k + 1) * b]                       # (b, n): rows w_i
     G_ref = c.X.astype(np.float64) @ W.T               # (N, b)
     G = bf16_pair_to_f64(ws, off["G"], N * b, N * b).reshape(N, b)
@@ -67,7 +68,7 @@ def test_wy_intermediates(n, h, N, op):
         T[i, i] = 2.0
         if i:
             T[:i, i] = -2.0 * T[:i, :i] @ (W[:i] @ W[i])
-    V_ref = W.T @ T                                    # (n, b)
+    V_ref = W.T @ (T if op == 0 else T.T)              # (n, b)
     V = bf16_pair_to_f64(ws, off["V"] + 2 * k * n_pad * b, n_pad * b,
                          nblk * n_pad * b).reshape(n_pad, b)[:n]
     assert rel_fro(V, V_ref) < 4e-5, rel_fro(V, V_ref)
@@ -132,3 +133,51 @@ def test_C5_full_size_sampled_auto(h):
     got = Yd[torch.from_numpy(idx).cuda()].cpu().numpy()
     assert np.all(np.isfinite(Yd.cpu().numpy()))
     assert_parity(got, oracle.apply(0, c.U, c.X[idx]), "f32", h, f"C5 full h={h}")
+
+
+SYM_SHAPES = [  # (n, h, N): one block (b = 32..128) and several (m = 2, 3), ragged tails
+    (2048, 32, 700), (256, 20, 300), (512, 100, 257), (1024, 129, 200), (4096, 300, 130),
+    (100, 40, 129),
+]
+
+
+def wy_sym(U, lam, X):
+    with hh.algo(hh.HH_ALGO_WY):
+        out = hh.hh_sym_apply(dev(U), dev(lam), dev(X))
+        assert hh.last_launch_info()["variant"].startswith("wy_sym"), hh.last_launch_info()
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,h,N", SYM_SHAPES)
+def test_wy_sym_parity(n, h, N):
+    """Q diag(lambda) Q^T X by the tensor-core block program vs the oracle (C3 spectrum
+    recipe: exp(-k/200) with 10% sign flips)."""
+    c = gi.make_case("sym", n, h, N, "f32", seed=24)
+    got = wy_sym(c.U, c.lam, c.X)
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", h, f"WY sym n{n} h{h}")
+
+
+def test_wy_sym_special_cases():
+    """lambda == 1 -> X (Q Q^T = I up to fp32 u); lambda == -1 -> -X; alias Y == X."""
+    c = gi.make_case("sym", 1024, 48, 300, "f32", seed=25)
+    ones = np.ones(1024, dtype=np.float32)
+    assert rel_fro(wy_sym(c.U, ones, c.X), c.X) < 2e-5 * np.sqrt(48)
+    assert rel_fro(wy_sym(c.U, -ones, c.X), -c.X) < 2e-5 * np.sqrt(48)
+    X = dev(c.X)
+    with hh.algo(hh.HH_ALGO_WY):
+        hh.hh_sym_apply(dev(c.U), dev(c.lam), X, Y=X)
+    torch.cuda.synchronize()
+    assert_parity(X.cpu().numpy(), oracle.sym_apply(c.U, c.lam, c.X), "f32", 48, "sym alias")
+
+
+def test_C3_full_size_sampled_auto():
+    """configs[2] at full size through the auto path the bench times."""
+    c = gi.make_config(3)
+    Yd = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X))
+    torch.cuda.synchronize()
+    assert hh.last_launch_info()["variant"].startswith("wy_sym")
+    idx = np.unique(np.concatenate([np.linspace(0, c.N - 1, 300).astype(np.int64),
+                                    np.arange(c.N - 8, c.N)]))
+    got = Yd[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X[idx]), "f32", c.h, "C3 full auto")
