@@ -65,8 +65,9 @@ def test_C2_full_size_sampled(op):
 def test_C3_sym_small():
     """configs[2] shapes: fp32 sym n=2048 h=32, 1500 columns (U 256 KiB -> chunked)."""
     c = gi.make_config(3, N=1500)
-    got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
-    info = hh.last_launch_info()
+    with hh.algo(hh.HH_ALGO_FUSED):            # the SIMT K2 kernel with U streamed in chunks
+        got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+        info = hh.last_launch_info()
     assert info["nchunks"] > 1, info
     assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", c.h, "C3")
 
