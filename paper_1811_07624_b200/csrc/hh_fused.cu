@@ -235,13 +235,29 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
     // one reflector: x <- x - 2 (u^T x) u   for the C columns of this group
     auto reflect = [&](const V *ub) {
         T p[C];
+        // multi-warp groups: keep the u chunk in registers across the cross-warp
+        // reduction (a shared-memory store + barrier the compiler cannot see through),
+        // so u is read from shared memory once per reflector, not twice
+        constexpr bool kKeepU = TPC > 32;
+        V uk[kKeepU ? CH : 1];
+        if constexpr (kKeepU) {
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                if (valid_k(k)) uk[k] = ub[gt + TPC * k];
+                else vzero(uk[k]);
+            }
+        }
+        auto uget = [&](int k) -> V {
+            if constexpr (kKeepU) return uk[k];
+            else return ub[gt + TPC * k];
+        };
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             V acc;
             vzero(acc);
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) vfma(acc, ub[gt + TPC * k], x[c][k]);
+                if (valid_k(k)) vfma(acc, uget(k), x[c][k]);
             }
             p[c] = vsum(acc);
         }
@@ -271,7 +287,7 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
             const T s = p[c] + p[c];
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) vaxpy(x[c][k], s, ub[gt + TPC * k]);
+                if (valid_k(k)) vaxpy(x[c][k], s, uget(k));
             }
         }
     };
@@ -483,7 +499,7 @@ const Variant kF32[] = {
     HH_VAR(float, 32, 4, 2, 256, "f32_tpc32_ch4_c2"),   // n <= 512
     HH_VAR(float, 32, 8, 2, 256, "f32_tpc32_ch8_c2"),   // n <= 1024
     HH_VAR(float, 64, 8, 2, 256, "f32_tpc64_ch8_c2"),   // n <= 2048
-    HH_VAR(float, 128, 8, 1, 256, "f32_tpc128_ch8_c1"), // n <= 4096
+    HH_VAR(float, 128, 8, 2, 384, "f32_tpc128_ch8_c2"), // n <= 4096
     HH_VAR(float, 256, 8, 1, 256, "f32_tpc256_ch8_c1"), // n <= 8192
 };
 const Variant kF64[] = {
@@ -530,33 +546,40 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     const size_t maxs = static_cast<size_t>(da.max_smem_optin);
     const int64_t h = a.h;
 
-    int stage = a.mode == MODE_PAIR ? 0 : 1;
-    int R = 0, nc = 1;
+    // Shared-memory plan, in order of preference: (1) staged column tiles + resident U,
+    // (2) resident U with columns loaded straight into registers (a chunked U would be
+    // re-streamed from L2 for every tile: h*n*s bytes per tile), (3) staged tiles + U
+    // chunks through two buffers, (4) unstaged + U chunks.
+    const size_t xs_st = static_cast<size_t>(NU) * UC * colB;
+    const size_t ub = static_cast<size_t>(h) * colB;
+    const bool pair = a.mode == MODE_PAIR;
+    int stage = 0, R = 0, nc = 1;
     size_t smem = 0;
-    for (;;) {
-        const size_t xs = stage ? static_cast<size_t>(NU) * UC * colB : 0;
-        const size_t fixed = xs + red + bars;
-        if (h == 0) {
-            R = 0;
-            nc = 1;
-            smem = fixed;
-            break;
-        }
-        if (static_cast<size_t>(h) * colB + fixed <= maxs) {
-            R = static_cast<int>(h);
-            nc = 1;
-            smem = static_cast<size_t>(h) * colB + fixed;
-            break;
-        }
-        const int64_t r = fixed < maxs ? static_cast<int64_t>((maxs - fixed) / (2 * colB)) : 0;
-        if (r >= 1) {
-            R = static_cast<int>(std::min<int64_t>(r, h));
-            nc = static_cast<int>((h + R - 1) / R);
-            smem = 2 * static_cast<size_t>(R) * colB + fixed;
-            break;
-        }
-        if (!stage) return cudaErrorNotSupported;
+    if (h == 0) {
+        stage = pair ? 0 : 1;
+        smem = (stage ? xs_st : 0) + red + bars;
+    } else if (!pair && ub + xs_st + red + bars <= maxs) {
+        stage = 1;
+        R = static_cast<int>(h);
+        smem = ub + xs_st + red + bars;
+    } else if (ub + red + bars <= maxs) {
         stage = 0;
+        R = static_cast<int>(h);
+        smem = ub + red + bars;
+    } else {
+        bool ok = false;
+        for (int st = pair ? 0 : 1; st >= 0 && !ok; --st) {
+            const size_t fixed = (st ? xs_st : 0) + red + bars;
+            const int64_t r = fixed < maxs ? static_cast<int64_t>((maxs - fixed) / (2 * colB)) : 0;
+            if (r >= 1) {
+                stage = st;
+                R = static_cast<int>(std::min<int64_t>(r, h));
+                nc = static_cast<int>((h + R - 1) / R);
+                smem = 2 * static_cast<size_t>(R) * colB + fixed;
+                ok = true;
+            }
+        }
+        if (!ok) return cudaErrorNotSupported;
     }
     a.R = R;
     a.nchunks = nc;
