@@ -52,7 +52,10 @@ constexpr int kRowChunk = 128;    // K5b rows r per accumulator (MMA M)
 constexpr int kTileCols = 128;    // columns of X per tile (K5a MMA M, K5b MMA N)
 constexpr int kRaw1 = 4;          // K5a raw fp32 X ring depth
 constexpr int kStages1 = 3;       // K5a converted X + W ring depth
-constexpr int kStages3 = 6;       // K5b V ring depth
+constexpr int kStages3 = 3;       // K5b V ring depth
+constexpr int kXStages = 6;       // K5b X box ring depth (even: see the epilogue)
+constexpr int kXBoxCols = 16;     // columns per X box
+constexpr int kXBoxBytes = 8192;  // fp32 X box (128 rows x 16 columns)
 constexpr int kRawBytes = 16384;     // fp32 X tile (128 columns x 32 rows)
 constexpr int kConv1Bytes = 49152;   // X hi/lo 16K + W hi/lo 32K (b = 256)
 constexpr int kStage3Bytes = 16384;  // V hi/lo tile (128 rows x 32 bf16) x 2
@@ -209,30 +212,62 @@ __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict
         }
     }
     __syncthreads();
+    // extension steps; each thread owns (row l, 4 consecutive columns): 2 shared loads
+    // (one broadcast, one 16-B) per 4 FMAs
+    float *T22 = Pm + 224 * 32;                        // 32 x 32 dense diagonal block
     for (int c = 32; c < b; c += 32) {
-        // S panel S[0:c, c:c+32] -> Sb (c x 32)
+        // S panel S[0:c, c:c+32] -> Sb (c x 32); T22 = T[c:c+32, c:c+32] (dense)
         for (int e = t; e < c * 32; e += 1024) Sb[e] = S[(e / 32) * b + c + (e % 32)];
-        __syncthreads();
-        for (int e = t; e < c * 32; e += 1024) {
-            const int l = e / 32, j = e % 32;
-            float s = 0.f;
-            for (int m = 0; m <= j; ++m) s = fmaf(Sb[l * 32 + m], tp(c + m, c + j), s);
-            Pm[e] = s;
+        {
+            const int mm = t / 32, jj = t % 32;
+            T22[t] = jj >= mm ? tp(c + mm, c + jj) : 0.f;
         }
         __syncthreads();
-        for (int e = t; e < c * 32; e += 1024) {
-            const int l = e / 32, j = e % 32;
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        for (int e = t; e < c * 8; e += 1024) {
+            const int l = e / 8, j0 = (e % 8) * 4;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int m = 0; m < j0 + 4; ++m) {
+                const float sv = Sb[l * 32 + m];
+                const float4 tv = *reinterpret_cast<const float4 *>(T22 + m * 32 + j0);
+                acc.x = fmaf(sv, tv.x, acc.x);
+                acc.y = fmaf(sv, tv.y, acc.y);
+                acc.z = fmaf(sv, tv.z, acc.z);
+                acc.w = fmaf(sv, tv.w, acc.w);
+            }
+            *reinterpret_cast<float4 *>(Pm + l * 32 + j0) = acc;
+        }
+        __syncthreads();
+        for (int e = t; e < c * 8; e += 1024) {
+            const int l = e / 8, j0 = (e % 8) * 4;
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
             const float *trow = &tp(l, l);
             int m = l;
-            for (; m + 3 < c; m += 4) {
-                s0 = fmaf(trow[m - l], Pm[m * 32 + j], s0);
-                s1 = fmaf(trow[m - l + 1], Pm[(m + 1) * 32 + j], s1);
-                s2 = fmaf(trow[m - l + 2], Pm[(m + 2) * 32 + j], s2);
-                s3 = fmaf(trow[m - l + 3], Pm[(m + 3) * 32 + j], s3);
+            for (; m + 1 < c; m += 2) {
+                const float t0 = trow[m - l], t1 = trow[m - l + 1];
+                const float4 p0 = *reinterpret_cast<const float4 *>(Pm + m * 32 + j0);
+                const float4 p1 = *reinterpret_cast<const float4 *>(Pm + (m + 1) * 32 + j0);
+                a0.x = fmaf(t0, p0.x, a0.x);
+                a0.y = fmaf(t0, p0.y, a0.y);
+                a0.z = fmaf(t0, p0.z, a0.z);
+                a0.w = fmaf(t0, p0.w, a0.w);
+                a1.x = fmaf(t1, p1.x, a1.x);
+                a1.y = fmaf(t1, p1.y, a1.y);
+                a1.z = fmaf(t1, p1.z, a1.z);
+                a1.w = fmaf(t1, p1.w, a1.w);
             }
-            for (; m < c; ++m) s0 = fmaf(trow[m - l], Pm[m * 32 + j], s0);
-            tp(l, c + j) = -((s0 + s1) + (s2 + s3));
+            if (m < c) {
+                const float t0 = trow[m - l];
+                const float4 p0 = *reinterpret_cast<const float4 *>(Pm + m * 32 + j0);
+                a0.x = fmaf(t0, p0.x, a0.x);
+                a0.y = fmaf(t0, p0.y, a0.y);
+                a0.z = fmaf(t0, p0.z, a0.z);
+                a0.w = fmaf(t0, p0.w, a0.w);
+            }
+            float *o = &tp(l, c + j0);
+            o[0] = -(a0.x + a1.x);
+            o[1] = -(a0.y + a1.y);
+            o[2] = -(a0.z + a1.z);
+            o[3] = -(a0.w + a1.w);
         }
         __syncthreads();
     }
@@ -528,20 +563,28 @@ __global__ void __launch_bounds__(480, 1)
 }
 
 // ------------------------------------------------------------------ K5b: X <- X - V G
-// D[r][j] = sum_i V[r][i] G[j][i] with TMEM lane = row r, TMEM column = column j, so
-// the epilogue's global loads / stores of X[j][r] are 128-B coalesced per warp.
-// 10 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2-9 epilogue.
+// D[r][j] = sum_i V[r][i] G[j][i] with TMEM lane = row r, TMEM column = column j.
+// 12 warps: w0 TMA producer (G tile, V tiles), w1 MMA issuer (+TMEM owner), w2 TMA
+// producer of the X boxes (128 rows x 16 columns, fp32, 6-deep ring: the epilogue's
+// HBM reads are asynchronous and need no registers), w3 idle, w4-11 epilogue in two
+// groups of four (one warp per TMEM lane quarter); group g takes the boxes of parity
+// g (so with an even ring depth every stage has one consumer group and the groups
+// can never lap each other on a stage's mbarrier phase), reads X from shared memory
+// (conflict-free) and stores Y = lam (.) X - D with 128-B coalesced global stores
+// (lanes = consecutive rows).
 struct Bars3 {
     uint64_t gfull, gempty;
     uint64_t full[kStages3], empty[kStages3];
+    uint64_t xfull[kXStages], xempty[kXStages];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(384, 1)
     wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
-                     const float *X, float *Y, const float *__restrict__ lam, int n, int n_pad,
-                     int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles) {
+                     const __grid_constant__ CUtensorMap tmXb, float *Y,
+                     const float *__restrict__ lam, int n, int n_pad, int64_t N, int b, int vrow_hi,
+                     int vrow_lo, int ntiles) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -549,9 +592,11 @@ __global__ void __launch_bounds__(320, 1)
     unsigned char *Ghi = smem;                       // nslab x 8 KB (128 columns x 32 K)
     unsigned char *Glo = smem + nslab * 8192;
     unsigned char *stg = smem + kGresBytes;
-    Bars3 *bars = reinterpret_cast<Bars3 *>(stg + kStages3 * kStage3Bytes);
+    unsigned char *xst = stg + kStages3 * kStage3Bytes;
+    Bars3 *bars = reinterpret_cast<Bars3 *>(xst + kXStages * kXBoxBytes);
     auto Vhi = [&](int s) { return stg + s * kStage3Bytes; };
     auto Vlo = [&](int s) { return stg + s * kStage3Bytes + 8192; };
+    auto Xs = [&](int s) { return reinterpret_cast<float *>(xst + s * kXBoxBytes); };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nrc = n_pad / kRowChunk;
@@ -561,6 +606,10 @@ __global__ void __launch_bounds__(320, 1)
         for (int s = 0; s < kStages3; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
+        }
+        for (int s = 0; s < kXStages; ++s) {
+            mbar_init(&bars->xfull[s], 1);
+            mbar_init(&bars->xempty[s], 128);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->acc_full[a], 1);
@@ -646,45 +695,62 @@ __global__ void __launch_bounds__(320, 1)
             }
         }
         __syncwarp();
-    } else {
-        // 8 epilogue warps: lane quarter q = warp % 4 (rows), column half hf (64 of the
-        // 128 columns).  The X values of the next r-chunk are loaded before waiting for
-        // its accumulator (they do not depend on the MMA): 64 loads in flight per thread.
-        const int q = warp & 3, hf = (warp - 2) >> 2;
+    } else if (warp == 2) {
+        if (lane == 0) {
+            tc::prefetch_tmap(&tmXb);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int rc = 0; rc < nrc; ++rc) {
+                    for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb) {
+                        mbar_wait(&bars->xempty[s], ph ^ 1u);
+                        mbar_arrive_expect_tx(&bars->xfull[s], static_cast<uint32_t>(kXBoxBytes));
+                        tc::tma_load_2d(Xs(s), &tmXb, rc * kRowChunk,
+                                        tile * kTileCols + cb * kXBoxCols, &bars->xfull[s]);
+                        if (++s == kXStages) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3, grp = (warp - 4) >> 2;
+        const int r_in = q * 32 + lane;
         int a = 0;
         uint32_t aph = 0;
+        constexpr int kBoxes = kTileCols / kXBoxCols;   // X boxes per r-chunk
+        static_assert(kXStages % 2 == 0 && kBoxes % 2 == 0, "one consumer group per stage");
+        int64_t seq = 0;   // position in the X box ring (both groups follow it)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + hf * 64;
-            const int ncol = static_cast<int>(N - j0 < 64 ? N - j0 : 64);
-            float xb[64];
-            auto load = [&](int rc) {
-                const int r = rc * kRowChunk + q * 32 + lane;
-                const bool rv = rc < nrc && r < n;
-                const float *src = X + j0 * n + r;
-#pragma unroll
-                for (int e = 0; e < 64; ++e)
-                    if (rv && e < ncol) xb[e] = src[static_cast<int64_t>(e) * n];
-            };
-            load(0);
-            for (int rc = 0; rc < nrc; ++rc) {
+            for (int rc = 0; rc < nrc; ++rc, seq += kBoxes) {
                 mbar_wait(&bars->acc_full[a], aph);
                 tc::fence_after_sync();
-                const int r = rc * kRowChunk + q * 32 + lane;
-                float *dst = Y + j0 * n + r;
+                const int r = rc * kRowChunk + r_in;
                 const float lr = (lam && r < n) ? lam[r] : 1.f;   // symmetric block: Lambda X
 #pragma unroll
-                for (int sc = 0; sc < 2; ++sc) {
-                    float v[32];
-                    tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                                      static_cast<uint32_t>(a * kTileCols + hf * 64 + sc * 32),
+                for (int k = 0; k < kBoxes / 2; ++k) {
+                    const int cb = grp + 2 * k;
+                    const int64_t sq = seq + cb;
+                    const int s = static_cast<int>(sq % kXStages);
+                    mbar_wait(&bars->xfull[s], static_cast<uint32_t>((sq / kXStages) & 1));
+                    const float *xs = Xs(s);
+                    const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + cb * kXBoxCols;
+                    float *dst = Y + j0 * n + r;
+                    float v[16];
+                    tc::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                      static_cast<uint32_t>(a * kTileCols + cb * kXBoxCols),
                                   v);
                     if (r < n) {
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            if (sc * 32 + e < ncol)
-                                dst[static_cast<int64_t>(sc * 32 + e) * n] =
-                                    fmaf(lr, xb[sc * 32 + e], -v[e]);
+                        for (int e = 0; e < kXBoxCols; ++e) {
+                            if (j0 + e < N)
+                                dst[static_cast<int64_t>(e) * n] =
+                                    fmaf(lr, xs[e * kRowChunk + r_in], -v[e]);
+                        }
                     }
+                    tc::mbar_arrive(&bars->xempty[s]);
                 }
                 tc::fence_before_sync();
                 tc::mbar_arrive(&bars->acc_empty[a]);
@@ -692,7 +758,6 @@ __global__ void __launch_bounds__(320, 1)
                     a = 0;
                     aph ^= 1u;
                 }
-                load(rc + 1);
             }
         }
     }
@@ -731,7 +796,8 @@ bool make_map(CUtensorMap *m, CUtensorMapDataType dt, int esize, const void *bas
 }
 
 size_t tbuild_smem(int b) {
-    return (static_cast<size_t>((b * (b + 1) / 2 + 31) / 32 * 32) + 8 * 32 * 33 + 224 * 32) * 4;
+    return (static_cast<size_t>((b * (b + 1) / 2 + 31) / 32 * 32) + 8 * 32 * 33 + 224 * 32 + 32 * 32) *
+           4;
 }
 
 size_t smem1() {
@@ -739,7 +805,8 @@ size_t smem1() {
            sizeof(Bars1) + 1024;
 }
 size_t smem3() {
-    return kGresBytes + static_cast<size_t>(kStages3) * kStage3Bytes + sizeof(Bars3) + 1024;
+    return kGresBytes + static_cast<size_t>(kStages3) * kStage3Bytes +
+           static_cast<size_t>(kXStages) * kXBoxBytes + sizeof(Bars3) + 1024;
 }
 
 std::once_flag g_attr_once;
@@ -902,7 +969,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
 
     // ---------------- tensor maps
     const int64_t N = p.N;
-    CUtensorMap mWb, mW2b, mGb, mG2b, mV, mV2, mAs, mX, mY;
+    CUtensorMap mWb, mW2b, mGb, mG2b, mV, mV2, mAs, mX, mY, mXb, mYb;
     bool ok = make_map(&mWb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, n_pad, 2 * R, 32, b,
                        CU_TENSOR_MAP_SWIZZLE_64B) &&
               make_map(&mGb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Gt, b, 2 * N, 32, kTileCols,
@@ -911,8 +978,12 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                        kRowChunk, CU_TENSOR_MAP_SWIZZLE_64B) &&
               make_map(&mX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, X, p.n, N, 32, kTileCols,
                        CU_TENSOR_MAP_SWIZZLE_NONE) &&
-              (!Y || make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, 32, kTileCols,
-                              CU_TENSOR_MAP_SWIZZLE_NONE));
+              make_map(&mXb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, X, p.n, N, kRowChunk, kXBoxCols,
+                       CU_TENSOR_MAP_SWIZZLE_NONE) &&
+              (!Y || (make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, 32, kTileCols,
+                               CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                      make_map(&mYb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, kRowChunk, kXBoxCols,
+                               CU_TENSOR_MAP_SWIZZLE_NONE)));
     if (ok && sym)
         ok = make_map(&mW2b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, n_pad, 2 * R, 32, 2 * b,
                       CU_TENSOR_MAP_SWIZZLE_64B) &&
@@ -951,8 +1022,8 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                                                           N, ps.kw, ps.wrow,
                                                           static_cast<int>(R) + ps.wrow, ntiles);
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
-        wy_update_kernel<<<grid, 320, smem3(), stream>>>(
-            *ps.mG, *ps.mV, cur, Y, ps.lam ? lam : nullptr, static_cast<int>(p.n),
+        wy_update_kernel<<<grid, 384, smem3(), stream>>>(
+            *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.lam ? lam : nullptr, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles);
         cur = Y;
     }
