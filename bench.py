@@ -441,7 +441,7 @@ def run_hh(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="hh", choices=["hh", "reference"])
     ap.add_argument("--workload", default="C2")

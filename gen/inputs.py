@@ -72,6 +72,11 @@ def c3_spectrum(g: np.random.Generator, n: int, dtype: str = "f64", frac: float 
     return lam.astype(np_dtype(dtype))
 
 
+def sign_diag(g: np.random.Generator, n: int, dtype: str = "f64") -> np.ndarray:
+    """d in {+-1}^n, each sign fair (the diagonal D of Eq. 1)."""
+    return np.where(g.random(n) < 0.5, -1.0, 1.0).astype(np_dtype(dtype))
+
+
 def metric_diag(g: np.random.Generator, n: int, dtype: str = "f64") -> np.ndarray:
     return g.uniform(0.1, 10.0, n).astype(np_dtype(dtype))
 

@@ -95,6 +95,11 @@ typedef enum {
  *                    HH_ERR_UNSUPPORTED for fp64). */
 typedef enum { HH_ALGO_AUTO = 0, HH_ALGO_FUSED = 1, HH_ALGO_WY = 2 } hh_algo;
 
+/* Side of the diagonal D of Eq. 1 (NEXT-f1, reading R2): the paper writes
+ * Ubar = D U_h ... U_1 (D on the left) and Ubar_2 D in Result 3 (P:212,
+ * P:237, D on the right). */
+typedef enum { HH_SIDE_LEFT = 0, HH_SIDE_RIGHT = 1 } hh_side;
+
 typedef enum {
     HH_CALL_APPLY = 0,
     HH_CALL_SYM = 1,
@@ -134,6 +139,31 @@ hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
 hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda,
                        const void *X, void *Y, int64_t N, hh_dtype dtype,
                        void *workspace, size_t workspace_bytes, hh_stream_t stream);
+
+/*
+ * hh_apply_signed -- the paper's exact operator forms with the diagonal D of Eq. 1
+ * (D = diag(d), d in {+-1}^n fixes det(Ubar)):
+ *   side = HH_SIDE_LEFT :  Y = D op(Q) X      (Eq. 1, eq:thesbar)
+ *   side = HH_SIDE_RIGHT:  Y = op(Q) D X      (Result 3)
+ *   op(Q) = Q (HH_OP_N) or Q^T (HH_OP_T) as in hh_apply.  d: n values of dtype (+-1 by
+ *   the paper; any diagonal is applied as given, not validated).  D is fused as a
+ *   prologue/epilogue of the same kernels (n multiplies per column, no extra HBM
+ *   pass).  Workspace as hh_apply.  Errors as hh_apply, plus HH_ERR_INVALID_VALUE
+ *   for a bad side or a NULL d with N > 0.
+ */
+hh_status hh_apply_signed(hh_op op, hh_side side, int64_t n, int64_t h, const void *U,
+                          const void *d, const void *X, void *Y, int64_t N, hh_dtype dtype,
+                          void *workspace, size_t workspace_bytes, hh_stream_t stream);
+
+/*
+ * hh_sym_apply_signed -- Y = D Q diag(lambda) Q^T D X, the symmetric form of
+ * eq:thesbar with its diagonal D on both sides.  Workspace as
+ * hh_sym_apply (HH_CALL_SYM).
+ */
+hh_status hh_sym_apply_signed(int64_t n, int64_t h, const void *U, const void *d,
+                              const void *lambda, const void *X, void *Y, int64_t N,
+                              hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                              hh_stream_t stream);
 
 /*
  * hh_mahalanobis -- dist[j] = || D^{1/2} Q^T (P[:, ia[j]] - P[:, ib[j]]) ||^2

@@ -50,6 +50,10 @@ def lib():
         L.hh_ref_mahalanobis.argtypes = [i64, i64, p, p, p, i64, p, p, i64, p]
         for f in (L.hh_ref_apply, L.hh_ref_sym_apply, L.hh_ref_mahalanobis):
             f.restype = i32
+        L.hh_ref_apply_signed.argtypes = [i32, i32, i64, i64, p, p, p, p, i64]
+        L.hh_ref_sym_apply_signed.argtypes = [i64, i64, p, p, p, p, p, i64]
+        L.hh_ref_apply_signed.restype = i32
+        L.hh_ref_sym_apply_signed.restype = i32
         L.hh_ref_num_threads.restype = i32
         L.hh_ref_set_threads.argtypes = [i32]
         _lib = L
@@ -112,3 +116,32 @@ def mahalanobis(U, d, P, ia, ib) -> np.ndarray:
     if rc:
         raise ValueError(f"hh_ref_mahalanobis rc={rc}")
     return dist
+
+
+def apply_signed(op: int, side: int, U, d, X) -> np.ndarray:
+    """side 0: Y = D op(Q) X (Eq. 1); side 1: Y = op(Q) D X (Result 3)
+    (hh_ref.c: hh_ref_apply_signed, NEXT-f1)."""
+    X = _f64(X)
+    n = X.shape[-1]
+    U = _f64(U).reshape(-1, n) if np.size(U) else np.zeros((0, n))
+    d = _f64(d)
+    Y = np.empty_like(X)
+    rc = lib().hh_ref_apply_signed(int(op), int(side), n, U.shape[0], _ptr(U), _ptr(d), _ptr(X),
+                                   _ptr(Y), X.shape[0])
+    if rc:
+        raise ValueError(f"hh_ref_apply_signed rc={rc}")
+    return Y
+
+
+def sym_apply_signed(U, d, lam, X) -> np.ndarray:
+    """Y = D Q diag(lam) Q^T D X (hh_ref.c: hh_ref_sym_apply_signed, NEXT-f1)."""
+    X = _f64(X)
+    n = X.shape[-1]
+    U = _f64(U).reshape(-1, n)
+    d, lam = _f64(d), _f64(lam)
+    Y = np.empty_like(X)
+    rc = lib().hh_ref_sym_apply_signed(n, U.shape[0], _ptr(U), _ptr(d), _ptr(lam), _ptr(X),
+                                       _ptr(Y), X.shape[0])
+    if rc:
+        raise ValueError(f"hh_ref_sym_apply_signed rc={rc}")
+    return Y

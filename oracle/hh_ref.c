@@ -144,6 +144,65 @@ int hh_ref_mahalanobis(int64_t n, int64_t h, const double *U, const double *d,
     return bad ? 2 : 0;
 }
 
+/* NEXT-f1: the paper's exact forms with the diagonal D = diag(d) of Eq. 1.
+ * side 0 (left, Eq. 1 / eq:thesbar):   Y = D op(Q) X
+ * side 1 (right, Result 3):  Y = op(Q) D X
+ * Written out literally: scale, then the same reflector-by-reflector apply. */
+int hh_ref_apply_signed(int op, int side, int64_t n, int64_t h, const double *U,
+                        const double *d, const double *X, double *Y, int64_t N) {
+    if ((op != 0 && op != 1) || (side != 0 && side != 1) || n < 1 || h < 0 || N < 0) return 1;
+    int bad = 0;
+#pragma omp parallel
+    {
+        double *x = (double *)malloc(sizeof(double) * (size_t)n);
+        if (!x) {
+#pragma omp atomic write
+            bad = 1;
+        } else {
+#pragma omp for schedule(static)
+            for (int64_t j = 0; j < N; ++j) {
+                memcpy(x, X + j * n, sizeof(double) * (size_t)n);
+                if (side == 1)
+                    for (int64_t r = 0; r < n; ++r) x[r] *= d[r];
+                apply_one(op, n, h, U, x);
+                if (side == 0)
+                    for (int64_t r = 0; r < n; ++r) x[r] *= d[r];
+                memcpy(Y + j * n, x, sizeof(double) * (size_t)n);
+            }
+            free(x);
+        }
+    }
+    return bad ? 2 : 0;
+}
+
+/* S-bar X = D Q diag(lambda) Q^T D X  (eq:thesbar, D on both sides). */
+int hh_ref_sym_apply_signed(int64_t n, int64_t h, const double *U, const double *d,
+                            const double *lam, const double *X, double *Y, int64_t N) {
+    if (n < 1 || h < 0 || N < 0) return 1;
+    int bad = 0;
+#pragma omp parallel
+    {
+        double *x = (double *)malloc(sizeof(double) * (size_t)n);
+        if (!x) {
+#pragma omp atomic write
+            bad = 1;
+        } else {
+#pragma omp for schedule(static)
+            for (int64_t j = 0; j < N; ++j) {
+                memcpy(x, X + j * n, sizeof(double) * (size_t)n);
+                for (int64_t r = 0; r < n; ++r) x[r] *= d[r];
+                apply_one(1, n, h, U, x);
+                for (int64_t r = 0; r < n; ++r) x[r] *= lam[r];
+                apply_one(0, n, h, U, x);
+                for (int64_t r = 0; r < n; ++r) x[r] *= d[r];
+                memcpy(Y + j * n, x, sizeof(double) * (size_t)n);
+            }
+            free(x);
+        }
+    }
+    return bad ? 2 : 0;
+}
+
 int hh_ref_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -192,15 +192,18 @@ hh_status hh_set_algo(hh_algo algo) {
 
 hh_algo hh_get_algo(void) { return static_cast<hh_algo>(t_algo); }
 
-hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
-                   int64_t N, hh_dtype dtype, void *workspace, size_t workspace_bytes,
-                   hh_stream_t stream) {
+static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
+                            void *Y, int64_t N, hh_dtype dtype, void *workspace,
+                            size_t workspace_bytes, hh_stream_t stream, const void *dsign,
+                            int dside) {
     if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
     hh_status st = check_common(n, h, U, N, dtype);
     if (st != HH_OK) return st;
     if (N == 0) return HH_OK;
     if (!X || !Y) return HH_ERR_INVALID_VALUE;
     if (!aligned16(X) || !aligned16(Y)) return HH_ERR_UNSUPPORTED;
+    if (dside && !dsign) return HH_ERR_INVALID_VALUE;
+    if (dside && !aligned16(dsign)) return HH_ERR_UNSUPPORTED;
     if (h > 0 && use_wy(dtype, n, h, N, t_algo)) {
         const WyPlan p = wy_plan(op == HH_OP_T ? WY_APPLY_T : WY_APPLY_N, n, h, N);
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
@@ -210,7 +213,8 @@ hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
             LaunchInfo info;
             cudaError_t e = launch_wy(p, static_cast<const float *>(U), nullptr,
                                       static_cast<const float *>(X), static_cast<float *>(Y),
-                                      workspace, stream, &info);
+                                      workspace, stream, &info, -1,
+                                      static_cast<const float *>(dsign), dside);
             if (info.variant) {
                 t_last = info;
                 t_has_last = true;
@@ -227,17 +231,36 @@ hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
     a.h = h;
     a.N = N;
     a.mode = op == HH_OP_N ? MODE_APPLY_N : MODE_APPLY_T;
+    a.dsign = dsign;
+    a.dside = dside;
     return run_fused(a, dtype, stream);
 }
 
-hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda, const void *X,
-                       void *Y, int64_t N, hh_dtype dtype, void *workspace,
-                       size_t workspace_bytes, hh_stream_t stream) {
+hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
+                   int64_t N, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                   hh_stream_t stream) {
+    return apply_impl(op, n, h, U, X, Y, N, dtype, workspace, workspace_bytes, stream, nullptr, 0);
+}
+
+hh_status hh_apply_signed(hh_op op, hh_side side, int64_t n, int64_t h, const void *U,
+                          const void *d, const void *X, void *Y, int64_t N, hh_dtype dtype,
+                          void *workspace, size_t workspace_bytes, hh_stream_t stream) {
+    if (side != HH_SIDE_LEFT && side != HH_SIDE_RIGHT) return HH_ERR_INVALID_VALUE;
+    if (N > 0 && !d) return HH_ERR_INVALID_VALUE;
+    return apply_impl(op, n, h, U, X, Y, N, dtype, workspace, workspace_bytes, stream, d,
+                      side == HH_SIDE_RIGHT ? 1 : 2);
+}
+
+
+static hh_status sym_impl(int64_t n, int64_t h, const void *U, const void *lambda, const void *X,
+                          void *Y, int64_t N, hh_dtype dtype, void *workspace,
+                          size_t workspace_bytes, hh_stream_t stream, const void *dsign) {
     hh_status st = check_common(n, h, U, N, dtype);
     if (st != HH_OK) return st;
     if (N == 0) return HH_OK;
     if (!X || !Y || !lambda) return HH_ERR_INVALID_VALUE;
     if (!aligned16(X) || !aligned16(Y) || !aligned16(lambda)) return HH_ERR_UNSUPPORTED;
+    if (dsign && !aligned16(dsign)) return HH_ERR_UNSUPPORTED;
     if (h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
         const WyPlan p = wy_plan(WY_SYM, n, h, N);
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
@@ -248,7 +271,8 @@ hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda, 
             cudaError_t e = launch_wy(p, static_cast<const float *>(U),
                                       static_cast<const float *>(lambda),
                                       static_cast<const float *>(X), static_cast<float *>(Y),
-                                      workspace, stream, &info);
+                                      workspace, stream, &info, -1,
+                                      static_cast<const float *>(dsign), dsign ? 3 : 0);
             if (info.variant) {
                 t_last = info;
                 t_has_last = true;
@@ -265,8 +289,25 @@ hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda, 
     a.h = h;
     a.N = N;
     a.mode = MODE_SYM;
+    a.dsign = dsign;
+    a.dside = dsign ? 3 : 0;
     return run_fused(a, dtype, stream);
 }
+
+hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda, const void *X,
+                       void *Y, int64_t N, hh_dtype dtype, void *workspace,
+                       size_t workspace_bytes, hh_stream_t stream) {
+    return sym_impl(n, h, U, lambda, X, Y, N, dtype, workspace, workspace_bytes, stream, nullptr);
+}
+
+hh_status hh_sym_apply_signed(int64_t n, int64_t h, const void *U, const void *d,
+                              const void *lambda, const void *X, void *Y, int64_t N,
+                              hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                              hh_stream_t stream) {
+    if (N > 0 && !d) return HH_ERR_INVALID_VALUE;
+    return sym_impl(n, h, U, lambda, X, Y, N, dtype, workspace, workspace_bytes, stream, d);
+}
+
 
 hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, const void *P,
                          int64_t M, const int32_t *ia, const int32_t *ib, int64_t npairs,

@@ -369,6 +369,19 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
             }
         }
 
+        // NEXT-f1 right factor (Y = Q D X): x <- D x before the first reflector
+        if (tv && (a.dside & 1)) {
+            const V *dg = reinterpret_cast<const V *>(a.dsign);
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                if (valid_k(k)) {
+                    const V dv = ldg_v(dg + gt + TPC * k);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) vmul(x[c][k], dv);
+                }
+            }
+        }
+
         // ---- 2. reflector passes
         if (nc == 1) {
             if (!u_ready) {
@@ -454,6 +467,17 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
                             const V dv = ldg_v(vecg + gt + TPC * k);
 #pragma unroll
                             for (int c = 0; c < C; ++c) vmulsqrt(x[c][k], dv);
+                        }
+                    }
+                }
+                if (a.dside & 2) {   // NEXT-f1 left factor (Y = D Q X)
+                    const V *dg = reinterpret_cast<const V *>(a.dsign);
+#pragma unroll
+                    for (int k = 0; k < CH; ++k) {
+                        if (valid_k(k)) {
+                            const V dv = ldg_v(dg + gt + TPC * k);
+#pragma unroll
+                            for (int c = 0; c < C; ++c) vmul(x[c][k], dv);
                         }
                     }
                 }

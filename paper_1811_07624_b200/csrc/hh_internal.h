@@ -27,6 +27,8 @@ struct FusedArgs {
     int nchunks;        // ceil(h / R); 1 = U resident for the whole kernel
     int stage_x;        // 1 = stage column tiles through shared memory (bulk copy)
     int nbatches;       // batches per unit (uniform over the grid)
+    const void *dsign;  // NEXT-f1: the diagonal D of Eq. 1 (n values) or NULL
+    int dside;          // bit 0: x <- D x before the reflectors, bit 1: y <- D y after
 };
 
 struct LaunchInfo {
@@ -66,14 +68,18 @@ struct WyPlan {
     int b = 0, nblk = 0, h_pad = 0, extra = 0, nsplit = 0;
     int64_t n_pad = 0;
     size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_v = 0, off_v2 = 0,
-           off_asym = 0, off_vf = 0, off_vpf = 0, off_pp = 0, off_p = 0, off_m = 0, off_gt = 0;
+           off_asym = 0, off_vf = 0, off_vpf = 0, off_pp = 0, off_p = 0, off_m = 0, off_gt = 0,
+           off_ld = 0;
     size_t bytes = 0;
 };
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N);
 bool wy_supported(int64_t n, int64_t h, int64_t N);
 // Y = Q X / Q^T X / Q diag(lam) Q^T X by the compact-WY block program (fp32 in/out).
 // debug_stop_blocks >= 0: run the preparation and only the first projection (test hook).
+// dsign/dside: optional diagonal D (bit 0: right factor, D applied first; bit 1: left
+// factor, D applied last), fused into the first project/update and the last update.
 cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const float *X, float *Y,
-                      void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks = -1);
+                      void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks = -1,
+                      const float *dsign = nullptr, int dside = 0);
 
 }  // namespace hh

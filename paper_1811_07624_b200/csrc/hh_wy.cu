@@ -100,6 +100,14 @@ __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h
     }
 }
 
+// out[r] = a[r] * b[r] (the symmetric block's pre-scale Lambda D for a two-sided D)
+__global__ void wy_vmul_kernel(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
+                               float *__restrict__ out) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[r] = a[r] * b[r];
+}
+
 // Sp[blk][split][l][m] = sum_{r in split} w_l[r] wt[r] w_m[r] over 128-row splits
 // of n_pad (wt = 1 or lambda), blocks blk0.., upper 64x64 tiles only unless `full`
 // (the reduction over splits is done in fixed order by wy_gram_reduce_kernel:
@@ -371,7 +379,7 @@ struct Bars1 {
 __global__ void __launch_bounds__(480, 1)
     wy_project_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       uint16_t *__restrict__ Gt, int n, int64_t N, int b, int wrow_hi, int wrow_lo,
-                      int ntiles) {
+                      int ntiles, const float *__restrict__ dscale) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -492,6 +500,19 @@ __global__ void __launch_bounds__(480, 1)
                 float4 v[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) v[q] = raw[ct + 256 * q];
+                if (dscale) {   // NEXT-f1 right factor: project D X
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int r = ks * 32 + ((ct + 256 * q) & 7) * 4;
+                        if (r < n) {
+                            const float4 dv = *reinterpret_cast<const float4 *>(dscale + r);
+                            v[q].x *= dv.x;
+                            v[q].y *= dv.y;
+                            v[q].z *= dv.z;
+                            v[q].w *= dv.w;
+                        }
+                    }
+                }
                 mbar_wait(&bars->cempty[cs], cph ^ 1u);
                 unsigned char *xh = Xhi(cs), *xl = Xlo(cs);
 #pragma unroll
@@ -583,8 +604,8 @@ struct Bars3 {
 __global__ void __launch_bounds__(384, 1)
     wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmXb, float *Y,
-                     const float *__restrict__ lam, int n, int n_pad, int64_t N, int b, int vrow_hi,
-                     int vrow_lo, int ntiles) {
+                     const float *__restrict__ lam, const float *__restrict__ post, int n,
+                     int n_pad, int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -728,7 +749,10 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_wait(&bars->acc_full[a], aph);
                 tc::fence_after_sync();
                 const int r = rc * kRowChunk + r_in;
-                const float lr = (lam && r < n) ? lam[r] : 1.f;   // symmetric block: Lambda X
+                // pre-scale of X (Lambda for the symmetric block, D for a right factor D)
+                // and post-scale of the result (a left factor D, NEXT-f1)
+                const float lr = (lam && r < n) ? lam[r] : 1.f;
+                const float pr = (post && r < n) ? post[r] : 1.f;
 #pragma unroll
                 for (int k = 0; k < kBoxes / 2; ++k) {
                     const int cb = grp + 2 * k;
@@ -747,7 +771,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int e = 0; e < kXBoxCols; ++e) {
                             if (j0 + e < N)
                                 dst[static_cast<int64_t>(e) * n] =
-                                    fmaf(lr, xs[e * kRowChunk + r_in], -v[e]);
+                                    pr * fmaf(lr, xs[e * kRowChunk + r_in], -v[e]);
                         }
                     }
                     tc::mbar_arrive(&bars->xempty[s]);
@@ -850,6 +874,7 @@ WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
         p.off_pp = take(static_cast<size_t>(p.nsplit) * bb);
         p.off_p = take(bb);
         p.off_m = take(bb);
+        p.off_ld = take(static_cast<size_t>(n) * 4);
     }
     const int kmax = kind == WY_SYM ? 2 * p.b : p.b;
     p.off_gt = take(static_cast<size_t>(std::max<int64_t>(N, 1)) * kmax * 2 * 2);
@@ -871,12 +896,16 @@ struct Pass {
     const CUtensorMap *mW, *mG, *mV;
     int vrow_hi, vrow_lo;
     bool lam;            // symmetric block: Lambda X in the update epilogue
+    const float *dscale = nullptr;   // project D X (first pass, right factor D)
+    const float *pre = nullptr;      // update pre-scale of X (Lambda, D, or Lambda D)
+    const float *post = nullptr;     // update post-scale (last pass, left factor D)
 };
 
 }  // namespace
 
 cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const float *X, float *Y,
-                      void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks) {
+                      void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks,
+                      const float *dsign, int dside) {
     if (!encoder()) return cudaErrorNotSupported;
     std::call_once(g_attr_once, []() {
         g_attr_err = cudaFuncSetAttribute(wy_project_kernel,
@@ -999,8 +1028,9 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     Pass prog[2 * 64];
     int np = 0;
     auto blockpass = [&](int k, const CUtensorMap *mv) {
-        prog[np++] = Pass{k * b, b, &mWb, &mGb, mv, static_cast<int>(k * n_pad),
-                          static_cast<int>((m + k) * n_pad), false};
+        Pass ps{k * b, b, &mWb, &mGb, mv, static_cast<int>(k * n_pad),
+                static_cast<int>((m + k) * n_pad), false};
+        prog[np++] = ps;
     };
     if (p.kind == WY_APPLY_N) {
         for (int k = m - 1; k >= 0; --k) blockpass(k, &mV);          // Q X: last block first
@@ -1008,9 +1038,27 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         for (int k = 0; k < m; ++k) blockpass(k, &mV);               // Q^T X: first block first
     } else {
         for (int k = 0; k < m - 1; ++k) blockpass(k, &mV);           // Q_k^T, k < m-1
-        prog[np++] = Pass{(m - 1) * b, 2 * b, &mW2b, &mG2b, &mAs, 0, static_cast<int>(n_pad), true};
+        Pass ps{(m - 1) * b, 2 * b, &mW2b, &mG2b, &mAs, 0, static_cast<int>(n_pad), true};
+        ps.pre = lam;
+        prog[np++] = ps;
         for (int k = m - 2; k >= 0; --k) blockpass(k, &mV2);         // Q_k, k < m-1
     }
+
+    // NEXT-f1: the diagonal D as a prologue of the first pass (right factor) and an
+    // epilogue of the last pass (left factor); no extra pass over X.
+    if (dsign && (dside & 1)) {
+        Pass &f = prog[0];
+        f.dscale = dsign;
+        if (f.pre) {   // first pass is the symmetric block: pre-scale Lambda D
+            float *ld = F(p.off_ld);
+            wy_vmul_kernel<<<std::max(1, static_cast<int>((p.n + 255) / 256)), 256, 0, stream>>>(
+                f.pre, dsign, p.n, ld);
+            f.pre = ld;
+        } else {
+            f.pre = dsign;
+        }
+    }
+    if (dsign && (dside & 2)) prog[np - 1].post = dsign;
 
     const int ntiles = static_cast<int>((N + kTileCols - 1) / kTileCols);
     const int grid = std::max(1, std::min(ntiles, sms));
@@ -1020,10 +1068,11 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
         wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, *ps.mW, Gt, static_cast<int>(p.n),
                                                           N, ps.kw, ps.wrow,
-                                                          static_cast<int>(R) + ps.wrow, ntiles);
+                                                          static_cast<int>(R) + ps.wrow, ntiles,
+                                                          ps.dscale);
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
         wy_update_kernel<<<grid, 384, smem3(), stream>>>(
-            *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.lam ? lam : nullptr, static_cast<int>(p.n),
+            *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles);
         cur = Y;
     }

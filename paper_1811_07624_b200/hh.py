@@ -26,6 +26,7 @@ HH_F32, HH_F64 = 0, 1
 HH_OP_N, HH_OP_T = 0, 1
 HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST = range(4)
 HH_ALGO_AUTO, HH_ALGO_FUSED, HH_ALGO_WY = range(3)
+HH_SIDE_LEFT, HH_SIDE_RIGHT = range(2)
 
 _DT = {torch.float32: HH_F32, torch.float64: HH_F64}
 
@@ -53,6 +54,10 @@ def lib() -> ctypes.CDLL:
         L.hh_mahalanobis.argtypes = [i64, i64, p, p, p, i64, p, p, i64, p, i32, p, sz, p]
         L.hh_apply_host.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
         L.hh_workspace_bytes.argtypes = [i32, i64, i64, i64, i64, i32, ctypes.POINTER(sz)]
+        L.hh_apply_signed.argtypes = [i32, i32, i64, i64, p, p, p, p, i64, i32, p, sz, p]
+        L.hh_sym_apply_signed.argtypes = [i64, i64, p, p, p, p, p, i64, i32, p, sz, p]
+        L.hh_apply_signed.restype = i32
+        L.hh_sym_apply_signed.restype = i32
         L.hh_set_algo.argtypes = [i32]
         L.hh_set_algo.restype = i32
         L.hh_get_algo.restype = i32
@@ -213,6 +218,54 @@ def hh_sym_apply(U: torch.Tensor, lam: torch.Tensor, X: torch.Tensor,
                             _dtype(X), _ptr(workspace) if wsb else None,
                             workspace.numel() if wsb else 0, _stream(stream))
     _check(st, "hh_sym_apply")
+    return Y
+
+
+def hh_apply_signed(op: int, side: int, U: torch.Tensor, d: torch.Tensor, X: torch.Tensor,
+                    Y: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    """Y = D op(Q) X (side HH_SIDE_LEFT, Eq. 1) or op(Q) D X (HH_SIDE_RIGHT, Result 3)
+    (hh.h: hh_apply_signed)."""
+    _dev(X, "X")
+    _dev(d, "d")
+    N, n = X.shape
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    if Y is None:
+        Y = torch.empty_like(X)
+    _dev(Y, "Y")
+    wsb = hh_workspace_bytes(HH_CALL_APPLY, n, h, N, 0, X.dtype) if N else 0
+    if wsb and (workspace is None or workspace.numel() < wsb):
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
+    st = lib().hh_apply_signed(int(op), int(side), n, h, _ptr(U) if h else None, _ptr(d), _ptr(X),
+                               _ptr(Y), N, _dtype(X), _ptr(workspace) if wsb else None,
+                               workspace.numel() if wsb else 0, _stream(stream))
+    _check(st, "hh_apply_signed")
+    return Y
+
+
+def hh_sym_apply_signed(U: torch.Tensor, d: torch.Tensor, lam: torch.Tensor, X: torch.Tensor,
+                        Y: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                        stream=None) -> torch.Tensor:
+    """Y = D Q diag(lam) Q^T D X (hh.h: hh_sym_apply_signed, eq:thesbar)."""
+    _dev(X, "X")
+    _dev(d, "d")
+    _dev(lam, "lambda")
+    N, n = X.shape
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    if Y is None:
+        Y = torch.empty_like(X)
+    _dev(Y, "Y")
+    wsb = hh_workspace_bytes(HH_CALL_SYM, n, h, N, 0, X.dtype) if N else 0
+    if wsb and (workspace is None or workspace.numel() < wsb):
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
+    st = lib().hh_sym_apply_signed(n, h, _ptr(U) if h else None, _ptr(d), _ptr(lam), _ptr(X),
+                                   _ptr(Y), N, _dtype(X), _ptr(workspace) if wsb else None,
+                                   workspace.numel() if wsb else 0, _stream(stream))
+    _check(st, "hh_sym_apply_signed")
     return Y
 
 

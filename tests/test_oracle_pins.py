@@ -354,3 +354,43 @@ def test_threads_control():
     oracle.set_threads(1)
     assert oracle.num_threads() == 1
     oracle.set_threads(t)
+
+
+
+# --------------------------------------------------------------------------- NEXT-f1: D
+@pytest.mark.parametrize("n,h", [(6, 3), (16, 9), (64, 6)])
+def test_signed_dense_bruteforce(n, h):
+    """Ubar = D U_h...U_1 (Eq. 1) and Ubar_2 D (Result 3) against the
+    explicit dense products, both ops; S-bar = D Q Lambda Q^T D (eq:thesbar)."""
+    g = gi.rng(905, n, h)
+    U = unit_rows(g, h, n)
+    X = g.standard_normal((7, n))
+    d = gi.sign_diag(g, n)
+    D = np.diag(d)
+    Q = dense_Q(U)
+    for op, Qop in ((0, Q), (1, Q.T)):
+        assert rel(oracle.apply_signed(op, 0, U, d, X), (D @ Qop @ X.T).T) < 1e-13
+        assert rel(oracle.apply_signed(op, 1, U, d, X), (Qop @ D @ X.T).T) < 1e-13
+    lam = g.standard_normal(n)
+    S = D @ Q @ np.diag(lam) @ Q.T @ D
+    assert rel(oracle.sym_apply_signed(U, d, lam, X), (S @ X.T).T) < 1e-13
+
+
+def test_signed_determinant_and_identity():
+    """det(D U_h...U_1) = det(D) (-1)^h ("we use the diagonal D to ensure that the
+    choice of h does not fix the determinant"); D = I reduces to the unsigned apply; the
+    symmetric form keeps the spectrum (D orthonormal)."""
+    n, h = 8, 3
+    g = gi.rng(906)
+    U = unit_rows(g, h, n)
+    d = np.array([1, -1, 1, 1, -1, 1, 1, -1], dtype=np.float64)
+    M = oracle.apply_signed(1, 0, U, d, np.eye(n)).T        # columns = images of e_i
+    assert abs(np.linalg.det(M) - np.prod(d) * (-1) ** h) < 1e-12
+    X = g.standard_normal((5, n))
+    ones = np.ones(n)
+    for op in (0, 1):
+        for side in (0, 1):
+            assert np.array_equal(oracle.apply_signed(op, side, U, ones, X), oracle.apply(op, U, X))
+    lam = g.standard_normal(n)
+    S = oracle.sym_apply_signed(U, d, lam, np.eye(n)).T
+    assert np.allclose(np.linalg.eigvalsh((S + S.T) / 2), np.sort(lam), atol=1e-13)
