@@ -104,7 +104,8 @@ typedef enum {
     HH_CALL_APPLY = 0,
     HH_CALL_SYM = 1,
     HH_CALL_MAHALANOBIS = 2,
-    HH_CALL_APPLY_HOST = 3
+    HH_CALL_APPLY_HOST = 3,
+    HH_CALL_KNN = 4
 } hh_call;
 
 /*
@@ -187,6 +188,25 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d,
                          hh_stream_t stream);
 
 /*
+ * hh_knn -- test-time k nearest neighbours under the learned metric (NEXT-f3):
+ *   "perform the transformation x <- L x before running the k-NN",
+ *   L = diag(sqrt d) Q^T (reading R4), so d_S(q, r) = ||L x_q - L x_r||^2.
+ *   For every query q (column of P_query, n x M_query column-major) return the k
+ *   references (columns of P_ref, n x M_ref) with the smallest d_S, ascending, ties by
+ *   the smaller reference index: nn_idx[q*k + t] (int32), nn_dist[q*k + t] (dtype).
+ *   Each point is transformed once (fused kernel), then distances
+ *   ||z_q||^2 + ||z_r||^2 - 2 z_q.z_r run on the tcgen05 tensor cores (bf16x3 split,
+ *   fp32 accumulation) with a fused per-query top-k.
+ *   v1 limits (HH_ERR_UNSUPPORTED otherwise): fp32, n % 4 == 0, n <= 256, 1 <= k <= 16.
+ *   HH_ERR_INVALID_VALUE: M_ref < k, NULL operands.  workspace (DEVICE) >=
+ *   hh_workspace_bytes(HH_CALL_KNN, n, h, M_ref, M_query, dtype).
+ */
+hh_status hh_knn(int64_t n, int64_t h, const void *U, const void *d, const void *P_ref,
+                 int64_t M_ref, const void *P_query, int64_t M_query, int k, int32_t *nn_idx,
+                 void *nn_dist, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                 hh_stream_t stream);
+
+/*
  * hh_apply_host -- hh_apply with HOST U, X, Y (end-to-end path).
  *   Streams column chunks host -> device, applies Q or Q^T with the same fused
  *   kernel, and streams them back, overlapping H2D copy, compute and D2H copy on
@@ -210,7 +230,8 @@ hh_algo hh_get_algo(void);
 
 /*
  * hh_workspace_bytes -- scratch bytes the call needs (cuBLAS bufferSize style).
- *   N_or_M: N for apply/sym/apply_host, M for Mahalanobis.  Writes *bytes.
+ *   N_or_M: N for apply/sym/apply_host, M for Mahalanobis, M_ref for kNN (with
+ *   npairs = M_query).  Writes *bytes.
  *   HH_CALL_APPLY: the compact-WY scratch when this thread's hh_algo selection
  *   picks K5 for (n, h, N, dtype) (packed W, T, V = W T and one G block), else 0.
  *   HH_CALL_SYM: the compact-WY scratch when the symmetric call picks the tensor-core

@@ -53,6 +53,8 @@ def lib():
         L.hh_ref_apply_signed.argtypes = [i32, i32, i64, i64, p, p, p, p, i64]
         L.hh_ref_sym_apply_signed.argtypes = [i64, i64, p, p, p, p, p, i64]
         L.hh_ref_apply_signed.restype = i32
+        L.hh_ref_knn.argtypes = [i64, i64, p, p, p, i64, p, i64, i32, p, p]
+        L.hh_ref_knn.restype = i32
         L.hh_ref_sym_apply_signed.restype = i32
         L.hh_ref_num_threads.restype = i32
         L.hh_ref_set_threads.argtypes = [i32]
@@ -145,3 +147,20 @@ def sym_apply_signed(U, d, lam, X) -> np.ndarray:
     if rc:
         raise ValueError(f"hh_ref_sym_apply_signed rc={rc}")
     return Y
+
+
+def knn(U, d, P_ref, P_query, k: int):
+    """(idx int32 (Mq, k), dist fp64 (Mq, k)): the k smallest d_S(q, r), ascending by
+    (distance, reference index) (hh_ref.c: hh_ref_knn, NEXT-f3)."""
+    Pr, Pq = _f64(P_ref), _f64(P_query)
+    n = Pr.shape[-1]
+    U = _f64(U).reshape(-1, n) if np.size(U) else np.zeros((0, n))
+    d = _f64(d)
+    Mq = Pq.shape[0]
+    idx = np.empty((Mq, k), dtype=np.int32)
+    dist = np.empty((Mq, k), dtype=np.float64)
+    rc = lib().hh_ref_knn(n, U.shape[0], _ptr(U), _ptr(d), _ptr(Pr), Pr.shape[0], _ptr(Pq), Mq,
+                          int(k), _ptr(idx), _ptr(dist))
+    if rc:
+        raise ValueError(f"hh_ref_knn rc={rc}")
+    return idx, dist

@@ -203,6 +203,55 @@ int hh_ref_sym_apply_signed(int64_t n, int64_t h, const double *U, const double 
     return bad ? 2 : 0;
 }
 
+/* NEXT-f3: k nearest references of each query under d_S:
+ * d_S(q, r) = || D^{1/2} Q^T (x_q - x_r) ||^2, the literal per-pair form of
+ * hh_ref_mahalanobis for every (query, reference) pair, then the k smallest in
+ * ascending (distance, reference index) order. */
+int hh_ref_knn(int64_t n, int64_t h, const double *U, const double *d, const double *Pr,
+               int64_t Mr, const double *Pq, int64_t Mq, int k, int32_t *idx, double *dist) {
+    if (n < 1 || h < 0 || Mr < k || Mq < 0 || k < 1) return 1;
+    int bad = 0;
+#pragma omp parallel
+    {
+        double *z = (double *)malloc(sizeof(double) * (size_t)n);
+        double *bd = (double *)malloc(sizeof(double) * (size_t)k);
+        int32_t *bi = (int32_t *)malloc(sizeof(int32_t) * (size_t)k);
+        if (!z || !bd || !bi) {
+#pragma omp atomic write
+            bad = 1;
+        } else {
+#pragma omp for schedule(dynamic, 4)
+            for (int64_t q = 0; q < Mq; ++q) {
+                int cnt = 0;
+                for (int64_t r = 0; r < Mr; ++r) {
+                    for (int64_t e = 0; e < n; ++e) z[e] = Pq[q * n + e] - Pr[r * n + e];
+                    apply_one(1, n, h, U, z);
+                    double s = 0.0;
+                    for (int64_t e = 0; e < n; ++e) s += d[e] * (z[e] * z[e]);
+                    if (cnt == k && !(s < bd[k - 1])) continue;   /* ties keep the earlier r */
+                    int pos = cnt < k ? cnt : k - 1;
+                    while (pos > 0 && bd[pos - 1] > s) {
+                        bd[pos] = bd[pos - 1];
+                        bi[pos] = bi[pos - 1];
+                        --pos;
+                    }
+                    bd[pos] = s;
+                    bi[pos] = (int32_t)r;
+                    if (cnt < k) ++cnt;
+                }
+                for (int t = 0; t < k; ++t) {
+                    idx[q * k + t] = bi[t];
+                    dist[q * k + t] = bd[t];
+                }
+            }
+        }
+        free(z);
+        free(bd);
+        free(bi);
+    }
+    return bad ? 2 : 0;
+}
+
 int hh_ref_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -172,6 +172,9 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
         case HH_CALL_MAHALANOBIS:
             *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype));
             return HH_OK;
+        case HH_CALL_KNN:   /* N_or_M = M_ref, npairs = M_query; k = h is not needed: max */
+            *bytes = knn_plan(n, N_or_M, npairs, 16, device_attr().sm_count).bytes;
+            return HH_OK;
         case HH_CALL_APPLY_HOST: {
             const size_t ub = round256(static_cast<size_t>(n) * static_cast<size_t>(h) * elem(dtype));
             const int64_t cols = host_chunk_cols(n, std::max<int64_t>(N_or_M, 1), dtype);
@@ -362,6 +365,34 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
     a.N = npairs;
     a.mode = MODE_PAIR;
     return run_fused(a, dtype, stream);
+}
+
+hh_status hh_knn(int64_t n, int64_t h, const void *U, const void *d, const void *P_ref,
+                 int64_t M_ref, const void *P_query, int64_t M_query, int k, int32_t *nn_idx,
+                 void *nn_dist, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                 hh_stream_t stream) {
+    if (dtype != HH_F32 && dtype != HH_F64) return HH_ERR_INVALID_VALUE;
+    if (n < 1 || h < 0 || M_ref < 0 || M_query < 0 || k < 1) return HH_ERR_INVALID_VALUE;
+    if (M_query == 0) return HH_OK;
+    if (M_ref < k) return HH_ERR_INVALID_VALUE;
+    if ((h > 0 && !U) || !d || !P_ref || !P_query || !nn_idx || !nn_dist)
+        return HH_ERR_INVALID_VALUE;
+    if (dtype != HH_F32 || !knn_supported(n, M_ref, M_query, k)) return HH_ERR_UNSUPPORTED;
+    if (!aligned16(d) || !aligned16(P_ref) || !aligned16(P_query) || (h > 0 && !aligned16(U)))
+        return HH_ERR_UNSUPPORTED;
+    const KnnPlan p = knn_plan(n, M_ref, M_query, k, device_attr().sm_count);
+    if (!workspace || workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+    LaunchInfo info;
+    cudaError_t e = launch_knn(p, static_cast<const float *>(U), h, static_cast<const float *>(d),
+                               static_cast<const float *>(P_ref),
+                               static_cast<const float *>(P_query), nn_idx,
+                               static_cast<float *>(nn_dist), workspace, stream, &info);
+    if (info.variant) {
+        t_last = info;
+        t_has_last = true;
+    }
+    return map_err(e);
 }
 
 hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host, const void *X_host,

@@ -83,3 +83,21 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                       const float *dsign = nullptr, int dside = 0);
 
 }  // namespace hh
+
+namespace hh {
+
+// ---- NEXT-f3: test-time k-NN under the learned metric (hh_knn.cu) ----
+struct KnnPlan {
+    int64_t n = 0, Mr = 0, Mq = 0;
+    int k = 0, n_pad = 0, splits = 0, tiles_per_split = 0;
+    size_t off_zr = 0, off_zq = 0, off_zrb = 0, off_zqb = 0, off_rn = 0, off_qn = 0, off_pd = 0,
+           off_pi = 0;
+    size_t bytes = 0;
+};
+KnnPlan knn_plan(int64_t n, int64_t Mr, int64_t Mq, int k, int sm_count);
+bool knn_supported(int64_t n, int64_t Mr, int64_t Mq, int k);
+cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float *d,
+                       const float *Pr, const float *Pq, int32_t *nn_idx, float *nn_dist, void *ws,
+                       cudaStream_t stream, LaunchInfo *info);
+
+}  // namespace hh

@@ -1,0 +1,415 @@
+// hh_knn.cu -- NEXT-f3: test-time k-nearest neighbours under the learned metric.
+//
+// The paper's deployment of the path: with S = Q diag(d) Q^T
+// (reading R4) and L = diag(sqrt d) Q^T, "perform the transformation x <- L x before
+// running the k-NN"; each point is transformed once (4nh operations instead of 2n^2)
+// and neighbours are found by Euclidean distance between transformed points:
+//
+//   d_S(q, r) = || z_q - z_r ||^2 = ||z_q||^2 + ||z_r||^2 - 2 z_q . z_r,   z = L x.
+//
+// Steps (all on the GPU):
+//   1. K3a (hh_fused.cu, MODE_TRANSFORM): Z = diag(sqrt d) Q^T P for queries and
+//      references (one HBM read + write per point).
+//   2. knn_pack_kernel: bf16 hi/lo split of Z (K padded to a multiple of 32) and the
+//      fp32 squared norms.
+//   3. knn_topk_kernel (tcgen05): a CTA owns 128 queries (resident in SMEM, MMA M) and
+//      streams a range of reference tiles (128 refs, MMA N) through a TMA ring; the
+//      dot products z_q . z_r accumulate in TMEM (bf16x3, fp32 accumulation); the
+//      epilogue turns them into distances and keeps a per-query sorted top-k list in
+//      registers (ties: smaller reference index first).
+//   4. knn_merge_kernel: merges the per-split lists (k-way, same tie rule).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <mutex>
+
+#include "hh_internal.h"
+#include "hh_tc.cuh"
+
+namespace hh {
+
+namespace {
+
+constexpr int kQ = 128;           // queries per CTA (MMA M)
+constexpr int kRT = 128;          // references per tile (MMA N)
+constexpr int kKS = 4;            // reference slab ring depth
+constexpr int kKnnMaxK = 16;      // largest k
+constexpr int kKnnMaxNpad = 256;  // resident query tile: n_pad x 128 x 4 B <= 128 KB
+
+size_t al(size_t x) { return (x + 1023) & ~static_cast<size_t>(1023); }
+
+__device__ __forceinline__ uint16_t f2bf(float x) {
+    uint16_t b;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(b) : "f"(x));
+    return b;
+}
+__device__ __forceinline__ float bf2f(uint16_t b) {
+    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+// one warp per point: Zb[hi: row][0..n_pad), Zb[lo: M + row][..] and nrm[row] = ||z||^2
+__global__ void knn_pack_kernel(const float *__restrict__ Z, int64_t M, int n, int n_pad,
+                                uint16_t *__restrict__ Zb, float *__restrict__ nrm) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t row = w0; row < M; row += nw) {
+        float ss = 0.f;
+        for (int c = lane; c < n_pad; c += 32) {
+            const float v = c < n ? Z[row * n + c] : 0.f;
+            ss = fmaf(v, v, ss);
+            const uint16_t h = f2bf(v);
+            Zb[row * n_pad + c] = h;
+            Zb[(M + row) * n_pad + c] = f2bf(v - bf2f(h));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        if (lane == 0) nrm[row] = ss;
+    }
+}
+
+struct BarsK {
+    uint64_t qfull;
+    uint64_t full[kKS], empty[kKS];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem;
+};
+
+// grid (query tiles, splits).  6 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner),
+// w2-5 epilogue (one per TMEM lane quarter: thread = query).
+__global__ void __launch_bounds__(192, 1)
+    knn_topk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmR,
+                    const float *__restrict__ qn, const float *__restrict__ rn, int64_t Mq,
+                    int64_t Mr, int n_pad, int k, int tiles_per_split, float *__restrict__ pd,
+                    int32_t *__restrict__ pi) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int nslab = n_pad / 32;
+    unsigned char *Qhi = smem;                        // nslab x 8 KB
+    unsigned char *Qlo = smem + nslab * 8192;
+    unsigned char *stg = smem + 2 * nslab * 8192;
+    BarsK *bars = reinterpret_cast<BarsK *>(stg + kKS * 16384);
+    auto Rhi = [&](int s) { return stg + s * 16384; };
+    auto Rlo = [&](int s) { return stg + s * 16384 + 8192; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qt = blockIdx.x, split = blockIdx.y;
+    const int64_t rtiles = (Mr + kRT - 1) / kRT;
+    const int64_t t0 = static_cast<int64_t>(split) * tiles_per_split;
+    const int64_t t1 = rtiles < t0 + tiles_per_split ? rtiles : t0 + tiles_per_split;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->qfull, 1);
+        for (int s = 0; s < kKS; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->acc_full[a], 1);
+            mbar_init(&bars->acc_empty[a], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc<256>(&bars->tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tbase = bars->tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tc::prefetch_tmap(&tmQ);
+            tc::prefetch_tmap(&tmR);
+            mbar_arrive_expect_tx(&bars->qfull, static_cast<uint32_t>(nslab) * 16384u);
+            for (int c = 0; c < nslab; ++c) {
+                tc::tma_load_2d(Qhi + c * 8192, &tmQ, c * 32, qt * kQ, &bars->qfull);
+                tc::tma_load_2d(Qlo + c * 8192, &tmQ, c * 32, static_cast<int>(Mq) + qt * kQ,
+                                &bars->qfull);
+            }
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t t = t0; t < t1; ++t) {
+                for (int c = 0; c < nslab; ++c) {
+                    mbar_wait(&bars->empty[s], ph ^ 1u);
+                    mbar_arrive_expect_tx(&bars->full[s], 16384u);
+                    tc::tma_load_2d(Rhi(s), &tmR, c * 32, static_cast<int>(t * kRT), &bars->full[s]);
+                    tc::tma_load_2d(Rlo(s), &tmR, c * 32, static_cast<int>(Mr + t * kRT),
+                                    &bars->full[s]);
+                    if (++s == kKS) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_bf16(kQ, kRT);
+            int s = 0, a = 0;
+            uint32_t ph = 0, aph = 0;
+            mbar_wait(&bars->qfull, 0);
+            tc::fence_after_sync();
+            const uint32_t qh = smem_u32(Qhi), ql = smem_u32(Qlo);
+            for (int64_t t = t0; t < t1; ++t) {
+                mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+                tc::fence_after_sync();
+                const uint32_t d = tbase + static_cast<uint32_t>(a * kRT);
+                for (int c = 0; c < nslab; ++c) {
+                    mbar_wait(&bars->full[s], ph);
+                    tc::fence_after_sync();
+                    const uint32_t rh = smem_u32(Rhi(s)), rl = smem_u32(Rlo(s));
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const uint64_t ah = tc::sdesc_sw64(qh + c * 8192 + kk * 32);
+                        const uint64_t alo = tc::sdesc_sw64(ql + c * 8192 + kk * 32);
+                        const uint64_t bh = tc::sdesc_sw64(rh + kk * 32), blo = tc::sdesc_sw64(rl + kk * 32);
+                        tc::mma_bf16(d, ah, bh, idesc, (c | kk) != 0);
+                        tc::mma_bf16(d, ah, blo, idesc, 1u);
+                        tc::mma_bf16(d, alo, bh, idesc, 1u);
+                    }
+                    tc::mma_commit(&bars->empty[s]);
+                    if (++s == kKS) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                tc::mma_commit(&bars->acc_full[a]);
+                if (++a == 2) {
+                    a = 0;
+                    aph ^= 1u;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3;
+        const int64_t row = static_cast<int64_t>(qt) * kQ + q * 32 + lane;
+        const float qnorm = row < Mq ? qn[row] : 0.f;
+        float bd[kKnnMaxK];
+        int32_t bi[kKnnMaxK];
+#pragma unroll
+        for (int e = 0; e < kKnnMaxK; ++e) {
+            bd[e] = FLT_MAX;
+            bi[e] = -1;
+        }
+        float worst = FLT_MAX;   // bd[k-1], kept in a register (no dynamic indexing)
+        int a = 0;
+        uint32_t aph = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            mbar_wait(&bars->acc_full[a], aph);
+            tc::fence_after_sync();
+#pragma unroll 1
+            for (int cc = 0; cc < kRT / 32; ++cc) {
+                float v[32];
+                tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                  static_cast<uint32_t>(a * kRT + cc * 32),
+                              v);
+                const int64_t j0 = t * kRT + cc * 32;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int64_t j = j0 + e;
+                    const float dist =
+                        j < Mr ? fmaf(-2.f, v[e], qnorm + __ldg(rn + j)) : FLT_MAX;
+                    if (dist < worst) {   // sorted insertion; an equal distance keeps the earlier j
+                        float cd = dist;
+                        int32_t ci = static_cast<int32_t>(j);
+#pragma unroll
+                        for (int u = 0; u < kKnnMaxK; ++u) {
+                            if (u < k) {
+                                const bool sw = cd < bd[u];
+                                const float td = bd[u];
+                                const int32_t ti = bi[u];
+                                bd[u] = sw ? cd : td;
+                                bi[u] = sw ? ci : ti;
+                                cd = sw ? td : cd;
+                                ci = sw ? ti : ci;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kKnnMaxK; ++u)
+                            if (u == k - 1) worst = bd[u];
+                    }
+                }
+            }
+            tc::fence_before_sync();
+            tc::mbar_arrive(&bars->acc_empty[a]);
+            if (++a == 2) {
+                a = 0;
+                aph ^= 1u;
+            }
+        }
+        if (row < Mq) {
+            const int64_t o = (static_cast<int64_t>(split) * Mq + row) * k;
+#pragma unroll
+            for (int u = 0; u < kKnnMaxK; ++u) {
+                if (u < k) {
+                    pd[o + u] = bd[u];
+                    pi[o + u] = bi[u];
+                }
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) tc::tmem_free<256>(tbase);
+}
+
+// thread per query: k-way merge of the sorted per-split lists, ties by smaller index
+__global__ void knn_merge_kernel(const float *__restrict__ pd, const int32_t *__restrict__ pi,
+                                 int64_t Mq, int k, int splits, float *__restrict__ od,
+                                 int32_t *__restrict__ oi) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (q >= Mq) return;
+    int pos[64];
+    for (int s = 0; s < splits; ++s) pos[s] = 0;
+    for (int u = 0; u < k; ++u) {
+        int best = -1;
+        float bdv = 0.f;
+        int32_t biv = 0;
+        for (int s = 0; s < splits; ++s) {
+            if (pos[s] >= k) continue;
+            const int64_t o = (static_cast<int64_t>(s) * Mq + q) * k + pos[s];
+            const int32_t idx = pi[o];
+            if (idx < 0) continue;
+            const float dv = pd[o];
+            if (best < 0 || dv < bdv || (dv == bdv && idx < biv)) {
+                best = s;
+                bdv = dv;
+                biv = idx;
+            }
+        }
+        if (best >= 0) ++pos[best];
+        od[q * k + u] = best >= 0 ? bdv : FLT_MAX;
+        oi[q * k + u] = best >= 0 ? biv : -1;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
+std::once_flag g_enc_once, g_knn_attr_once;
+cudaError_t g_knn_attr_err = cudaSuccess;
+
+bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer) {
+    std::call_once(g_enc_once, []() {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!g_enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * 2};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    return g_enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
+                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
+size_t knn_smem(int n_pad) {
+    return static_cast<size_t>(2 * (n_pad / 32) * 8192) + kKS * 16384 + sizeof(BarsK) + 1024;
+}
+
+}  // namespace
+
+KnnPlan knn_plan(int64_t n, int64_t Mr, int64_t Mq, int k, int sm_count) {
+    KnnPlan p{};
+    p.n = n;
+    p.Mr = Mr;
+    p.Mq = Mq;
+    p.k = k;
+    p.n_pad = static_cast<int>((n + 31) / 32 * 32);
+    const int64_t qtiles = (Mq + kQ - 1) / kQ;
+    const int64_t rtiles = (Mr + kRT - 1) / kRT;
+    int64_t splits = std::max<int64_t>(1, (sm_count + qtiles - 1) / std::max<int64_t>(qtiles, 1));
+    splits = std::min<int64_t>({splits, rtiles, 64});
+    p.tiles_per_split = static_cast<int>((rtiles + splits - 1) / splits);
+    p.splits = static_cast<int>((rtiles + p.tiles_per_split - 1) / p.tiles_per_split);
+    size_t off = 0;
+    auto take = [&](size_t b) {
+        const size_t o = off;
+        off += al(b);
+        return o;
+    };
+    p.off_zr = take(static_cast<size_t>(Mr) * n * 4);
+    p.off_zq = take(static_cast<size_t>(Mq) * n * 4);
+    p.off_zrb = take(static_cast<size_t>(Mr) * p.n_pad * 2 * 2);
+    p.off_zqb = take(static_cast<size_t>(Mq) * p.n_pad * 2 * 2);
+    p.off_rn = take(static_cast<size_t>(Mr) * 4);
+    p.off_qn = take(static_cast<size_t>(Mq) * 4);
+    p.off_pd = take(static_cast<size_t>(p.splits) * Mq * k * 4);
+    p.off_pi = take(static_cast<size_t>(p.splits) * Mq * k * 4);
+    p.bytes = off;
+    return p;
+}
+
+bool knn_supported(int64_t n, int64_t Mr, int64_t Mq, int k) {
+    return n >= 4 && n % 4 == 0 && (n + 31) / 32 * 32 <= kKnnMaxNpad && k >= 1 &&
+           k <= kKnnMaxK && Mr >= k && Mq >= 1 && 2 * Mr < (int64_t(1) << 31) &&
+           2 * Mq < (int64_t(1) << 31);
+}
+
+cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float *d,
+                       const float *Pr, const float *Pq, int32_t *nn_idx, float *nn_dist, void *ws,
+                       cudaStream_t stream, LaunchInfo *info) {
+    std::call_once(g_knn_attr_once, []() {
+        g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(knn_smem(kKnnMaxNpad)));
+    });
+    if (g_knn_attr_err != cudaSuccess) return g_knn_attr_err;
+    char *w = static_cast<char *>(ws);
+    float *Zr = reinterpret_cast<float *>(w + p.off_zr);
+    float *Zq = reinterpret_cast<float *>(w + p.off_zq);
+    uint16_t *Zrb = reinterpret_cast<uint16_t *>(w + p.off_zrb);
+    uint16_t *Zqb = reinterpret_cast<uint16_t *>(w + p.off_zqb);
+    float *rn = reinterpret_cast<float *>(w + p.off_rn);
+    float *qn = reinterpret_cast<float *>(w + p.off_qn);
+    float *pd = reinterpret_cast<float *>(w + p.off_pd);
+    int32_t *pi = reinterpret_cast<int32_t *>(w + p.off_pi);
+
+    // 1. transform once: Z = diag(sqrt d) Q^T P
+    for (int which = 0; which < 2; ++which) {
+        FusedArgs a{};
+        a.U = U;
+        a.X = which ? Pq : Pr;
+        a.Y = which ? Zq : Zr;
+        a.vec = d;
+        a.n = p.n;
+        a.h = h;
+        a.N = which ? p.Mq : p.Mr;
+        a.mode = MODE_TRANSFORM;
+        cudaError_t e = launch_fused(a, 0, stream, nullptr);
+        if (e != cudaSuccess) return e;
+    }
+    // 2. bf16 hi/lo split + squared norms
+    const int sms = device_attr().sm_count;
+    knn_pack_kernel<<<sms * 4, 256, 0, stream>>>(Zr, p.Mr, static_cast<int>(p.n), p.n_pad, Zrb, rn);
+    knn_pack_kernel<<<sms * 4, 256, 0, stream>>>(Zq, p.Mq, static_cast<int>(p.n), p.n_pad, Zqb, qn);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // 3. distances on the tensor cores + per-query top-k
+    CUtensorMap mQ, mR;
+    if (!make_map_bf16(&mQ, Zqb, p.n_pad, 2 * p.Mq) || !make_map_bf16(&mR, Zrb, p.n_pad, 2 * p.Mr))
+        return cudaErrorNotSupported;
+    const dim3 grid(static_cast<unsigned>((p.Mq + kQ - 1) / kQ), static_cast<unsigned>(p.splits));
+    knn_topk_kernel<<<grid, 192, knn_smem(p.n_pad), stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad,
+                                                              p.k, p.tiles_per_split, pd, pi);
+    // 4. merge the per-split lists
+    knn_merge_kernel<<<static_cast<int>((p.Mq + 127) / 128), 128, 0, stream>>>(
+        pd, pi, p.Mq, p.k, p.splits, nn_dist, nn_idx);
+    if (info) {
+        info->variant = "knn_bf16x3_tcgen05_topk";
+        info->grid = static_cast<int>(grid.x * grid.y);
+        info->block = 192;
+        info->smem = static_cast<int>(knn_smem(p.n_pad));
+        info->nchunks = p.splits;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace hh

@@ -24,7 +24,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "hh.h")
 HH_OK, HH_ERR_INVALID_VALUE, HH_ERR_UNSUPPORTED, HH_ERR_WORKSPACE, HH_ERR_CUDA = range(5)
 HH_F32, HH_F64 = 0, 1
 HH_OP_N, HH_OP_T = 0, 1
-HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST = range(4)
+HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST, HH_CALL_KNN = range(5)
 HH_ALGO_AUTO, HH_ALGO_FUSED, HH_ALGO_WY = range(3)
 HH_SIDE_LEFT, HH_SIDE_RIGHT = range(2)
 
@@ -58,6 +58,8 @@ def lib() -> ctypes.CDLL:
         L.hh_sym_apply_signed.argtypes = [i64, i64, p, p, p, p, p, i64, i32, p, sz, p]
         L.hh_apply_signed.restype = i32
         L.hh_sym_apply_signed.restype = i32
+        L.hh_knn.argtypes = [i64, i64, p, p, p, i64, p, i64, i32, p, p, i32, p, sz, p]
+        L.hh_knn.restype = i32
         L.hh_set_algo.argtypes = [i32]
         L.hh_set_algo.restype = i32
         L.hh_get_algo.restype = i32
@@ -303,6 +305,29 @@ def hh_mahalanobis(U: torch.Tensor, d: torch.Tensor, P: torch.Tensor, ia: torch.
                               None if fused else _ptr(workspace), wsb, _stream(stream))
     _check(st, "hh_mahalanobis")
     return dist
+
+
+def hh_knn(U: torch.Tensor, d: torch.Tensor, P_ref: torch.Tensor, P_query: torch.Tensor, k: int,
+           workspace: Optional[torch.Tensor] = None, stream=None):
+    """k nearest references of every query under d_S = ||diag(sqrt d) Q^T (x_q - x_r)||^2
+    (hh.h: hh_knn).  Returns (idx int32 (M_query, k), dist (M_query, k)), ascending."""
+    for t, nm in ((d, "d"), (P_ref, "P_ref"), (P_query, "P_query")):
+        _dev(t, nm)
+    Mr, n = P_ref.shape
+    Mq = P_query.shape[0]
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    idx = torch.empty(Mq, k, dtype=torch.int32, device=P_ref.device)
+    dist = torch.empty(Mq, k, dtype=P_ref.dtype, device=P_ref.device)
+    wsb = hh_workspace_bytes(HH_CALL_KNN, n, h, Mr, Mq, P_ref.dtype)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=P_ref.device)
+    st = lib().hh_knn(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P_ref), Mr, _ptr(P_query), Mq,
+                      int(k), _ptr(idx), _ptr(dist), _dtype(P_ref), _ptr(workspace),
+                      workspace.numel(), _stream(stream))
+    _check(st, "hh_knn")
+    return idx, dist
 
 
 def hh_apply_host(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor] = None,

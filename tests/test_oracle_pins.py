@@ -394,3 +394,33 @@ def test_signed_determinant_and_identity():
     lam = g.standard_normal(n)
     S = oracle.sym_apply_signed(U, d, lam, np.eye(n)).T
     assert np.allclose(np.linalg.eigvalsh((S + S.T) / 2), np.sort(lam), atol=1e-13)
+
+
+
+# --------------------------------------------------------------------------- NEXT-f3: kNN
+def test_knn_bruteforce_and_invariants():
+    """k-NN under d_S: against the dense quadratic form (x_q - x_r)^T
+    Q diag(d) Q^T (x_q - x_r) with numpy argsort (stable: ties by index); a query equal to
+    a reference finds it at distance 0; d == 1 with orthonormal Q reduces to Euclidean
+    k-NN (orthogonal invariance)."""
+    g = gi.rng(907)
+    n, h, Mr, Mq, k = 12, 4, 40, 9, 5
+    U = unit_rows(g, h, n)
+    d = g.uniform(0.1, 10.0, n)
+    Pr = g.standard_normal((Mr, n))
+    Pq = g.standard_normal((Mq, n))
+    Pq[3] = Pr[17]
+    Q = dense_Q(U)
+    S = Q @ np.diag(d) @ Q.T
+    idx, dist = oracle.knn(U, d, Pr, Pq, k)
+    for q in range(Mq):
+        diff = Pq[q] - Pr
+        dd = np.einsum("ij,jk,ik->i", diff, S, diff)
+        order = np.argsort(dd, kind="stable")[:k]
+        assert np.array_equal(idx[q], order)
+        assert np.allclose(dist[q], dd[order], rtol=1e-12, atol=1e-12)
+    assert idx[3, 0] == 17 and dist[3, 0] == 0.0
+    ie, de = oracle.knn(U, np.ones(n), Pr, Pq, k)
+    for q in range(Mq):
+        e = ((Pq[q] - Pr) ** 2).sum(1)
+        assert np.array_equal(ie[q], np.argsort(e, kind="stable")[:k])
