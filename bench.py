@@ -50,12 +50,19 @@ def workload_case(name: str, N_override=None):
         return gi.make_config(4, N=N_override)
     if name.startswith("C5H"):
         return gi.make_config(5, h=int(name[3:]), N=N_override)
+    if name == "KNN":   # NEXT-f3, Table-I-shaped (MNIST after PCA) synthetic stand-in
+        return gi.make_knn_case()
     raise SystemExit(f"unknown workload {name}")
 
 
 def alg_cost(c, op_count=1):
     """Algorithmic bytes and flops of one step."""
     s = 4 if c.dtype == "f32" else 8
+    if c.call == "knn":
+        Mq = c.lam.shape[0]
+        byts = (c.N + Mq) * c.n * s + Mq * c.k * 8           # points read once + results
+        flops = 4 * c.h * c.n * (c.N + Mq) + 2 * c.n * c.N * Mq   # transform once + dots
+        return byts, flops, Mq
     if c.call == "mahalanobis":
         P = c.npairs
         byts = c.N * c.n * s + 2 * P * 4 + P * s          # points once + indices + dist
@@ -164,7 +171,9 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
 
     def run(k):
         t0 = time.perf_counter()
-        if c.call == "mahalanobis":
+        if c.call == "knn":
+            oracle.knn(c.U, c.d, c.X, c.lam[:k], c.k)
+        elif c.call == "mahalanobis":
             oracle.mahalanobis(c.U, c.d, c.X, c.ia[:k], c.ib[:k])
         elif c.call == "sym":
             oracle.sym_apply(c.U, c.lam, c.X[:k])
@@ -173,7 +182,7 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
         return time.perf_counter() - t0
 
     total = units
-    k = min(total, 256 if c.call != "mahalanobis" else 2048)
+    k = min(total, {"mahalanobis": 2048, "knn": 4}.get(c.call, 256))
     dt = run(k)
     while dt < 0.5 and k < total:
         k = min(total, k * 4)
@@ -184,7 +193,7 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
     if k2 != k:
         dt = run(k2)
         k = k2
-    what = "pairs" if c.call == "mahalanobis" else "columns"
+    what = {"mahalanobis": "pairs", "knn": "queries"}.get(c.call, "columns")
     return (per_unit_bytes * k / dt / 1e9, k / dt, dt,
             f"{k} of {total} {what} of {c.name} (fp64 oracle, {threads} threads)", threads)
 
@@ -208,7 +217,9 @@ def run_reference(args):
     times = []
     for i in range(warm + steps):
         t0 = time.perf_counter()
-        if c.call == "mahalanobis":
+        if c.call == "knn":
+            oracle.knn(sub.U, sub.d, sub.X, sub.lam[:k], sub.k)
+        elif c.call == "mahalanobis":
             oracle.mahalanobis(sub.U, sub.d, sub.X, sub.ia[:k], sub.ib[:k])
         elif c.call == "sym":
             oracle.sym_apply(sub.U, sub.lam, sub.X[:k])
@@ -219,7 +230,7 @@ def run_reference(args):
             times.append(dt)
     tot = sum(times)
     value = per_unit_bytes * k * steps / tot / 1e9
-    what = "pairs" if c.call == "mahalanobis" else "columns"
+    what = {"mahalanobis": "pairs", "knn": "queries"}.get(c.call, "columns")
     sample = f"{k} of {units} {what} of {c.name} per step (fp64 oracle, {threads} threads)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
@@ -244,6 +255,9 @@ def config_of(c, args):
          > 256 << 20 else "L2-resident inputs (warm L2, labelled)"}
     if c.call == "mahalanobis":
         d["npairs"] = c.npairs
+    if c.call == "knn":
+        d.update({"M_ref": c.N, "M_query": int(c.lam.shape[0]), "k": c.k,
+                  "stand_in_for": "Table I MNIST after PCA (P:670), iid N(0,1)"})
     if c.call == "apply":
         d["op"] = args.op
     return d
@@ -270,9 +284,21 @@ def run_hh(args):
     Y = torch.empty_like(X)
     stream = torch.cuda.current_stream(dev)
     extra = {}
-    if c.call == "sym":
+    if c.call == "knn":
+        d = torch.from_numpy(c.d).to(dev)
+        Pq = torch.from_numpy(c.lam).to(dev)
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_KNN, c.n, c.h, c.N, Pq.shape[0], X.dtype)
+        wsp = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        knn_out = {}
+
+        def step():
+            knn_out["r"] = hh.hh_knn(U, d, X, Pq, c.k, workspace=wsp, stream=stream)
+        launches = 6
+    elif c.call == "sym":
         lam = torch.from_numpy(c.lam).to(dev)
-        step = lambda: hh.hh_sym_apply(U, lam, X, Y, stream=stream)  # noqa: E731
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_SYM, c.n, c.h, c.N, 0, X.dtype)
+        wsp = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        step = lambda: hh.hh_sym_apply(U, lam, X, Y, workspace=wsp, stream=stream)  # noqa: E731
         launches = 1
     elif c.call == "mahalanobis":
         d = torch.from_numpy(c.d).to(dev)
@@ -303,7 +329,14 @@ def run_hh(args):
     parity = None
     if rank == 0 and not args.no_parity:
         import oracle
-        if c.call == "apply":
+        if c.call == "knn":
+            idx = np.linspace(0, c.lam.shape[0] - 1, 64).astype(np.int64)
+            gi_, gd_ = knn_out["r"]
+            got = gd_[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
+            ri, ref = oracle.knn(c.U, c.d, c.X, c.lam[idx], c.k)
+            extra["knn_index_agreement"] = float(
+                (gi_[torch.from_numpy(idx).to(dev)].cpu().numpy() == ri).mean())
+        elif c.call == "apply":
             idx = np.linspace(0, c.N - 1, 256).astype(np.int64)
             got = Y[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
             ref = oracle.apply(op, c.U, c.X[idx])
@@ -397,7 +430,21 @@ def run_hh(args):
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
                 "frac_of_8TBps": achieved / 8000.0,
                 "kernel": info.get("variant"), "launch": info}
-        if wy_path:
+        if str(info.get("variant", "")).startswith("knn_"):
+            pk = peaks()[2]
+            tpeak = float(pk.get("bf16_tflops", 1590.0)) if pk else 1590.0
+            Mq = c.lam.shape[0]
+            exe = 3 * 2 * ((c.n + 31) // 32 * 32) * c.N * Mq
+            roof = {"bound": "tensor", "achieved": flops / (ms_step * 1e-3) / 1e12,
+                    "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": flops / (ms_step * 1e-3) / 1e12 / tpeak, "traffic": traffic,
+                    "peak_source": "measured bf16 (MEASURED_PEAKS.json bf16_tflops)",
+                    "executed_tflops": exe / (ms_step * 1e-3) / 1e12,
+                    "executed_frac": exe / (ms_step * 1e-3) / 1e12 / tpeak,
+                    "pairs_per_s": c.N * Mq / (ms_step * 1e-3),
+                    "kernel": info.get("variant"), "launch": info,
+                    "scope": "whole step (transform, pack, distance GEMM + top-k, merge)"}
+        elif wy_path:
             # compact-WY on the bf16 tensor pipe: algorithmic 4hnN flops and the
             # executed bf16x3 MMA flops (3 products of 2*b_pad*n per column per GEMM)
             pk = peaks()[2]
@@ -428,7 +475,7 @@ def run_hh(args):
             "gflops": ws * flops / (ms_step * 1e-3) / 1e9,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps,
-            "clocks": clocks, "parity": parity,
+            "clocks": clocks, "parity": parity, **extra,
             "gpu": torch.cuda.get_device_name(dev),
         }
         print(json.dumps(out), flush=True)

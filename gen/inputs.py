@@ -174,3 +174,20 @@ def paper_context_shapes():
         for mult in (1, 2, 3):
             out.append((n, int(math.ceil(mult * math.log2(n))), Nt))
     return out
+
+
+def make_knn_case(n: int = 40, h: int = 6, M_ref: int = 49000, M_query: int = 21000,
+                  k: int = 3, seed: int = 0) -> Case:
+    """NEXT-f3 workload: synthetic stand-in for PAPER.md Table I's test-time k-NN (l.670:
+    MNIST after PCA to n = 40, 70/30 split of 70000 points, h = ceil(log2 n) = 6).  The
+    dataset is not in the container: iid N(0,1) points, unit Gaussian reflectors, metric
+    diagonal U[0.1, 10].  X holds the references; `ia` is unused; the queries are in
+    `lam` (reused field) -- see bench.py."""
+    key = (500, seed, n, h, M_ref, M_query)
+    U = unit_reflectors(rng(*key, S_U), h, n, "f32")
+    Pr = gaussian_columns(rng(*key, S_X), M_ref, n, "f32")
+    Pq = gaussian_columns(rng(*key, S_FLIP), M_query, n, "f32")
+    d = metric_diag(rng(*key, S_D), n, "f32")
+    c = Case(f"KNN-n{n}-h{h}", "knn", n, h, M_ref, "f32", U, Pr, lam=Pq, d=d)
+    c.k = k
+    return c

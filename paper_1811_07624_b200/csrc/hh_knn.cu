@@ -77,9 +77,9 @@ struct BarsK {
     uint32_t tmem;
 };
 
-// grid (query tiles, splits).  6 warps: w0 TMA producer, w1 MMA issuer (+TMEM owner),
-// w2-5 epilogue (one per TMEM lane quarter: thread = query).
-__global__ void __launch_bounds__(192, 1)
+// grid (query tiles, splits).  18 warps: w0 TMA producer, w1 MMA issuer (+TMEM
+// owner), w2-17 epilogue (TMEM lane quarter x column group; thread = query).
+__global__ void __launch_bounds__(576, 1)
     knn_topk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmR,
                     const float *__restrict__ qn, const float *__restrict__ rn, int64_t Mq,
                     int64_t Mr, int n_pad, int k, int tiles_per_split, float *__restrict__ pd,
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->acc_full[a], 1);
-            mbar_init(&bars->acc_empty[a], 128);
+            mbar_init(&bars->acc_empty[a], 512);
         }
         fence_mbar_init();
     }
@@ -184,7 +184,11 @@ __global__ void __launch_bounds__(192, 1)
         }
         __syncwarp();
     } else {
-        const int q = warp & 3;
+        // 16 epilogue warps: lane quarter q (thread = query), column group grp (32 of
+        // the 128 references of a tile).  Per reference: one shuffle (its norm), one FMA
+        // and one compare against the current k-th distance; the rare insertions run
+        // off a per-thread hit mask, outside the streaming loop.
+        const int q = warp & 3, grp = (warp - 2) >> 2;
         const int64_t row = static_cast<int64_t>(qt) * kQ + q * 32 + lane;
         const float qnorm = row < Mq ? qn[row] : 0.f;
         float bd[kKnnMaxK];
@@ -198,56 +202,94 @@ __global__ void __launch_bounds__(192, 1)
         int a = 0;
         uint32_t aph = 0;
         for (int64_t t = t0; t < t1; ++t) {
+            const int64_t j0 = t * kRT + grp * 32;
+            const float rnl = j0 + lane < Mr ? __ldg(rn + j0 + lane) : FLT_MAX;
             mbar_wait(&bars->acc_full[a], aph);
             tc::fence_after_sync();
-#pragma unroll 1
-            for (int cc = 0; cc < kRT / 32; ++cc) {
-                float v[32];
-                tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                                  static_cast<uint32_t>(a * kRT + cc * 32),
-                              v);
-                const int64_t j0 = t * kRT + cc * 32;
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int64_t j = j0 + e;
-                    const float dist =
-                        j < Mr ? fmaf(-2.f, v[e], qnorm + __ldg(rn + j)) : FLT_MAX;
-                    if (dist < worst) {   // sorted insertion; an equal distance keeps the earlier j
-                        float cd = dist;
-                        int32_t ci = static_cast<int32_t>(j);
-#pragma unroll
-                        for (int u = 0; u < kKnnMaxK; ++u) {
-                            if (u < k) {
-                                const bool sw = cd < bd[u];
-                                const float td = bd[u];
-                                const int32_t ti = bi[u];
-                                bd[u] = sw ? cd : td;
-                                bi[u] = sw ? ci : ti;
-                                cd = sw ? td : cd;
-                                ci = sw ? ti : ci;
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < kKnnMaxK; ++u)
-                            if (u == k - 1) worst = bd[u];
-                    }
-                }
-            }
+            float v[32];
+            tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                              static_cast<uint32_t>(a * kRT + grp * 32),
+                          v);
             tc::fence_before_sync();
-            tc::mbar_arrive(&bars->acc_empty[a]);
+            tc::mbar_arrive(&bars->acc_empty[a]);   // the accumulator is in registers
             if (++a == 2) {
                 a = 0;
                 aph ^= 1u;
             }
-        }
-        if (row < Mq) {
-            const int64_t o = (static_cast<int64_t>(split) * Mq + row) * k;
+            // dist = qnorm + rn[j] - 2 dot  <  worst   <=>   rn[j] - 2 dot < worst - qnorm
+            const float thr = worst - qnorm;
+            uint32_t hit = 0;
 #pragma unroll
-            for (int u = 0; u < kKnnMaxK; ++u) {
-                if (u < k) {
-                    pd[o + u] = bd[u];
-                    pi[o + u] = bi[u];
+            for (int e = 0; e < 32; ++e) {
+                const float rj = __shfl_sync(0xffffffffu, rnl, e);
+                v[e] = fmaf(-2.f, v[e], rj);
+                hit |= (v[e] < thr ? 1u : 0u) << e;
+            }
+            while (hit) {   // ascending j: an equal distance keeps the earlier reference
+                const int e = __ffs(hit) - 1;
+                hit &= hit - 1;
+                float cd = 0.f;
+#pragma unroll
+                for (int u = 0; u < 32; ++u)
+                    if (u == e) cd = v[u];
+                cd += qnorm;
+                if (!(cd < worst)) continue;
+                int32_t ci = static_cast<int32_t>(j0 + e);
+#pragma unroll
+                for (int u = 0; u < kKnnMaxK; ++u) {
+                    if (u < k) {
+                        const bool sw = cd < bd[u];
+                        const float td = bd[u];
+                        const int32_t ti = bi[u];
+                        bd[u] = sw ? cd : td;
+                        bi[u] = sw ? ci : ti;
+                        cd = sw ? td : cd;
+                        ci = sw ? ti : ci;
+                    }
                 }
+#pragma unroll
+                for (int u = 0; u < kKnnMaxK; ++u)
+                    if (u == k - 1) worst = bd[u];
+            }
+        }
+        // merge the four column groups' lists of each query through shared memory (the
+        // reference ring is free: every MMA has completed)
+        float *md = reinterpret_cast<float *>(stg);
+        int32_t *mi = reinterpret_cast<int32_t *>(stg + 4 * kQ * kKnnMaxK * 4);
+        fence_proxy_async_smem();
+        const int qi = q * 32 + lane;
+#pragma unroll
+        for (int u = 0; u < kKnnMaxK; ++u) {
+            if (u < k) {
+                md[(grp * kQ + qi) * kKnnMaxK + u] = bd[u];
+                mi[(grp * kQ + qi) * kKnnMaxK + u] = bi[u];
+            }
+        }
+        named_bar_sync(1, 512);
+        if (grp == 0 && row < Mq) {
+            int pos[4] = {0, 0, 0, 0};
+            const int64_t o = (static_cast<int64_t>(split) * Mq + row) * k;
+            for (int u = 0; u < k; ++u) {
+                int best = -1;
+                float bdv = 0.f;
+                int32_t biv = 0;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (pos[g] >= k) continue;
+                    const int32_t idx = mi[(g * kQ + qi) * kKnnMaxK + pos[g]];
+                    if (idx < 0) continue;
+                    const float dv = md[(g * kQ + qi) * kKnnMaxK + pos[g]];
+                    if (best < 0 || dv < bdv || (dv == bdv && idx < biv)) {
+                        best = g;
+                        bdv = dv;
+                        biv = idx;
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+                    if (g == best) ++pos[g];
+                pd[o + u] = best >= 0 ? bdv : FLT_MAX;
+                pi[o + u] = best >= 0 ? biv : -1;
             }
         }
     }
@@ -325,8 +367,20 @@ KnnPlan knn_plan(int64_t n, int64_t Mr, int64_t Mq, int k, int sm_count) {
     p.n_pad = static_cast<int>((n + 31) / 32 * 32);
     const int64_t qtiles = (Mq + kQ - 1) / kQ;
     const int64_t rtiles = (Mr + kRT - 1) / kRT;
-    int64_t splits = std::max<int64_t>(1, (sm_count + qtiles - 1) / std::max<int64_t>(qtiles, 1));
-    splits = std::min<int64_t>({splits, rtiles, 64});
+    // one CTA per SM (registers): pick the split count whose CTA total fills the last
+    // wave best (ties: fewer splits), keeping >= 8 reference tiles per CTA
+    int64_t splits = 1;
+    double best_eff = -1.0;
+    for (int64_t sp = 1; sp <= 64 && sp <= rtiles; ++sp) {
+        if (sp > 1 && (rtiles + sp - 1) / sp < 8) break;
+        const int64_t ctas = qtiles * sp;
+        const int64_t waves = (ctas + sm_count - 1) / sm_count;
+        const double eff = static_cast<double>(ctas) / static_cast<double>(waves * sm_count);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            splits = sp;
+        }
+    }
     p.tiles_per_split = static_cast<int>((rtiles + splits - 1) / splits);
     p.splits = static_cast<int>((rtiles + p.tiles_per_split - 1) / p.tiles_per_split);
     size_t off = 0;
@@ -397,7 +451,7 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
     if (!make_map_bf16(&mQ, Zqb, p.n_pad, 2 * p.Mq) || !make_map_bf16(&mR, Zrb, p.n_pad, 2 * p.Mr))
         return cudaErrorNotSupported;
     const dim3 grid(static_cast<unsigned>((p.Mq + kQ - 1) / kQ), static_cast<unsigned>(p.splits));
-    knn_topk_kernel<<<grid, 192, knn_smem(p.n_pad), stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad,
+    knn_topk_kernel<<<grid, 576, knn_smem(p.n_pad), stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad,
                                                               p.k, p.tiles_per_split, pd, pi);
     // 4. merge the per-split lists
     knn_merge_kernel<<<static_cast<int>((p.Mq + 127) / 128), 128, 0, stream>>>(
@@ -405,7 +459,7 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
     if (info) {
         info->variant = "knn_bf16x3_tcgen05_topk";
         info->grid = static_cast<int>(grid.x * grid.y);
-        info->block = 192;
+        info->block = 576;
         info->smem = static_cast<int>(knn_smem(p.n_pad));
         info->nchunks = p.splits;
     }
