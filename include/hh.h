@@ -256,6 +256,10 @@ const char *hh_version(void);
 hh_status hh_last_launch_info(const char **variant, int *grid, int *block,
                               int *smem_bytes, int *nchunks);
 
+/* Number of kernels the calling thread's last call enqueued (all of them this
+ * library's own).  HH_ERR_INVALID_VALUE before any launch or for a NULL pointer. */
+hh_status hh_last_launch_count(int *kernels);
+
 #ifdef __cplusplus
 }
 #endif

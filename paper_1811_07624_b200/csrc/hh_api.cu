@@ -145,6 +145,12 @@ hh_status hh_debug_wy_project(int op, int64_t n, int64_t h, const void *U, const
                              static_cast<const float *>(X), nullptr, workspace, stream, nullptr, 1));
 }
 
+hh_status hh_last_launch_count(int *kernels) {
+    if (!t_has_last || !kernels) return HH_ERR_INVALID_VALUE;
+    *kernels = t_last.launches;
+    return HH_OK;
+}
+
 hh_status hh_last_launch_info(const char **variant, int *grid, int *block, int *smem_bytes,
                               int *nchunks) {
     if (!t_has_last) return HH_ERR_INVALID_VALUE;
@@ -347,6 +353,7 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
                                            dtype == HH_F32 ? 0 : 1, stream, &info);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (info.variant) {
+            info.launches = 2;   // K3a + K3b
             t_last = info;
             t_has_last = true;
         }

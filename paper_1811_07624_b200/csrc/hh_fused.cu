@@ -631,6 +631,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
         info->block = v->nt;
         info->smem = static_cast<int>(smem);
         info->nchunks = nc;
+        info->launches = 1;
     }
     return e;
 }

@@ -168,6 +168,7 @@ cudaError_t launch_gather_dist(const void *Z, int64_t n, const int32_t *ia, cons
         info->block = v->nt;
         info->smem = 0;
         info->nchunks = 0;
+        info->launches = 1;
     }
     return e;
 }

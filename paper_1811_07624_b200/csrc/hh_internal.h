@@ -34,6 +34,7 @@ struct FusedArgs {
 struct LaunchInfo {
     const char *variant = nullptr;
     int grid = 0, block = 0, smem = 0, nchunks = 0;
+    int launches = 0;   // kernels this call enqueued
 };
 
 // Launch the fused reflector kernel (K1 / K2 / K3a / K3c).  dtype: 0 f32, 1 f64.

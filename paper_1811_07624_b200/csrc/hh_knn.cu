@@ -462,6 +462,7 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
         info->block = 576;
         info->smem = static_cast<int>(knn_smem(p.n_pad));
         info->nchunks = p.splits;
+        info->launches = 6;   // 2 transforms, 2 packs, distance/top-k, merge
     }
     return cudaGetLastError();
 }

@@ -923,6 +923,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     if (g_attr_err != cudaSuccess) return g_attr_err;
     const bool sym = p.kind == WY_SYM;
     if (sym && !lam) return cudaErrorInvalidValue;
+    int nlaunch = 0;   // kernels enqueued by this call (reported through LaunchInfo)
     char *w = static_cast<char *>(ws);
     auto F = [&](size_t o) { return reinterpret_cast<float *>(w + o); };
     auto H = [&](size_t o) { return reinterpret_cast<uint16_t *>(w + o); };
@@ -937,21 +938,21 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     {
         const int64_t tot = R * n_pad;
         const int g = static_cast<int>(std::min<int64_t>((tot + 255) / 256, sms * 16));
-        wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b, p.extra,
+        ++nlaunch, wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b, p.extra,
                                               Wf, Wb);
         const int tb = (b + 63) / 64;
-        wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, 0,
+        ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, 0,
                                                                        nullptr, 0, Sp);
         const int64_t ns = static_cast<int64_t>(m) * b * b;
-        wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, sms * 8)),
+        ++nlaunch, wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, sms * 8)),
                                 256, 0, stream>>>(Sp, b, m, p.nsplit, 0, S);
         if (sym) {   // P = W^T Lambda W of the last block (full)
-            wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit,
+            ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit,
                                                                        m - 1, lam, 1, F(p.off_pp));
-            wy_gram_reduce_kernel<<<std::max(1, (b * b + 255) / 256), 256, 0, stream>>>(
+            ++nlaunch, wy_gram_reduce_kernel<<<std::max(1, (b * b + 255) / 256), 256, 0, stream>>>(
                 F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p));
         }
-        wy_tbuild_kernel<<<m, 1024, tbuild_smem(b), stream>>>(S, b, T);
+        ++nlaunch, wy_tbuild_kernel<<<m, 1024, tbuild_smem(b), stream>>>(S, b, T);
         const dim3 gv(static_cast<unsigned>(n_pad / 64), b / 32);
         for (int k = 0; k < m; ++k) {
             const float *Wk = Wf + static_cast<int64_t>(k) * b * n_pad;
@@ -963,11 +964,11 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             uint16_t *Vn = H(p.kind == WY_APPLY_N ? p.off_v : p.off_v2);
             uint16_t *Vt = H(p.off_v);
             if (need_n)
-                wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                ++nlaunch, wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
                     Vn + static_cast<int64_t>(k) * n_pad * b, b, vlo);
             if (need_t)
-                wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
+                ++nlaunch, wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
                     Vt + static_cast<int64_t>(k) * n_pad * b, b, vlo);
             if (last_sym) {
@@ -975,19 +976,19 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                 // M = P T^T; A1 = Lambda V' - V M (columns [0, b)).  DESIGN.md §4.
                 uint16_t *As = H(p.off_asym);
                 const int64_t alo = n_pad * 2 * b;
-                wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                ++nlaunch, wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_vf),
                     nullptr, b, 0);
-                wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                ++nlaunch, wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr, As + b,
                     2 * b, alo);
-                wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
+                ++nlaunch, wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_vpf),
                     nullptr, b, 0);
-                wy_rowgemm_kernel<false, true><<<dim3((b + 63) / 64, b / 32), 256, 0, stream>>>(
+                ++nlaunch, wy_rowgemm_kernel<false, true><<<dim3((b + 63) / 64, b / 32), 256, 0, stream>>>(
                     b, F(p.off_p), b, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_m), nullptr,
                     b, 0);
-                wy_rowgemm_kernel<false, false><<<gv, 256, 0, stream>>>(
+                ++nlaunch, wy_rowgemm_kernel<false, false><<<gv, 256, 0, stream>>>(
                     n_pad, F(p.off_vf), b, F(p.off_m), b, b, F(p.off_vpf), b, lam, p.n, -1.f,
                     nullptr, As, 2 * b, alo);
             }
@@ -1051,7 +1052,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         f.dscale = dsign;
         if (f.pre) {   // first pass is the symmetric block: pre-scale Lambda D
             float *ld = F(p.off_ld);
-            wy_vmul_kernel<<<std::max(1, static_cast<int>((p.n + 255) / 256)), 256, 0, stream>>>(
+            ++nlaunch, wy_vmul_kernel<<<std::max(1, static_cast<int>((p.n + 255) / 256)), 256, 0, stream>>>(
                 f.pre, dsign, p.n, ld);
             f.pre = ld;
         } else {
@@ -1066,12 +1067,12 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     for (int q = 0; q < np; ++q) {
         const Pass &ps = prog[q];
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
-        wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, *ps.mW, Gt, static_cast<int>(p.n),
+        ++nlaunch, wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, *ps.mW, Gt, static_cast<int>(p.n),
                                                           N, ps.kw, ps.wrow,
                                                           static_cast<int>(R) + ps.wrow, ntiles,
                                                           ps.dscale);
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
-        wy_update_kernel<<<grid, 384, smem3(), stream>>>(
+        ++nlaunch, wy_update_kernel<<<grid, 384, smem3(), stream>>>(
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles);
         cur = Y;
@@ -1082,6 +1083,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         info->block = 480;
         info->smem = static_cast<int>(smem1());
         info->nchunks = np;
+        info->launches = nlaunch;
     }
     return cudaGetLastError();
 }

@@ -60,6 +60,8 @@ def lib() -> ctypes.CDLL:
         L.hh_sym_apply_signed.restype = i32
         L.hh_knn.argtypes = [i64, i64, p, p, p, i64, p, i64, i32, p, p, i32, p, sz, p]
         L.hh_knn.restype = i32
+        L.hh_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
+        L.hh_last_launch_count.restype = i32
         L.hh_set_algo.argtypes = [i32]
         L.hh_set_algo.restype = i32
         L.hh_get_algo.restype = i32
@@ -99,8 +101,10 @@ def last_launch_info() -> dict:
                                    ctypes.byref(s), ctypes.byref(c))
     if st != HH_OK:
         return {}
+    kc = ctypes.c_int()
+    lib().hh_last_launch_count(ctypes.byref(kc))
     return {"variant": v.value.decode(), "grid": g.value, "block": b.value, "smem": s.value,
-            "nchunks": c.value}
+            "nchunks": c.value, "launches": kc.value}
 
 
 def _check(st: int, what: str):
