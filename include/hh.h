@@ -105,7 +105,8 @@ typedef enum {
     HH_CALL_SYM = 1,
     HH_CALL_MAHALANOBIS = 2,
     HH_CALL_APPLY_HOST = 3,
-    HH_CALL_KNN = 4
+    HH_CALL_KNN = 4,
+    HH_CALL_CONGRUENCE = 5
 } hh_call;
 
 /*
@@ -188,6 +189,19 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d,
                          hh_stream_t stream);
 
 /*
+ * hh_congruence -- M_out[b] = op(Q) M[b] op(Q)^T for `count` n x n column-major
+ *   matrices (NEXT-f4): the two-sided reflector products of the SHF fitting loop,
+ *   eq:ak / eq:bk: A_k = (U_{k-1}...U_1) DSD (U_1...U_{k-1}) is HH_OP_T
+ *   with U = [u_1 .. u_{k-1}] and M = DSD.  Computed as two hh_apply passes around a
+ *   batched transpose ((op(Q) (op(Q) M)^T)^T); M need not be symmetric.
+ *   workspace (DEVICE) >= hh_workspace_bytes(HH_CALL_CONGRUENCE, n, h, count, 0, dtype)
+ *   (two n*n*count scratch matrices + the apply's own scratch).  M_out may alias M.
+ */
+hh_status hh_congruence(hh_op op, int64_t n, int64_t h, const void *U, const void *M, void *Mout,
+                        int64_t count, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                        hh_stream_t stream);
+
+/*
  * hh_knn -- test-time k nearest neighbours under the learned metric (NEXT-f3):
  *   "perform the transformation x <- L x before running the k-NN",
  *   L = diag(sqrt d) Q^T (reading R4), so d_S(q, r) = ||L x_q - L x_r||^2.
@@ -231,7 +245,7 @@ hh_algo hh_get_algo(void);
 /*
  * hh_workspace_bytes -- scratch bytes the call needs (cuBLAS bufferSize style).
  *   N_or_M: N for apply/sym/apply_host, M for Mahalanobis, M_ref for kNN (with
- *   npairs = M_query).  Writes *bytes.
+ *   npairs = M_query), the matrix count for the congruence.  Writes *bytes.
  *   HH_CALL_APPLY: the compact-WY scratch when this thread's hh_algo selection
  *   picks K5 for (n, h, N, dtype) (packed W, T, V = W T and one G block), else 0.
  *   HH_CALL_SYM: the compact-WY scratch when the symmetric call picks the tensor-core

@@ -55,6 +55,8 @@ def lib():
         L.hh_ref_apply_signed.restype = i32
         L.hh_ref_knn.argtypes = [i64, i64, p, p, p, i64, p, i64, i32, p, p]
         L.hh_ref_knn.restype = i32
+        L.hh_ref_congruence.argtypes = [i32, i64, i64, p, p, p, i64]
+        L.hh_ref_congruence.restype = i32
         L.hh_ref_sym_apply_signed.restype = i32
         L.hh_ref_num_threads.restype = i32
         L.hh_ref_set_threads.argtypes = [i32]
@@ -164,3 +166,16 @@ def knn(U, d, P_ref, P_query, k: int):
     if rc:
         raise ValueError(f"hh_ref_knn rc={rc}")
     return idx, dist
+
+
+def congruence(op: int, U, M) -> np.ndarray:
+    """op(Q) M_b op(Q)^T for M of shape (count, n, n) holding column-major matrices, i.e.
+    M[b] is the TRANSPOSE of the math matrix (hh_ref.c: hh_ref_congruence, NEXT-f4)."""
+    M = _f64(M)
+    count, n, _ = M.shape
+    U = _f64(U).reshape(-1, n) if np.size(U) else np.zeros((0, n))
+    out = np.empty_like(M)
+    rc = lib().hh_ref_congruence(int(op), n, U.shape[0], _ptr(U), _ptr(M), _ptr(out), count)
+    if rc:
+        raise ValueError(f"hh_ref_congruence rc={rc}")
+    return out

@@ -252,6 +252,34 @@ int hh_ref_knn(int64_t n, int64_t h, const double *U, const double *d, const dou
     return bad ? 2 : 0;
 }
 
+/* NEXT-f4: M_out = op(Q) M op(Q)^T for `count` n x n column-major matrices (the
+ * congruences A_k, B_k of eq:ak / eq:bk), literally: apply op(Q) to every
+ * column of M, transpose, apply again, transpose back. */
+int hh_ref_congruence(int op, int64_t n, int64_t h, const double *U, const double *M,
+                      double *Mout, int64_t count) {
+    if ((op != 0 && op != 1) || n < 1 || h < 0 || count < 0) return 1;
+    const size_t nn = (size_t)n * (size_t)n;
+    double *A = (double *)malloc(sizeof(double) * nn);
+    double *B = (double *)malloc(sizeof(double) * nn);
+    if (!A || !B) {
+        free(A);
+        free(B);
+        return 2;
+    }
+    int rc = 0;
+    for (int64_t b = 0; b < count && !rc; ++b) {
+        rc = hh_ref_apply(op, n, h, U, M + (size_t)b * nn, A, n);     /* A = op(Q) M */
+        for (int64_t c = 0; c < n; ++c)                              /* B = A^T */
+            for (int64_t r = 0; r < n; ++r) B[c * n + r] = A[r * n + c];
+        if (!rc) rc = hh_ref_apply(op, n, h, U, B, A, n);             /* A = op(Q) B */
+        for (int64_t c = 0; c < n; ++c)                              /* out = A^T */
+            for (int64_t r = 0; r < n; ++r) Mout[(size_t)b * nn + c * n + r] = A[r * n + c];
+    }
+    free(A);
+    free(B);
+    return rc;
+}
+
 int hh_ref_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -178,6 +178,15 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
         case HH_CALL_MAHALANOBIS:
             *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype));
             return HH_OK;
+        case HH_CALL_CONGRUENCE: {   /* N_or_M = count */
+            const size_t mb =
+                round256(static_cast<size_t>(n) * n * N_or_M * elem(dtype));
+            const size_t aw = use_wy(dtype, n, h, n * N_or_M, t_algo)
+                                  ? wy_plan(WY_APPLY_N, n, h, n * N_or_M).bytes
+                                  : 0;
+            *bytes = 2 * mb + aw;
+            return HH_OK;
+        }
         case HH_CALL_KNN:   /* N_or_M = M_ref, npairs = M_query; k = h is not needed: max */
             *bytes = knn_plan(n, N_or_M, npairs, 16, device_attr().sm_count).bytes;
             return HH_OK;
@@ -372,6 +381,40 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
     a.N = npairs;
     a.mode = MODE_PAIR;
     return run_fused(a, dtype, stream);
+}
+
+hh_status hh_congruence(hh_op op, int64_t n, int64_t h, const void *U, const void *M, void *Mout,
+                        int64_t count, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                        hh_stream_t stream) {
+    if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
+    if (count < 0) return HH_ERR_INVALID_VALUE;
+    hh_status st = check_common(n, h, U, n * count, dtype);
+    if (st != HH_OK) return st;
+    if (count == 0) return HH_OK;
+    if (!M || !Mout) return HH_ERR_INVALID_VALUE;
+    if (!aligned16(M) || !aligned16(Mout)) return HH_ERR_UNSUPPORTED;
+    size_t need = 0;
+    hh_workspace_bytes(HH_CALL_CONGRUENCE, n, h, count, 0, dtype, &need);
+    if (!workspace || workspace_bytes < need) return HH_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+    const size_t mb = round256(static_cast<size_t>(n) * n * count * elem(dtype));
+    char *w = static_cast<char *>(workspace);
+    void *T1 = w, *T2 = w + mb;
+    void *aws = w + 2 * mb;
+    const size_t awsb = need - 2 * mb;
+    const int64_t NC = n * count;
+    const int dt = dtype == HH_F32 ? 0 : 1;
+    // (op(Q) (op(Q) M)^T)^T = op(Q) M op(Q)^T
+    st = apply_impl(op, n, h, U, M, T1, NC, dtype, awsb ? aws : nullptr, awsb, stream, nullptr, 0);
+    if (st != HH_OK) return st;
+    if (map_err(launch_transpose(T1, T2, n, count, dt, stream)) != HH_OK) return HH_ERR_CUDA;
+    st = apply_impl(op, n, h, U, T2, T1, NC, dtype, awsb ? aws : nullptr, awsb, stream, nullptr, 0);
+    if (st != HH_OK) return st;
+    if (map_err(launch_transpose(T1, Mout, n, count, dt, stream)) != HH_OK) return HH_ERR_CUDA;
+    if (t_has_last) {
+        t_last.launches = 2 * t_last.launches + 2;
+    }
+    return HH_OK;
 }
 
 hh_status hh_knn(int64_t n, int64_t h, const void *U, const void *d, const void *P_ref,

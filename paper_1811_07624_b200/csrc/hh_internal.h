@@ -102,3 +102,9 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
                        cudaStream_t stream, LaunchInfo *info);
 
 }  // namespace hh
+
+namespace hh {
+// NEXT-f4 (hh_cong.cu): B_b = A_b^T for `count` column-major n x n matrices.
+cudaError_t launch_transpose(const void *A, void *B, int64_t n, int64_t count, int dtype,
+                             cudaStream_t stream);
+}  // namespace hh

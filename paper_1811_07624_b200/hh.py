@@ -24,7 +24,8 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "hh.h")
 HH_OK, HH_ERR_INVALID_VALUE, HH_ERR_UNSUPPORTED, HH_ERR_WORKSPACE, HH_ERR_CUDA = range(5)
 HH_F32, HH_F64 = 0, 1
 HH_OP_N, HH_OP_T = 0, 1
-HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST, HH_CALL_KNN = range(5)
+HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST, HH_CALL_KNN, \
+    HH_CALL_CONGRUENCE = range(6)
 HH_ALGO_AUTO, HH_ALGO_FUSED, HH_ALGO_WY = range(3)
 HH_SIDE_LEFT, HH_SIDE_RIGHT = range(2)
 
@@ -58,6 +59,8 @@ def lib() -> ctypes.CDLL:
         L.hh_sym_apply_signed.argtypes = [i64, i64, p, p, p, p, p, i64, i32, p, sz, p]
         L.hh_apply_signed.restype = i32
         L.hh_sym_apply_signed.restype = i32
+        L.hh_congruence.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
+        L.hh_congruence.restype = i32
         L.hh_knn.argtypes = [i64, i64, p, p, p, i64, p, i64, i32, p, p, i32, p, sz, p]
         L.hh_knn.restype = i32
         L.hh_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
@@ -309,6 +312,26 @@ def hh_mahalanobis(U: torch.Tensor, d: torch.Tensor, P: torch.Tensor, ia: torch.
                               None if fused else _ptr(workspace), wsb, _stream(stream))
     _check(st, "hh_mahalanobis")
     return dist
+
+
+def hh_congruence(op: int, U: torch.Tensor, M: torch.Tensor, out: Optional[torch.Tensor] = None,
+                  workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """op(Q) M_b op(Q)^T for M of shape (count, n, n), each M[b] a column-major n x n
+    matrix (i.e. the math matrix is M[b].T) (hh.h: hh_congruence, NEXT-f4)."""
+    _dev(M, "M")
+    count, n, _ = M.shape
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    if out is None:
+        out = torch.empty_like(M)
+    wsb = hh_workspace_bytes(HH_CALL_CONGRUENCE, n, h, count, 0, M.dtype)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=M.device)
+    st = lib().hh_congruence(int(op), n, h, _ptr(U) if h else None, _ptr(M), _ptr(out), count,
+                             _dtype(M), _ptr(workspace), workspace.numel(), _stream(stream))
+    _check(st, "hh_congruence")
+    return out
 
 
 def hh_knn(U: torch.Tensor, d: torch.Tensor, P_ref: torch.Tensor, P_query: torch.Tensor, k: int,

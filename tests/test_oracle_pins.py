@@ -424,3 +424,33 @@ def test_knn_bruteforce_and_invariants():
     for q in range(Mq):
         e = ((Pq[q] - Pr) ** 2).sum(1)
         assert np.array_equal(ie[q], np.argsort(e, kind="stable")[:k])
+
+
+
+# --------------------------------------------------------------------------- NEXT-f4
+def test_congruence_dense_and_shf_identity():
+    """op(Q) M op(Q)^T against the dense product; and the SHF identity
+    eq:symmetricWithHouseholder (P:291-304) with D = I:
+        ||S - Q diag(s) Q^T||_F = ||A_k - U_k B_k U_k||_F,
+    A_k = (U_{k-1}..U_1) S (U_1..U_{k-1}) = congruence(op T, u_1..u_{k-1}, S),
+    B_k = (U_{k+1}..U_h) diag(s) (U_h..U_{k+1}) = congruence(op N, u_{k+1}..u_h, diag(s))."""
+    g = gi.rng(908)
+    n, h = 10, 6
+    U = unit_rows(g, h, n)
+    M = g.standard_normal((3, n, n))            # storage: column-major (math matrix = M[b].T)
+    Q = dense_Q(U)
+    for op, Qop in ((0, Q), (1, Q.T)):
+        out = oracle.congruence(op, U, M)
+        for b in range(3):
+            assert rel(out[b].T, Qop @ M[b].T @ Qop.T) < 1e-13
+    A = g.standard_normal((n, n))
+    S = A + A.T
+    s = g.standard_normal(n)
+    Sbar = Q @ np.diag(s) @ Q.T
+    for k in range(1, h + 1):                   # 1-based k as in the paper
+        Ak = oracle.congruence(1, U[:k - 1], S[None])[0].T
+        Bk = oracle.congruence(0, U[k:], np.diag(s)[None])[0].T
+        Hk = dense_reflector(U[k - 1])
+        lhs = np.linalg.norm(S - Sbar)
+        rhs = np.linalg.norm(Ak - Hk @ Bk @ Hk)
+        assert abs(lhs - rhs) < 1e-12 * max(1.0, lhs)
