@@ -191,3 +191,14 @@ def make_knn_case(n: int = 40, h: int = 6, M_ref: int = 49000, M_query: int = 21
     c = Case(f"KNN-n{n}-h{h}", "knn", n, h, M_ref, "f32", U, Pr, lam=Pq, d=d)
     c.k = k
     return c
+
+
+def qr_reflectors(g: np.random.Generator, h: int, n: int, dtype: str = "f64") -> np.ndarray:
+    """(h, n) unit reflectors with the partial-QR structure of Result 3 (PAPER.md l.218-261:
+    J_k has k-1 leading zeros): row i is zero before column i, Gaussian after, normalised."""
+    u = g.standard_normal((h, n))
+    for i in range(h):
+        u[i, :i] = 0.0
+    if h:
+        u /= np.sqrt((u * u).sum(axis=1, keepdims=True))
+    return np.ascontiguousarray(u.astype(np_dtype(dtype)))

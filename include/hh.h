@@ -158,6 +158,20 @@ hh_status hh_apply_signed(hh_op op, hh_side side, int64_t n, int64_t h, const vo
                           void *workspace, size_t workspace_bytes, hh_stream_t stream);
 
 /*
+ * hh_apply_qr -- hh_apply for QR-structured ("trapezoidal") reflectors (NEXT-f2):
+ *   the caller guarantees u_i[r] = 0 for r < i (0-based), the structure of the partial
+ *   QR reflectors J_k of Result 3 ("k-1 leading zeros ... 4(n-k+1) operations", P:218-237,
+ *   P:261; h = n-1 of them reproduce any orthonormal matrix up to +-1).  The
+ *   kernels skip the zero prefix (warp-uniform vector chunks in K1; the leading K steps
+ *   of the projection and the leading row chunks of the update in K5), so a reflector
+ *   costs ~4(n-i) instead of 4n.  Same arguments, workspace and errors as hh_apply; the
+ *   result is identical to hh_apply on the same U when the precondition holds.
+ */
+hh_status hh_apply_qr(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
+                      int64_t N, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                      hh_stream_t stream);
+
+/*
  * hh_sym_apply_signed -- Y = D Q diag(lambda) Q^T D X, the symmetric form of
  * eq:thesbar with its diagonal D on both sides.  Workspace as
  * hh_sym_apply (HH_CALL_SYM).

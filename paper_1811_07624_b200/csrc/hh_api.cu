@@ -213,7 +213,7 @@ hh_algo hh_get_algo(void) { return static_cast<hh_algo>(t_algo); }
 static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
                             void *Y, int64_t N, hh_dtype dtype, void *workspace,
                             size_t workspace_bytes, hh_stream_t stream, const void *dsign,
-                            int dside) {
+                            int dside, int qr = 0) {
     if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
     hh_status st = check_common(n, h, U, N, dtype);
     if (st != HH_OK) return st;
@@ -223,7 +223,8 @@ static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const
     if (dside && !dsign) return HH_ERR_INVALID_VALUE;
     if (dside && !aligned16(dsign)) return HH_ERR_UNSUPPORTED;
     if (h > 0 && use_wy(dtype, n, h, N, t_algo)) {
-        const WyPlan p = wy_plan(op == HH_OP_T ? WY_APPLY_T : WY_APPLY_N, n, h, N);
+        WyPlan p = wy_plan(op == HH_OP_T ? WY_APPLY_T : WY_APPLY_N, n, h, N);
+        p.qr = qr;
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
         if (workspace && !aligned16(workspace)) return HH_ERR_UNSUPPORTED;
         if (!workspace && t_algo == HH_ALGO_WY) return HH_ERR_WORKSPACE;
@@ -251,7 +252,15 @@ static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const
     a.mode = op == HH_OP_N ? MODE_APPLY_N : MODE_APPLY_T;
     a.dsign = dsign;
     a.dside = dside;
+    a.qr = qr;
     return run_fused(a, dtype, stream);
+}
+
+hh_status hh_apply_qr(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
+                      int64_t N, hh_dtype dtype, void *workspace, size_t workspace_bytes,
+                      hh_stream_t stream) {
+    return apply_impl(op, n, h, U, X, Y, N, dtype, workspace, workspace_bytes, stream, nullptr, 0,
+                      1);
 }
 
 hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,

@@ -29,6 +29,7 @@ struct FusedArgs {
     int nbatches;       // batches per unit (uniform over the grid)
     const void *dsign;  // NEXT-f1: the diagonal D of Eq. 1 (n values) or NULL
     int dside;          // bit 0: x <- D x before the reflectors, bit 1: y <- D y after
+    int qr;             // NEXT-f2: u_i[r] = 0 for r < i (partial-QR reflectors)
 };
 
 struct LaunchInfo {
@@ -67,6 +68,7 @@ struct WyPlan {
     int kind = 0;
     int64_t n = 0, h = 0, N = 0;
     int b = 0, nblk = 0, h_pad = 0, extra = 0, nsplit = 0;
+    int qr = 0;   // NEXT-f2: block k's W rows (and V rows) are zero above row k*b
     int64_t n_pad = 0;
     size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_v = 0, off_v2 = 0,
            off_asym = 0, off_vf = 0, off_vpf = 0, off_pp = 0, off_p = 0, off_m = 0, off_gt = 0,

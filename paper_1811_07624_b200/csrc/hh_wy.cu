@@ -379,7 +379,7 @@ struct Bars1 {
 __global__ void __launch_bounds__(480, 1)
     wy_project_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       uint16_t *__restrict__ Gt, int n, int64_t N, int b, int wrow_hi, int wrow_lo,
-                      int ntiles, const float *__restrict__ dscale) {
+                      int ntiles, const float *__restrict__ dscale, int ks0) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(480, 1)
             int s = 0;
             uint32_t ph = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int ks = 0; ks < nk; ++ks) {
+                for (int ks = ks0; ks < nk; ++ks) {
                     mbar_wait(&bars->rempty[s], ph ^ 1u);
                     mbar_arrive_expect_tx(&bars->rfull[s], static_cast<uint32_t>(kRawBytes));
                     tc::tma_load_2d(rawX(s), &tmX, ks * 32, tile * kTileCols, &bars->rfull[s]);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(480, 1)
             uint32_t ph = 0;
             const uint32_t bytes = 128u * static_cast<uint32_t>(b);
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int ks = 0; ks < nk; ++ks) {
+                for (int ks = ks0; ks < nk; ++ks) {
                     mbar_wait(&bars->cempty[s], ph ^ 1u);
                     mbar_arrive_expect_tx(&bars->wfull[s], bytes);
                     tc::tma_load_2d(Whi(s), &tmW, ks * 32, wrow_hi, &bars->wfull[s]);
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(480, 1)
                 mbar_wait(&bars->acc_empty[a], aph ^ 1u);
                 tc::fence_after_sync();
                 const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
-                for (int ks = 0; ks < nk; ++ks) {
+                for (int ks = ks0; ks < nk; ++ks) {
                     mbar_wait(&bars->wfull[s], ph);
                     mbar_wait(&bars->cfull[s], ph);
                     tc::fence_after_sync();
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(480, 1)
                     for (int kk = 0; kk < 2; ++kk) {
                         const uint64_t ah = tc::sdesc_sw64(xh + kk * 32), alo = tc::sdesc_sw64(xl + kk * 32);
                         const uint64_t bh = tc::sdesc_sw64(wh + kk * 32), blo = tc::sdesc_sw64(wl + kk * 32);
-                        tc::mma_bf16(d, ah, bh, idesc, (ks | kk) != 0);
+                        tc::mma_bf16(d, ah, bh, idesc, (ks != ks0 || kk != 0) ? 1u : 0u);
                         tc::mma_bf16(d, ah, blo, idesc, 1u);
                         tc::mma_bf16(d, alo, bh, idesc, 1u);
                     }
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(480, 1)
         int rs = 0, cs = 0;
         uint32_t rph = 0, cph = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            for (int ks = 0; ks < nk; ++ks) {
+            for (int ks = ks0; ks < nk; ++ks) {
                 mbar_wait(&bars->rfull[rs], rph);
                 const float4 *raw = reinterpret_cast<const float4 *>(rawX(rs));
                 float4 v[4];
@@ -605,7 +605,8 @@ __global__ void __launch_bounds__(384, 1)
     wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmXb, float *Y,
                      const float *__restrict__ lam, const float *__restrict__ post, int n,
-                     int n_pad, int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles) {
+                     int n_pad, int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles, int rc0,
+                     int copy_below) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -659,7 +660,7 @@ __global__ void __launch_bounds__(384, 1)
                                     static_cast<int>(N) + tile * kTileCols, &bars->gfull);
                 }
                 gph ^= 1u;
-                for (int rc = 0; rc < nrc; ++rc) {
+                for (int rc = rc0; rc < nrc; ++rc) {
                     for (int c = 0; c < nslab; ++c) {
                         mbar_wait(&bars->empty[s], ph ^ 1u);
                         mbar_arrive_expect_tx(&bars->full[s], static_cast<uint32_t>(kStage3Bytes));
@@ -683,7 +684,7 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_wait(&bars->gfull, gph);
                 gph ^= 1u;
                 tc::fence_after_sync();
-                for (int rc = 0; rc < nrc; ++rc) {
+                for (int rc = rc0; rc < nrc; ++rc) {
                     mbar_wait(&bars->acc_empty[a], aph ^ 1u);
                     tc::fence_after_sync();
                     const uint32_t d = tbase + static_cast<uint32_t>(a * kTileCols);
@@ -721,8 +722,9 @@ __global__ void __launch_bounds__(384, 1)
             tc::prefetch_tmap(&tmXb);
             int s = 0;
             uint32_t ph = 0;
+            const int xrc0 = copy_below ? 0 : rc0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int rc = 0; rc < nrc; ++rc) {
+                for (int rc = xrc0; rc < nrc; ++rc) {
                     for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb) {
                         mbar_wait(&bars->xempty[s], ph ^ 1u);
                         mbar_arrive_expect_tx(&bars->xfull[s], static_cast<uint32_t>(kXBoxBytes));
@@ -744,10 +746,16 @@ __global__ void __launch_bounds__(384, 1)
         constexpr int kBoxes = kTileCols / kXBoxCols;   // X boxes per r-chunk
         static_assert(kXStages % 2 == 0 && kBoxes % 2 == 0, "one consumer group per stage");
         int64_t seq = 0;   // position in the X box ring (both groups follow it)
+        const int xrc0 = copy_below ? 0 : rc0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            for (int rc = 0; rc < nrc; ++rc, seq += kBoxes) {
-                mbar_wait(&bars->acc_full[a], aph);
-                tc::fence_after_sync();
+            for (int rc = xrc0; rc < nrc; ++rc, seq += kBoxes) {
+                // NEXT-f2: below row rc0*128 the block's V rows are zero, no MMA ran: those
+                // rows are copied (scaled) when the pass is out of place
+                const bool mma_rc = rc >= rc0;
+                if (mma_rc) {
+                    mbar_wait(&bars->acc_full[a], aph);
+                    tc::fence_after_sync();
+                }
                 const int r = rc * kRowChunk + r_in;
                 // pre-scale of X (Lambda for the symmetric block, D for a right factor D)
                 // and post-scale of the result (a left factor D, NEXT-f1)
@@ -763,9 +771,14 @@ __global__ void __launch_bounds__(384, 1)
                     const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + cb * kXBoxCols;
                     float *dst = Y + j0 * n + r;
                     float v[16];
-                    tc::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                                      static_cast<uint32_t>(a * kTileCols + cb * kXBoxCols),
-                                  v);
+                    if (mma_rc) {
+                        tc::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                          static_cast<uint32_t>(a * kTileCols + cb * kXBoxCols),
+                                      v);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                    }
                     if (r < n) {
 #pragma unroll
                         for (int e = 0; e < kXBoxCols; ++e) {
@@ -776,11 +789,13 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     tc::mbar_arrive(&bars->xempty[s]);
                 }
-                tc::fence_before_sync();
-                tc::mbar_arrive(&bars->acc_empty[a]);
-                if (++a == 2) {
-                    a = 0;
-                    aph ^= 1u;
+                if (mma_rc) {
+                    tc::fence_before_sync();
+                    tc::mbar_arrive(&bars->acc_empty[a]);
+                    if (++a == 2) {
+                        a = 0;
+                        aph ^= 1u;
+                    }
                 }
             }
         }
@@ -899,6 +914,7 @@ struct Pass {
     const float *dscale = nullptr;   // project D X (first pass, right factor D)
     const float *pre = nullptr;      // update pre-scale of X (Lambda, D, or Lambda D)
     const float *post = nullptr;     // update post-scale (last pass, left factor D)
+    int row0 = 0;                    // NEXT-f2: first row where the block's W / V are nonzero
 };
 
 }  // namespace
@@ -1031,6 +1047,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     auto blockpass = [&](int k, const CUtensorMap *mv) {
         Pass ps{k * b, b, &mWb, &mGb, mv, static_cast<int>(k * n_pad),
                 static_cast<int>((m + k) * n_pad), false};
+        if (p.qr) ps.row0 = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(k) * b, p.n - 1));
         prog[np++] = ps;
     };
     if (p.kind == WY_APPLY_N) {
@@ -1070,11 +1087,12 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         ++nlaunch, wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, *ps.mW, Gt, static_cast<int>(p.n),
                                                           N, ps.kw, ps.wrow,
                                                           static_cast<int>(R) + ps.wrow, ntiles,
-                                                          ps.dscale);
+                                                          ps.dscale, ps.row0 / 32);
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
         ++nlaunch, wy_update_kernel<<<grid, 384, smem3(), stream>>>(
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
-            static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles);
+            static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
+            ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0);
         cur = Y;
     }
     if (info) {

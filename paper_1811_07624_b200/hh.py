@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         L.hh_sym_apply_signed.argtypes = [i64, i64, p, p, p, p, p, i64, i32, p, sz, p]
         L.hh_apply_signed.restype = i32
         L.hh_sym_apply_signed.restype = i32
+        L.hh_apply_qr.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
+        L.hh_apply_qr.restype = i32
         L.hh_congruence.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
         L.hh_congruence.restype = i32
         L.hh_knn.argtypes = [i64, i64, p, p, p, i64, p, i64, i32, p, p, i32, p, sz, p]
@@ -312,6 +314,28 @@ def hh_mahalanobis(U: torch.Tensor, d: torch.Tensor, P: torch.Tensor, ia: torch.
                               None if fused else _ptr(workspace), wsb, _stream(stream))
     _check(st, "hh_mahalanobis")
     return dist
+
+
+def hh_apply_qr(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor] = None,
+                workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """hh_apply for QR-structured reflectors (u_i[r] = 0 for r < i), skipping the zero
+    prefix (hh.h: hh_apply_qr, NEXT-f2)."""
+    _dev(X, "X")
+    N, n = X.shape
+    h = U.shape[0] if U.numel() else 0
+    if h:
+        _dev(U, "U")
+    if Y is None:
+        Y = torch.empty_like(X)
+    _dev(Y, "Y")
+    wsb = hh_workspace_bytes(HH_CALL_APPLY, n, h, N, 0, X.dtype) if N else 0
+    if wsb and (workspace is None or workspace.numel() < wsb):
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
+    st = lib().hh_apply_qr(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N, _dtype(X),
+                           _ptr(workspace) if wsb else None, workspace.numel() if wsb else 0,
+                           _stream(stream))
+    _check(st, "hh_apply_qr")
+    return Y
 
 
 def hh_congruence(op: int, U: torch.Tensor, M: torch.Tensor, out: Optional[torch.Tensor] = None,
