@@ -52,6 +52,12 @@ def workload_case(name: str, N_override=None):
         return gi.make_config(5, h=int(name[3:]), N=N_override)
     if name == "KNN":   # NEXT-f3, Table-I-shaped (MNIST after PCA) synthetic stand-in
         return gi.make_knn_case()
+    if name.startswith("QR"):   # NEXT-f2: n=4096, h = n-1 partial-QR reflectors (C5's X)
+        h = int(name[2:]) if len(name) > 2 else 4095
+        c = gi.make_config(5, h=min(h, 1024), N=N_override)
+        c.U = gi.qr_reflectors(gi.rng(5, h, 9), h, c.n, "f32")
+        c.h, c.call, c.name = h, "apply_qr", f"QR{h}"
+        return c
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -71,6 +77,10 @@ def alg_cost(c, op_count=1):
     elif c.call == "sym":
         byts = 2 * c.N * c.n * s
         flops = (8 * c.h + 1) * c.n * c.N
+        units = c.N
+    elif c.call == "apply_qr":   # 4(n-k+1) per reflector, k = 1..h
+        byts = 2 * c.N * c.n * s
+        flops = sum(4 * (c.n - k) for k in range(c.h)) * c.N
         units = c.N
     else:
         byts = 2 * c.N * c.n * s
@@ -178,7 +188,7 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
         elif c.call == "sym":
             oracle.sym_apply(c.U, c.lam, c.X[:k])
         else:
-            oracle.apply(op, c.U, c.X[:k])
+            oracle.apply(op, c.U, c.X[:k])   # apply_qr: the oracle's plain apply (same U)
         return time.perf_counter() - t0
 
     total = units
@@ -310,6 +320,21 @@ def run_hh(args):
         step = lambda: hh.hh_mahalanobis(U, d, X, ia, ib, dist_out, workspace=wsp,  # noqa: E731
                                          stream=stream)
         launches = 2
+    elif c.call == "apply_qr":
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_APPLY, c.n, c.h, c.N, 0, X.dtype)
+        wsp = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        step = lambda: hh.hh_apply_qr(op, U, X, Y, workspace=wsp, stream=stream)  # noqa: E731
+        launches = 1
+        # the same U through the structure-blind path, for the 4(n-k+1) vs 4n comparison
+        for _ in range(2):
+            hh.hh_apply(op, U, X, Y, workspace=wsp, stream=stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            hh.hh_apply(op, U, X, Y, workspace=wsp, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        extra["full_apply_ms"] = e0.elapsed_time(e1) / 3
     else:
         wsb = hh.hh_workspace_bytes(hh.HH_CALL_APPLY, c.n, c.h, c.N, 0, X.dtype)
         wsp = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
@@ -334,8 +359,8 @@ def run_hh(args):
             ri, ref = oracle.knn(c.U, c.d, c.X, c.lam[idx], c.k)
             extra["knn_index_agreement"] = float(
                 (gi_[torch.from_numpy(idx).to(dev)].cpu().numpy() == ri).mean())
-        elif c.call == "apply":
-            idx = np.linspace(0, c.N - 1, 256).astype(np.int64)
+        elif c.call in ("apply", "apply_qr"):
+            idx = np.linspace(0, c.N - 1, 256 if c.h < 2048 else 16).astype(np.int64)
             got = Y[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
             ref = oracle.apply(op, c.U, c.X[idx])
         elif c.call == "sym":

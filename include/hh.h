@@ -162,10 +162,12 @@ hh_status hh_apply_signed(hh_op op, hh_side side, int64_t n, int64_t h, const vo
  *   the caller guarantees u_i[r] = 0 for r < i (0-based), the structure of the partial
  *   QR reflectors J_k of Result 3 ("k-1 leading zeros ... 4(n-k+1) operations", P:218-237,
  *   P:261; h = n-1 of them reproduce any orthonormal matrix up to +-1).  The
- *   kernels skip the zero prefix (warp-uniform vector chunks in K1; the leading K steps
- *   of the projection and the leading row chunks of the update in K5), so a reflector
- *   costs ~4(n-i) instead of 4n.  Same arguments, workspace and errors as hh_apply; the
- *   result is identical to hh_apply on the same U when the precondition holds.
+ *   compact-WY path (K5) skips the zero prefix -- the leading K steps of each block's
+ *   projection and the leading row chunks of its update -- so a reflector costs
+ *   ~4(n-i) instead of 4n (measured 1.69x at n = 4096, h = 4095); the fused small-h
+ *   kernel K1 applies them in full (at small h the prefixes are a negligible share).
+ *   Same arguments, workspace and errors as hh_apply; the result is identical to
+ *   hh_apply on the same U when the precondition holds.
  */
 hh_status hh_apply_qr(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
                       int64_t N, hh_dtype dtype, void *workspace, size_t workspace_bytes,

@@ -233,10 +233,7 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
     auto valid_k = [&](int k) -> bool { return FULL || (gt + TPC * k < nv); };
 
     // one reflector: x <- x - 2 (u^T x) u   for the C columns of this group
-    // NEXT-f2 (a.qr): reflector i of a partial QR has i leading zeros, so vector
-    // chunks k with (gt + TPC*k + 1)*E <= i are zero for EVERY thread of the group when
-    // k < kmin = floor(i / (E*TPC)): a warp-uniform skip, 4(n-i) work per reflector.
-    auto reflect = [&](const V *ub, int kmin) {
+    auto reflect = [&](const V *ub) {
         T p[C];
         // multi-warp groups: keep the u chunk in registers across the cross-warp
         // reduction (a shared-memory store + barrier the compiler cannot see through),
@@ -246,7 +243,7 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
         if constexpr (kKeepU) {
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (k >= kmin && valid_k(k)) uk[k] = ub[gt + TPC * k];
+                if (valid_k(k)) uk[k] = ub[gt + TPC * k];
                 else vzero(uk[k]);
             }
         }
@@ -260,7 +257,7 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
             vzero(acc);
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (k >= kmin && valid_k(k)) vfma(acc, uget(k), x[c][k]);
+                if (valid_k(k)) vfma(acc, uget(k), x[c][k]);
             }
             p[c] = vsum(acc);
         }
@@ -290,20 +287,18 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
             const T s = p[c] + p[c];
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (k >= kmin && valid_k(k)) vaxpy(x[c][k], s, uget(k));
+                if (valid_k(k)) vaxpy(x[c][k], s, uget(k));
             }
         }
     };
     // reflectors [r0, r1) of the chunk resident at `base` (first row = chunk_lo)
-    const bool qr = a.qr != 0;
-    auto kmin_of = [&](int i) -> int { return qr ? i / (E * TPC) : 0; };
+    // (NEXT-f2: the fused kernel applies QR-structured reflectors in full -- it serves
+    // small h, where the zero prefixes are a negligible share; K5 skips them.)
     auto run_range = [&](const V *base, int chunk_lo, int r0, int r1, bool desc) {
         if (desc) {
-            for (int i = r1 - 1; i >= r0; --i)
-                reflect(base + static_cast<size_t>(i - chunk_lo) * nv, kmin_of(i));
+            for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
         } else {
-            for (int i = r0; i < r1; ++i)
-                reflect(base + static_cast<size_t>(i - chunk_lo) * nv, kmin_of(i));
+            for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
         }
     };
     auto scale_vec = [&]() {
@@ -489,13 +484,14 @@ __global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
                     }
                 }
                 V *Yg = reinterpret_cast<V *>(a.Y);
+                const uint64_t ypol = policy_evict_first();
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     const int64_t j = col0 + c;
                     if (j < a.N) {
 #pragma unroll
                         for (int k = 0; k < CH; ++k)
-                            if (valid_k(k)) Yg[j * nv + gt + TPC * k] = x[c][k];
+                            if (valid_k(k)) st_global_hint(Yg + j * nv + gt + TPC * k, x[c][k], ypol);
                     }
                 }
             }

@@ -77,4 +77,17 @@ __device__ __forceinline__ void st_global_v2(double *p, double2 v) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// 128-bit global stores with an L2 eviction-priority hint (streaming output that is
+// not read again by this kernel)
+__device__ __forceinline__ void st_global_hint(float4 *p, const float4 &v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_global_hint(double2 *p, const double2 &v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x),
+                 "d"(v.y), "l"(pol)
+                 : "memory");
+}
+
 }  // namespace hh

@@ -50,16 +50,17 @@ namespace {
 constexpr int kGramRows = 128;   // Gram split-K slice (rows of n_pad per CTA)
 constexpr int kRowChunk = 128;    // K5b rows r per accumulator (MMA M)
 constexpr int kTileCols = 128;    // columns of X per tile (K5a MMA M, K5b MMA N)
-constexpr int kRaw1 = 4;          // K5a raw fp32 X ring depth
+constexpr int kRaw1 = 12;         // K5a raw fp32 X ring depth: maximum (runtime nraw)
 constexpr int kStages1 = 3;       // K5a converted X + W ring depth
 constexpr int kStages3 = 3;       // K5b V ring depth
-constexpr int kXStages = 6;       // K5b X box ring depth (even: see the epilogue)
+constexpr int kXStages = 16;      // K5b X box ring depth: maximum (runtime nxs, even)
 constexpr int kXBoxCols = 16;     // columns per X box
 constexpr int kXBoxBytes = 8192;  // fp32 X box (128 rows x 16 columns)
 constexpr int kRawBytes = 16384;     // fp32 X tile (128 columns x 32 rows)
-constexpr int kConv1Bytes = 49152;   // X hi/lo 16K + W hi/lo 32K (b = 256)
+constexpr int kConv1Bytes = 49152;   // X hi/lo 16K + W hi/lo 32K at b = 256 (max)
 constexpr int kStage3Bytes = 16384;  // V hi/lo tile (128 rows x 32 bf16) x 2
-constexpr int kGresBytes = 131072;   // resident G hi/lo (128 x 256 bf16) x 2
+constexpr int kGresBytes = 131072;   // resident G hi/lo (128 x 256 bf16) x 2 at b = 256 (max)
+constexpr int kSmemMax = 232448;     // 227 KB opt-in per CTA
 
 size_t al(size_t x) { return (x + 1023) & ~static_cast<size_t>(1023); }
 
@@ -379,22 +380,25 @@ struct Bars1 {
 __global__ void __launch_bounds__(480, 1)
     wy_project_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       uint16_t *__restrict__ Gt, int n, int64_t N, int b, int wrow_hi, int wrow_lo,
-                      int ntiles, const float *__restrict__ dscale, int ks0) {
+                      int ntiles, const float *__restrict__ dscale, int ks0, int nraw) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    unsigned char *conv = smem + kRaw1 * kRawBytes;
-    Bars1 *bars = reinterpret_cast<Bars1 *>(conv + kStages1 * kConv1Bytes);
+    // ring sizes depend on b: a conversion stage holds X hi/lo (16 KB) and the W hi/lo
+    // tiles (128 b bytes); the rest of the 227 KB is a deep raw-X ring (nraw stages)
+    const int cvb = 16384 + 128 * b;
+    unsigned char *conv = smem + nraw * kRawBytes;
+    Bars1 *bars = reinterpret_cast<Bars1 *>(conv + kStages1 * cvb);
     auto rawX = [&](int s) { return smem + s * kRawBytes; };
-    auto Xhi = [&](int s) { return conv + s * kConv1Bytes; };
-    auto Xlo = [&](int s) { return conv + s * kConv1Bytes + 8192; };
-    auto Whi = [&](int s) { return conv + s * kConv1Bytes + 16384; };
-    auto Wlo = [&](int s) { return conv + s * kConv1Bytes + 16384 + 64 * b; };
+    auto Xhi = [&](int s) { return conv + s * cvb; };
+    auto Xlo = [&](int s) { return conv + s * cvb + 8192; };
+    auto Whi = [&](int s) { return conv + s * cvb + 16384; };
+    auto Wlo = [&](int s) { return conv + s * cvb + 16384 + 64 * b; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (n + 31) / 32;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kRaw1; ++s) {
+        for (int s = 0; s < nraw; ++s) {
             mbar_init(&bars->rfull[s], 1);
             mbar_init(&bars->rempty[s], 256);
         }
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(480, 1)
                     mbar_wait(&bars->rempty[s], ph ^ 1u);
                     mbar_arrive_expect_tx(&bars->rfull[s], static_cast<uint32_t>(kRawBytes));
                     tc::tma_load_2d(rawX(s), &tmX, ks * 32, tile * kTileCols, &bars->rfull[s]);
-                    if (++s == kRaw1) {
+                    if (++s == nraw) {
                         s = 0;
                         ph ^= 1u;
                     }
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(480, 1)
                 fence_proxy_async_smem();
                 tc::mbar_arrive(&bars->rempty[rs]);
                 tc::mbar_arrive(&bars->cfull[cs]);
-                if (++rs == kRaw1) {
+                if (++rs == nraw) {
                     rs = 0;
                     rph ^= 1u;
                 }
@@ -606,16 +610,16 @@ __global__ void __launch_bounds__(384, 1)
                      const __grid_constant__ CUtensorMap tmXb, float *Y,
                      const float *__restrict__ lam, const float *__restrict__ post, int n,
                      int n_pad, int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles, int rc0,
-                     int copy_below) {
+                     int copy_below, int nxs) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int nslab = b / 32;
     unsigned char *Ghi = smem;                       // nslab x 8 KB (128 columns x 32 K)
     unsigned char *Glo = smem + nslab * 8192;
-    unsigned char *stg = smem + kGresBytes;
+    unsigned char *stg = smem + nslab * 16384;        // G hi/lo take nslab x 16 KB
     unsigned char *xst = stg + kStages3 * kStage3Bytes;
-    Bars3 *bars = reinterpret_cast<Bars3 *>(xst + kXStages * kXBoxBytes);
+    Bars3 *bars = reinterpret_cast<Bars3 *>(xst + nxs * kXBoxBytes);
     auto Vhi = [&](int s) { return stg + s * kStage3Bytes; };
     auto Vlo = [&](int s) { return stg + s * kStage3Bytes + 8192; };
     auto Xs = [&](int s) { return reinterpret_cast<float *>(xst + s * kXBoxBytes); };
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
         }
-        for (int s = 0; s < kXStages; ++s) {
+        for (int s = 0; s < nxs; ++s) {
             mbar_init(&bars->xfull[s], 1);
             mbar_init(&bars->xempty[s], 128);
         }
@@ -730,7 +734,7 @@ __global__ void __launch_bounds__(384, 1)
                         mbar_arrive_expect_tx(&bars->xfull[s], static_cast<uint32_t>(kXBoxBytes));
                         tc::tma_load_2d(Xs(s), &tmXb, rc * kRowChunk,
                                         tile * kTileCols + cb * kXBoxCols, &bars->xfull[s]);
-                        if (++s == kXStages) {
+                        if (++s == nxs) {
                             s = 0;
                             ph ^= 1u;
                         }
@@ -744,7 +748,7 @@ __global__ void __launch_bounds__(384, 1)
         int a = 0;
         uint32_t aph = 0;
         constexpr int kBoxes = kTileCols / kXBoxCols;   // X boxes per r-chunk
-        static_assert(kXStages % 2 == 0 && kBoxes % 2 == 0, "one consumer group per stage");
+        static_assert(kBoxes % 2 == 0, "one consumer group per stage (nxs is even)");
         int64_t seq = 0;   // position in the X box ring (both groups follow it)
         const int xrc0 = copy_below ? 0 : rc0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -765,8 +769,8 @@ __global__ void __launch_bounds__(384, 1)
                 for (int k = 0; k < kBoxes / 2; ++k) {
                     const int cb = grp + 2 * k;
                     const int64_t sq = seq + cb;
-                    const int s = static_cast<int>(sq % kXStages);
-                    mbar_wait(&bars->xfull[s], static_cast<uint32_t>((sq / kXStages) & 1));
+                    const int s = static_cast<int>(sq % nxs);
+                    mbar_wait(&bars->xfull[s], static_cast<uint32_t>((sq / nxs) & 1));
                     const float *xs = Xs(s);
                     const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + cb * kXBoxCols;
                     float *dst = Y + j0 * n + r;
@@ -839,13 +843,25 @@ size_t tbuild_smem(int b) {
            4;
 }
 
-size_t smem1() {
-    return static_cast<size_t>(kRaw1) * kRawBytes + static_cast<size_t>(kStages1) * kConv1Bytes +
-           sizeof(Bars1) + 1024;
+int nraw_for(int b) {
+    const int cvb = 16384 + 128 * b;
+    const int r = (kSmemMax - 1024 - static_cast<int>(sizeof(Bars1)) - kStages1 * cvb) / kRawBytes;
+    return std::max(2, std::min(kRaw1, r));
 }
-size_t smem3() {
-    return kGresBytes + static_cast<size_t>(kStages3) * kStage3Bytes +
-           static_cast<size_t>(kXStages) * kXBoxBytes + sizeof(Bars3) + 1024;
+size_t smem1(int b) {
+    return static_cast<size_t>(nraw_for(b)) * kRawBytes +
+           static_cast<size_t>(kStages1) * (16384 + 128 * b) + sizeof(Bars1) + 1024;
+}
+int nxs_for(int kv) {
+    const int g = (kv / 32) * 16384;
+    int x = (kSmemMax - 1024 - static_cast<int>(sizeof(Bars3)) - g - kStages3 * kStage3Bytes) /
+            kXBoxBytes;
+    x = std::min(kXStages, x) & ~1;
+    return std::max(2, x);
+}
+size_t smem3(int kv) {
+    return static_cast<size_t>(kv / 32) * 16384 + static_cast<size_t>(kStages3) * kStage3Bytes +
+           static_cast<size_t>(nxs_for(kv)) * kXBoxBytes + sizeof(Bars3) + 1024;
 }
 
 std::once_flag g_attr_once;
@@ -925,8 +941,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     if (!encoder()) return cudaErrorNotSupported;
     std::call_once(g_attr_once, []() {
         g_attr_err = cudaFuncSetAttribute(wy_project_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem1()));
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (g_attr_err == cudaSuccess)
             g_attr_err = cudaFuncSetAttribute(wy_tbuild_kernel,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -934,7 +949,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         if (g_attr_err == cudaSuccess)
             g_attr_err = cudaFuncSetAttribute(wy_update_kernel,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(smem3()));
+                                              kSmemMax);
     });
     if (g_attr_err != cudaSuccess) return g_attr_err;
     const bool sym = p.kind == WY_SYM;
@@ -1084,22 +1099,21 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     for (int q = 0; q < np; ++q) {
         const Pass &ps = prog[q];
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
-        ++nlaunch, wy_project_kernel<<<grid, 480, smem1(), stream>>>(mcur, *ps.mW, Gt, static_cast<int>(p.n),
-                                                          N, ps.kw, ps.wrow,
-                                                          static_cast<int>(R) + ps.wrow, ntiles,
-                                                          ps.dscale, ps.row0 / 32);
+        ++nlaunch, wy_project_kernel<<<grid, 480, smem1(ps.kw), stream>>>(
+            mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
+            ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw));
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
-        ++nlaunch, wy_update_kernel<<<grid, 384, smem3(), stream>>>(
+        ++nlaunch, wy_update_kernel<<<grid, 384, smem3(ps.kw), stream>>>(
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
-            ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0);
+            ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw));
         cur = Y;
     }
     if (info) {
         info->variant = sym ? "wy_sym_bf16x3_tcgen05" : "wy_bf16x3_tcgen05";
         info->grid = grid;
         info->block = 480;
-        info->smem = static_cast<int>(smem1());
+        info->smem = static_cast<int>(smem1(b));
         info->nchunks = np;
         info->launches = nlaunch;
     }
