@@ -487,14 +487,20 @@ def run_hh(args):
             exe_bytes = sum(3 * c.N * c.n * s_ + 2 * c.N * k_ * 4 for k_ in kw)
             t_s = ms_step * 1e-3
             ef_t, ef_h = exe / t_s / 1e12 / tpeak, exe_bytes / t_s / 1e9 / hbm
-            if ef_t >= ef_h:
+            # the binding floor of the METHOD on this hardware: its HBM bytes at the copy
+            # rate vs its flops as bf16x3 products (3 per fp32-accurate product) at the
+            # bf16 rate; `floor_frac` = that floor / measured time
+            t_hbm, t_ten = byts / (hbm * 1e9), 3 * flops / (tpeak * 1e12)
+            if t_ten >= t_hbm:
                 roof = {"bound": "tensor", "achieved": flops / t_s / 1e12, "peak": tpeak,
                         "unit": "TFLOP/s", "frac": flops / t_s / 1e12 / tpeak,
                         "peak_source": "measured bf16 (MEASURED_PEAKS.json bf16_tflops)"}
             else:
                 roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                         "frac": achieved / hbm, "peak_source": hbm_src}
-            roof.update({"traffic": traffic, "executed_tflops": exe / t_s / 1e12,
+            roof.update({"floor_ms": 1e3 * max(t_hbm, t_ten),
+                         "floor_frac": max(t_hbm, t_ten) / t_s,
+                         "traffic": traffic, "executed_tflops": exe / t_s / 1e12,
                          "executed_tensor_frac": ef_t, "executed_gbs": exe_bytes / t_s / 1e9,
                          "executed_hbm_frac": ef_h, "kernel": info.get("variant"),
                          "launch": info, "passes": npass,
