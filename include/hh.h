@@ -192,8 +192,10 @@ hh_status hh_sym_apply_signed(int64_t n, int64_t h, const void *U, const void *d
  *   P: n x M column-major points; ia, ib: npairs int32 indices in [0, M);
  *   dist: npairs values of dtype.
  *   workspace >= hh_workspace_bytes(HH_CALL_MAHALANOBIS, n, h, M, npairs, dtype):
- *     transform-once: Z = diag(sqrt d) Q^T P into the workspace, then a
- *     gather kernel dist[j] = ||Z[:,ia[j]] - Z[:,ib[j]]||^2.
+ *     transform-once: Z = diag(sqrt d) Q^T P into the workspace, the pairs
+ *     counting-sorted by ia on the device (histogram, scan, scatter into the
+ *     workspace), then a gather kernel dist[j] = ||Z[:,ia[j]] - Z[:,ib[j]]||^2 that
+ *     loads each z_a once per bucket.
  *   workspace == NULL: per-pair fused kernel (gather x_a - x_b, Q^T, weighted
  *     norm) -- no scratch, 4nh + 3n flops per pair.
  *   A non-NULL workspace smaller than the query -> HH_ERR_WORKSPACE.
@@ -266,7 +268,8 @@ hh_algo hh_get_algo(void);
  *   picks K5 for (n, h, N, dtype) (packed W, T, V = W T and one G block), else 0.
  *   HH_CALL_SYM: the compact-WY scratch when the symmetric call picks the tensor-core
  *   block program, else 0.  HH_CALL_MAHALANOBIS: n*M*sizeof(dtype) (the
- *   transform-once Z).  Errors: HH_ERR_INVALID_VALUE for bad arguments.
+ *   transform-once Z) + the pair buckets (2 M + (M+1) + npairs int32, each 256-B
+ *   rounded).  Errors: HH_ERR_INVALID_VALUE for bad arguments.
  */
 hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
                              int64_t npairs, hh_dtype dtype, size_t *bytes);

@@ -176,7 +176,8 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
                                                             : 0;
             return HH_OK;
         case HH_CALL_MAHALANOBIS:
-            *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype));
+            *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype)) +
+                     bucket_ws_bytes(N_or_M, npairs);
             return HH_OK;
         case HH_CALL_CONGRUENCE: {   /* N_or_M = count */
             const size_t mb =
@@ -365,13 +366,15 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
         a.mode = MODE_TRANSFORM;
         st = run_fused(a, dtype, stream);
         if (st != HH_OK) return st;
-        // K3b: dist[j] = ||Z[:,ia[j]] - Z[:,ib[j]]||^2
+        // K3b: dist[j] = ||Z[:,ia[j]] - Z[:,ib[j]]||^2, pairs bucketed by ia on device
         LaunchInfo info;
-        cudaError_t e = launch_gather_dist(workspace, n, ia, ib, npairs, dist,
-                                           dtype == HH_F32 ? 0 : 1, stream, &info);
+        const size_t zb = round256(static_cast<size_t>(n) * static_cast<size_t>(M) * elem(dtype));
+        cudaError_t e = launch_gather_bucketed(workspace, n, M, ia, ib, npairs, dist,
+                                               static_cast<char *>(workspace) + zb,
+                                               dtype == HH_F32 ? 0 : 1, stream, &info);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (info.variant) {
-            info.launches = 2;   // K3a + K3b
+            info.launches += 1;   // + K3a
             t_last = info;
             t_has_last = true;
         }

@@ -133,7 +133,240 @@ const GVariant kG64[] = {
 };
 #undef HH_GVAR
 
+// ---------------------------------------------------------------------------------
+// Bucketed gather: pairs grouped by their first point a (a counting sort on device),
+// so z_a is read once per bucket (~P/M pairs share it) and only z_b is gathered per
+// pair -- half the gathered bytes of the per-pair kernel.
+// ---------------------------------------------------------------------------------
+__global__ void bucket_hist_kernel(const int32_t *__restrict__ ia, int64_t npairs,
+                                   int32_t *__restrict__ cnt) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < npairs;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(cnt + ia[j], 1);
+}
+
+// exclusive scan of cnt[0..M) into off[0..M] and cur[0..M): one CTA, chunks of 32K
+// counts, each thread owning 32 contiguous counts (8 x int4 loads)
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(const int32_t *__restrict__ cnt,
+                                                           int64_t M, int32_t *__restrict__ off,
+                                                           int32_t *__restrict__ cur) {
+    __shared__ int32_t wsum[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    constexpr int PER = 32;
+    int32_t carry = 0;
+    for (int64_t base = 0; base < M; base += 1024 * PER) {
+        const int64_t i0 = base + static_cast<int64_t>(t) * PER;
+        int4 v[PER / 4];
+        int32_t s = 0;
+        const bool full = i0 + PER <= M;
+#pragma unroll
+        for (int q = 0; q < PER / 4; ++q) {
+            if (full) {
+                v[q] = *reinterpret_cast<const int4 *>(cnt + i0 + 4 * q);
+            } else {
+                const int64_t i = i0 + 4 * q;
+                v[q] = make_int4(i < M ? cnt[i] : 0, i + 1 < M ? cnt[i + 1] : 0,
+                                 i + 2 < M ? cnt[i + 2] : 0, i + 3 < M ? cnt[i + 3] : 0);
+            }
+            s += v[q].x + v[q].y + v[q].z + v[q].w;
+        }
+        int32_t x = s;   // inclusive scan of the per-thread sums
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int32_t z = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                if (lane >= o) z += y;
+            }
+            wsum[lane] = z;
+        }
+        __syncthreads();
+        int32_t run = carry + (w ? wsum[w - 1] : 0) + x - s;
+        const int32_t total = wsum[31];
+#pragma unroll
+        for (int q = 0; q < PER / 4; ++q) {
+            int4 o;
+            o.x = run;
+            o.y = run + v[q].x;
+            o.z = o.y + v[q].y;
+            o.w = o.z + v[q].z;
+            run = o.w + v[q].w;
+            if (full) {
+                *reinterpret_cast<int4 *>(off + i0 + 4 * q) = o;
+                *reinterpret_cast<int4 *>(cur + i0 + 4 * q) = o;
+            } else {
+                const int64_t i = i0 + 4 * q;
+                const int32_t ov[4] = {o.x, o.y, o.z, o.w};
+                for (int e = 0; e < 4; ++e)
+                    if (i + e < M) off[i + e] = cur[i + e] = ov[e];
+            }
+        }
+        carry += total;
+        __syncthreads();
+    }
+    if (t == 0) off[M] = carry;
+}
+
+__global__ void bucket_scatter_kernel(const int32_t *__restrict__ ia, int64_t npairs,
+                                      int32_t *__restrict__ cur, int32_t *__restrict__ perm) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < npairs;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        perm[atomicAdd(cur + ia[j], 1)] = static_cast<int32_t>(j);
+}
+
+// a group of TPC threads per bucket a: z_a in registers, PP pairs of the bucket in flight
+template <typename T, int TPC, int CH, int PP, int NT, bool FULL>
+__global__ void __launch_bounds__(NT)
+    hh_gather_bucket_kernel(const T *__restrict__ Z, int64_t n, int64_t M,
+                            const int32_t *__restrict__ off, const int32_t *__restrict__ perm,
+                            const int32_t *__restrict__ ib, T *__restrict__ dist) {
+    using V = typename GV<T>::V;
+    constexpr int E = GV<T>::E;
+    const int nv = static_cast<int>(n / E);
+    const int gt = threadIdx.x % TPC;
+    const int64_t groups = static_cast<int64_t>(gridDim.x) * (NT / TPC);
+    const V *Zv = reinterpret_cast<const V *>(Z);
+    for (int64_t a = static_cast<int64_t>(blockIdx.x) * (NT / TPC) + threadIdx.x / TPC; a < M;
+         a += groups) {
+        const int32_t p0 = __ldg(off + a), p1 = __ldg(off + a + 1);
+        if (p0 == p1) continue;
+        V za[CH];
+        const V *pa = Zv + a * nv;
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const int v = gt + TPC * k;
+            za[k] = (FULL || v < nv) ? __ldg(pa + v) : V{};
+        }
+        for (int32_t q = p0; q < p1; q += PP) {
+            int32_t jj[PP];
+            const V *pb[PP];
+#pragma unroll
+            for (int p = 0; p < PP; ++p) {
+                const bool ok = q + p < p1;
+                jj[p] = ok ? __ldg(perm + q + p) : -1;
+                pb[p] = Zv + (ok ? static_cast<int64_t>(__ldg(ib + jj[p])) : a) * nv;
+            }
+            T s[PP];
+#pragma unroll
+            for (int p = 0; p < PP; ++p) {
+                s[p] = T(0);
+#pragma unroll
+                for (int k = 0; k < CH; ++k) {
+                    const int v = gt + TPC * k;
+                    if (FULL || v < nv) s[p] += GV<T>::sqd(za[k], __ldg(pb[p] + v));
+                }
+            }
+#pragma unroll
+            for (int o = TPC / 2; o > 0; o >>= 1) {
+#pragma unroll
+                for (int p = 0; p < PP; ++p) s[p] += __shfl_xor_sync(0xffffffffu, s[p], o);
+            }
+            if (gt == 0) {
+#pragma unroll
+                for (int p = 0; p < PP; ++p)
+                    if (jj[p] >= 0) dist[jj[p]] = s[p];
+            }
+        }
+    }
+}
+
+#define HH_GVAR_B(T, TPC, CH, PP, NT, NAME)                                                   \
+    GVariant {                                                                                  \
+        reinterpret_cast<const void *>(&hh_gather_bucket_kernel<T, TPC, CH, PP, NT, true>),     \
+            reinterpret_cast<const void *>(&hh_gather_bucket_kernel<T, TPC, CH, PP, NT, false>), \
+            TPC, CH, PP, NT, NAME                                                               \
+    }
+
+const GVariant kB32[] = {
+    HH_GVAR_B(float, 8, 2, 4, 256, "bucket_f32_tpc8_ch2"),
+    HH_GVAR_B(float, 8, 4, 4, 256, "bucket_f32_tpc8_ch4"),
+    HH_GVAR_B(float, 16, 4, 4, 256, "bucket_f32_tpc16_ch4"),
+    HH_GVAR_B(float, 32, 4, 8, 256, "bucket_f32_tpc32_ch4"),
+    HH_GVAR_B(float, 32, 8, 2, 256, "bucket_f32_tpc32_ch8"),
+    HH_GVAR_B(float, 32, 16, 2, 256, "bucket_f32_tpc32_ch16"),
+    HH_GVAR_B(float, 32, 32, 1, 256, "bucket_f32_tpc32_ch32"),
+    HH_GVAR_B(float, 32, 64, 1, 128, "bucket_f32_tpc32_ch64"),
+};
+const GVariant kB64[] = {
+    HH_GVAR_B(double, 8, 4, 4, 256, "bucket_f64_tpc8_ch4"),
+    HH_GVAR_B(double, 16, 4, 4, 256, "bucket_f64_tpc16_ch4"),
+    HH_GVAR_B(double, 32, 4, 4, 256, "bucket_f64_tpc32_ch4"),
+    HH_GVAR_B(double, 32, 8, 2, 256, "bucket_f64_tpc32_ch8"),
+    HH_GVAR_B(double, 32, 16, 2, 256, "bucket_f64_tpc32_ch16"),
+    HH_GVAR_B(double, 32, 32, 1, 256, "bucket_f64_tpc32_ch32"),
+    HH_GVAR_B(double, 32, 64, 1, 128, "bucket_f64_tpc32_ch64"),
+};
+#undef HH_GVAR_B
+
 }  // namespace
+
+size_t bucket_ws_bytes(int64_t M, int64_t npairs) {
+    auto r = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+    return r(static_cast<size_t>(M) * 4) * 2 + r(static_cast<size_t>(M + 1) * 4) +
+           r(static_cast<size_t>(npairs) * 4);
+}
+
+cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const int32_t *ia,
+                                   const int32_t *ib, int64_t npairs, void *dist, void *ws,
+                                   int dtype, cudaStream_t stream, LaunchInfo *info) {
+    auto r = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+    char *w = static_cast<char *>(ws);
+    int32_t *cnt = reinterpret_cast<int32_t *>(w);
+    int32_t *cur = reinterpret_cast<int32_t *>(w + r(static_cast<size_t>(M) * 4));
+    int32_t *off = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4));
+    int32_t *perm = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4) +
+                                                r(static_cast<size_t>(M + 1) * 4));
+    const int sms = device_attr().sm_count;
+    cudaError_t e = cudaMemsetAsync(cnt, 0, static_cast<size_t>(M) * 4, stream);
+    if (e != cudaSuccess) return e;
+    const int g = static_cast<int>(std::min<int64_t>((npairs + 255) / 256, sms * 8));
+    bucket_hist_kernel<<<g, 256, 0, stream>>>(ia, npairs, cnt);
+    bucket_scan_kernel<<<1, 1024, 0, stream>>>(cnt, M, off, cur);
+    bucket_scatter_kernel<<<g, 256, 0, stream>>>(ia, npairs, cur, perm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+
+    const int E = dtype == 0 ? 4 : 2;
+    const int64_t nv = n / E;
+    const GVariant *tab = dtype == 0 ? kB32 : kB64;
+    const int cntv = dtype == 0 ? static_cast<int>(sizeof(kB32) / sizeof(kB32[0]))
+                                : static_cast<int>(sizeof(kB64) / sizeof(kB64[0]));
+    const GVariant *v = nullptr;
+    for (int i = 0; i < cntv; ++i)
+        if (static_cast<int64_t>(tab[i].tpc) * tab[i].ch >= nv) {
+            v = &tab[i];
+            break;
+        }
+    if (!v) return cudaErrorNotSupported;
+    const bool full = static_cast<int64_t>(v->tpc) * v->ch == nv;
+    const void *fn = full ? v->full : v->ragged;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, v->nt, 0);
+    if (e != cudaSuccess) return e;
+    const int64_t per_block = v->nt / v->tpc;
+    const int64_t need = (M + per_block - 1) / per_block;
+    const int64_t cap = static_cast<int64_t>(std::max(occ, 1)) * sms;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min(need, cap)));
+    void *args[] = {const_cast<void **>(&Z), &n, &M, &off, &perm, const_cast<int32_t **>(&ib),
+                    &dist};
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(v->nt), args, 0, stream);
+    if (info) {
+        info->variant = v->name;
+        info->grid = grid;
+        info->block = v->nt;
+        info->smem = 0;
+        info->nchunks = 0;
+        info->launches = 4;   // histogram, scan, scatter, gather (+ one memset)
+    }
+    return e;
+}
 
 cudaError_t launch_gather_dist(const void *Z, int64_t n, const int32_t *ia, const int32_t *ib,
                                int64_t npairs, void *dist, int dtype, cudaStream_t stream,

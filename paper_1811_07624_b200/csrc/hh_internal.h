@@ -47,6 +47,13 @@ cudaError_t launch_gather_dist(const void *Z, int64_t n, const int32_t *ia, cons
                                int64_t npairs, void *dist, int dtype, cudaStream_t stream,
                                LaunchInfo *info);
 
+// K3b, bucketed: pairs counting-sorted by their first point on device (histogram, scan,
+// scatter), then one z_a load per bucket; needs bucket_ws_bytes(M, npairs) of scratch.
+size_t bucket_ws_bytes(int64_t M, int64_t npairs);
+cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const int32_t *ia,
+                                   const int32_t *ib, int64_t npairs, void *dist, void *ws,
+                                   int dtype, cudaStream_t stream, LaunchInfo *info);
+
 // Largest n the vector kernels support for this dtype.
 int64_t max_n(int dtype);
 
