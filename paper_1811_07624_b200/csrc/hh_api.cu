@@ -126,6 +126,13 @@ const char *hh_status_string(hh_status s) {
 
 const char *hh_version(void) { return "0.2.0"; }
 
+// Debug hook (not part of hh.h): a device buffer of >= 16 uint64 that CTA 0 of every
+// subsequent K5b launch fills with per-role barrier wait cycles (NULL switches it off).
+hh_status hh_debug_wy_timeline(void *device_buf) {
+    wy_set_timeline(static_cast<unsigned long long *>(device_buf));
+    return HH_OK;
+}
+
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first
 // projection only, leaving G (bf16 hi/lo rows) and V in the workspace at the
 // offsets written to off[0..1] (G, V) and the block size b / count nblk to off[2..3].

@@ -42,11 +42,6 @@ struct LaunchInfo {
 // Returns cudaSuccess or the launch error; cudaErrorNotSupported if n is too big.
 cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info);
 
-// K3b: dist[j] = || Z[:, ia[j]] - Z[:, ib[j]] ||^2.
-cudaError_t launch_gather_dist(const void *Z, int64_t n, const int32_t *ia, const int32_t *ib,
-                               int64_t npairs, void *dist, int dtype, cudaStream_t stream,
-                               LaunchInfo *info);
-
 // K3b, bucketed: pairs counting-sorted by their first point on device (histogram, scan,
 // scatter), then one z_a load per bucket; needs bucket_ws_bytes(M, npairs) of scratch.
 size_t bucket_ws_bytes(int64_t M, int64_t npairs);
@@ -83,6 +78,7 @@ struct WyPlan {
     size_t bytes = 0;
 };
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N);
+void wy_set_timeline(unsigned long long *buf);   // debug: per-role barrier wait cycles
 bool wy_supported(int64_t n, int64_t h, int64_t N);
 // Y = Q X / Q^T X / Q diag(lam) Q^T X by the compact-WY block program (fp32 in/out).
 // debug_stop_blocks >= 0: run the preparation and only the first projection (test hook).

@@ -605,12 +605,16 @@ struct Bars3 {
     uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(640, 1)
     wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmXb, float *Y,
                      const float *__restrict__ lam, const float *__restrict__ post, int n,
                      int n_pad, int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles, int rc0,
-                     int copy_below, int nxs) {
+                     int copy_below, int nxs, unsigned long long *tl) {
+    // tl (debug, CTA 0 only): per-role cycles spent waiting on each barrier (see
+    // hh_debug_wy_timeline); NULL in production
+    const bool dbg = tl != nullptr && blockIdx.x == 0;
+    unsigned long long t_k0 = clock64(), w_a = 0, w_b = 0;
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -639,7 +643,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->acc_full[a], 1);
-            mbar_init(&bars->acc_empty[a], 256);
+            mbar_init(&bars->acc_empty[a], 512);
         }
         fence_mbar_init();
     }
@@ -666,7 +670,9 @@ __global__ void __launch_bounds__(384, 1)
                 gph ^= 1u;
                 for (int rc = rc0; rc < nrc; ++rc) {
                     for (int c = 0; c < nslab; ++c) {
+                        const unsigned long long t0 = clock64();
                         mbar_wait(&bars->empty[s], ph ^ 1u);
+                        w_a += clock64() - t0;
                         mbar_arrive_expect_tx(&bars->full[s], static_cast<uint32_t>(kStage3Bytes));
                         tc::tma_load_2d(Vhi(s), &tmV, c * 32, vrow_hi + rc * kRowChunk, &bars->full[s]);
                         tc::tma_load_2d(Vlo(s), &tmV, c * 32, vrow_lo + rc * kRowChunk, &bars->full[s]);
@@ -689,11 +695,15 @@ __global__ void __launch_bounds__(384, 1)
                 gph ^= 1u;
                 tc::fence_after_sync();
                 for (int rc = rc0; rc < nrc; ++rc) {
+                    const unsigned long long t1 = clock64();
                     mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+                    w_b += clock64() - t1;
                     tc::fence_after_sync();
                     const uint32_t d = tbase + static_cast<uint32_t>(a * kTileCols);
                     for (int c = 0; c < nslab; ++c) {
+                        const unsigned long long t0 = clock64();
                         mbar_wait(&bars->full[s], ph);
+                        w_a += clock64() - t0;
                         tc::fence_after_sync();
                         const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
 #pragma unroll
@@ -730,7 +740,9 @@ __global__ void __launch_bounds__(384, 1)
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int rc = xrc0; rc < nrc; ++rc) {
                     for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb) {
+                        const unsigned long long t0 = clock64();
                         mbar_wait(&bars->xempty[s], ph ^ 1u);
+                        w_a += clock64() - t0;
                         mbar_arrive_expect_tx(&bars->xfull[s], static_cast<uint32_t>(kXBoxBytes));
                         tc::tma_load_2d(Xs(s), &tmXb, rc * kRowChunk,
                                         tile * kTileCols + cb * kXBoxCols, &bars->xfull[s]);
@@ -743,12 +755,15 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp >= 4) {
+        // 16 epilogue warps: 4 groups of 4 (one warp per TMEM lane quarter); group g takes
+        // the boxes with index = g (mod 4) -- nxs is a multiple of 4, so every ring stage
+        // has exactly one consumer group
         const int q = warp & 3, grp = (warp - 4) >> 2;
         const int r_in = q * 32 + lane;
         int a = 0;
         uint32_t aph = 0;
         constexpr int kBoxes = kTileCols / kXBoxCols;   // X boxes per r-chunk
-        static_assert(kBoxes % 2 == 0, "one consumer group per stage (nxs is even)");
+        static_assert(kBoxes % 4 == 0, "one consumer group per stage (nxs % 4 == 0)");
         int64_t seq = 0;   // position in the X box ring (both groups follow it)
         const int xrc0 = copy_below ? 0 : rc0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -757,7 +772,9 @@ __global__ void __launch_bounds__(384, 1)
                 // rows are copied (scaled) when the pass is out of place
                 const bool mma_rc = rc >= rc0;
                 if (mma_rc) {
+                    const unsigned long long t0 = clock64();
                     mbar_wait(&bars->acc_full[a], aph);
+                    w_a += clock64() - t0;
                     tc::fence_after_sync();
                 }
                 const int r = rc * kRowChunk + r_in;
@@ -766,11 +783,13 @@ __global__ void __launch_bounds__(384, 1)
                 const float lr = (lam && r < n) ? lam[r] : 1.f;
                 const float pr = (post && r < n) ? post[r] : 1.f;
 #pragma unroll
-                for (int k = 0; k < kBoxes / 2; ++k) {
-                    const int cb = grp + 2 * k;
+                for (int k = 0; k < kBoxes / 4; ++k) {
+                    const int cb = grp + 4 * k;
                     const int64_t sq = seq + cb;
                     const int s = static_cast<int>(sq % nxs);
+                    const unsigned long long t0 = clock64();
                     mbar_wait(&bars->xfull[s], static_cast<uint32_t>((sq / nxs) & 1));
+                    w_b += clock64() - t0;
                     const float *xs = Xs(s);
                     const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + cb * kXBoxCols;
                     float *dst = Y + j0 * n + r;
@@ -803,6 +822,15 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
         }
+    }
+    if (dbg && lane == 0) {
+        // [0] kernel cycles  [1,2] V producer: empty waits  [3,4] MMA: full waits, acc_empty
+        // waits  [5,6] X producer: xempty waits  [7,8] epilogue warp 4: acc_full, xfull waits
+        const unsigned long long tot = clock64() - t_k0;
+        if (warp == 0) { tl[0] = tot; tl[1] = w_a; }
+        if (warp == 1) { tl[3] = w_a; tl[4] = w_b; }
+        if (warp == 2) { tl[5] = w_a; }
+        if (warp == 4) { tl[7] = w_a; tl[8] = w_b; }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -856,8 +884,8 @@ int nxs_for(int kv) {
     const int g = (kv / 32) * 16384;
     int x = (kSmemMax - 1024 - static_cast<int>(sizeof(Bars3)) - g - kStages3 * kStage3Bytes) /
             kXBoxBytes;
-    x = std::min(kXStages, x) & ~1;
-    return std::max(2, x);
+    x = std::min(kXStages, x) & ~3;   // a multiple of the 4 epilogue groups
+    return std::max(4, x);
 }
 size_t smem3(int kv) {
     return static_cast<size_t>(kv / 32) * 16384 + static_cast<size_t>(kStages3) * kStage3Bytes +
@@ -865,9 +893,12 @@ size_t smem3(int kv) {
 }
 
 std::once_flag g_attr_once;
+unsigned long long *g_timeline = nullptr;   // debug: hh_debug_wy_timeline
 cudaError_t g_attr_err = cudaSuccess;
 
 }  // namespace
+
+void wy_set_timeline(unsigned long long *buf) { g_timeline = buf; }
 
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     WyPlan p{};
@@ -1103,10 +1134,11 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
             ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw));
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
-        ++nlaunch, wy_update_kernel<<<grid, 384, smem3(ps.kw), stream>>>(
+        ++nlaunch, wy_update_kernel<<<grid, 640, smem3(ps.kw), stream>>>(
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
-            ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw));
+            ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw),
+            g_timeline);
         cur = Y;
     }
     if (info) {
