@@ -1,0 +1,91 @@
+"""Randomised GPU parity sweep (seeded): random shapes across every kernel path, both
+dtypes where supported, against the oracle -- plus concurrent launches of the
+tensor-core paths on two streams (TMEM allocation under contention)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import inputs as gi
+from tests._util import assert_parity
+
+pytestmark = pytest.mark.gpu
+hh = pytest.importorskip("paper_1811_07624_b200")
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def shapes(seed, count):
+    g = gi.rng(800, seed)
+    out = []
+    for _ in range(count):
+        n = int(g.integers(1, 96)) * 4 * int(g.choice([1, 1, 2, 4, 8]))
+        h = int(g.integers(0, min(n, 300)))
+        N = int(g.integers(1, 700))
+        out.append((n, h, N))
+    return out
+
+
+@pytest.mark.parametrize("n,h,N", shapes(1, 24))
+@pytest.mark.parametrize("algo", ["auto", "fused"])
+def test_fuzz_apply(n, h, N, algo):
+    a = hh.HH_ALGO_AUTO if algo == "auto" else hh.HH_ALGO_FUSED
+    for dt in ("f32", "f64"):
+        if dt == "f64" and n % 2:
+            continue
+        c = gi.make_case("apply", n, h, N, dt, seed=n + h)
+        op = (n + h + N) % 2
+        with hh.algo(a):
+            got = hh.hh_apply(op, dev(c.U) if h else torch.empty(0, n, device="cuda",
+                                                                 dtype=torch.float32 if dt == "f32"
+                                                                 else torch.float64),
+                              dev(c.X)).cpu().numpy()
+        assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"fuzz apply n{n} h{h} N{N} {dt}")
+
+
+@pytest.mark.parametrize("n,h,N", shapes(2, 12))
+def test_fuzz_sym_and_signed(n, h, N):
+    h = max(h, 1)
+    c = gi.make_case("sym", n, h, N, "f32", seed=h)
+    d = gi.sign_diag(gi.rng(801, n), n, "f32")
+    got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", h, f"fuzz sym n{n} h{h}")
+    got = hh.hh_apply_signed(1, hh.HH_SIDE_LEFT, dev(c.U), dev(d), dev(c.X)).cpu().numpy()
+    assert_parity(got, oracle.apply_signed(1, 0, c.U, d, c.X), "f32", h, f"fuzz signed n{n} h{h}")
+
+
+@pytest.mark.parametrize("n,h,M", [(s[0], s[1] % 40, s[2]) for s in shapes(3, 10)])
+def test_fuzz_mahalanobis(n, h, M):
+    c = gi.make_case("mahalanobis", n, h, max(M, 2), "f32", seed=M, npairs=int(3 * M + 17))
+    for fused in (False, True):
+        got = hh.hh_mahalanobis(dev(c.U) if h else torch.empty(0, n, device="cuda"), dev(c.d),
+                                dev(c.X), dev(c.ia), dev(c.ib), fused=fused).cpu().numpy()
+        assert_parity(got, oracle.mahalanobis(c.U, c.d, c.X, c.ia, c.ib), "f32", h,
+                      f"fuzz maha n{n} h{h} fused={fused}")
+
+
+def test_concurrent_streams_tensor_paths():
+    """Two streams running the compact-WY apply and the k-NN kernel concurrently (both
+    allocate TMEM): results equal the serial ones."""
+    c = gi.make_case("apply", 1024, 200, 3000, "f32", seed=5)
+    U, X = dev(c.U), dev(c.X)
+    ref_apply = hh.hh_apply(0, U, X).clone()
+    Pr, Pq = torch.randn(3000, 64, device="cuda"), torch.randn(500, 64, device="cuda")
+    Uk, dk = torch.nn.functional.normalize(torch.randn(6, 64, device="cuda"), dim=1), \
+        torch.rand(64, device="cuda") + 0.1
+    ref_idx, ref_d = hh.hh_knn(Uk, dk, Pr, Pq, 4)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            y = hh.hh_apply(0, U, X)
+        with torch.cuda.stream(s2):
+            r = hh.hh_knn(Uk, dk, Pr, Pq, 4)
+        outs.append((y, r))
+    torch.cuda.synchronize()
+    for y, (i, d) in outs:
+        assert torch.equal(y, ref_apply)
+        assert torch.equal(i, ref_idx) and torch.equal(d, ref_d)
