@@ -81,7 +81,8 @@ __device__ __forceinline__ float bf2f(uint16_t b) {
 // (the Lambda W operand of the symmetric block).
 __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h, int h_pad,
                                int64_t n_pad, const float *__restrict__ lam, int lam_blk, int b,
-                               int extra, float *__restrict__ Wf, uint16_t *__restrict__ Wb) {
+                               int extra, int reverse, float *__restrict__ Wf,
+                               uint16_t *__restrict__ Wb) {
     const int64_t R = h_pad + extra;
     const int64_t total = R * n_pad;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -89,7 +90,7 @@ __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h
         const int64_t i = idx / n_pad, r = idx % n_pad;
         float v = 0.f;
         if (i < h_pad) {
-            if (i < h && r < n) v = U[i * n + r];
+            if (i < h && r < n) v = U[(reverse ? h - 1 - i : i) * n + r];
             Wf[idx] = v;
         } else {
             const int64_t src = static_cast<int64_t>(lam_blk) * b + (i - h_pad);
@@ -186,7 +187,7 @@ __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int n
 // then 32 columns at a time (block form of the same product, H-blocks 1 = [0,c),
 // 2 = [c,c+32)):  T[0:c, c:c+32] = -T[0:c,0:c] * (S[0:c, c:c+32] * T[c:c+32, c:c+32]).
 __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict__ Sg, int b,
-                                                          float *__restrict__ Tg) {
+                                                          float *__restrict__ Tg, int diag_only) {
     extern __shared__ float tsm[];
     const int blk = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -222,9 +223,10 @@ __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict
     }
     __syncthreads();
     // extension steps; each thread owns (row l, 4 consecutive columns): 2 shared loads
-    // (one broadcast, one 16-B) per 4 FMAs
+    // (one broadcast, one 16-B) per 4 FMAs.  diag_only: only the 32 x 32 diagonal blocks
+    // are wanted (wy_vrec_kernel builds V = W T from them without the rest of T)
     float *T22 = Pm + 224 * 32;                        // 32 x 32 dense diagonal block
-    for (int c = 32; c < b; c += 32) {
+    for (int c = 32; c < (diag_only ? 0 : b); c += 32) {
         // S panel S[0:c, c:c+32] -> Sb (c x 32); T22 = T[c:c+32, c:c+32] (dense)
         for (int e = t; e < c * 32; e += 1024) Sb[e] = S[(e / 32) * b + c + (e % 32)];
         {
@@ -282,8 +284,91 @@ __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict
     }
     for (int64_t e = t; e < bb; e += 1024) {
         const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
-        Tout[e] = m >= l ? tp(l, m) : 0.f;
+        Tout[e] = (m >= l && (!diag_only || l / 32 == m / 32)) ? tp(l, m) : 0.f;
     }
+}
+
+// V = W T for the apply program WITHOUT forming T: over 32-column chunks c of a block,
+//   T[:, c] = [-T[0:c,0:c] S[0:c,c] T_cc ; T_cc]   =>   V_c = (W_c - V_{<c} S_{<c,c}) T_cc
+// (the block form of the same product used by wy_tbuild_kernel), so only the diagonal
+// 32 x 32 blocks T_cc are needed and the work is parallel over rows: a CTA owns 64 rows
+// of one block, keeps its V rows in SMEM and walks the chunks.  Output: bf16 hi/lo V
+// rows (Vt[hi: blk*n_pad + r][i], Vt[lo: lo_off + ...]).
+__global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ Wf,
+                                                      const float *__restrict__ Sg,
+                                                      const float *__restrict__ Tg, int64_t n_pad,
+                                                      int b, uint16_t *__restrict__ Vt,
+                                                      int64_t lo_off) {
+    extern __shared__ float vsm[];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+    const int blk = blockIdx.y;
+    const int t = threadIdx.x, tx = t % 8, ty = t / 8;   // 8 x 32: 4 columns x 2 rows
+    const int64_t bb = static_cast<int64_t>(b) * b;
+    const float *S = Sg + blk * bb;
+    const float *T = Tg + blk * bb;
+    const float *W = Wf + static_cast<int64_t>(blk) * b * n_pad;
+    float *Vs = vsm;                    // 64 x (b + 1)
+    float *Sp = Vs + 64 * (b + 1);      // (b - 32) x 32 panel S[0:c, c:c+32]
+    float *Tc = Sp + (b - 32 > 0 ? (b - 32) * 32 : 32);   // 32 x 33
+    float *Zs = Tc + 32 * 33;           // 64 x 33
+    const int ld = b + 1;
+    for (int c = 0; c < b; c += 32) {
+        for (int e = t; e < c * 32; e += 256) Sp[e] = S[(e / 32) * b + c + (e % 32)];
+        for (int e = t; e < 32 * 32; e += 256) {
+            const int m = e / 32, j = e % 32;
+            Tc[m * 33 + j] = T[(c + m) * b + c + j];
+        }
+        __syncthreads();
+        // Z = W_c - V_{<c} S_{<c,c}   (64 x 32): thread rows ty*2.., columns tx*4..
+        float z[2][4];
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                z[p][q] = W[static_cast<int64_t>(c + tx * 4 + q) * n_pad + r0 + ty * 2 + p];
+        for (int l = 0; l < c; ++l) {
+            const float v0 = Vs[(ty * 2) * ld + l], v1 = Vs[(ty * 2 + 1) * ld + l];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float sv = Sp[l * 32 + tx * 4 + q];
+                z[0][q] = fmaf(-v0, sv, z[0][q]);
+                z[1][q] = fmaf(-v1, sv, z[1][q]);
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Zs[(ty * 2 + p) * 33 + tx * 4 + q] = z[p][q];
+        __syncthreads();
+        // V_c = Z T_cc  (T_cc upper triangular)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int rr = ty * 2 + p;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = tx * 4 + q;
+                float v = 0.f;
+                for (int m = 0; m <= j; ++m) v = fmaf(Zs[rr * 33 + m], Tc[m * 33 + j], v);
+                Vs[rr * ld + c + j] = v;
+            }
+        }
+        __syncthreads();
+    }
+    // bf16 hi/lo rows out
+    for (int e = t; e < 64 * b; e += 256) {
+        const int rr = e / b, i = e % b;
+        const float v = Vs[rr * ld + i];
+        const uint16_t hv = f2bf(v);
+        const int64_t o = (static_cast<int64_t>(blk) * n_pad + r0 + rr) * b + i;
+        Vt[o] = hv;
+        Vt[lo_off + o] = f2bf(v - bf2f(hv));
+    }
+}
+
+size_t vrec_smem(int b) {
+    return (static_cast<size_t>(64) * (b + 1) + static_cast<size_t>(std::max(b - 32, 1)) * 32 +
+            32 * 33 + 64 * 33) *
+           4;
 }
 
 // Small SIMT GEMM of the preparation (fp32):
@@ -974,6 +1059,10 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         g_attr_err = cudaFuncSetAttribute(wy_project_kernel,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (g_attr_err == cudaSuccess)
+            g_attr_err = cudaFuncSetAttribute(wy_vrec_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(vrec_smem(256)));
+        if (g_attr_err == cudaSuccess)
             g_attr_err = cudaFuncSetAttribute(wy_tbuild_kernel,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tbuild_smem(256)));
@@ -1000,8 +1089,12 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     {
         const int64_t tot = R * n_pad;
         const int g = static_cast<int>(std::min<int64_t>((tot + 255) / 256, sms * 16));
-        ++nlaunch, wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b, p.extra,
-                                              Wf, Wb);
+        // Q^T X applies the reversed list as a Q X program (transposing a
+        // product of symmetric reflectors reverses it); the symmetric program keeps the
+        // natural order and uses T and T^T explicitly
+        const int rev = p.kind == WY_APPLY_T ? 1 : 0;
+        ++nlaunch, wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b,
+                                                         p.extra, rev, Wf, Wb);
         const int tb = (b + 63) / 64;
         ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, 0,
                                                                        nullptr, 0, Sp);
@@ -1014,26 +1107,28 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             ++nlaunch, wy_gram_reduce_kernel<<<std::max(1, (b * b + 255) / 256), 256, 0, stream>>>(
                 F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p));
         }
-        ++nlaunch, wy_tbuild_kernel<<<m, 1024, tbuild_smem(b), stream>>>(S, b, T);
+        ++nlaunch, wy_tbuild_kernel<<<m, 1024, tbuild_smem(b), stream>>>(S, b, T, sym ? 0 : 1);
+        if (!sym) {
+            // V = W T per block, row-parallel from the diagonal T blocks (wy_vrec_kernel)
+            ++nlaunch, wy_vrec_kernel<<<dim3(static_cast<unsigned>(n_pad / 64), m), 256,
+                                        vrec_smem(b), stream>>>(Wf, S, T, n_pad, b, H(p.off_v), vlo);
+        }
         const dim3 gv(static_cast<unsigned>(n_pad / 64), b / 32);
-        for (int k = 0; k < m; ++k) {
+        for (int k = 0; k < (sym ? m : 0); ++k) {
             const float *Wk = Wf + static_cast<int64_t>(k) * b * n_pad;
             const float *Tk = T + static_cast<int64_t>(k) * b * b;
-            const bool last_sym = sym && k == m - 1;
-            const bool need_n = p.kind == WY_APPLY_N || (sym && !last_sym);
-            const bool need_t = p.kind == WY_APPLY_T || (sym && !last_sym);
-            // op N:  V = W T ;  op T:  V' = W T^T
-            uint16_t *Vn = H(p.kind == WY_APPLY_N ? p.off_v : p.off_v2);
+            const bool last_sym = k == m - 1;
+            // symmetric program: blocks k < m-1 need V = W T (Q_k) and V' = W T^T (Q_k^T)
+            uint16_t *Vn = H(p.off_v2);
             uint16_t *Vt = H(p.off_v);
-            if (need_n)
+            if (!last_sym) {
                 ++nlaunch, wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
                     Vn + static_cast<int64_t>(k) * n_pad * b, b, vlo);
-            if (need_t)
                 ++nlaunch, wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
                     Vt + static_cast<int64_t>(k) * n_pad * b, b, vlo);
-            if (last_sym) {
+            } else {
                 // A2 = W T (bf16 into columns [b, 2b) of Asym, fp32 copy Vf); V' = W T^T;
                 // M = P T^T; A1 = Lambda V' - V M (columns [0, b)).  DESIGN.md §4.
                 uint16_t *As = H(p.off_asym);
@@ -1093,13 +1188,19 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     auto blockpass = [&](int k, const CUtensorMap *mv) {
         Pass ps{k * b, b, &mWb, &mGb, mv, static_cast<int>(k * n_pad),
                 static_cast<int>((m + k) * n_pad), false};
-        if (p.qr) ps.row0 = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(k) * b, p.n - 1));
+        if (p.qr) {
+            // first row where the block's W (and V) can be nonzero: u_i[r] = 0 for r < i;
+            // on the reversed list (Q^T) position q holds reflector h-1-q
+            int64_t r0q = static_cast<int64_t>(k) * b;
+            if (p.kind == WY_APPLY_T)
+                r0q = std::max<int64_t>(0, p.h - std::min<int64_t>(static_cast<int64_t>(k + 1) * b, p.h));
+            ps.row0 = static_cast<int>(std::min<int64_t>(r0q, p.n - 1));
+        }
         prog[np++] = ps;
     };
-    if (p.kind == WY_APPLY_N) {
-        for (int k = m - 1; k >= 0; --k) blockpass(k, &mV);          // Q X: last block first
-    } else if (p.kind == WY_APPLY_T) {
-        for (int k = 0; k < m; ++k) blockpass(k, &mV);               // Q^T X: first block first
+    if (p.kind == WY_APPLY_N || p.kind == WY_APPLY_T) {
+        // Q X (or Q^T X = the reversed list's Q X): last block first
+        for (int k = m - 1; k >= 0; --k) blockpass(k, &mV);
     } else {
         for (int k = 0; k < m - 1; ++k) blockpass(k, &mV);           // Q_k^T, k < m-1
         Pass ps{(m - 1) * b, 2 * b, &mW2b, &mG2b, &mAs, 0, static_cast<int>(n_pad), true};

@@ -42,9 +42,10 @@ def bf16_pair_to_f64(ws, off, count, lo_off):
 @pytest.mark.parametrize("n,h,N,op", [(256, 40, 300, 0), (512, 70, 257, 1), (4096, 256, 130, 0),
                                       (1024, 300, 129, 1)])
 def test_wy_intermediates(n, h, N, op):
-    """G = W^T X and V of the first applied block match fp64 numpy.  Blocks are cut in
-    product order; Q X applies the last block with V = W T, Q^T X the first block with
-    V' = W T^T, T by the forward recurrence T[:i, i] = -2 T[:i,:i] W[:, :i]^T w_i."""
+    """G = W^T X and V = W T of the first applied block match fp64 numpy.  Blocks are cut in
+    product order -- Q^T X runs the REVERSED reflector list as a Q X program --
+    and the last block is applied first; T by the forward recurrence
+    T[:i, i] = -2 T[:i,:i] W[:, :i]^T w_i."""
     c = gi.make_case("apply", n, h, N, "f32", seed=21)
     U, X = dev(c.U), dev(c.X)
     with hh.algo(hh.HH_ALGO_WY):
@@ -53,9 +54,10 @@ def test_wy_intermediates(n, h, N, op):
     off = hh.debug_wy_project(op, U, X, ws)
     torch.cuda.synchronize()
     b, nblk, n_pad = off["b"], off["nblk"], off["n_pad"]
+    order = np.arange(h) if op == 0 else np.arange(h)[::-1]
     Wfull = np.zeros((nblk * b, n))
-    Wfull[:h] = c.U.astype(np.float64)
-    k = nblk - 1 if op == 0 else 0
+    Wfull[:h] = c.U.astype(np.float64)[order]
+    k = nblk - 1
     W = Wfull[k * b:(k + 1) * b]                       # (b, n): rows w_i
     G_ref = c.X.astype(np.float64) @ W.T               # (N, b)
     G = bf16_pair_to_f64(ws, off["G"], N * b, N * b).reshape(N, b)
@@ -68,7 +70,7 @@ def test_wy_intermediates(n, h, N, op):
         T[i, i] = 2.0
         if i:
             T[:i, i] = -2.0 * T[:i, :i] @ (W[:i] @ W[i])
-    V_ref = W.T @ (T if op == 0 else T.T)              # (n, b)
+    V_ref = W.T @ T                                    # (n, b)
     V = bf16_pair_to_f64(ws, off["V"] + 2 * k * n_pad * b, n_pad * b,
                          nblk * n_pad * b).reshape(n_pad, b)[:n]
     assert rel_fro(V, V_ref) < 4e-5, rel_fro(V, V_ref)
