@@ -1,549 +1,16 @@
-// hh_fused.cu -- fused SIMT Householder-product kernels for sm_100a.
-//
-// K1 (apply Q X / Q^T X), K2 (Q diag(lambda) Q^T X), K3a (Mahalanobis
-// transform-once Z = diag(sqrt d) Q^T P) and K3c (per-pair fused distance) are one
-// kernel template with a run-time mode.  Each column costs h dot products
-// alpha_i = u_i^T x and h rank-1 updates x <- x - 2 alpha_i u_i ("4nh
-// operations"), applied in the order fixed by Q = H_1 ... H_h (reading R1).
-//
-// Data movement:
-//   * U (n x h, column-major == (h, n)) is staged once per persistent CTA into
-//     shared memory by 1-D bulk copies (TMA engine, UBLKCP).  When h*n*s does not
-//     fit next to the column staging, U is streamed in chunks of R reflectors
-//     through two shared buffers (mbarrier ring, one CTA barrier per chunk).
-//   * X is processed in "tiles" of UC contiguous columns (one contiguous
-//     UC*n*s-byte range).  Each unit (a warp, or a multi-warp group when one column
-//     needs more than 32 threads) owns a one-tile shared staging slot: it copies
-//     the landed tile into registers, then immediately issues the bulk copy of its
-//     next tile, so the HBM read of tile t+1 overlaps the arithmetic of tile t.
-//   * The column lives in registers for all h reflectors; the result is written
-//     once with 128-bit coalesced stores.  HBM traffic = one read + one write of X.
-//   * A group of TPC threads owns a column (vector chunk v = t + TPC*k of a thread);
-//     dots are reduced by an xor-shuffle butterfly (plus a shared-memory stage when
-//     TPC > 32), so every thread of the group holds the identical alpha.
+// hh_fused.cu -- host launcher of the fused SIMT kernel (K1 / K2 / K3a / K3c): variant
+// choice by n, the shared-memory plan and the persistent grid.
 #include <algorithm>
 #include <cstdio>
 
-#include "hh_internal.h"
-#include "hh_ptx.cuh"
+#include "hh_fused_kernel.cuh"
 
 namespace hh {
-
-template <typename T>
-struct VT;
-template <>
-struct VT<float> {
-    using V = float4;
-    static constexpr int E = 4;
-};
-template <>
-struct VT<double> {
-    using V = double2;
-    static constexpr int E = 2;
-};
-
-__device__ __forceinline__ void vzero(float4 &a) { a = make_float4(0.f, 0.f, 0.f, 0.f); }
-__device__ __forceinline__ void vzero(double2 &a) { a = make_double2(0.0, 0.0); }
-// Packed fp32 FMA (sm_100 FFMA2): two IEEE round-to-nearest FMAs per instruction,
-// bit-identical to two fmaf calls; halves the FMA issue slots of the hot loop.
-__device__ __forceinline__ void ffma2(float &d0, float &d1, float a0, float a1, float b0, float b1,
-                                      float c0, float c1) {
-    asm("{\n\t.reg .b64 A, B, C, D;\n\t"
-        "mov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\tmov.b64 C, {%6, %7};\n\t"
-        "fma.rn.f32x2 D, A, B, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
-        : "=f"(d0), "=f"(d1)
-        : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-__device__ __forceinline__ void vfma(float4 &acc, const float4 &u, const float4 &x) {
-    ffma2(acc.x, acc.y, u.x, u.y, x.x, x.y, acc.x, acc.y);
-    ffma2(acc.z, acc.w, u.z, u.w, x.z, x.w, acc.z, acc.w);
-}
-__device__ __forceinline__ void vfma(double2 &acc, const double2 &u, const double2 &x) {
-    acc.x = fma(u.x, x.x, acc.x);
-    acc.y = fma(u.y, x.y, acc.y);
-}
-__device__ __forceinline__ float vsum(const float4 &a) { return (a.x + a.y) + (a.z + a.w); }
-__device__ __forceinline__ double vsum(const double2 &a) { return a.x + a.y; }
-// x <- x - s * u
-__device__ __forceinline__ void vaxpy(float4 &x, float s, const float4 &u) {
-    ffma2(x.x, x.y, -s, -s, u.x, u.y, x.x, x.y);
-    ffma2(x.z, x.w, -s, -s, u.z, u.w, x.z, x.w);
-}
-__device__ __forceinline__ void vaxpy(double2 &x, double s, const double2 &u) {
-    x.x = fma(-s, u.x, x.x);
-    x.y = fma(-s, u.y, x.y);
-}
-__device__ __forceinline__ void vmul(float4 &x, const float4 &l) {
-    x.x *= l.x;
-    x.y *= l.y;
-    x.z *= l.z;
-    x.w *= l.w;
-}
-__device__ __forceinline__ void vmul(double2 &x, const double2 &l) {
-    x.x *= l.x;
-    x.y *= l.y;
-}
-__device__ __forceinline__ void vmulsqrt(float4 &x, const float4 &d) {
-    x.x *= sqrtf(d.x);
-    x.y *= sqrtf(d.y);
-    x.z *= sqrtf(d.z);
-    x.w *= sqrtf(d.w);
-}
-__device__ __forceinline__ void vmulsqrt(double2 &x, const double2 &d) {
-    x.x *= sqrt(d.x);
-    x.y *= sqrt(d.y);
-}
-__device__ __forceinline__ void vsub(float4 &a, const float4 &b) {
-    a.x -= b.x;
-    a.y -= b.y;
-    a.z -= b.z;
-    a.w -= b.w;
-}
-__device__ __forceinline__ void vsub(double2 &a, const double2 &b) {
-    a.x -= b.x;
-    a.y -= b.y;
-}
-// sum_e d_e * x_e^2
-__device__ __forceinline__ float vwsq(const float4 &x, const float4 &d) {
-    return (d.x * (x.x * x.x) + d.y * (x.y * x.y)) + (d.z * (x.z * x.z) + d.w * (x.w * x.w));
-}
-__device__ __forceinline__ double vwsq(const double2 &x, const double2 &d) {
-    return d.x * (x.x * x.x) + d.y * (x.y * x.y);
-}
-
-template <typename V>
-__device__ __forceinline__ V ldg_v(const V *p) {
-    return __ldg(p);
-}
-
-// ---------------------------------------------------------------------------------
-// Kernel template
-//   T   element type       TPC threads per column group      CH vector chunks / thread
-//   C   columns per group   NT threads per CTA                FULL: nv == TPC*CH exactly
-// ---------------------------------------------------------------------------------
-template <typename T, int TPC, int CH, int C, int NT, bool FULL>
-__global__ void __launch_bounds__(NT) hh_fused_kernel(const FusedArgs a) {
-    using V = typename VT<T>::V;
-    constexpr int E = VT<T>::E;
-    constexpr int UT = TPC > 32 ? TPC : 32;  // threads per scheduling unit
-    constexpr int GPU_ = UT / TPC;           // groups per unit
-    constexpr int UC = GPU_ * C;             // columns per unit tile
-    constexpr int NU = NT / UT;              // units per CTA
-    constexpr int WPU = UT / 32;             // warps per unit
-    static_assert(NT % UT == 0, "block must hold whole units");
-    static_assert(NU <= 15, "named barrier ids");
-
-    const int tid = threadIdx.x;
-    const int unit = tid / UT;
-    const int ut = tid % UT;
-    const int grp = ut / TPC;
-    const int gt = ut % TPC;
-    const int lane = tid & 31;
-    const int wiu = ut >> 5;
-
-    const int mode = a.mode;
-    const int64_t n = a.n;
-    const int nv = static_cast<int>(n / E);
-    const int h = static_cast<int>(a.h);
-    const int R = a.R;
-    const int nc = a.nchunks;
-    const int nbuf = nc > 1 ? 2 : 1;
-    const bool stage = a.stage_x != 0;
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    V *Us = reinterpret_cast<V *>(smem);
-    V *Xs = Us + static_cast<size_t>(nbuf) * R * nv;
-    T *red = reinterpret_cast<T *>(Xs + (stage ? static_cast<size_t>(NU) * UC * nv : 0));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(red + (TPC > 32 ? 2 * NU * WPU * C : 0));
-    uint64_t *ubar = bars;      // [2]
-    uint64_t *xbar = bars + 2;  // [NU]
-
-    const V *Ug = reinterpret_cast<const V *>(a.U);
-    const V *Xg = reinterpret_cast<const V *>(a.X);
-    const V *vecg = reinterpret_cast<const V *>(a.vec);
-
-    const int64_t ntiles = (a.N + UC - 1) / UC;
-    const int nb = a.nbatches;
-    const int L = (mode == MODE_SYM ? 2 : 1) * nc;  // U-chunk visits per batch (nc > 1)
-    const int64_t nvisits = static_cast<int64_t>(nb) * L;
-
-    auto tile_of = [&](int b) -> int64_t {
-        return (static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * NU + unit;
-    };
-    auto chunk_of = [&](int q) -> int {
-        if (mode == MODE_APPLY_N) return nc - 1 - q;
-        if (mode == MODE_SYM) return q < nc ? q : 2 * nc - 1 - q;
-        return q;
-    };
-    // issue the bulk copy of U chunk `c` into buffer `buf`
-    auto issue_u = [&](int c, int buf) {
-        const int r0 = c * R;
-        const int r1 = min(h, r0 + R);
-        const uint32_t bytes = static_cast<uint32_t>((r1 - r0) * nv * sizeof(V));
-        mbar_arrive_expect_tx(&ubar[buf], bytes);
-        const uint64_t pol = policy_evict_last();
-        const char *src = reinterpret_cast<const char *>(Ug + static_cast<size_t>(r0) * nv);
-        char *dst = reinterpret_cast<char *>(Us + static_cast<size_t>(buf) * R * nv);
-        for (uint32_t off = 0; off < bytes; off += 32768u)
-            bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &ubar[buf], pol);
-    };
-    auto issue_x = [&](int64_t t) {
-        const int64_t c0 = t * UC;
-        const int64_t cols = min(static_cast<int64_t>(UC), a.N - c0);
-        const uint32_t bytes = static_cast<uint32_t>(cols * nv * sizeof(V));
-        mbar_arrive_expect_tx(&xbar[unit], bytes);
-        const uint64_t pol = policy_evict_first();
-        const char *src = reinterpret_cast<const char *>(Xg + c0 * nv);
-        char *dst = reinterpret_cast<char *>(Xs + static_cast<size_t>(unit) * UC * nv);
-        for (uint32_t off = 0; off < bytes; off += 32768u)
-            bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &xbar[unit], pol);
-    };
-    auto unit_sync = [&]() {
-        if (UT == 32)
-            __syncwarp();
-        else
-            named_bar_sync(1 + unit, UT);
-    };
-
-    if (tid == 0) {
-        mbar_init(&ubar[0], 1);
-        mbar_init(&ubar[1], 1);
-    }
-    if (ut == 0) mbar_init(&xbar[unit], 1);
-    fence_mbar_init();
-    __syncthreads();
-
-    // prologue: U (resident, or the first two chunk visits) and each unit's first tile
-    if (tid == 0 && h > 0) {
-        if (nc == 1) {
-            issue_u(0, 0);
-        } else {
-            for (int64_t g = 0; g < (nvisits < 2 ? nvisits : 2); ++g)
-                issue_u(chunk_of(static_cast<int>(g % L)), static_cast<int>(g & 1));
-        }
-    }
-    if (stage && ut == 0 && tile_of(0) < ntiles) issue_x(tile_of(0));
-
-    V x[C][CH];
-    uint32_t xphase = 0;
-    int rpar = 0;       // reduction-buffer parity (TPC > 32)
-    int64_t g = 0;      // chunk-visit counter (nc > 1)
-    bool u_ready = (h == 0) || (nc > 1);
-
-    auto valid_k = [&](int k) -> bool { return FULL || (gt + TPC * k < nv); };
-
-    // one reflector: x <- x - 2 (u^T x) u   for the C columns of this group
-    auto reflect = [&](const V *ub) {
-        T p[C];
-        // multi-warp groups: keep the u chunk in registers across the cross-warp
-        // reduction (a shared-memory store + barrier the compiler cannot see through),
-        // so u is read from shared memory once per reflector, not twice
-        constexpr bool kKeepU = TPC > 32;
-        V uk[kKeepU ? CH : 1];
-        if constexpr (kKeepU) {
-#pragma unroll
-            for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) uk[k] = ub[gt + TPC * k];
-                else vzero(uk[k]);
-            }
-        }
-        auto uget = [&](int k) -> V {
-            if constexpr (kKeepU) return uk[k];
-            else return ub[gt + TPC * k];
-        };
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            V acc;
-            vzero(acc);
-#pragma unroll
-            for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) vfma(acc, uget(k), x[c][k]);
-            }
-            p[c] = vsum(acc);
-        }
-#pragma unroll
-        for (int off = (TPC < 32 ? TPC : 32) / 2; off > 0; off >>= 1) {
-#pragma unroll
-            for (int c = 0; c < C; ++c) p[c] += __shfl_xor_sync(0xffffffffu, p[c], off);
-        }
-        if constexpr (TPC > 32) {
-            T *rb = red + (static_cast<size_t>(rpar) * NU + unit) * WPU * C;
-            if (lane == 0) {
-#pragma unroll
-                for (int c = 0; c < C; ++c) rb[wiu * C + c] = p[c];
-            }
-            named_bar_sync(1 + unit, UT);
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                T s = rb[c];
-#pragma unroll
-                for (int w = 1; w < WPU; ++w) s += rb[w * C + c];
-                p[c] = s;
-            }
-            rpar ^= 1;
-        }
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const T s = p[c] + p[c];
-#pragma unroll
-            for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) vaxpy(x[c][k], s, uget(k));
-            }
-        }
-    };
-    // reflectors [r0, r1) of the chunk resident at `base` (first row = chunk_lo)
-    // (NEXT-f2: the fused kernel applies QR-structured reflectors in full -- it serves
-    // small h, where the zero prefixes are a negligible share; K5 skips them.)
-    auto run_range = [&](const V *base, int chunk_lo, int r0, int r1, bool desc) {
-        if (desc) {
-            for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
-        } else {
-            for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
-        }
-    };
-    auto scale_vec = [&]() {
-#pragma unroll
-        for (int k = 0; k < CH; ++k) {
-            if (valid_k(k)) {
-                const V l = ldg_v(vecg + gt + TPC * k);
-#pragma unroll
-                for (int c = 0; c < C; ++c) vmul(x[c][k], l);
-            }
-        }
-    };
-
-    for (int b = 0; b < nb; ++b) {
-        const int64_t t = tile_of(b);
-        const bool tv = t < ntiles;
-        const int64_t col0 = t * UC + static_cast<int64_t>(grp) * C;
-
-        // ---- 1. columns -> registers
-        if (tv) {
-            if (mode == MODE_PAIR) {
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    const int64_t j = col0 + c;
-                    const bool cv = j < a.N;
-                    const V *pa = Xg + (cv ? static_cast<int64_t>(a.ia[j]) : 0) * nv;
-                    const V *pb = Xg + (cv ? static_cast<int64_t>(a.ib[j]) : 0) * nv;
-#pragma unroll
-                    for (int k = 0; k < CH; ++k) {
-                        vzero(x[c][k]);
-                        if (cv && valid_k(k)) {
-                            x[c][k] = ldg_v(pa + gt + TPC * k);
-                            vsub(x[c][k], ldg_v(pb + gt + TPC * k));
-                        }
-                    }
-                }
-            } else if (stage) {
-                mbar_wait(&xbar[unit], xphase);
-                xphase ^= 1u;
-                const V *xs = Xs + (static_cast<size_t>(unit) * UC + grp * C) * nv;
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-#pragma unroll
-                    for (int k = 0; k < CH; ++k) {
-                        if (valid_k(k))
-                            x[c][k] = xs[static_cast<size_t>(c) * nv + gt + TPC * k];
-                        else
-                            vzero(x[c][k]);
-                    }
-                }
-                unit_sync();  // every thread of the unit has its columns in registers
-                if (ut == 0) {
-                    const int64_t t1 = tile_of(b + 1);
-                    if (b + 1 < nb && t1 < ntiles) {
-                        fence_proxy_async_smem();
-                        issue_x(t1);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    const int64_t j = col0 + c;
-                    const bool cv = j < a.N;
-#pragma unroll
-                    for (int k = 0; k < CH; ++k) {
-                        vzero(x[c][k]);
-                        if (cv && valid_k(k)) x[c][k] = ldg_v(Xg + j * nv + gt + TPC * k);
-                    }
-                }
-            }
-        }
-
-        // NEXT-f1 right factor (Y = Q D X): x <- D x before the first reflector
-        if (tv && (a.dside & 1)) {
-            const V *dg = reinterpret_cast<const V *>(a.dsign);
-#pragma unroll
-            for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) {
-                    const V dv = ldg_v(dg + gt + TPC * k);
-#pragma unroll
-                    for (int c = 0; c < C; ++c) vmul(x[c][k], dv);
-                }
-            }
-        }
-
-        // ---- 2. reflector passes
-        if (nc == 1) {
-            if (!u_ready) {
-                mbar_wait(&ubar[0], 0);
-                u_ready = true;
-            }
-            if (tv) {
-                if (mode == MODE_APPLY_N) {
-                    run_range(Us, 0, 0, h, true);
-                } else if (mode == MODE_SYM) {
-                    run_range(Us, 0, 0, h, false);
-                    scale_vec();
-                    run_range(Us, 0, 0, h, true);
-                } else {
-                    run_range(Us, 0, 0, h, false);
-                }
-            }
-        } else {
-            for (int q = 0; q < L; ++q, ++g) {
-                const int buf = static_cast<int>(g & 1);
-                mbar_wait(&ubar[buf], static_cast<uint32_t>((g >> 1) & 1));
-                const int c = chunk_of(q);
-                const bool desc = (mode == MODE_APPLY_N) || (mode == MODE_SYM && q >= nc);
-                if (tv) {
-                    run_range(Us + static_cast<size_t>(buf) * R * nv, c * R, c * R,
-                              min(h, (c + 1) * R), desc);
-                    if (mode == MODE_SYM && q == nc - 1) scale_vec();
-                }
-                __syncthreads();  // every unit is done with buffer `buf`
-                if (tid == 0 && g + 2 < nvisits) {
-                    fence_proxy_async_smem();
-                    issue_u(chunk_of(static_cast<int>((g + 2) % L)), buf);
-                }
-            }
-        }
-
-        // ---- 3. epilogue
-        if (tv) {
-            if (mode == MODE_PAIR) {
-                T s[C];
-#pragma unroll
-                for (int c = 0; c < C; ++c) s[c] = T(0);
-#pragma unroll
-                for (int k = 0; k < CH; ++k) {
-                    if (valid_k(k)) {
-                        const V dv = ldg_v(vecg + gt + TPC * k);
-#pragma unroll
-                        for (int c = 0; c < C; ++c) s[c] += vwsq(x[c][k], dv);
-                    }
-                }
-#pragma unroll
-                for (int off = (TPC < 32 ? TPC : 32) / 2; off > 0; off >>= 1) {
-#pragma unroll
-                    for (int c = 0; c < C; ++c) s[c] += __shfl_xor_sync(0xffffffffu, s[c], off);
-                }
-                if constexpr (TPC > 32) {
-                    T *rb = red + (static_cast<size_t>(rpar) * NU + unit) * WPU * C;
-                    if (lane == 0) {
-#pragma unroll
-                        for (int c = 0; c < C; ++c) rb[wiu * C + c] = s[c];
-                    }
-                    named_bar_sync(1 + unit, UT);
-#pragma unroll
-                    for (int c = 0; c < C; ++c) {
-                        T v = rb[c];
-#pragma unroll
-                        for (int w = 1; w < WPU; ++w) v += rb[w * C + c];
-                        s[c] = v;
-                    }
-                    rpar ^= 1;
-                }
-                if (gt == 0) {
-                    T *dist = reinterpret_cast<T *>(a.Y);
-#pragma unroll
-                    for (int c = 0; c < C; ++c)
-                        if (col0 + c < a.N) dist[col0 + c] = s[c];
-                }
-            } else {
-                if (mode == MODE_TRANSFORM) {
-#pragma unroll
-                    for (int k = 0; k < CH; ++k) {
-                        if (valid_k(k)) {
-                            const V dv = ldg_v(vecg + gt + TPC * k);
-#pragma unroll
-                            for (int c = 0; c < C; ++c) vmulsqrt(x[c][k], dv);
-                        }
-                    }
-                }
-                if (a.dside & 2) {   // NEXT-f1 left factor (Y = D Q X)
-                    const V *dg = reinterpret_cast<const V *>(a.dsign);
-#pragma unroll
-                    for (int k = 0; k < CH; ++k) {
-                        if (valid_k(k)) {
-                            const V dv = ldg_v(dg + gt + TPC * k);
-#pragma unroll
-                            for (int c = 0; c < C; ++c) vmul(x[c][k], dv);
-                        }
-                    }
-                }
-                V *Yg = reinterpret_cast<V *>(a.Y);
-                const uint64_t ypol = policy_evict_first();
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    const int64_t j = col0 + c;
-                    if (j < a.N) {
-#pragma unroll
-                        for (int k = 0; k < CH; ++k)
-                            if (valid_k(k)) st_global_hint(Yg + j * nv + gt + TPC * k, x[c][k], ypol);
-                    }
-                }
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------------
-// Host-side variant table and launcher
-// ---------------------------------------------------------------------------------
 namespace {
 
-struct Variant {
-    const void *fn_full;
-    const void *fn_ragged;
-    int tpc, ch, c, nt;
-    int elem;  // bytes
-    const char *name;
-};
-
-#define HH_VAR(T, TPC, CH, C, NT, NAME)                                                 \
-    Variant {                                                                           \
-        reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true>),      \
-            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false>), \
-            TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME                           \
-    }
-
-const Variant kF32[] = {
-    HH_VAR(float, 8, 2, 1, 256, "f32_tpc8_ch2_c1"),     // n <= 64
-    HH_VAR(float, 8, 4, 1, 256, "f32_tpc8_ch4_c1"),     // n <= 128
-    HH_VAR(float, 16, 4, 1, 256, "f32_tpc16_ch4_c1"),   // n <= 256
-    HH_VAR(float, 32, 4, 2, 256, "f32_tpc32_ch4_c2"),   // n <= 512
-    HH_VAR(float, 32, 8, 2, 256, "f32_tpc32_ch8_c2"),   // n <= 1024
-    HH_VAR(float, 64, 8, 2, 256, "f32_tpc64_ch8_c2"),   // n <= 2048
-    HH_VAR(float, 128, 8, 2, 384, "f32_tpc128_ch8_c2"), // n <= 4096
-    HH_VAR(float, 256, 8, 1, 256, "f32_tpc256_ch8_c1"), // n <= 8192
-};
-const Variant kF64[] = {
-    HH_VAR(double, 8, 4, 1, 256, "f64_tpc8_ch4_c1"),     // n <= 64
-    HH_VAR(double, 16, 4, 1, 256, "f64_tpc16_ch4_c1"),   // n <= 128
-    HH_VAR(double, 32, 4, 1, 256, "f64_tpc32_ch4_c1"),   // n <= 256
-    HH_VAR(double, 32, 8, 1, 256, "f64_tpc32_ch8_c1"),   // n <= 512
-    HH_VAR(double, 64, 8, 1, 256, "f64_tpc64_ch8_c1"),   // n <= 1024
-    HH_VAR(double, 128, 8, 1, 256, "f64_tpc128_ch8_c1"), // n <= 2048
-    HH_VAR(double, 256, 8, 1, 256, "f64_tpc256_ch8_c1"), // n <= 4096
-};
-#undef HH_VAR
-
-const Variant *pick(int dtype, int64_t nv) {
-    const Variant *tab = dtype == 0 ? kF32 : kF64;
-    const int cnt = dtype == 0 ? static_cast<int>(sizeof(kF32) / sizeof(kF32[0]))
-                               : static_cast<int>(sizeof(kF64) / sizeof(kF64[0]));
+const FusedVariant *pick(int dtype, int64_t nv) {
+    int cnt = 0;
+    const FusedVariant *tab = dtype == 0 ? fused_table_f32(&cnt) : fused_table_f64(&cnt);
     for (int i = 0; i < cnt; ++i)
         if (static_cast<int64_t>(tab[i].tpc) * tab[i].ch >= nv) return &tab[i];
     return nullptr;
@@ -557,10 +24,9 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     const int E = dtype == 0 ? 4 : 2;
     const int s = dtype == 0 ? 4 : 8;
     const int64_t nv = a.n / E;
-    const Variant *v = pick(dtype, nv);
+    const FusedVariant *v = pick(dtype, nv);
     if (!v) return cudaErrorNotSupported;
     const bool full = static_cast<int64_t>(v->tpc) * v->ch == nv;
-    const void *fn = full ? v->fn_full : v->fn_ragged;
 
     const DevAttr &da = device_attr();
     const int UT = v->tpc > 32 ? v->tpc : 32;
@@ -578,8 +44,8 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     // re-streamed from L2 for every tile: h*n*s bytes per tile), (3) staged tiles + U
     // chunks through two buffers, (4) unstaged + U chunks.
     const size_t xs_st = static_cast<size_t>(NU) * UC * colB;
-    const size_t ub = static_cast<size_t>(h) * colB;
     const bool pair = a.mode == MODE_PAIR;
+    const size_t ub = static_cast<size_t>(h) * colB;
     int stage = 0, R = 0, nc = 1;
     size_t smem = 0;
     if (h == 0) {
@@ -611,6 +77,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     a.R = R;
     a.nchunks = nc;
     a.stage_x = stage;
+    const void *fn = full ? v->fn_full : v->fn_ragged;
 
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

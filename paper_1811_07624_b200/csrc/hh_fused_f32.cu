@@ -1,0 +1,24 @@
+// hh_fused_f32.cu -- fp32 instantiations of the fused kernel.
+#include "hh_fused_kernel.cuh"
+
+namespace hh {
+
+namespace {
+const FusedVariant kF32[] = {
+    HH_FUSED_VAR(float, 8, 2, 1, 256, "f32_tpc8_ch2_c1"),      // n <= 64
+    HH_FUSED_VAR(float, 8, 4, 1, 256, "f32_tpc8_ch4_c1"),      // n <= 128
+    HH_FUSED_VAR(float, 16, 4, 1, 256, "f32_tpc16_ch4_c1"),    // n <= 256
+    HH_FUSED_VAR(float, 32, 4, 2, 256, "f32_tpc32_ch4_c2"),    // n <= 512
+    HH_FUSED_VAR(float, 32, 8, 2, 256, "f32_tpc32_ch8_c2"),    // n <= 1024
+    HH_FUSED_VAR(float, 64, 8, 2, 256, "f32_tpc64_ch8_c2"),    // n <= 2048
+    HH_FUSED_VAR(float, 128, 8, 2, 384, "f32_tpc128_ch8_c2"),  // n <= 4096
+    HH_FUSED_VAR(float, 256, 8, 1, 256, "f32_tpc256_ch8_c1"),  // n <= 8192
+};
+}  // namespace
+
+const FusedVariant *fused_table_f32(int *count) {
+    *count = static_cast<int>(sizeof(kF32) / sizeof(kF32[0]));
+    return kF32;
+}
+
+}  // namespace hh

@@ -18,7 +18,7 @@ from typing import Optional
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhh.so")
+LIB_PATH = os.environ.get("HH_LIB_PATH") or os.path.join(_PKG, "libhh.so")  # override: A/B runs only
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "hh.h")
 
 HH_OK, HH_ERR_INVALID_VALUE, HH_ERR_UNSUPPORTED, HH_ERR_WORKSPACE, HH_ERR_CUDA = range(5)
