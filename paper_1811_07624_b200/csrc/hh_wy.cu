@@ -692,7 +692,8 @@ struct Bars3 {
 
 __global__ void __launch_bounds__(640, 1)
     wy_update_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
-                     const __grid_constant__ CUtensorMap tmXb, float *Y,
+                     const __grid_constant__ CUtensorMap tmXb,
+                     const __grid_constant__ CUtensorMap tmYs, float *Y,
                      const float *__restrict__ lam, const float *__restrict__ post, int n,
                      int n_pad, int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles, int rc0,
                      int copy_below, int nxs, unsigned long long *tl) {
@@ -724,7 +725,7 @@ __global__ void __launch_bounds__(640, 1)
         }
         for (int s = 0; s < nxs; ++s) {
             mbar_init(&bars->xfull[s], 1);
-            mbar_init(&bars->xempty[s], 128);
+            mbar_init(&bars->xempty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->acc_full[a], 1);
@@ -875,9 +876,10 @@ __global__ void __launch_bounds__(640, 1)
                     const unsigned long long t0 = clock64();
                     mbar_wait(&bars->xfull[s], static_cast<uint32_t>((sq / nxs) & 1));
                     w_b += clock64() - t0;
-                    const float *xs = Xs(s);
-                    const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + cb * kXBoxCols;
-                    float *dst = Y + j0 * n + r;
+                    // this thread's row of the box: X[j0 + e][r] at xs + (e * 128 + r_in) * 4;
+                    // Y overwrites X in the box and one TMA store writes the box back (rows
+                    // >= n and columns >= N are clipped by the tensor map)
+                    const uint32_t xs = smem_u32(Xs(s)) + static_cast<uint32_t>(r_in) * 4u;
                     float v[16];
                     if (mma_rc) {
                         tc::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) +
@@ -887,15 +889,19 @@ __global__ void __launch_bounds__(640, 1)
 #pragma unroll
                         for (int e = 0; e < 16; ++e) v[e] = 0.f;
                     }
-                    if (r < n) {
 #pragma unroll
-                        for (int e = 0; e < kXBoxCols; ++e) {
-                            if (j0 + e < N)
-                                dst[static_cast<int64_t>(e) * n] =
-                                    pr * fmaf(lr, xs[e * kRowChunk + r_in], -v[e]);
-                        }
+                    for (int e = 0; e < kXBoxCols; ++e) {
+                        const uint32_t ad = xs + e * kRowChunk * 4;
+                        sts_f32(ad, pr * fmaf(lr, lds_f32(ad), -v[e]));
                     }
-                    tc::mbar_arrive(&bars->xempty[s]);
+                    fence_proxy_async_smem();
+                    named_bar_sync(1 + grp, 128);
+                    if (q == 0 && lane == 0) {
+                        tc::tma_store_2d(&tmYs, Xs(s), rc * kRowChunk, tile * kTileCols + cb * kXBoxCols);
+                        tc::bulk_commit();
+                        tc::bulk_wait_read0();   // the box may be refilled once TMA has read it
+                        tc::mbar_arrive(&bars->xempty[s]);
+                    }
                 }
                 if (mma_rc) {
                     tc::fence_before_sync();
@@ -908,6 +914,7 @@ __global__ void __launch_bounds__(640, 1)
             }
         }
     }
+    if (warp >= 4 && (warp & 3) == 0 && lane == 0) tc::bulk_wait0();
     if (dbg && lane == 0) {
         // [0] kernel cycles  [1,2] V producer: empty waits  [3,4] MMA: full waits, acc_empty
         // waits  [5,6] X producer: xempty waits  [7,8] epilogue warp 4: acc_full, xfull waits
@@ -1236,7 +1243,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw));
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
         ++nlaunch, wy_update_kernel<<<grid, 640, smem3(ps.kw), stream>>>(
-            *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
+            *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
             ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw),
             g_timeline);
