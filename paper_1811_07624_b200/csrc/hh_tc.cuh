@@ -188,10 +188,25 @@ __device__ __forceinline__ uint32_t bf16_bits(float x) {
 }
 __device__ __forceinline__ float bf16_val(uint32_t b) { return __uint_as_float(b << 16); }
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t &hi, uint32_t &lo) {
-    const uint32_t h0 = bf16_bits(x0), h1 = bf16_bits(x1);
-    const uint32_t l0 = bf16_bits(x0 - bf16_val(h0)), l1 = bf16_bits(x1 - bf16_val(h1));
-    hi = h0 | (h1 << 16);
-    lo = l0 | (l1 << 16);
+    // packed conversions (one cvt.rn.bf16x2.f32 per pair): hi = {bf16(x1), bf16(x0)},
+    // the residuals x - hi are exact in fp32, lo = {bf16(x1 - hi1), bf16(x0 - hi0)}
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
+    const float r0 = x0 - __uint_as_float(hi << 16);
+    const float r1 = x1 - __uint_as_float(hi & 0xFFFF0000u);
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r1), "f"(r0));
+}
+// shared-memory accesses by 32-bit shared address (the dynamic-smem base is realigned
+// through an integer, after which the compiler no longer knows the address space)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
 
 // byte offset of the 16-byte chunk `c` (0..7) of row `r` in a K-major SWIZZLE_128B

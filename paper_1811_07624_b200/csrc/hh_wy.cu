@@ -585,10 +585,10 @@ __global__ void __launch_bounds__(480, 1)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             for (int ks = ks0; ks < nk; ++ks) {
                 mbar_wait(&bars->rfull[rs], rph);
-                const float4 *raw = reinterpret_cast<const float4 *>(rawX(rs));
+                const uint32_t raw = smem_u32(rawX(rs));
                 float4 v[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v[q] = raw[ct + 256 * q];
+                for (int q = 0; q < 4; ++q) v[q] = tc::lds128(raw + (ct + 256 * q) * 16);
                 if (dscale) {   // NEXT-f1 right factor: project D X
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(480, 1)
                     }
                 }
                 mbar_wait(&bars->cempty[cs], cph ^ 1u);
-                unsigned char *xh = Xhi(cs), *xl = Xlo(cs);
+                const uint32_t xh = smem_u32(Xhi(cs)), xl = smem_u32(Xlo(cs));
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int idx = ct + 256 * q;
@@ -612,8 +612,8 @@ __global__ void __launch_bounds__(480, 1)
                     tc::split2(v[q].x, v[q].y, H.x, L.x);
                     tc::split2(v[q].z, v[q].w, H.y, L.y);
                     const uint32_t off = tc::sw64_off(r, c4 >> 1) + (c4 & 1) * 8;
-                    *reinterpret_cast<uint2 *>(xh + off) = H;
-                    *reinterpret_cast<uint2 *>(xl + off) = L;
+                    tc::sts64(xh + off, H.x, H.y);
+                    tc::sts64(xl + off, L.x, L.y);
                 }
                 // the raw tile is released only after its values were consumed (the
                 // stores above depend on them) and ordered against the async proxy that
