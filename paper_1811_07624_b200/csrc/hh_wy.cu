@@ -716,6 +716,24 @@ __global__ void __launch_bounds__(640, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nrc = n_pad / kRowChunk;
+    // balanced schedule: the (tile, row chunk) units, tile-major, are split into equal
+    // contiguous ranges per CTA (512 tiles over 148 SMs would otherwise leave a 4th-tile
+    // tail on some SMs); every role walks the same segments [rlo, rhi) of each tile.
+    // Rows below rc0 are copy-only (no MMA) and exist only when copy_below.
+    const int xrc0 = copy_below ? 0 : rc0;
+    const int64_t per = nrc - xrc0;
+    const int64_t utot = static_cast<int64_t>(ntiles) * per;
+    const int64_t ubeg = utot * blockIdx.x / gridDim.x, uend = utot * (blockIdx.x + 1) / gridDim.x;
+    auto for_segments = [&](auto &&fn) {
+        for (int64_t u = ubeg; u < uend;) {
+            const int tile = static_cast<int>(u / per);
+            const int64_t t0 = static_cast<int64_t>(tile) * per;
+            const int rlo = xrc0 + static_cast<int>(u - t0);
+            const int rhi = xrc0 + static_cast<int>(uend - t0 < per ? uend - t0 : per);
+            fn(tile, rlo, rhi);
+            u = t0 + per;
+        }
+    };
     if (threadIdx.x == 0) {
         mbar_init(&bars->gfull, 1);
         mbar_init(&bars->gempty, 1);
@@ -745,7 +763,9 @@ __global__ void __launch_bounds__(640, 1)
             tc::prefetch_tmap(&tmV);
             int s = 0;
             uint32_t ph = 0, gph = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for_segments([&](int tile, int rlo, int rhi) {
+                const int mlo = rlo > rc0 ? rlo : rc0;
+                if (mlo >= rhi) return;   // copy-only segment: no G, no V
                 mbar_wait(&bars->gempty, gph ^ 1u);
                 mbar_arrive_expect_tx(&bars->gfull, static_cast<uint32_t>(nslab) * 16384u);
                 for (int c = 0; c < nslab; ++c) {
@@ -754,7 +774,7 @@ __global__ void __launch_bounds__(640, 1)
                                     static_cast<int>(N) + tile * kTileCols, &bars->gfull);
                 }
                 gph ^= 1u;
-                for (int rc = rc0; rc < nrc; ++rc) {
+                for (int rc = mlo; rc < rhi; ++rc) {
                     for (int c = 0; c < nslab; ++c) {
                         const unsigned long long t0 = clock64();
                         mbar_wait(&bars->empty[s], ph ^ 1u);
@@ -768,7 +788,7 @@ __global__ void __launch_bounds__(640, 1)
                         }
                     }
                 }
-            }
+            });
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -776,11 +796,13 @@ __global__ void __launch_bounds__(640, 1)
             int s = 0, a = 0;
             uint32_t ph = 0, aph = 0, gph = 0;
             const uint32_t gh0 = smem_u32(Ghi), gl0 = smem_u32(Glo);
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for_segments([&](int tile, int rlo, int rhi) {
+                const int mlo = rlo > rc0 ? rlo : rc0;
+                if (mlo >= rhi) return;
                 mbar_wait(&bars->gfull, gph);
                 gph ^= 1u;
                 tc::fence_after_sync();
-                for (int rc = rc0; rc < nrc; ++rc) {
+                for (int rc = mlo; rc < rhi; ++rc) {
                     const unsigned long long t1 = clock64();
                     mbar_wait(&bars->acc_empty[a], aph ^ 1u);
                     w_b += clock64() - t1;
@@ -814,7 +836,7 @@ __global__ void __launch_bounds__(640, 1)
                     }
                 }
                 tc::mma_commit(&bars->gempty);
-            }
+            });
         }
         __syncwarp();
     } else if (warp == 2) {
@@ -822,9 +844,8 @@ __global__ void __launch_bounds__(640, 1)
             tc::prefetch_tmap(&tmXb);
             int s = 0;
             uint32_t ph = 0;
-            const int xrc0 = copy_below ? 0 : rc0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int rc = xrc0; rc < nrc; ++rc) {
+            for_segments([&](int tile, int rlo, int rhi) {
+                for (int rc = rlo; rc < rhi; ++rc) {
                     for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb) {
                         const unsigned long long t0 = clock64();
                         mbar_wait(&bars->xempty[s], ph ^ 1u);
@@ -838,7 +859,7 @@ __global__ void __launch_bounds__(640, 1)
                         }
                     }
                 }
-            }
+            });
         }
     } else if (warp >= 4) {
         // 16 epilogue warps: 4 groups of 4 (one warp per TMEM lane quarter); group g takes
@@ -851,9 +872,8 @@ __global__ void __launch_bounds__(640, 1)
         constexpr int kBoxes = kTileCols / kXBoxCols;   // X boxes per r-chunk
         static_assert(kBoxes % 4 == 0, "one consumer group per stage (nxs % 4 == 0)");
         int64_t seq = 0;   // position in the X box ring (both groups follow it)
-        const int xrc0 = copy_below ? 0 : rc0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            for (int rc = xrc0; rc < nrc; ++rc, seq += kBoxes) {
+        for_segments([&](int tile, int rlo, int rhi) {
+            for (int rc = rlo; rc < rhi; ++rc, seq += kBoxes) {
                 // NEXT-f2: below row rc0*128 the block's V rows are zero, no MMA ran: those
                 // rows are copied (scaled) when the pass is out of place
                 const bool mma_rc = rc >= rc0;
@@ -912,7 +932,7 @@ __global__ void __launch_bounds__(640, 1)
                     }
                 }
             }
-        }
+        });
     }
     if (warp >= 4 && (warp & 3) == 0 && lane == 0) tc::bulk_wait0();
     if (dbg && lane == 0) {
@@ -1242,7 +1262,10 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
             ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw));
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
-        ++nlaunch, wy_update_kernel<<<grid, 640, smem3(ps.kw), stream>>>(
+        const int64_t uxrc = (cur != Y && ps.row0 >= kRowChunk) ? 0 : ps.row0 / kRowChunk;
+        const int64_t units = static_cast<int64_t>(ntiles) * (n_pad / kRowChunk - uxrc);
+        const int grid3 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
+        ++nlaunch, wy_update_kernel<<<grid3, 640, smem3(ps.kw), stream>>>(
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
             ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw),
