@@ -74,7 +74,7 @@ struct WyPlan {
     int64_t n_pad = 0;
     size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_v = 0, off_v2 = 0,
            off_asym = 0, off_vf = 0, off_vpf = 0, off_pp = 0, off_p = 0, off_m = 0, off_gt = 0,
-           off_ld = 0;
+           off_ld = 0, off_part = 0, off_flag = 0;
     size_t bytes = 0;
 };
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N);

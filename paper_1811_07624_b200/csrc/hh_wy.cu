@@ -61,6 +61,8 @@ constexpr int kConv1Bytes = 49152;   // X hi/lo 16K + W hi/lo 32K at b = 256 (ma
 constexpr int kStage3Bytes = 16384;  // V hi/lo tile (128 rows x 32 bf16) x 2
 constexpr int kGresBytes = 131072;   // resident G hi/lo (128 x 256 bf16) x 2 at b = 256 (max)
 constexpr int kSmemMax = 232448;     // 227 KB opt-in per CTA
+constexpr int kKChunk1 = 8;          // K5a schedule unit: 8 K steps (256 rows of X)
+constexpr int kSlots1 = 256;         // K5a split-tile hand-off slots (>= the grid)
 
 size_t al(size_t x) { return (x + 1023) & ~static_cast<size_t>(1023); }
 
@@ -461,11 +463,25 @@ struct Bars1 {
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem;
 };
+// ld/st of the split-tile hand-off (L2, bypassing L1: written by another CTA)
+__device__ __forceinline__ void st_cg4(float *p, float a, float b, float c, float d) {
+    asm volatile("st.global.cg.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ float4 ld_cg4(const float *p) {
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
 
 __global__ void __launch_bounds__(480, 1)
     wy_project_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       uint16_t *__restrict__ Gt, int n, int64_t N, int b, int wrow_hi, int wrow_lo,
-                      int ntiles, const float *__restrict__ dscale, int ks0, int nraw) {
+                      int ntiles, const float *__restrict__ dscale, int ks0, int nraw,
+                      float *__restrict__ part, int *__restrict__ flag) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -482,6 +498,31 @@ __global__ void __launch_bounds__(480, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (n + 31) / 32;
+    // balanced schedule: (tile, K chunk) units, tile-major, in equal contiguous ranges per
+    // CTA (whole tiles would leave 512 tiles on 148 SMs with a 4th-tile tail).  A tile cut
+    // by a range boundary is shared by two CTAs: the next CTA computes the tile's trailing
+    // K chunks as its first segment and leaves that fp32 partial G in slot blockIdx-1
+    // (+ a flag); this CTA computes the leading chunks as its last segment, adds the
+    // partial (long since available) and writes G.  grid <= ntiles, so a tile has at
+    // most two owners, and no CTA waits before its last segment.
+    const int64_t nkc = (nk - ks0 + kKChunk1 - 1) / kKChunk1;
+    const int64_t utot = static_cast<int64_t>(ntiles) * nkc;
+    const int64_t ubeg = utot * blockIdx.x / gridDim.x, uend = utot * (blockIdx.x + 1) / gridDim.x;
+    auto for_segments = [&](auto &&fn) {   // fn(tile, ks_lo, ks_hi, head, tail)
+        for (int64_t u = ubeg; u < uend;) {
+            const int tile = static_cast<int>(u / nkc);
+            const int64_t t0 = static_cast<int64_t>(tile) * nkc;
+            const int plo = static_cast<int>(u - t0);
+            const int phi = static_cast<int>(uend - t0 < nkc ? uend - t0 : nkc);
+            const int klo = ks0 + plo * kKChunk1;
+            const int khi = ks0 + phi * kKChunk1 < nk ? ks0 + phi * kKChunk1 : nk;
+            // head: this CTA's first segment holds a tile's trailing chunks (hand the
+            // partial to the previous CTA); tail: its last segment holds a tile's leading
+            // chunks (take the next CTA's partial, write G)
+            fn(tile, klo, khi, plo > 0, plo == 0 && phi < nkc);
+            u = t0 + nkc;
+        }
+    };
     if (threadIdx.x == 0) {
         for (int s = 0; s < nraw; ++s) {
             mbar_init(&bars->rfull[s], 1);
@@ -509,8 +550,8 @@ __global__ void __launch_bounds__(480, 1)
             tc::prefetch_tmap(&tmX);
             int s = 0;
             uint32_t ph = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int ks = ks0; ks < nk; ++ks) {
+            for_segments([&](int tile, int klo, int khi, bool, bool) {
+                for (int ks = klo; ks < khi; ++ks) {
                     mbar_wait(&bars->rempty[s], ph ^ 1u);
                     mbar_arrive_expect_tx(&bars->rfull[s], static_cast<uint32_t>(kRawBytes));
                     tc::tma_load_2d(rawX(s), &tmX, ks * 32, tile * kTileCols, &bars->rfull[s]);
@@ -519,7 +560,7 @@ __global__ void __launch_bounds__(480, 1)
                         ph ^= 1u;
                     }
                 }
-            }
+            });
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -527,8 +568,8 @@ __global__ void __launch_bounds__(480, 1)
             int s = 0;
             uint32_t ph = 0;
             const uint32_t bytes = 128u * static_cast<uint32_t>(b);
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int ks = ks0; ks < nk; ++ks) {
+            for_segments([&](int, int klo, int khi, bool, bool) {
+                for (int ks = klo; ks < khi; ++ks) {
                     mbar_wait(&bars->cempty[s], ph ^ 1u);
                     mbar_arrive_expect_tx(&bars->wfull[s], bytes);
                     tc::tma_load_2d(Whi(s), &tmW, ks * 32, wrow_hi, &bars->wfull[s]);
@@ -538,18 +579,18 @@ __global__ void __launch_bounds__(480, 1)
                         ph ^= 1u;
                     }
                 }
-            }
+            });
         }
     } else if (warp == 2) {
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_bf16(128, b);
             int s = 0, a = 0;
             uint32_t ph = 0, aph = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for_segments([&](int, int klo, int khi, bool, bool) {
                 mbar_wait(&bars->acc_empty[a], aph ^ 1u);
                 tc::fence_after_sync();
                 const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
-                for (int ks = ks0; ks < nk; ++ks) {
+                for (int ks = klo; ks < khi; ++ks) {
                     mbar_wait(&bars->wfull[s], ph);
                     mbar_wait(&bars->cfull[s], ph);
                     tc::fence_after_sync();
@@ -559,7 +600,7 @@ __global__ void __launch_bounds__(480, 1)
                     for (int kk = 0; kk < 2; ++kk) {
                         const uint64_t ah = tc::sdesc_sw64(xh + kk * 32), alo = tc::sdesc_sw64(xl + kk * 32);
                         const uint64_t bh = tc::sdesc_sw64(wh + kk * 32), blo = tc::sdesc_sw64(wl + kk * 32);
-                        tc::mma_bf16(d, ah, bh, idesc, (ks != ks0 || kk != 0) ? 1u : 0u);
+                        tc::mma_bf16(d, ah, bh, idesc, (ks != klo || kk != 0) ? 1u : 0u);
                         tc::mma_bf16(d, ah, blo, idesc, 1u);
                         tc::mma_bf16(d, alo, bh, idesc, 1u);
                     }
@@ -574,7 +615,7 @@ __global__ void __launch_bounds__(480, 1)
                     a = 0;
                     aph ^= 1u;
                 }
-            }
+            });
         }
         __syncwarp();
     } else if (warp < 11) {
@@ -582,8 +623,8 @@ __global__ void __launch_bounds__(480, 1)
         const int ct = threadIdx.x - 96;
         int rs = 0, cs = 0;
         uint32_t rph = 0, cph = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            for (int ks = ks0; ks < nk; ++ks) {
+        for_segments([&](int, int klo, int khi, bool, bool) {
+            for (int ks = klo; ks < khi; ++ks) {
                 mbar_wait(&bars->rfull[rs], rph);
                 const uint32_t raw = smem_u32(rawX(rs));
                 float4 v[4];
@@ -630,22 +671,56 @@ __global__ void __launch_bounds__(480, 1)
                     cph ^= 1u;
                 }
             }
-        }
+        });
     } else {
         // epilogue: TMEM lane quarter q = warp % 4
         const int q = warp & 3;
         int a = 0;
         uint32_t aph = 0;
         uint16_t *Glo = Gt + N * b;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int jl = q * 32 + lane;
+        for_segments([&](int tile, int, int, bool head, bool tail) {
             mbar_wait(&bars->acc_full[a], aph);
             tc::fence_after_sync();
-            const int64_t j = static_cast<int64_t>(tile) * kTileCols + q * 32 + lane;
+            const int64_t j = static_cast<int64_t>(tile) * kTileCols + jl;
+            if (tail) {
+                // wait for the next CTA's partial of this tile (it computed it first thing)
+                if (jl == 0) {
+                    volatile int *f = flag + blockIdx.x;
+                    // the partner CTA is co-resident (grid <= SMs) and produces this first
+                    // thing; a missing hand-off is a bug: trap rather than hang
+                    for (uint32_t it = 0; *f == 0; ++it) {
+                        if (it > (1u << 24)) __trap();
+                        __nanosleep(256);
+                    }
+                    __threadfence();
+                }
+                named_bar_sync(1, 128);
+            }
+            float *slot_w = part + (static_cast<size_t>(blockIdx.x) - 1) * kTileCols * b;   // head
+            const float *slot_r = part + static_cast<size_t>(blockIdx.x) * kTileCols * b;  // tail
             for (int c = 0; c < b / 32; ++c) {
                 float v[32];
                 tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
                                   static_cast<uint32_t>(a * 256 + c * 32),
                               v);
+                if (head) {
+                    float *dst = slot_w + (static_cast<size_t>(c) * kTileCols + jl) * 32;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) st_cg4(dst + 4 * e, v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+                    continue;
+                }
+                if (tail) {
+                    const float *src = slot_r + (static_cast<size_t>(c) * kTileCols + jl) * 32;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float4 pv = ld_cg4(src + 4 * e);
+                        v[4 * e] += pv.x;
+                        v[4 * e + 1] += pv.y;
+                        v[4 * e + 2] += pv.z;
+                        v[4 * e + 3] += pv.w;
+                    }
+                }
                 if (j < N) {
                     uint32_t H[16], L[16];
 #pragma unroll
@@ -659,13 +734,19 @@ __global__ void __launch_bounds__(480, 1)
                     }
                 }
             }
+            if (head) {
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (jl == 0) atomicExch(flag + blockIdx.x - 1, 1);
+            }
+            if (tail && jl == 0) flag[blockIdx.x] = 0;   // ready for the next launch
             tc::fence_before_sync();
             tc::mbar_arrive(&bars->acc_empty[a]);
             if (++a == 2) {
                 a = 0;
                 aph ^= 1u;
             }
-        }
+        });
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -1052,6 +1133,8 @@ WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     }
     const int kmax = kind == WY_SYM ? 2 * p.b : p.b;
     p.off_gt = take(static_cast<size_t>(std::max<int64_t>(N, 1)) * kmax * 2 * 2);
+    p.off_part = take(static_cast<size_t>(kSlots1) * kTileCols * kmax * 4);   // K5a hand-off
+    p.off_flag = take(static_cast<size_t>(kSlots1) * 4);
     p.bytes = off;
     return p;
 }
@@ -1253,14 +1336,18 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     if (dsign && (dside & 2)) prog[np - 1].post = dsign;
 
     const int ntiles = static_cast<int>((N + kTileCols - 1) / kTileCols);
-    const int grid = std::max(1, std::min(ntiles, sms));
+    const int grid = std::max(1, std::min(std::min(ntiles, sms), kSlots1));
+    // K5a hand-off flags start at zero (each tail resets its flag after use)
+    e = cudaMemsetAsync(w + p.off_flag, 0, static_cast<size_t>(kSlots1) * 4, stream);
+    if (e != cudaSuccess) return e;
     const float *cur = X;
     for (int q = 0; q < np; ++q) {
         const Pass &ps = prog[q];
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
         ++nlaunch, wy_project_kernel<<<grid, 480, smem1(ps.kw), stream>>>(
             mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
-            ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw));
+            ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw), F(p.off_part),
+            reinterpret_cast<int *>(w + p.off_flag));
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
         const int64_t uxrc = (cur != Y && ps.row0 >= kRowChunk) ? 0 : ps.row0 / kRowChunk;
         const int64_t units = static_cast<int64_t>(ntiles) * (n_pad / kRowChunk - uxrc);
