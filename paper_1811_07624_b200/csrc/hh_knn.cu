@@ -36,7 +36,8 @@ constexpr int kQ = 128;           // queries per CTA (MMA M)
 constexpr int kRT = 128;          // references per tile (MMA N)
 constexpr int kKS = 4;            // reference slab ring depth
 constexpr int kKnnMaxK = 16;      // largest k
-constexpr int kKnnMaxNpad = 256;  // resident query tile: n_pad x 128 x 4 B <= 128 KB
+constexpr int kKnnMaxN = 256;     // largest n (K = n + 1 augmented, padded to 32)
+constexpr int kKnnMaxNpad = 288;  // resident query tile: n_pad x 128 x 4 B <= 144 KB
 
 size_t al(size_t x) { return (x + 1023) & ~static_cast<size_t>(1023); }
 
@@ -49,23 +50,30 @@ __device__ __forceinline__ float bf2f(uint16_t b) {
     return __uint_as_float(static_cast<uint32_t>(b) << 16);
 }
 
-// one warp per point: Zb[hi: row][0..n_pad), Zb[lo: M + row][..] and nrm[row] = ||z||^2
+// one warp per point: Zb[hi: row][0..n_pad), Zb[lo: M + row][..] and nrm[row] = ||z||^2.
+// Column n is the augmentation that folds the reference norm into the tensor-core dot:
+// queries carry 1, references -||z_r||^2 / 2, so the accumulator holds
+// D = z_q . z_r - ||z_r||^2 / 2 and d_S(q, r) = ||z_q||^2 - 2 D.
 __global__ void knn_pack_kernel(const float *__restrict__ Z, int64_t M, int n, int n_pad,
-                                uint16_t *__restrict__ Zb, float *__restrict__ nrm) {
+                                int is_query, uint16_t *__restrict__ Zb, float *__restrict__ nrm) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     for (int64_t row = w0; row < M; row += nw) {
         float ss = 0.f;
-        for (int c = lane; c < n_pad; c += 32) {
-            const float v = c < n ? Z[row * n + c] : 0.f;
+        for (int c = lane; c < n; c += 32) {
+            const float v = Z[row * n + c];
             ss = fmaf(v, v, ss);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        const float aug = is_query ? 1.f : -0.5f * ss;
+        for (int c = lane; c < n_pad; c += 32) {
+            const float v = c < n ? Z[row * n + c] : (c == n ? aug : 0.f);
             const uint16_t h = f2bf(v);
             Zb[row * n_pad + c] = h;
             Zb[(M + row) * n_pad + c] = f2bf(v - bf2f(h));
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
         if (lane == 0) nrm[row] = ss;
     }
 }
@@ -78,7 +86,9 @@ struct BarsK {
 };
 
 // grid (query tiles, splits).  18 warps: w0 TMA producer, w1 MMA issuer (+TMEM
-// owner), w2-17 epilogue (TMEM lane quarter x column group; thread = query).
+// owner), w2-17 epilogue (TMEM lane quarter x column group; thread = query).  KM: the
+// register top-k capacity (k <= KM).
+template <int KM>
 __global__ void __launch_bounds__(576, 1)
     knn_topk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmR,
                     const float *__restrict__ qn, const float *__restrict__ rn, int64_t Mq,
@@ -185,16 +195,17 @@ __global__ void __launch_bounds__(576, 1)
         __syncwarp();
     } else {
         // 16 epilogue warps: lane quarter q (thread = query), column group grp (32 of
-        // the 128 references of a tile).  Per reference: one shuffle (its norm), one FMA
-        // and one compare against the current k-th distance; the rare insertions run
-        // off a per-thread hit mask, outside the streaming loop.
+        // the 128 references of a tile).  The accumulator already holds
+        // D = z_q.z_r - ||z_r||^2/2 (augmented K column), so per reference the streaming
+        // loop is one compare into a hit mask: d_S < worst  <=>  D > (||z_q||^2 - worst)/2.
+        // The rare insertions run off the mask, outside the streaming loop.
         const int q = warp & 3, grp = (warp - 2) >> 2;
         const int64_t row = static_cast<int64_t>(qt) * kQ + q * 32 + lane;
         const float qnorm = row < Mq ? qn[row] : 0.f;
-        float bd[kKnnMaxK];
-        int32_t bi[kKnnMaxK];
+        float bd[KM];
+        int32_t bi[KM];
 #pragma unroll
-        for (int e = 0; e < kKnnMaxK; ++e) {
+        for (int e = 0; e < KM; ++e) {
             bd[e] = FLT_MAX;
             bi[e] = -1;
         }
@@ -203,7 +214,7 @@ __global__ void __launch_bounds__(576, 1)
         uint32_t aph = 0;
         for (int64_t t = t0; t < t1; ++t) {
             const int64_t j0 = t * kRT + grp * 32;
-            const float rnl = j0 + lane < Mr ? __ldg(rn + j0 + lane) : FLT_MAX;
+            const int jvalid = Mr - j0 >= 32 ? 32 : static_cast<int>(Mr - j0);   // may be <= 0
             mbar_wait(&bars->acc_full[a], aph);
             tc::fence_after_sync();
             float v[32];
@@ -216,27 +227,29 @@ __global__ void __launch_bounds__(576, 1)
                 a = 0;
                 aph ^= 1u;
             }
-            // dist = qnorm + rn[j] - 2 dot  <  worst   <=>   rn[j] - 2 dot < worst - qnorm
-            const float thr = worst - qnorm;
+            const float c = 0.5f * (qnorm - worst);
             uint32_t hit = 0;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                const float rj = __shfl_sync(0xffffffffu, rnl, e);
-                v[e] = fmaf(-2.f, v[e], rj);
-                hit |= (v[e] < thr ? 1u : 0u) << e;
-            }
+            for (int e = 0; e < 32; ++e) hit |= (v[e] > c ? 1u : 0u) << e;
+            if (jvalid < 32) hit &= jvalid > 0 ? (0xffffffffu >> (32 - jvalid)) : 0u;
             while (hit) {   // ascending j: an equal distance keeps the earlier reference
                 const int e = __ffs(hit) - 1;
                 hit &= hit - 1;
-                float cd = 0.f;
+                // v[e] by a 5-level select tree (no dynamic register indexing)
+                float t16[16], t8[8], t4[4], t2[2];
 #pragma unroll
-                for (int u = 0; u < 32; ++u)
-                    if (u == e) cd = v[u];
-                cd += qnorm;
+                for (int u = 0; u < 16; ++u) t16[u] = (e & 16) ? v[u + 16] : v[u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t8[u] = (e & 8) ? t16[u + 8] : t16[u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) t4[u] = (e & 4) ? t8[u + 4] : t8[u];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) t2[u] = (e & 2) ? t4[u + 2] : t4[u];
+                float cd = fmaf(-2.f, (e & 1) ? t2[1] : t2[0], qnorm);
                 if (!(cd < worst)) continue;
                 int32_t ci = static_cast<int32_t>(j0 + e);
 #pragma unroll
-                for (int u = 0; u < kKnnMaxK; ++u) {
+                for (int u = 0; u < KM; ++u) {
                     if (u < k) {
                         const bool sw = cd < bd[u];
                         const float td = bd[u];
@@ -248,7 +261,7 @@ __global__ void __launch_bounds__(576, 1)
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < kKnnMaxK; ++u)
+                for (int u = 0; u < KM; ++u)
                     if (u == k - 1) worst = bd[u];
             }
         }
@@ -259,7 +272,7 @@ __global__ void __launch_bounds__(576, 1)
         fence_proxy_async_smem();
         const int qi = q * 32 + lane;
 #pragma unroll
-        for (int u = 0; u < kKnnMaxK; ++u) {
+        for (int u = 0; u < KM; ++u) {
             if (u < k) {
                 md[(grp * kQ + qi) * kKnnMaxK + u] = bd[u];
                 mi[(grp * kQ + qi) * kKnnMaxK + u] = bi[u];
@@ -364,7 +377,7 @@ KnnPlan knn_plan(int64_t n, int64_t Mr, int64_t Mq, int k, int sm_count) {
     p.Mr = Mr;
     p.Mq = Mq;
     p.k = k;
-    p.n_pad = static_cast<int>((n + 31) / 32 * 32);
+    p.n_pad = static_cast<int>((n + 1 + 31) / 32 * 32);   // + the augmentation column
     const int64_t qtiles = (Mq + kQ - 1) / kQ;
     const int64_t rtiles = (Mr + kRT - 1) / kRT;
     // one CTA per SM (registers): pick the split count whose CTA total fills the last
@@ -402,7 +415,7 @@ KnnPlan knn_plan(int64_t n, int64_t Mr, int64_t Mq, int k, int sm_count) {
 }
 
 bool knn_supported(int64_t n, int64_t Mr, int64_t Mq, int k) {
-    return n >= 4 && n % 4 == 0 && (n + 31) / 32 * 32 <= kKnnMaxNpad && k >= 1 &&
+    return n >= 4 && n % 4 == 0 && n <= kKnnMaxN && k >= 1 &&
            k <= kKnnMaxK && Mr >= k && Mq >= 1 && 2 * Mr < (int64_t(1) << 31) &&
            2 * Mq < (int64_t(1) << 31);
 }
@@ -411,9 +424,15 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
                        const float *Pr, const float *Pq, int32_t *nn_idx, float *nn_dist, void *ws,
                        cudaStream_t stream, LaunchInfo *info) {
     std::call_once(g_knn_attr_once, []() {
-        g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(knn_smem(kKnnMaxNpad)));
+        const int sm = static_cast<int>(knn_smem(kKnnMaxNpad));
+        g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel<4>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        if (g_knn_attr_err == cudaSuccess)
+            g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel<8>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        if (g_knn_attr_err == cudaSuccess)
+            g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel<kKnnMaxK>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     });
     if (g_knn_attr_err != cudaSuccess) return g_knn_attr_err;
     char *w = static_cast<char *>(ws);
@@ -442,8 +461,8 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
     }
     // 2. bf16 hi/lo split + squared norms
     const int sms = device_attr().sm_count;
-    knn_pack_kernel<<<sms * 4, 256, 0, stream>>>(Zr, p.Mr, static_cast<int>(p.n), p.n_pad, Zrb, rn);
-    knn_pack_kernel<<<sms * 4, 256, 0, stream>>>(Zq, p.Mq, static_cast<int>(p.n), p.n_pad, Zqb, qn);
+    knn_pack_kernel<<<sms * 4, 256, 0, stream>>>(Zr, p.Mr, static_cast<int>(p.n), p.n_pad, 0, Zrb, rn);
+    knn_pack_kernel<<<sms * 4, 256, 0, stream>>>(Zq, p.Mq, static_cast<int>(p.n), p.n_pad, 1, Zqb, qn);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // 3. distances on the tensor cores + per-query top-k
@@ -451,8 +470,16 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
     if (!make_map_bf16(&mQ, Zqb, p.n_pad, 2 * p.Mq) || !make_map_bf16(&mR, Zrb, p.n_pad, 2 * p.Mr))
         return cudaErrorNotSupported;
     const dim3 grid(static_cast<unsigned>((p.Mq + kQ - 1) / kQ), static_cast<unsigned>(p.splits));
-    knn_topk_kernel<<<grid, 576, knn_smem(p.n_pad), stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad,
-                                                              p.k, p.tiles_per_split, pd, pi);
+    const size_t sm = knn_smem(p.n_pad);
+    if (p.k <= 4)
+        knn_topk_kernel<4><<<grid, 576, sm, stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad, p.k,
+                                                      p.tiles_per_split, pd, pi);
+    else if (p.k <= 8)
+        knn_topk_kernel<8><<<grid, 576, sm, stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad, p.k,
+                                                      p.tiles_per_split, pd, pi);
+    else
+        knn_topk_kernel<kKnnMaxK><<<grid, 576, sm, stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad,
+                                                             p.k, p.tiles_per_split, pd, pi);
     // 4. merge the per-split lists
     knn_merge_kernel<<<static_cast<int>((p.Mq + 127) / 128), 128, 0, stream>>>(
         pd, pi, p.Mq, p.k, p.splits, nn_dist, nn_idx);
