@@ -34,7 +34,8 @@ namespace {
 
 constexpr int kQ = 128;           // queries per CTA (MMA M)
 constexpr int kRT = 128;          // references per tile (MMA N)
-constexpr int kKS = 4;            // reference slab ring depth
+constexpr int kKS = 12;           // reference slab ring depth: maximum (runtime nks)
+constexpr int kNAcc = 4;          // TMEM accumulators (4 x 128 columns)
 constexpr int kKnnMaxK = 16;      // largest k
 constexpr int kKnnMaxN = 256;     // largest n (K = n + 1 augmented, padded to 32)
 constexpr int kKnnMaxNpad = 288;  // resident query tile: n_pad x 128 x 4 B <= 144 KB
@@ -81,7 +82,7 @@ __global__ void knn_pack_kernel(const float *__restrict__ Z, int64_t M, int n, i
 struct BarsK {
     uint64_t qfull;
     uint64_t full[kKS], empty[kKS];
-    uint64_t acc_full[2], acc_empty[2];
+    uint64_t acc_full[kNAcc], acc_empty[kNAcc];
     uint32_t tmem;
 };
 
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(576, 1)
     knn_topk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmR,
                     const float *__restrict__ qn, const float *__restrict__ rn, int64_t Mq,
                     int64_t Mr, int n_pad, int k, int tiles_per_split, float *__restrict__ pd,
-                    int32_t *__restrict__ pi) {
+                    int32_t *__restrict__ pi, int nks, int nk16) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(576, 1)
     unsigned char *Qhi = smem;                        // nslab x 8 KB
     unsigned char *Qlo = smem + nslab * 8192;
     unsigned char *stg = smem + 2 * nslab * 8192;
-    BarsK *bars = reinterpret_cast<BarsK *>(stg + kKS * 16384);
+    BarsK *bars = reinterpret_cast<BarsK *>(stg + nks * 16384);
     auto Rhi = [&](int s) { return stg + s * 16384; };
     auto Rlo = [&](int s) { return stg + s * 16384 + 8192; };
 
@@ -112,17 +113,17 @@ __global__ void __launch_bounds__(576, 1)
     const int64_t t1 = rtiles < t0 + tiles_per_split ? rtiles : t0 + tiles_per_split;
     if (threadIdx.x == 0) {
         mbar_init(&bars->qfull, 1);
-        for (int s = 0; s < kKS; ++s) {
+        for (int s = 0; s < nks; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < kNAcc; ++a) {
             mbar_init(&bars->acc_full[a], 1);
             mbar_init(&bars->acc_empty[a], 512);
         }
         fence_mbar_init();
     }
-    if (warp == 1) tc::tmem_alloc<256>(&bars->tmem);
+    if (warp == 1) tc::tmem_alloc<kNAcc * kRT>(&bars->tmem);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(576, 1)
                     tc::tma_load_2d(Rhi(s), &tmR, c * 32, static_cast<int>(t * kRT), &bars->full[s]);
                     tc::tma_load_2d(Rlo(s), &tmR, c * 32, static_cast<int>(Mr + t * kRT),
                                     &bars->full[s]);
-                    if (++s == kKS) {
+                    if (++s == nks) {
                         s = 0;
                         ph ^= 1u;
                     }
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(576, 1)
                     const uint32_t rh = smem_u32(Rhi(s)), rl = smem_u32(Rlo(s));
 #pragma unroll
                     for (int kk = 0; kk < 2; ++kk) {
+                        if (2 * c + kk >= nk16) break;   // all-zero K16 step of the padding
                         const uint64_t ah = tc::sdesc_sw64(qh + c * 8192 + kk * 32);
                         const uint64_t alo = tc::sdesc_sw64(ql + c * 8192 + kk * 32);
                         const uint64_t bh = tc::sdesc_sw64(rh + kk * 32), blo = tc::sdesc_sw64(rl + kk * 32);
@@ -180,13 +182,13 @@ __global__ void __launch_bounds__(576, 1)
                         tc::mma_bf16(d, alo, bh, idesc, 1u);
                     }
                     tc::mma_commit(&bars->empty[s]);
-                    if (++s == kKS) {
+                    if (++s == nks) {
                         s = 0;
                         ph ^= 1u;
                     }
                 }
                 tc::mma_commit(&bars->acc_full[a]);
-                if (++a == 2) {
+                if (++a == kNAcc) {
                     a = 0;
                     aph ^= 1u;
                 }
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(576, 1)
                           v);
             tc::fence_before_sync();
             tc::mbar_arrive(&bars->acc_empty[a]);   // the accumulator is in registers
-            if (++a == 2) {
+            if (++a == kNAcc) {
                 a = 0;
                 aph ^= 1u;
             }
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(576, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 1) tc::tmem_free<256>(tbase);
+    if (warp == 1) tc::tmem_free<kNAcc * kRT>(tbase);
 }
 
 // thread per query: k-way merge of the sorted per-split lists, ties by smaller index
@@ -365,8 +367,15 @@ bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t ou
            CUDA_SUCCESS;
 }
 
+constexpr size_t kKnnSmemMax = 232448;
+int knn_nks(int n_pad) {   // reference ring stages that fit next to the resident queries
+    const long r = (static_cast<long>(kKnnSmemMax) - 2 * (n_pad / 32) * 8192 -
+                    static_cast<long>(sizeof(BarsK)) - 1024) / 16384;
+    return static_cast<int>(std::max(2L, std::min(static_cast<long>(kKS), r)));
+}
 size_t knn_smem(int n_pad) {
-    return static_cast<size_t>(2 * (n_pad / 32) * 8192) + kKS * 16384 + sizeof(BarsK) + 1024;
+    return static_cast<size_t>(2 * (n_pad / 32) * 8192) + knn_nks(n_pad) * 16384 + sizeof(BarsK) +
+           1024;
 }
 
 }  // namespace
@@ -424,7 +433,7 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
                        const float *Pr, const float *Pq, int32_t *nn_idx, float *nn_dist, void *ws,
                        cudaStream_t stream, LaunchInfo *info) {
     std::call_once(g_knn_attr_once, []() {
-        const int sm = static_cast<int>(knn_smem(kKnnMaxNpad));
+        const int sm = static_cast<int>(kKnnSmemMax);
         g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel<4>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
         if (g_knn_attr_err == cudaSuccess)
@@ -473,13 +482,16 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
     const size_t sm = knn_smem(p.n_pad);
     if (p.k <= 4)
         knn_topk_kernel<4><<<grid, 576, sm, stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad, p.k,
-                                                      p.tiles_per_split, pd, pi);
+                                                      p.tiles_per_split, pd, pi, knn_nks(p.n_pad),
+            static_cast<int>((p.n + 1 + 15) / 16));
     else if (p.k <= 8)
         knn_topk_kernel<8><<<grid, 576, sm, stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad, p.k,
-                                                      p.tiles_per_split, pd, pi);
+                                                      p.tiles_per_split, pd, pi, knn_nks(p.n_pad),
+            static_cast<int>((p.n + 1 + 15) / 16));
     else
         knn_topk_kernel<kKnnMaxK><<<grid, 576, sm, stream>>>(mQ, mR, qn, rn, p.Mq, p.Mr, p.n_pad,
-                                                             p.k, p.tiles_per_split, pd, pi);
+                                                             p.k, p.tiles_per_split, pd, pi, knn_nks(p.n_pad),
+            static_cast<int>((p.n + 1 + 15) / 16));
     // 4. merge the per-split lists
     knn_merge_kernel<<<static_cast<int>((p.Mq + 127) / 128), 128, 0, stream>>>(
         pd, pi, p.Mq, p.k, p.splits, nn_dist, nn_idx);
