@@ -84,6 +84,7 @@ struct BarsK {
     uint64_t full[kKS], empty[kKS];
     uint64_t acc_full[kNAcc], acc_empty[kNAcc];
     uint32_t tmem;
+    float thr[4 * kQ];   // per (column group, query): that group's k-th best distance
 };
 
 // grid (query tiles, splits).  18 warps: w0 TMA producer, w1 MMA issuer (+TMEM
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(576, 1)
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
         }
+        for (int i = 0; i < 4 * kQ; ++i) bars->thr[i] = FLT_MAX;
         for (int a = 0; a < kNAcc; ++a) {
             mbar_init(&bars->acc_full[a], 1);
             mbar_init(&bars->acc_empty[a], 512);
@@ -202,8 +204,10 @@ __global__ void __launch_bounds__(576, 1)
         // loop is one compare into a hit mask: d_S < worst  <=>  D > (||z_q||^2 - worst)/2.
         // The rare insertions run off the mask, outside the streaming loop.
         const int q = warp & 3, grp = (warp - 2) >> 2;
-        const int64_t row = static_cast<int64_t>(qt) * kQ + q * 32 + lane;
+        const int qi = q * 32 + lane;
+        const int64_t row = static_cast<int64_t>(qt) * kQ + qi;
         const float qnorm = row < Mq ? qn[row] : 0.f;
+        volatile float *thr_s = bars->thr;   // read racy on purpose: values only decrease
         float bd[KM];
         int32_t bi[KM];
 #pragma unroll
@@ -229,11 +233,44 @@ __global__ void __launch_bounds__(576, 1)
                 a = 0;
                 aph ^= 1u;
             }
-            const float c = 0.5f * (qnorm - worst);
+            // the first tile fills the empty list branch-free (every entry would be a hit)
+            if (t == t0) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    float cd = fmaf(-2.f, v[e], qnorm);
+                    int32_t ci = static_cast<int32_t>(j0 + e);
+                    if (e >= jvalid) cd = FLT_MAX;
+#pragma unroll
+                    for (int u = 0; u < KM; ++u) {
+                        const bool sw = u < k && cd < bd[u];
+                        const float td = bd[u];
+                        const int32_t ti = bi[u];
+                        bd[u] = sw ? cd : td;
+                        bi[u] = sw ? ci : ti;
+                        cd = sw ? td : cd;
+                        ci = sw ? ti : ci;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < KM; ++u)
+                    if (u == k - 1) worst = bd[u];
+                thr_s[grp * kQ + qi] = worst;
+                continue;
+            }
+            // prune with the best k-th distance of the query's four column groups (a
+            // candidate worse than any group's k-th best cannot be in the top k; <= keeps
+            // exact ties for the index rule of the final merge)
+            float gw = worst;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) gw = fminf(gw, thr_s[g * kQ + qi]);
+            // (a relative margin keeps every candidate whose rounded distance can reach gw;
+            // the exact decision is the insertion's cd < worst)
+            const float c = 0.5f * (qnorm - gw) - 1e-6f * (fabsf(qnorm) + fabsf(gw));
             uint32_t hit = 0;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) hit |= (v[e] > c ? 1u : 0u) << e;
+            for (int e = 0; e < 32; ++e) hit |= (v[e] >= c ? 1u : 0u) << e;
             if (jvalid < 32) hit &= jvalid > 0 ? (0xffffffffu >> (32 - jvalid)) : 0u;
+            const float worst0 = worst;
             while (hit) {   // ascending j: an equal distance keeps the earlier reference
                 const int e = __ffs(hit) - 1;
                 hit &= hit - 1;
@@ -266,13 +303,13 @@ __global__ void __launch_bounds__(576, 1)
                 for (int u = 0; u < KM; ++u)
                     if (u == k - 1) worst = bd[u];
             }
+            if (worst != worst0) thr_s[grp * kQ + qi] = worst;
         }
         // merge the four column groups' lists of each query through shared memory (the
         // reference ring is free: every MMA has completed)
         float *md = reinterpret_cast<float *>(stg);
         int32_t *mi = reinterpret_cast<int32_t *>(stg + 4 * kQ * kKnnMaxK * 4);
         fence_proxy_async_smem();
-        const int qi = q * 32 + lane;
 #pragma unroll
         for (int u = 0; u < KM; ++u) {
             if (u < k) {
