@@ -158,42 +158,41 @@ __global__ void __launch_bounds__(576, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc = tc::idesc_bf16(kQ, kRT);
-            int s = 0, a = 0;
-            uint32_t ph = 0, aph = 0;
-            mbar_wait(&bars->qfull, 0);
+        // the whole warp runs the issue loop (uniform descriptors); one lane issues
+        const uint32_t idesc = tc::idesc_bf16(kQ, kRT);
+        int s = 0, a = 0;
+        uint32_t ph = 0, aph = 0;
+        mbar_wait(&bars->qfull, 0);
+        tc::fence_after_sync();
+        const uint32_t qh = smem_u32(Qhi), ql = smem_u32(Qlo);
+        for (int64_t t = t0; t < t1; ++t) {
+            mbar_wait(&bars->acc_empty[a], aph ^ 1u);
             tc::fence_after_sync();
-            const uint32_t qh = smem_u32(Qhi), ql = smem_u32(Qlo);
-            for (int64_t t = t0; t < t1; ++t) {
-                mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+            const uint32_t d = tbase + static_cast<uint32_t>(a * kRT);
+            for (int c = 0; c < nslab; ++c) {
+                mbar_wait(&bars->full[s], ph);
                 tc::fence_after_sync();
-                const uint32_t d = tbase + static_cast<uint32_t>(a * kRT);
-                for (int c = 0; c < nslab; ++c) {
-                    mbar_wait(&bars->full[s], ph);
-                    tc::fence_after_sync();
-                    const uint32_t rh = smem_u32(Rhi(s)), rl = smem_u32(Rlo(s));
+                const uint32_t rh = smem_u32(Rhi(s)), rl = smem_u32(Rlo(s));
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) {
-                        if (2 * c + kk >= nk16) break;   // all-zero K16 step of the padding
-                        const uint64_t ah = tc::sdesc_sw64(qh + c * 8192 + kk * 32);
-                        const uint64_t alo = tc::sdesc_sw64(ql + c * 8192 + kk * 32);
-                        const uint64_t bh = tc::sdesc_sw64(rh + kk * 32), blo = tc::sdesc_sw64(rl + kk * 32);
-                        tc::mma_bf16(d, ah, bh, idesc, (c | kk) != 0);
-                        tc::mma_bf16(d, ah, blo, idesc, 1u);
-                        tc::mma_bf16(d, alo, bh, idesc, 1u);
-                    }
-                    tc::mma_commit(&bars->empty[s]);
-                    if (++s == nks) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
+                for (int kk = 0; kk < 2; ++kk) {
+                    if (2 * c + kk >= nk16) break;   // all-zero K16 step of the padding
+                    const uint64_t ah = tc::sdesc_sw64(qh + c * 8192 + kk * 32);
+                    const uint64_t alo = tc::sdesc_sw64(ql + c * 8192 + kk * 32);
+                    const uint64_t bh = tc::sdesc_sw64(rh + kk * 32), blo = tc::sdesc_sw64(rl + kk * 32);
+                    tc::mma_bf16_w(d, ah, bh, idesc, (c | kk) != 0);
+                    tc::mma_bf16_w(d, ah, blo, idesc, 1u);
+                    tc::mma_bf16_w(d, alo, bh, idesc, 1u);
                 }
-                tc::mma_commit(&bars->acc_full[a]);
-                if (++a == kNAcc) {
-                    a = 0;
-                    aph ^= 1u;
+                tc::mma_commit_w(&bars->empty[s]);
+                if (++s == nks) {
+                    s = 0;
+                    ph ^= 1u;
                 }
+            }
+            tc::mma_commit_w(&bars->acc_full[a]);
+            if (++a == kNAcc) {
+                a = 0;
+                aph ^= 1u;
             }
         }
         __syncwarp();
