@@ -582,41 +582,39 @@ __global__ void __launch_bounds__(480, 1)
             });
         }
     } else if (warp == 2) {
-        if (lane == 0) {
-            const uint32_t idesc = tc::idesc_bf16(128, b);
-            int s = 0, a = 0;
-            uint32_t ph = 0, aph = 0;
-            for_segments([&](int, int klo, int khi, bool, bool) {
-                mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+        const uint32_t idesc = tc::idesc_bf16(128, b);
+        int s = 0, a = 0;
+        uint32_t ph = 0, aph = 0;
+        for_segments([&](int, int klo, int khi, bool, bool) {
+            mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+            tc::fence_after_sync();
+            const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
+            for (int ks = klo; ks < khi; ++ks) {
+                mbar_wait(&bars->wfull[s], ph);
+                mbar_wait(&bars->cfull[s], ph);
                 tc::fence_after_sync();
-                const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
-                for (int ks = klo; ks < khi; ++ks) {
-                    mbar_wait(&bars->wfull[s], ph);
-                    mbar_wait(&bars->cfull[s], ph);
-                    tc::fence_after_sync();
-                    const uint32_t xh = smem_u32(Xhi(s)), xl = smem_u32(Xlo(s));
-                    const uint32_t wh = smem_u32(Whi(s)), wl = smem_u32(Wlo(s));
+                const uint32_t xh = smem_u32(Xhi(s)), xl = smem_u32(Xlo(s));
+                const uint32_t wh = smem_u32(Whi(s)), wl = smem_u32(Wlo(s));
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) {
-                        const uint64_t ah = tc::sdesc_sw64(xh + kk * 32), alo = tc::sdesc_sw64(xl + kk * 32);
-                        const uint64_t bh = tc::sdesc_sw64(wh + kk * 32), blo = tc::sdesc_sw64(wl + kk * 32);
-                        tc::mma_bf16(d, ah, bh, idesc, (ks != klo || kk != 0) ? 1u : 0u);
-                        tc::mma_bf16(d, ah, blo, idesc, 1u);
-                        tc::mma_bf16(d, alo, bh, idesc, 1u);
-                    }
-                    tc::mma_commit(&bars->cempty[s]);
-                    if (++s == kStages1) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
+                for (int kk = 0; kk < 2; ++kk) {
+                    const uint64_t ah = tc::sdesc_sw64(xh + kk * 32), alo = tc::sdesc_sw64(xl + kk * 32);
+                    const uint64_t bh = tc::sdesc_sw64(wh + kk * 32), blo = tc::sdesc_sw64(wl + kk * 32);
+                    tc::mma_bf16_w(d, ah, bh, idesc, (ks != klo || kk != 0) ? 1u : 0u);
+                    tc::mma_bf16_w(d, ah, blo, idesc, 1u);
+                    tc::mma_bf16_w(d, alo, bh, idesc, 1u);
                 }
-                tc::mma_commit(&bars->acc_full[a]);
-                if (++a == 2) {
-                    a = 0;
-                    aph ^= 1u;
+                tc::mma_commit_w(&bars->cempty[s]);
+                if (++s == kStages1) {
+                    s = 0;
+                    ph ^= 1u;
                 }
-            });
-        }
+            }
+            tc::mma_commit_w(&bars->acc_full[a]);
+            if (++a == 2) {
+                a = 0;
+                aph ^= 1u;
+            }
+        });
         __syncwarp();
     } else if (warp < 11) {
         // converters: 256 threads, 4 float4 each per k-step
@@ -872,53 +870,51 @@ __global__ void __launch_bounds__(640, 1)
             });
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc = tc::idesc_bf16(kRowChunk, kTileCols);
-            int s = 0, a = 0;
-            uint32_t ph = 0, aph = 0, gph = 0;
-            const uint32_t gh0 = smem_u32(Ghi), gl0 = smem_u32(Glo);
-            for_segments([&](int tile, int rlo, int rhi) {
-                const int mlo = rlo > rc0 ? rlo : rc0;
-                if (mlo >= rhi) return;
-                mbar_wait(&bars->gfull, gph);
-                gph ^= 1u;
+        const uint32_t idesc = tc::idesc_bf16(kRowChunk, kTileCols);
+        int s = 0, a = 0;
+        uint32_t ph = 0, aph = 0, gph = 0;
+        const uint32_t gh0 = smem_u32(Ghi), gl0 = smem_u32(Glo);
+        for_segments([&](int tile, int rlo, int rhi) {
+            const int mlo = rlo > rc0 ? rlo : rc0;
+            if (mlo >= rhi) return;
+            mbar_wait(&bars->gfull, gph);
+            gph ^= 1u;
+            tc::fence_after_sync();
+            for (int rc = mlo; rc < rhi; ++rc) {
+                const unsigned long long t1 = clock64();
+                mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+                w_b += clock64() - t1;
                 tc::fence_after_sync();
-                for (int rc = mlo; rc < rhi; ++rc) {
-                    const unsigned long long t1 = clock64();
-                    mbar_wait(&bars->acc_empty[a], aph ^ 1u);
-                    w_b += clock64() - t1;
+                const uint32_t d = tbase + static_cast<uint32_t>(a * kTileCols);
+                for (int c = 0; c < nslab; ++c) {
+                    const unsigned long long t0 = clock64();
+                    mbar_wait(&bars->full[s], ph);
+                    w_a += clock64() - t0;
                     tc::fence_after_sync();
-                    const uint32_t d = tbase + static_cast<uint32_t>(a * kTileCols);
-                    for (int c = 0; c < nslab; ++c) {
-                        const unsigned long long t0 = clock64();
-                        mbar_wait(&bars->full[s], ph);
-                        w_a += clock64() - t0;
-                        tc::fence_after_sync();
-                        const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
+                    const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
 #pragma unroll
-                        for (int kk = 0; kk < 2; ++kk) {
-                            const uint64_t ah = tc::sdesc_sw64(vh + kk * 32), alo = tc::sdesc_sw64(vl + kk * 32);
-                            const uint64_t bh = tc::sdesc_sw64(gh0 + c * 8192 + kk * 32);
-                            const uint64_t blo = tc::sdesc_sw64(gl0 + c * 8192 + kk * 32);
-                            tc::mma_bf16(d, ah, bh, idesc, (c | kk) != 0);
-                            tc::mma_bf16(d, ah, blo, idesc, 1u);
-                            tc::mma_bf16(d, alo, bh, idesc, 1u);
-                        }
-                        tc::mma_commit(&bars->empty[s]);
-                        if (++s == kStages3) {
-                            s = 0;
-                            ph ^= 1u;
-                        }
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const uint64_t ah = tc::sdesc_sw64(vh + kk * 32), alo = tc::sdesc_sw64(vl + kk * 32);
+                        const uint64_t bh = tc::sdesc_sw64(gh0 + c * 8192 + kk * 32);
+                        const uint64_t blo = tc::sdesc_sw64(gl0 + c * 8192 + kk * 32);
+                        tc::mma_bf16_w(d, ah, bh, idesc, (c | kk) != 0);
+                        tc::mma_bf16_w(d, ah, blo, idesc, 1u);
+                        tc::mma_bf16_w(d, alo, bh, idesc, 1u);
                     }
-                    tc::mma_commit(&bars->acc_full[a]);
-                    if (++a == 2) {
-                        a = 0;
-                        aph ^= 1u;
+                    tc::mma_commit_w(&bars->empty[s]);
+                    if (++s == kStages3) {
+                        s = 0;
+                        ph ^= 1u;
                     }
                 }
-                tc::mma_commit(&bars->gempty);
-            });
-        }
+                tc::mma_commit_w(&bars->acc_full[a]);
+                if (++a == 2) {
+                    a = 0;
+                    aph ^= 1u;
+                }
+            }
+            tc::mma_commit_w(&bars->gempty);
+        });
         __syncwarp();
     } else if (warp == 2) {
         if (lane == 0) {
