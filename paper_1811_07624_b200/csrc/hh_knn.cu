@@ -33,9 +33,10 @@ namespace hh {
 namespace {
 
 constexpr int kQ = 128;           // queries per CTA (MMA M)
-constexpr int kRT = 128;          // references per tile (MMA N)
+constexpr int kRT = 256;          // references per tile (MMA N)
+constexpr int kRStage = kRT * 64 * 2;   // one K slab of a tile, hi + lo (32 KB)
 constexpr int kKS = 12;           // reference slab ring depth: maximum (runtime nks)
-constexpr int kNAcc = 4;          // TMEM accumulators (4 x 128 columns)
+constexpr int kNAcc = 2;          // TMEM accumulators (2 x 256 columns)
 constexpr int kKnnMaxK = 16;      // largest k
 constexpr int kKnnMaxN = 256;     // largest n (K = n + 1 augmented, padded to 32)
 constexpr int kKnnMaxNpad = 288;  // resident query tile: n_pad x 128 x 4 B <= 144 KB
@@ -103,9 +104,9 @@ __global__ void __launch_bounds__(576, 1)
     unsigned char *Qhi = smem;                        // nslab x 8 KB
     unsigned char *Qlo = smem + nslab * 8192;
     unsigned char *stg = smem + 2 * nslab * 8192;
-    BarsK *bars = reinterpret_cast<BarsK *>(stg + nks * 16384);
-    auto Rhi = [&](int s) { return stg + s * 16384; };
-    auto Rlo = [&](int s) { return stg + s * 16384 + 8192; };
+    BarsK *bars = reinterpret_cast<BarsK *>(stg + nks * kRStage);
+    auto Rhi = [&](int s) { return stg + s * kRStage; };
+    auto Rlo = [&](int s) { return stg + s * kRStage + kRStage / 2; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qt = blockIdx.x, split = blockIdx.y;
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(576, 1)
             for (int64_t t = t0; t < t1; ++t) {
                 for (int c = 0; c < nslab; ++c) {
                     mbar_wait(&bars->empty[s], ph ^ 1u);
-                    mbar_arrive_expect_tx(&bars->full[s], 16384u);
+                    mbar_arrive_expect_tx(&bars->full[s], static_cast<uint32_t>(kRStage));
                     tc::tma_load_2d(Rhi(s), &tmR, c * 32, static_cast<int>(t * kRT), &bars->full[s]);
                     tc::tma_load_2d(Rlo(s), &tmR, c * 32, static_cast<int>(Mr + t * kRT),
                                     &bars->full[s]);
@@ -217,23 +218,11 @@ __global__ void __launch_bounds__(576, 1)
         float worst = FLT_MAX;   // bd[k-1], kept in a register (no dynamic indexing)
         int a = 0;
         uint32_t aph = 0;
-        for (int64_t t = t0; t < t1; ++t) {
-            const int64_t j0 = t * kRT + grp * 32;
+        // one 32-reference chunk of this group's columns (ascending j)
+        auto chunk = [&](float (&v)[32], int64_t j0, bool first) {
             const int jvalid = Mr - j0 >= 32 ? 32 : static_cast<int>(Mr - j0);   // may be <= 0
-            mbar_wait(&bars->acc_full[a], aph);
-            tc::fence_after_sync();
-            float v[32];
-            tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                              static_cast<uint32_t>(a * kRT + grp * 32),
-                          v);
-            tc::fence_before_sync();
-            tc::mbar_arrive(&bars->acc_empty[a]);   // the accumulator is in registers
-            if (++a == kNAcc) {
-                a = 0;
-                aph ^= 1u;
-            }
             // the first tile fills the empty list branch-free (every entry would be a hit)
-            if (t == t0) {
+            if (first) {
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
                     float cd = fmaf(-2.f, v[e], qnorm);
@@ -254,7 +243,7 @@ __global__ void __launch_bounds__(576, 1)
                 for (int u = 0; u < KM; ++u)
                     if (u == k - 1) worst = bd[u];
                 thr_s[grp * kQ + qi] = worst;
-                continue;
+                return;
             }
             // prune with the best k-th distance of the query's four column groups (a
             // candidate worse than any group's k-th best cannot be in the top k; <= keeps
@@ -303,6 +292,25 @@ __global__ void __launch_bounds__(576, 1)
                     if (u == k - 1) worst = bd[u];
             }
             if (worst != worst0) thr_s[grp * kQ + qi] = worst;
+        };
+        for (int64_t t = t0; t < t1; ++t) {
+            // group grp owns columns [64 grp, 64 grp + 64) of the 256-reference tile
+            const int64_t jg = t * kRT + grp * 64;
+            mbar_wait(&bars->acc_full[a], aph);
+            tc::fence_after_sync();
+            const uint32_t tcol = tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                  static_cast<uint32_t>(a * kRT + grp * 64);
+            float v[32];
+            tc::tmem_ld32(tcol, v);
+            chunk(v, jg, t == t0);
+            tc::tmem_ld32(tcol + 32, v);
+            tc::fence_before_sync();
+            tc::mbar_arrive(&bars->acc_empty[a]);   // both chunks are in registers / done
+            if (++a == kNAcc) {
+                a = 0;
+                aph ^= 1u;
+            }
+            chunk(v, jg + 32, false);
         }
         // merge the four column groups' lists of each query through shared memory (the
         // reference ring is free: every MMA has completed)
@@ -383,7 +391,7 @@ PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
 std::once_flag g_enc_once, g_knn_attr_once;
 cudaError_t g_knn_attr_err = cudaSuccess;
 
-bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer) {
+bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer, uint32_t rows) {
     std::call_once(g_enc_once, []() {
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -395,7 +403,7 @@ bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t ou
     if (!g_enc) return false;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {inner * 2};
-    cuuint32_t box[2] = {32, 128};
+    cuuint32_t box[2] = {32, rows};
     cuuint32_t es[2] = {1, 1};
     return g_enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -406,11 +414,11 @@ bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t ou
 constexpr size_t kKnnSmemMax = 232448;
 int knn_nks(int n_pad) {   // reference ring stages that fit next to the resident queries
     const long r = (static_cast<long>(kKnnSmemMax) - 2 * (n_pad / 32) * 8192 -
-                    static_cast<long>(sizeof(BarsK)) - 1024) / 16384;
+                    static_cast<long>(sizeof(BarsK)) - 1024) / kRStage;
     return static_cast<int>(std::max(2L, std::min(static_cast<long>(kKS), r)));
 }
 size_t knn_smem(int n_pad) {
-    return static_cast<size_t>(2 * (n_pad / 32) * 8192) + knn_nks(n_pad) * 16384 + sizeof(BarsK) +
+    return static_cast<size_t>(2 * (n_pad / 32) * 8192) + knn_nks(n_pad) * kRStage + sizeof(BarsK) +
            1024;
 }
 
@@ -512,7 +520,8 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
     if (e != cudaSuccess) return e;
     // 3. distances on the tensor cores + per-query top-k
     CUtensorMap mQ, mR;
-    if (!make_map_bf16(&mQ, Zqb, p.n_pad, 2 * p.Mq) || !make_map_bf16(&mR, Zrb, p.n_pad, 2 * p.Mr))
+    if (!make_map_bf16(&mQ, Zqb, p.n_pad, 2 * p.Mq, kQ) ||
+        !make_map_bf16(&mR, Zrb, p.n_pad, 2 * p.Mr, kRT))
         return cudaErrorNotSupported;
     const dim3 grid(static_cast<unsigned>((p.Mq + kQ - 1) / kQ), static_cast<unsigned>(p.splits));
     const size_t sm = knn_smem(p.n_pad);
