@@ -485,6 +485,14 @@ def run_hh(args):
                 kw = [b] * npass
             exe = sum(3 * 2 * 2 * k_ * c.n * c.N for k_ in kw)
             exe_bytes = sum(3 * c.N * c.n * s_ + 2 * c.N * k_ * 4 for k_ in kw)
+            if c.call == "apply_qr":
+                # NEXT-f2: block k's project starts at K row (k b) rounded down to 32 and its
+                # update at row chunk (k b) rounded down to 128 (op N); rows above are skipped
+                exe, exe_bytes = 0, 0
+                for kb in range(npass):
+                    p0, u0 = (kb * b // 32) * 32, (kb * b // 128) * 128
+                    exe += 3 * 2 * b * ((c.n - p0) + (c.n - u0)) * c.N
+                    exe_bytes += ((c.n - p0) + 2 * (c.n - u0)) * c.N * s_ + 2 * c.N * b * 4
             t_s = ms_step * 1e-3
             ef_t, ef_h = exe / t_s / 1e12 / tpeak, exe_bytes / t_s / 1e9 / hbm
             # the binding floor of the METHOD on this hardware: its HBM bytes at the copy
