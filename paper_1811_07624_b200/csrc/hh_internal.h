@@ -69,7 +69,7 @@ enum WyKind : int { WY_APPLY_N = 0, WY_APPLY_T = 1, WY_SYM = 2 };
 struct WyPlan {
     int kind = 0;
     int64_t n = 0, h = 0, N = 0;
-    int b = 0, nblk = 0, h_pad = 0, extra = 0, nsplit = 0;
+    int b = 0, nblk = 0, h_pad = 0, extra = 0, nsplit = 0, gram_rows = 0;
     int qr = 0;   // NEXT-f2: block k's W rows (and V rows) are zero above row k*b
     int64_t n_pad = 0;
     size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_v = 0, off_v2 = 0,

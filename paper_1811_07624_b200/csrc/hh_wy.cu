@@ -117,7 +117,7 @@ __global__ void wy_vmul_kernel(const float *__restrict__ a, const float *__restr
 // (the reduction over splits is done in fixed order by wy_gram_reduce_kernel:
 // deterministic).
 __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ Wf, int64_t n_pad,
-                                                      int b, int nsplit, int blk0,
+                                                      int b, int nsplit, int rows, int blk0,
                                                       const float *__restrict__ wt, int full,
                                                       float *__restrict__ Sp) {
     const int ti = blockIdx.x, tj = blockIdx.y;
@@ -126,11 +126,11 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
     __shared__ float Ls[32][65], Ms[32][65];
     const int t = threadIdx.x, tx = t % 16, ty = t / 16;
     float acc[4][4] = {};
-    const int64_t r0 = static_cast<int64_t>(sp) * kGramRows;
+    const int64_t r0 = static_cast<int64_t>(sp) * rows;
     const float *Wl = Wf + (static_cast<int64_t>(blk0 + blk) * b + ti * 64) * n_pad;
     const float *Wm = Wf + (static_cast<int64_t>(blk0 + blk) * b + tj * 64) * n_pad;
     const int rows_l = min(64, b - ti * 64), rows_m = min(64, b - tj * 64);
-    for (int64_t rc = r0; rc < r0 + kGramRows; rc += 32) {
+    for (int64_t rc = r0; rc < r0 + rows; rc += 32) {
         for (int e = t; e < 32 * 64; e += 256) {
             const int c = e / 32, k = e % 32;
             const float w = wt ? wt[rc + k] : 1.f;
@@ -188,7 +188,7 @@ __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int n
 //   T[l][i] = -2 sum_{m=l}^{i-1} T[l][m] S[m][i],  T[i][i] = 2,
 // then 32 columns at a time (block form of the same product, H-blocks 1 = [0,c),
 // 2 = [c,c+32)):  T[0:c, c:c+32] = -T[0:c,0:c] * (S[0:c, c:c+32] * T[c:c+32, c:c+32]).
-__global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict__ Sg, int b,
+__global__ void __launch_bounds__(256) wy_tbuild_kernel(const float *__restrict__ Sg, int b,
                                                           float *__restrict__ Tg, int diag_only) {
     extern __shared__ float tsm[];
     const int blk = blockIdx.x;
@@ -201,42 +201,43 @@ __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict
     float *Pm = Sb + 8 * 32 * 33;                      // c x 32
     auto tp = [&](int l, int m) -> float & { return Tp[l * b - (l * (l - 1)) / 2 + (m - l)]; };
     const int nb = b / 32;
-    // level 0: warp w builds diagonal block w
+    // level 0: warp w builds diagonal block w; lane l keeps row l of T_ww in registers
+    // (the recurrence fully unrolled: static register indices, S column i broadcast from
+    // shared memory, four accumulators per dot)
     if (warp < nb) {
         const int o = warp * 32;
         float(*sb)[33] = reinterpret_cast<float(*)[33]>(Sb + warp * 32 * 33);
         for (int r = 0; r < 32; ++r) sb[r][lane] = S[(o + r) * b + o + lane];
         __syncwarp();
+        float tr[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) tr[m] = 0.f;
+#pragma unroll
         for (int i = 0; i < 32; ++i) {
-            if (lane < i) {
-                float s0 = 0.f, s1 = 0.f;
-                int m = lane;
-                for (; m + 1 < i; m += 2) {
-                    s0 = fmaf(tp(o + lane, o + m), sb[m][i], s0);
-                    s1 = fmaf(tp(o + lane, o + m + 1), sb[m + 1][i], s1);
-                }
-                if (m < i) s0 = fmaf(tp(o + lane, o + m), sb[m][i], s0);
-                tp(o + lane, o + i) = -2.f * (s0 + s1);
-            } else if (lane == i) {
-                tp(o + i, o + i) = 2.f;
-            }
-            __syncwarp();
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int m = 0; m < i; ++m) a[m & 3] = fmaf(tr[m], sb[m][i], a[m & 3]);
+            const float v = -2.f * ((a[0] + a[1]) + (a[2] + a[3]));
+            tr[i] = lane < i ? v : (lane == i ? 2.f : 0.f);
         }
+#pragma unroll
+        for (int m = 0; m < 32; ++m)
+            if (m >= lane) tp(o + lane, o + m) = tr[m];
     }
     __syncthreads();
-    // extension steps; each thread owns (row l, 4 consecutive columns): 2 shared loads
+    // extension steps (256 threads); each thread owns (row l, 4 consecutive columns): 2 shared loads
     // (one broadcast, one 16-B) per 4 FMAs.  diag_only: only the 32 x 32 diagonal blocks
     // are wanted (wy_vrec_kernel builds V = W T from them without the rest of T)
     float *T22 = Pm + 224 * 32;                        // 32 x 32 dense diagonal block
     for (int c = 32; c < (diag_only ? 0 : b); c += 32) {
         // S panel S[0:c, c:c+32] -> Sb (c x 32); T22 = T[c:c+32, c:c+32] (dense)
-        for (int e = t; e < c * 32; e += 1024) Sb[e] = S[(e / 32) * b + c + (e % 32)];
-        {
-            const int mm = t / 32, jj = t % 32;
-            T22[t] = jj >= mm ? tp(c + mm, c + jj) : 0.f;
+        for (int e = t; e < c * 32; e += 256) Sb[e] = S[(e / 32) * b + c + (e % 32)];
+        for (int e = t; e < 1024; e += 256) {
+            const int mm = e / 32, jj = e % 32;
+            T22[e] = jj >= mm ? tp(c + mm, c + jj) : 0.f;
         }
         __syncthreads();
-        for (int e = t; e < c * 8; e += 1024) {
+        for (int e = t; e < c * 8; e += 256) {
             const int l = e / 8, j0 = (e % 8) * 4;
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int m = 0; m < j0 + 4; ++m) {
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict
             *reinterpret_cast<float4 *>(Pm + l * 32 + j0) = acc;
         }
         __syncthreads();
-        for (int e = t; e < c * 8; e += 1024) {
+        for (int e = t; e < c * 8; e += 256) {
             const int l = e / 8, j0 = (e % 8) * 4;
             float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
             const float *trow = &tp(l, l);
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(1024) wy_tbuild_kernel(const float *__restrict
         }
         __syncthreads();
     }
-    for (int64_t e = t; e < bb; e += 1024) {
+    for (int64_t e = t; e < bb; e += 256) {
         const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
         Tout[e] = (m >= l && (!diag_only || l / 32 == m / 32)) ? tp(l, m) : 0.f;
     }
@@ -1102,7 +1103,9 @@ WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     p.h_pad = p.b * p.nblk;
     p.extra = kind == WY_SYM ? p.b : 0;
     p.n_pad = (n + kRowChunk - 1) / kRowChunk * kRowChunk;
-    p.nsplit = static_cast<int>(p.n_pad / kGramRows);
+    // Gram split-K slices: 32 rows for small blocks (enough CTAs to fill the GPU), else 128
+    p.gram_rows = p.b <= 64 ? 32 : kGramRows;
+    p.nsplit = static_cast<int>(p.n_pad / p.gram_rows);
     const size_t bb = static_cast<size_t>(p.b) * p.b * 4;
     const size_t vblk = static_cast<size_t>(p.n_pad) * p.b * 2 * 2;   // bf16 hi/lo per block
     size_t off = 0;
@@ -1202,18 +1205,18 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         ++nlaunch, wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b,
                                                          p.extra, rev, Wf, Wb);
         const int tb = (b + 63) / 64;
-        ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, 0,
+        ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, p.gram_rows, 0,
                                                                        nullptr, 0, Sp);
         const int64_t ns = static_cast<int64_t>(m) * b * b;
         ++nlaunch, wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, sms * 8)),
                                 256, 0, stream>>>(Sp, b, m, p.nsplit, 0, S);
         if (sym) {   // P = W^T Lambda W of the last block (full)
-            ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit,
+            ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, p.gram_rows,
                                                                        m - 1, lam, 1, F(p.off_pp));
             ++nlaunch, wy_gram_reduce_kernel<<<std::max(1, (b * b + 255) / 256), 256, 0, stream>>>(
                 F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p));
         }
-        ++nlaunch, wy_tbuild_kernel<<<m, 1024, tbuild_smem(b), stream>>>(S, b, T, sym ? 0 : 1);
+        ++nlaunch, wy_tbuild_kernel<<<m, 256, tbuild_smem(b), stream>>>(S, b, T, sym ? 0 : 1);
         if (!sym) {
             // V = W T per block, row-parallel from the diagonal T blocks (wy_vrec_kernel)
             ++nlaunch, wy_vrec_kernel<<<dim3(static_cast<unsigned>(n_pad / 64), m), 256,
