@@ -924,6 +924,14 @@ __global__ void __launch_bounds__(640, 1)
             uint32_t ph = 0;
             for_segments([&](int tile, int rlo, int rhi) {
                 for (int rc = rlo; rc < rhi; ++rc) {
+                    // when the ring holds only one box per epilogue group (b = 256), pull the
+                    // next row chunk's boxes into L2 a chunk ahead, so a freed stage is refilled
+                    // at L2 rather than HBM latency (deeper rings do not need it: measured)
+                    if (nxs <= 4 && rc + 1 < nrc) {
+                        for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb)
+                            tc::tma_prefetch_2d(&tmXb, (rc + 1) * kRowChunk,
+                                                tile * kTileCols + cb * kXBoxCols);
+                    }
                     for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb) {
                         const unsigned long long t0 = clock64();
                         mbar_wait(&bars->xempty[s], ph ^ 1u);
