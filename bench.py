@@ -89,6 +89,38 @@ def alg_cost(c, op_count=1):
     return byts, flops, units
 
 
+def input_digest(c) -> str:
+    """SHA-256 of the exact input bytes (U, X, lambda, d, ia, ib as present): the oracle and
+    the GPU path provably saw the same inputs."""
+    import hashlib
+    hsh = hashlib.sha256()
+    for nm in ("U", "X", "lam", "d", "ia", "ib"):
+        a = getattr(c, nm, None)
+        if a is not None:
+            hsh.update(nm.encode())
+            hsh.update(np.ascontiguousarray(a).tobytes())
+    return hsh.hexdigest()
+
+
+def same_run_copy_gbs(dev) -> float:
+    """A 1 GiB device-to-device copy timed in this run (context for the roofline peak, which
+    stays the driver-measured MEASURED_PEAKS.json figure)."""
+    import torch
+    a = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+    b = torch.empty_like(a)
+    b.copy_(a)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    gbs = 2 * a.numel() * 4 * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del a, b
+    return gbs
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -378,19 +410,21 @@ def run_hh(args):
 
     sampler = ClockSampler(dev.index if dev.index is not None else 0).start()
     time.sleep(0.3)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    # one event between consecutive steps (recording costs nothing measurable): the total
+    # is first -> last, the per-step split gives the median and the minimum
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t_wall0 = time.time()
-    ev0.record(stream)
-    for _ in range(args.steps):
+    evs[0].record(stream)
+    for i in range(args.steps):
         step()
-    ev1.record(stream)
+        evs[i + 1].record(stream)
     torch.cuda.synchronize(dev)
     t_wall1 = time.time()
-    ms = ev0.elapsed_time(ev1)
+    ms = evs[0].elapsed_time(evs[-1])
+    per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
     if ws > 1:
         dist.barrier()
     # keep the GPU busy for >= 1 s of clock samples if the timed region was short
@@ -518,6 +552,8 @@ def run_hh(args):
             v, ups, secs, sample, thr = time_oracle(c, op, target_s=args.cpu_seconds)
             cpu = {"value": v, "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": sample,
                    "seconds": secs, "vectors_per_s": ups, "cpu": cpu_model()}
+        if not args.ncu and roof is not None:
+            roof["same_run_copy_gbs"] = same_run_copy_gbs(dev)
         out = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -526,10 +562,12 @@ def run_hh(args):
             "config": config_of(c, args),
             "vectors_per_s": ws * units / (ms_step * 1e-3),
             "gflops": ws * flops / (ms_step * 1e-3) / 1e9,
+            "ms_per_step_median": per_step[len(per_step) // 2], "ms_per_step_min": per_step[0],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "clocks": clocks, "parity": parity, **extra,
             "gpu": torch.cuda.get_device_name(dev),
+            "inputs_sha256": input_digest(c),
         }
         print(json.dumps(out), flush=True)
     if ws > 1:

@@ -39,6 +39,8 @@ def test_bench_line_contract():
     assert d["gpu_launches"] >= d["steps"]
     assert d["clocks"]["sm_max_mhz"] > 0
     assert d["parity"]["pass"]
+    assert d["ms_per_step_min"] <= d["ms_per_step_median"] and len(d["inputs_sha256"]) == 64
+    assert d["roofline"]["same_run_copy_gbs"] > 0
 
 
 def test_bench_reference_arm():
