@@ -47,6 +47,13 @@
  *   - Asynchronous device faults surface at the caller's next synchronising call
  *     (as in cuBLAS); HH_ERR_CUDA reports launch-time errors.
  *   - No C++ exception crosses this boundary.  All functions are thread-safe.
+ *   - A workspace belongs to one call at a time: calls that may run concurrently
+ *     (different streams) need distinct workspaces (as with cuBLAS workspaces).
+ *   - Every call enqueues only stream-ordered work (kernels, cudaMemsetAsync): it
+ *     can be captured into a CUDA graph and replayed (tests/test_graph_gpu.py).
+ *   - The compact-WY projection (large h) splits a few column tiles between two
+ *     co-resident CTAs of one launch (grid <= SM count); a hand-off that never
+ *     arrives traps instead of hanging (a bug, not a recoverable error).
  *
  * Preconditions NOT validated (documented): ||u_i|| = 1 or u_i = 0 for an
  * orthonormal Q; d_r >= 0; 0 <= ia[j], ib[j] < M; finite inputs.
