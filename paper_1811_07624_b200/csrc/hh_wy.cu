@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "hh_internal.h"
@@ -1035,6 +1036,294 @@ __global__ void __launch_bounds__(640, 1)
     if (warp == 1) tc::tmem_free<256>(tbase);
 }
 
+// ------------------------------------------------------------------ K5b-TS: X <- X - V G
+// The update with G as the TMEM-resident A operand (tcgen05.mma A from TMEM, B = V tiles
+// from shared memory): D'[j][r] = sum_i G[j][i] V[r][i], TMEM lane = column j, TMEM column
+// = row r of the current 128-row chunk.  Moving G (128 KB at b = 256) out of shared memory
+// leaves room for a 4-deep V ring and an 8-deep ring of X boxes (32 rows x 128 columns,
+// SWIZZLE_128B), which the b = 256 update needs (one box per group had exposed every X
+// load latency).  Shared-memory traffic per SM is still the bound at b = 256 (V operand
+// reads and TMA writes, X box write/read/write/store-read); reading X straight from global
+// memory instead was measured 30 % slower (uncoalesced per-column accesses).  TMEM: G hi at columns [0, 128), G lo at [128, 256), two accumulators of
+// 128 columns at 256 and 384.  20 warps: w0 V producer, w1 MMA (warp-wide issue), w2 X-box
+// producer, w4-19 epilogue = 4 lane quarters (32 columns) x 4 row groups (32 rows of the
+// chunk); the epilogue warps also stage each tile's G (global -> registers -> tcgen05.st).
+constexpr int kVS2 = 6;              // K5b-TS V ring depth (V arrives from L2; the TS timeline
+                                     // showed the MMA waiting 43 % on a 4-deep ring)
+constexpr int kXS2 = 8;              // K5b-TS X box ring depth (2 per row group)
+constexpr int kXB2Bytes = 16384;     // X box: 32 rows x 128 columns fp32 (rows of 128 B)
+
+struct Bars4 {
+    uint64_t gfull, gempty;
+    uint64_t full[kVS2], empty[kVS2];
+    uint64_t xfull[kXS2], xempty[kXS2];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem;
+};
+
+size_t smem4() { return 1024 + static_cast<size_t>(kVS2) * kStage3Bytes + kXS2 * kXB2Bytes + sizeof(Bars4); }
+
+__global__ void __launch_bounds__(640, 1)
+    wy_update_ts_kernel(const uint16_t *__restrict__ Gt, const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ CUtensorMap tmXb,
+                        const __grid_constant__ CUtensorMap tmYs, const float *__restrict__ lam,
+                        const float *__restrict__ post, int n, int n_pad, int64_t N, int b,
+                        int vrow_hi, int vrow_lo, int ntiles, int rc0, int copy_below,
+                        unsigned long long *tl) {
+    const bool dbg = tl != nullptr && blockIdx.x == 0;
+    unsigned long long t_k0 = clock64(), w_a = 0, w_b = 0, w_c = 0;
+    auto tw = [&](uint64_t *bar, uint32_t ph, unsigned long long &acc) {
+        const unsigned long long t0 = clock64();
+        mbar_wait(bar, ph);
+        acc += clock64() - t0;
+    };
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int nslab = b / 32;
+    unsigned char *stg = smem;
+    unsigned char *xst = stg + kVS2 * kStage3Bytes;
+    Bars4 *bars = reinterpret_cast<Bars4 *>(xst + kXS2 * kXB2Bytes);
+    auto Vhi = [&](int s) { return stg + s * kStage3Bytes; };
+    auto Vlo = [&](int s) { return stg + s * kStage3Bytes + 8192; };
+    auto Xs = [&](int s) { return xst + s * kXB2Bytes; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nrc = n_pad / kRowChunk;
+    const int xrc0 = copy_below ? 0 : rc0;
+    const int64_t per = nrc - xrc0;
+    const int64_t utot = static_cast<int64_t>(ntiles) * per;
+    const int64_t ubeg = utot * blockIdx.x / gridDim.x, uend = utot * (blockIdx.x + 1) / gridDim.x;
+    auto for_segments = [&](auto &&fn) {
+        for (int64_t u = ubeg; u < uend;) {
+            const int tile = static_cast<int>(u / per);
+            const int64_t t0 = static_cast<int64_t>(tile) * per;
+            const int rlo = xrc0 + static_cast<int>(u - t0);
+            const int rhi = xrc0 + static_cast<int>(uend - t0 < per ? uend - t0 : per);
+            fn(tile, rlo, rhi);
+            u = t0 + per;
+        }
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->gfull, 512);
+        mbar_init(&bars->gempty, 1);
+        for (int s = 0; s < kVS2; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int s = 0; s < kXS2; ++s) {
+            mbar_init(&bars->xfull[s], 1);
+            mbar_init(&bars->xempty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->acc_full[a], 1);
+            mbar_init(&bars->acc_empty[a], 512);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc<512>(&bars->tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tbase = bars->tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tc::prefetch_tmap(&tmV);
+            int s = 0;
+            uint32_t ph = 0;
+            for_segments([&](int, int rlo, int rhi) {
+                const int mlo = rlo > rc0 ? rlo : rc0;
+                for (int rc = mlo; rc < rhi; ++rc) {
+                    for (int c = 0; c < nslab; ++c) {
+                        tw(&bars->empty[s], ph ^ 1u, w_a);
+                        mbar_arrive_expect_tx(&bars->full[s], static_cast<uint32_t>(kStage3Bytes));
+                        tc::tma_load_2d(Vhi(s), &tmV, c * 32, vrow_hi + rc * kRowChunk, &bars->full[s]);
+                        tc::tma_load_2d(Vlo(s), &tmV, c * 32, vrow_lo + rc * kRowChunk, &bars->full[s]);
+                        if (++s == kVS2) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+            });
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc = tc::idesc_bf16(kTileCols, kRowChunk);
+        int s = 0, a = 0;
+        uint32_t ph = 0, aph = 0, gph = 0;
+        for_segments([&](int, int rlo, int rhi) {
+            const int mlo = rlo > rc0 ? rlo : rc0;
+            if (mlo >= rhi) return;
+            tw(&bars->gfull, gph, w_c);   // this tile's G is in TMEM
+            gph ^= 1u;
+            tc::fence_after_sync();
+            for (int rc = mlo; rc < rhi; ++rc) {
+                tw(&bars->acc_empty[a], aph ^ 1u, w_b);
+                tc::fence_after_sync();
+                const uint32_t d = tbase + 256u + static_cast<uint32_t>(a * kRowChunk);
+                for (int c = 0; c < nslab; ++c) {
+                    tw(&bars->full[s], ph, w_a);
+                    tc::fence_after_sync();
+                    const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const uint64_t bh = tc::sdesc_sw64(vh + kk * 32), bl = tc::sdesc_sw64(vl + kk * 32);
+                        const uint32_t ah = tbase + static_cast<uint32_t>(c * 16 + kk * 8);
+                        const uint32_t alo = ah + 128u;
+                        tc::mma_bf16_ts_w(d, ah, bh, idesc, (c | kk) != 0);
+                        tc::mma_bf16_ts_w(d, ah, bl, idesc, 1u);
+                        tc::mma_bf16_ts_w(d, alo, bh, idesc, 1u);
+                    }
+                    tc::mma_commit_w(&bars->empty[s]);
+                    if (++s == kVS2) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                tc::mma_commit_w(&bars->acc_full[a]);
+                if (++a == 2) {
+                    a = 0;
+                    aph ^= 1u;
+                }
+            }
+            tc::mma_commit_w(&bars->gempty);   // G may be replaced once these MMAs finish
+        });
+        __syncwarp();
+    } else if (warp == 2) {
+        if (lane == 0) {
+            tc::prefetch_tmap(&tmXb);
+            int s = 0;
+            uint32_t ph = 0;
+            for_segments([&](int tile, int rlo, int rhi) {
+                for (int rc = rlo; rc < rhi; ++rc) {
+                    for (int g = 0; g < 4; ++g) {
+                        tw(&bars->xempty[s], ph ^ 1u, w_a);
+                        mbar_arrive_expect_tx(&bars->xfull[s], static_cast<uint32_t>(kXB2Bytes));
+                        tc::tma_load_2d(Xs(s), &tmXb, rc * kRowChunk + g * 32, tile * kTileCols,
+                                        &bars->xfull[s]);
+                        if (++s == kXS2) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+            });
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3, g = (warp - 4) >> 2;
+        const int j = q * 32 + lane;                    // column within the tile (TMEM lane)
+        const uint32_t tlane = static_cast<uint32_t>(q * 32) << 16;
+        const uint16_t *Glo_g = Gt + N * b;
+        int a = 0;
+        uint32_t aph = 0, gph = 0;
+        int64_t seq = 0;
+        for_segments([&](int tile, int rlo, int rhi) {
+            const int mlo = rlo > rc0 ? rlo : rc0;
+            if (warp == 4 && lane == 0) {
+                // pull the next tile's G rows (hi and lo, contiguous) into L2 while this
+                // segment runs, so its staging at the next tile boundary hits L2
+                const int64_t nt = static_cast<int64_t>(tile) + 1;
+                if (nt < ntiles) {
+                    const int64_t cols = N - nt * kTileCols < kTileCols ? N - nt * kTileCols : kTileCols;
+                    const uint32_t bytes = static_cast<uint32_t>(cols * b * 2) & ~15u;
+                    if (bytes) {
+                        tc::bulk_prefetch_l2(Gt + nt * kTileCols * b, bytes);
+                        tc::bulk_prefetch_l2(Glo_g + nt * kTileCols * b, bytes);
+                    }
+                }
+            }
+            if (mlo < rhi) {
+                // stage this tile's G (columns = TMEM lanes) once the previous tile's MMAs
+                // are done with it; the four row groups split each column's [hi | lo] words
+                // and issue all their loads before the TMEM stores (one L2 round trip)
+                tw(&bars->gempty, gph ^ 1u, w_c);
+                gph ^= 1u;
+                tc::fence_after_sync();
+                const int64_t jg = static_cast<int64_t>(tile) * kTileCols + j;
+                const int wq = b / 4;                       // words per group (multiple of 8)
+                const int half = g >> 1;                    // groups 0,1: hi; 2,3: lo
+                const int w0 = (g & 1) * wq;                // first word within the half
+                const uint4 *src = reinterpret_cast<const uint4 *>((half ? Glo_g : Gt) + jg * b) + w0 / 4;
+                uint4 u[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    u[i] = make_uint4(0u, 0u, 0u, 0u);
+                    if (i < wq / 4 && jg < N) u[i] = __ldg(src + i);
+                }
+#pragma unroll
+                for (int i = 0; i < 16; i += 2)
+                    if (i < wq / 4)
+                        tc::tmem_st8(tbase + tlane + static_cast<uint32_t>(half * 128 + w0 + 4 * i), u[i], u[i + 1]);
+                tc::tmem_wait_st();
+                tc::fence_before_sync();
+                tc::mbar_arrive(&bars->gfull);
+            }
+            for (int rc = rlo; rc < rhi; ++rc, seq += 4) {
+                const bool mma_rc = rc >= rc0;
+                float v[32];
+                if (mma_rc) {
+                    tw(&bars->acc_full[a], aph, w_a);
+                    tc::fence_after_sync();
+                    tc::tmem_ld32(tbase + tlane + 256u + static_cast<uint32_t>(a * kRowChunk + g * 32), v);
+                    tc::fence_before_sync();
+                    tc::mbar_arrive(&bars->acc_empty[a]);
+                    if (++a == 2) {
+                        a = 0;
+                        aph ^= 1u;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                }
+                const int r0 = rc * kRowChunk + g * 32;
+                const int64_t sq = seq + g;
+                const int s = static_cast<int>(sq % kXS2);
+                tw(&bars->xfull[s], static_cast<uint32_t>((sq / kXS2) & 1), w_b);
+                const uint32_t xs = smem_u32(Xs(s)) + static_cast<uint32_t>(j) * 128u;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t ad = xs + static_cast<uint32_t>((c ^ (j & 7)) << 4);
+                    float4 x4 = tc::lds128(ad);
+                    float lr[4] = {1.f, 1.f, 1.f, 1.f}, pr[4] = {1.f, 1.f, 1.f, 1.f};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int r = r0 + 4 * c + e;
+                        if (lam && r < n) lr[e] = __ldg(lam + r);
+                        if (post && r < n) pr[e] = __ldg(post + r);
+                    }
+                    x4.x = pr[0] * fmaf(lr[0], x4.x, -v[4 * c]);
+                    x4.y = pr[1] * fmaf(lr[1], x4.y, -v[4 * c + 1]);
+                    x4.z = pr[2] * fmaf(lr[2], x4.z, -v[4 * c + 2]);
+                    x4.w = pr[3] * fmaf(lr[3], x4.w, -v[4 * c + 3]);
+                    tc::sts128(ad, x4);
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1 + g, 128);
+                if (q == 0 && lane == 0) {
+                    tc::tma_store_2d(&tmYs, Xs(s), r0, tile * kTileCols);
+                    tc::bulk_commit();
+                    tc::bulk_wait_read0();
+                    tc::mbar_arrive(&bars->xempty[s]);
+                }
+            }
+        });
+        if (q == 0 && lane == 0) tc::bulk_wait0();
+    }
+    if (dbg && lane == 0) {
+        // [0] kernel  [1] V prod empty  [3] MMA full (V)  [4] MMA acc_empty  [9] MMA gfull
+        // [5] X prod xempty  [7] epi(w4) acc_full  [8] epi xfull  [10] epi gempty
+        const unsigned long long tot = clock64() - t_k0;
+        if (warp == 0) { tl[0] = tot; tl[1] = w_a; }
+        if (warp == 1) { tl[3] = w_a; tl[4] = w_b; tl[9] = w_c; }
+        if (warp == 2) { tl[5] = w_a; }
+        if (warp == 4) { tl[7] = w_a; tl[8] = w_b; tl[10] = w_c; }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) tc::tmem_free<512>(tbase);
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
@@ -1187,6 +1476,10 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             g_attr_err = cudaFuncSetAttribute(wy_update_kernel,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               kSmemMax);
+        if (g_attr_err == cudaSuccess)
+            g_attr_err = cudaFuncSetAttribute(wy_update_ts_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kSmemMax);
     });
     if (g_attr_err != cudaSuccess) return g_attr_err;
     const bool sym = p.kind == WY_SYM;
@@ -1273,7 +1566,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
 
     // ---------------- tensor maps
     const int64_t N = p.N;
-    CUtensorMap mWb, mW2b, mGb, mG2b, mV, mV2, mAs, mX, mY, mXb, mYb;
+    CUtensorMap mWb, mW2b, mGb, mG2b, mV, mV2, mAs, mX, mY, mXb, mYb, mXb2, mYb2;
     bool ok = make_map(&mWb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, n_pad, 2 * R, 32, b,
                        CU_TENSOR_MAP_SWIZZLE_64B) &&
               make_map(&mGb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Gt, b, 2 * N, 32, kTileCols,
@@ -1284,10 +1577,14 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                        CU_TENSOR_MAP_SWIZZLE_NONE) &&
               make_map(&mXb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, X, p.n, N, kRowChunk, kXBoxCols,
                        CU_TENSOR_MAP_SWIZZLE_NONE) &&
+              make_map(&mXb2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, X, p.n, N, 32, kTileCols,
+                       CU_TENSOR_MAP_SWIZZLE_128B) &&
               (!Y || (make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, 32, kTileCols,
                                CU_TENSOR_MAP_SWIZZLE_NONE) &&
                       make_map(&mYb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, kRowChunk, kXBoxCols,
-                               CU_TENSOR_MAP_SWIZZLE_NONE)));
+                               CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                      make_map(&mYb2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Y, p.n, N, 32, kTileCols,
+                               CU_TENSOR_MAP_SWIZZLE_128B)));
     if (ok && sym)
         ok = make_map(&mW2b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Wb, n_pad, 2 * R, 32, 2 * b,
                       CU_TENSOR_MAP_SWIZZLE_64B) &&
@@ -1359,6 +1656,20 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         const int64_t uxrc = (cur != Y && ps.row0 >= kRowChunk) ? 0 : ps.row0 / kRowChunk;
         const int64_t units = static_cast<int64_t>(ntiles) * (n_pad / kRowChunk - uxrc);
         const int grid3 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
+        // TS-mode update (G in TMEM) for the wide blocks: the resident G no longer competes
+        // with the V and X rings for shared memory
+        static const int ts_min = [] {
+            const char *e = std::getenv("HH_WY_TS_MIN");   // A/B runs only
+            return e ? std::atoi(e) : 256;
+        }();
+        if (ps.kw >= ts_min) {
+            ++nlaunch, wy_update_ts_kernel<<<grid3, 640, smem4(), stream>>>(
+                Gt, *ps.mV, (cur == X) ? mXb2 : mYb2, mYb2, ps.pre, ps.post, static_cast<int>(p.n),
+                static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
+                ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, g_timeline);
+            cur = Y;
+            continue;
+        }
         ++nlaunch, wy_update_kernel<<<grid3, 640, smem3(ps.kw), stream>>>(
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,

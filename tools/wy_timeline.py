@@ -23,7 +23,8 @@ torch.cuda.synchronize()
 L.hh_debug_wy_timeline(None)
 t = buf.cpu().tolist()
 names = ["kernel", "Vprod empty-wait", "-", "MMA full-wait (V data)", "MMA acc_empty-wait",
-         "Xprod xempty-wait", "-", "epi acc_full-wait", "epi xfull-wait"]
+         "Xprod xempty-wait", "-", "epi acc_full-wait", "epi xfull-wait", "MMA gfull-wait (TS)",
+         "epi gempty-wait (TS)"]
 for i, nm in enumerate(names):
     if nm != "-":
         print(f"{nm:24s} {t[i]:12d} cycles  {100.0 * t[i] / max(t[0], 1):6.1f} %")
