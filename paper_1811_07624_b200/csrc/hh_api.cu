@@ -133,6 +133,11 @@ hh_status hh_debug_wy_timeline(void *device_buf) {
     return HH_OK;
 }
 
+// Test hook (not part of hh.h): block width from which the update runs in TS mode (G in
+// TMEM, wy_update_ts_kernel); default 256.  Lets the GPU tests cover the TS kernel at every
+// block width.  Returns the previous value.
+int hh_debug_wy_ts_min(int kw) { return wy_set_ts_min(kw); }
+
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first
 // projection only, leaving G (bf16 hi/lo rows) and V in the workspace at the
 // offsets written to off[0..1] (G, V) and the block size b / count nblk to off[2..3].

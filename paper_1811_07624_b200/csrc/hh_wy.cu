@@ -36,6 +36,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -1387,6 +1388,14 @@ cudaError_t g_attr_err = cudaSuccess;
 
 void wy_set_timeline(unsigned long long *buf) { g_timeline = buf; }
 
+// TS-mode update from this block width on (default 256; HH_WY_TS_MIN or the test hook
+// hh_debug_wy_ts_min override it)
+std::atomic<int> g_ts_min{[] {
+    const char *e = std::getenv("HH_WY_TS_MIN");
+    return e ? std::atoi(e) : 256;
+}()};
+int wy_set_ts_min(int kw) { return g_ts_min.exchange(kw); }
+
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     WyPlan p{};
     p.kind = kind;
@@ -1658,11 +1667,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         const int grid3 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
         // TS-mode update (G in TMEM) for the wide blocks: the resident G no longer competes
         // with the V and X rings for shared memory
-        static const int ts_min = [] {
-            const char *e = std::getenv("HH_WY_TS_MIN");   // A/B runs only
-            return e ? std::atoi(e) : 256;
-        }();
-        if (ps.kw >= ts_min) {
+        if (ps.kw >= g_ts_min.load(std::memory_order_relaxed)) {
             ++nlaunch, wy_update_ts_kernel<<<grid3, 640, smem4(), stream>>>(
                 Gt, *ps.mV, (cur == X) ? mXb2 : mYb2, mYb2, ps.pre, ps.post, static_cast<int>(p.n),
                 static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,

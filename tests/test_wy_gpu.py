@@ -183,3 +183,36 @@ def test_C3_full_size_sampled_auto():
                                     np.arange(c.N - 8, c.N)]))
     got = Yd[torch.from_numpy(idx).cuda()].cpu().numpy()
     assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X[idx]), "f32", c.h, "C3 full auto")
+
+
+@pytest.fixture
+def ts_everywhere():
+    """Run the update in TS mode (G in TMEM, wy_update_ts_kernel) at every block width."""
+    L = hh.hh.lib()
+    prev = L.hh_debug_wy_ts_min(32)
+    yield
+    L.hh_debug_wy_ts_min(prev)
+
+
+@pytest.mark.parametrize("n,h,N", [(256, 40, 300), (2048, 32, 1500), (100, 50, 129),
+                                   (4096, 300, 130), (1000, 257, 200)])
+@pytest.mark.parametrize("op", [0, 1])
+def test_wy_ts_parity_all_widths(ts_everywhere, n, h, N, op):
+    """The TS-mode update (used by default only for 256-wide blocks) at b = 32 ... 160 and
+    ragged shapes, against the oracle."""
+    c = gi.make_case("apply", n, h, N, "f32", seed=22)
+    got = wy(op, c.U, c.X)
+    assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"WY-TS n{n} h{h} N{N} op{op}")
+
+
+def test_wy_ts_sym_and_qr(ts_everywhere):
+    c = gi.make_case("sym", 512, 40, 333, "f32", seed=26)
+    got = wy_sym(c.U, c.lam, c.X)
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", 40, "WY-TS sym")
+    n, h, N = 512, 300, 200
+    U = gi.qr_reflectors(gi.rng(27, n, h), h, n, "f32")
+    X = gi.gaussian_columns(gi.rng(28, n, h), N, n, "f32")
+    with hh.algo(hh.HH_ALGO_WY):
+        out = hh.hh_apply_qr(0, dev(U), dev(X))
+    torch.cuda.synchronize()
+    assert_parity(out.cpu().numpy(), oracle.apply(0, U, X), "f32", h, "WY-TS QR")
