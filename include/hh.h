@@ -275,8 +275,8 @@ hh_algo hh_get_algo(void);
  *   picks K5 for (n, h, N, dtype) (packed W, T, V = W T and one G block), else 0.
  *   HH_CALL_SYM: the compact-WY scratch when the symmetric call picks the tensor-core
  *   block program, else 0.  HH_CALL_MAHALANOBIS: n*M*sizeof(dtype) (the
- *   transform-once Z) + the pair buckets (2 M + (M+1) + npairs int32, each 256-B
- *   rounded).  Errors: HH_ERR_INVALID_VALUE for bad arguments.
+ *   transform-once Z) + the pair buckets (2 M + (M+1) + npairs + ceil(M/4096) int32,
+ *   each 256-B rounded).  Errors: HH_ERR_INVALID_VALUE for bad arguments.
  */
 hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
                              int64_t npairs, hh_dtype dtype, size_t *bytes);

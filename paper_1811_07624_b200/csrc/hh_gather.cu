@@ -58,73 +58,81 @@ __global__ void bucket_hist_kernel(const int32_t *__restrict__ ia, int64_t npair
         atomicAdd(cnt + ia[j], 1);
 }
 
-// exclusive scan of cnt[0..M) into off[0..M] and cur[0..M): one CTA, chunks of 32K
-// counts, each thread owning 32 contiguous counts (8 x int4 loads)
-__global__ void __launch_bounds__(1024) bucket_scan_kernel(const int32_t *__restrict__ cnt,
-                                                           int64_t M, int32_t *__restrict__ off,
-                                                           int32_t *__restrict__ cur) {
+// exclusive scan of cnt[0..M) into off[0..M] and cur[0..M), two levels: each CTA scans
+// 4096 counts (4 per thread, int4 loads) and writes its total; then every CTA adds the sum
+// of the totals before it (a few dozen values, summed in fixed order: deterministic).
+// (One CTA scanning all of M had taken ~30 us at M = 65536.)
+constexpr int kScanPer = 4096;
+__global__ void __launch_bounds__(1024) bucket_scan_local_kernel(const int32_t *__restrict__ cnt,
+                                                                 int64_t M,
+                                                                 int32_t *__restrict__ off,
+                                                                 int32_t *__restrict__ tot) {
     __shared__ int32_t wsum[32];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    constexpr int PER = 32;
-    int32_t carry = 0;
-    for (int64_t base = 0; base < M; base += 1024 * PER) {
-        const int64_t i0 = base + static_cast<int64_t>(t) * PER;
-        int4 v[PER / 4];
-        int32_t s = 0;
-        const bool full = i0 + PER <= M;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kScanPer + 4 * t;
+    int4 v = make_int4(0, 0, 0, 0);
+    if (i0 + 3 < M) {
+        v = *reinterpret_cast<const int4 *>(cnt + i0);
+    } else {
+        if (i0 < M) v.x = cnt[i0];
+        if (i0 + 1 < M) v.y = cnt[i0 + 1];
+        if (i0 + 2 < M) v.z = cnt[i0 + 2];
+    }
+    const int32_t sthr = v.x + v.y + v.z + v.w;
+    int32_t x = sthr;
 #pragma unroll
-        for (int q = 0; q < PER / 4; ++q) {
-            if (full) {
-                v[q] = *reinterpret_cast<const int4 *>(cnt + i0 + 4 * q);
-            } else {
-                const int64_t i = i0 + 4 * q;
-                v[q] = make_int4(i < M ? cnt[i] : 0, i + 1 < M ? cnt[i + 1] : 0,
-                                 i + 2 < M ? cnt[i + 2] : 0, i + 3 < M ? cnt[i + 3] : 0);
-            }
-            s += v[q].x + v[q].y + v[q].z + v[q].w;
-        }
-        int32_t x = s;   // inclusive scan of the per-thread sums
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int32_t z = wsum[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
         }
-        if (lane == 31) wsum[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            int32_t z = wsum[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
-                if (lane >= o) z += y;
-            }
-            wsum[lane] = z;
-        }
-        __syncthreads();
-        int32_t run = carry + (w ? wsum[w - 1] : 0) + x - s;
-        const int32_t total = wsum[31];
-#pragma unroll
-        for (int q = 0; q < PER / 4; ++q) {
-            int4 o;
-            o.x = run;
-            o.y = run + v[q].x;
-            o.z = o.y + v[q].y;
-            o.w = o.z + v[q].z;
-            run = o.w + v[q].w;
-            if (full) {
-                *reinterpret_cast<int4 *>(off + i0 + 4 * q) = o;
-                *reinterpret_cast<int4 *>(cur + i0 + 4 * q) = o;
-            } else {
-                const int64_t i = i0 + 4 * q;
-                const int32_t ov[4] = {o.x, o.y, o.z, o.w};
-                for (int e = 0; e < 4; ++e)
-                    if (i + e < M) off[i + e] = cur[i + e] = ov[e];
-            }
-        }
-        carry += total;
-        __syncthreads();
+        wsum[lane] = z;
     }
-    if (t == 0) off[M] = carry;
+    __syncthreads();
+    const int32_t run = (w ? wsum[w - 1] : 0) + x - sthr;
+    int4 o;
+    o.x = run;
+    o.y = run + v.x;
+    o.z = o.y + v.y;
+    o.w = o.z + v.z;
+    if (i0 + 3 < M) {
+        *reinterpret_cast<int4 *>(off + i0) = o;
+    } else {
+        if (i0 < M) off[i0] = o.x;
+        if (i0 + 1 < M) off[i0 + 1] = o.y;
+        if (i0 + 2 < M) off[i0 + 2] = o.z;
+    }
+    if (t == 0) tot[blockIdx.x] = wsum[31];
+}
+
+__global__ void __launch_bounds__(1024) bucket_scan_add_kernel(const int32_t *__restrict__ tot,
+                                                               int64_t M, int32_t *__restrict__ off,
+                                                               int32_t *__restrict__ cur) {
+    __shared__ int32_t base;
+    if (threadIdx.x == 0) {
+        int32_t b = 0;
+        for (int c = 0; c < static_cast<int>(blockIdx.x); ++c) b += tot[c];
+        base = b;
+        if (blockIdx.x == gridDim.x - 1) off[M] = b + tot[blockIdx.x];
+    }
+    __syncthreads();
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kScanPer + 4 * threadIdx.x;
+    for (int e = 0; e < 4; ++e) {
+        const int64_t i = i0 + e;
+        if (i < M) {
+            const int32_t vv = off[i] + base;
+            off[i] = vv;
+            cur[i] = vv;
+        }
+    }
 }
 
 __global__ void bucket_scatter_kernel(const int32_t *__restrict__ ia, int64_t npairs,
@@ -223,7 +231,7 @@ const GVariant kB64[] = {
 size_t bucket_ws_bytes(int64_t M, int64_t npairs) {
     auto r = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
     return r(static_cast<size_t>(M) * 4) * 2 + r(static_cast<size_t>(M + 1) * 4) +
-           r(static_cast<size_t>(npairs) * 4);
+           r(static_cast<size_t>(npairs) * 4) + r(static_cast<size_t>((M + kScanPer - 1) / kScanPer) * 4);
 }
 
 cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const int32_t *ia,
@@ -236,12 +244,15 @@ cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const in
     int32_t *off = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4));
     int32_t *perm = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4) +
                                                 r(static_cast<size_t>(M + 1) * 4));
+    int32_t *tot = perm + r(static_cast<size_t>(npairs) * 4) / 4;   // per-CTA scan totals
     const int sms = device_attr().sm_count;
     cudaError_t e = cudaMemsetAsync(cnt, 0, static_cast<size_t>(M) * 4, stream);
     if (e != cudaSuccess) return e;
     const int g = static_cast<int>(std::min<int64_t>((npairs + 255) / 256, sms * 8));
     bucket_hist_kernel<<<g, 256, 0, stream>>>(ia, npairs, cnt);
-    bucket_scan_kernel<<<1, 1024, 0, stream>>>(cnt, M, off, cur);
+    const int nsb = static_cast<int>((M + kScanPer - 1) / kScanPer);
+    bucket_scan_local_kernel<<<nsb, 1024, 0, stream>>>(cnt, M, off, tot);
+    bucket_scan_add_kernel<<<nsb, 1024, 0, stream>>>(tot, M, off, cur);
     bucket_scatter_kernel<<<g, 256, 0, stream>>>(ia, npairs, cur, perm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -276,7 +287,7 @@ cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const in
         info->block = v->nt;
         info->smem = 0;
         info->nchunks = 0;
-        info->launches = 4;   // histogram, scan, scatter, gather (+ one memset)
+        info->launches = 5;   // histogram, scan (2), scatter, gather (+ one memset)
     }
     return e;
 }

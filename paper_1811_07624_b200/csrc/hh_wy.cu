@@ -168,20 +168,26 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
     }
 }
 
-// S[blk][l][m] = sum over splits (ascending) of the Gram partials, upper tiles.
+// S[blk][l][m] = sum over the splits of the Gram partials, upper tiles: one warp per
+// element, lane q adding splits q, q + 32, ... then a fixed butterfly (deterministic; a
+// thread-per-element loop over 128 splits had been latency-bound)
 __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int nblk, int nsplit,
                                       int full, float *__restrict__ S) {
     const int64_t bb = static_cast<int64_t>(b) * b;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < nblk * bb;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t idx = w0; idx < nblk * bb; idx += nw) {
         const int64_t blk = idx / bb, e = idx % bb;
         const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
         float s = 0.f;
         if (full || (l / 64) <= (m / 64)) {
             const float *p = Sp + blk * nsplit * bb + e;
-            for (int q = 0; q < nsplit; ++q) s += p[q * bb];
+            for (int q = lane; q < nsplit; q += 32) s += p[q * bb];
         }
-        S[idx] = s;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) S[idx] = s;
     }
 }
 
@@ -1518,12 +1524,12 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, p.gram_rows, 0,
                                                                        nullptr, 0, Sp);
         const int64_t ns = static_cast<int64_t>(m) * b * b;
-        ++nlaunch, wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, sms * 8)),
+        ++nlaunch, wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns * 32 + 255) / 256, sms * 16)),
                                 256, 0, stream>>>(Sp, b, m, p.nsplit, 0, S);
         if (sym) {   // P = W^T Lambda W of the last block (full)
             ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, p.gram_rows,
                                                                        m - 1, lam, 1, F(p.off_pp));
-            ++nlaunch, wy_gram_reduce_kernel<<<std::max(1, (b * b + 255) / 256), 256, 0, stream>>>(
+            ++nlaunch, wy_gram_reduce_kernel<<<std::max(1, std::min(sms * 16, (b * b * 32 + 255) / 256)), 256, 0, stream>>>(
                 F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p));
         }
         ++nlaunch, wy_tbuild_kernel<<<m, 256, tbuild_smem(b), stream>>>(S, b, T, sym ? 0 : 1);

@@ -73,8 +73,9 @@ def lib() -> ctypes.CDLL:
         L.hh_debug_wy_project.argtypes = [i32, i64, i64, p, p, i64, p, sz,
                                           ctypes.POINTER(i64), p]
         L.hh_debug_wy_project.restype = i32
-        L.hh_debug_wy_ts_min.argtypes = [i32]
-        L.hh_debug_wy_ts_min.restype = i32
+        if hasattr(L, "hh_debug_wy_ts_min"):   # test hook (absent from older builds)
+            L.hh_debug_wy_ts_min.argtypes = [i32]
+            L.hh_debug_wy_ts_min.restype = i32
         L.hh_status_string.argtypes = [i32]
         L.hh_status_string.restype = ctypes.c_char_p
         L.hh_version.restype = ctypes.c_char_p

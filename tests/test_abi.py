@@ -55,7 +55,7 @@ def test_workspace_query():
         assert hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 2048, 32, 131072, 0, 0) == 0
     r256 = lambda b: (b + 255) // 256 * 256  # noqa: E731
     assert hhpkg.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, 512, 9, 65536, 1 << 21, 0) == \
-        512 * 65536 * 4 + 2 * r256(65536 * 4) + r256(65537 * 4) + r256((1 << 21) * 4)
+        512 * 65536 * 4 + 2 * r256(65536 * 4) + r256(65537 * 4) + r256((1 << 21) * 4) + r256(16 * 4)
     b = hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY_HOST, 1024, 10, 262144, 0, 0)
     assert b >= 3 * (64 << 20) + 10 * 1024 * 4
     with pytest.raises(hh.HHError):
