@@ -88,11 +88,19 @@ __device__ __forceinline__ void vmul(double2 &x, const double2 &l) {
     x.x *= l.x;
     x.y *= l.y;
 }
+// sqrt(d) by the hardware approximation (MUFU, within ~1 ulp): the correctly rounded
+// sqrtf is a subroutine call per element, and K3a scales every element of every point
+// (an ulp of sqrt(d) is 4 orders of magnitude below the fp32 parity gate)
+__device__ __forceinline__ float sqrt_approx(float v) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
 __device__ __forceinline__ void vmulsqrt(float4 &x, const float4 &d) {
-    x.x *= sqrtf(d.x);
-    x.y *= sqrtf(d.y);
-    x.z *= sqrtf(d.z);
-    x.w *= sqrtf(d.w);
+    x.x *= sqrt_approx(d.x);
+    x.y *= sqrt_approx(d.y);
+    x.z *= sqrt_approx(d.z);
+    x.w *= sqrt_approx(d.w);
 }
 __device__ __forceinline__ void vmulsqrt(double2 &x, const double2 &d) {
     x.x *= sqrt(d.x);
