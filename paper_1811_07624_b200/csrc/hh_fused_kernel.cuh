@@ -275,6 +275,27 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             }
             p[c] = vsum(acc);
         }
+        if constexpr (TPC > 32 && C == 2) {
+            // two columns over a multi-warp group: reduce-scatter in the warp (the first step
+            // exchanges the other column's partial, then one value per lane: 5 shuffles
+            // instead of 10); lanes 0 and 16 hold the warp's sums of columns 0 and 1, and the
+            // shared-memory exchange that follows broadcasts them anyway
+            const bool hi = (lane & 16) != 0;
+            T v = (hi ? p[1] : p[0]) + __shfl_xor_sync(0xffffffffu, hi ? p[0] : p[1], 16);
+#pragma unroll
+            for (int off = 8; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            T *rb = red + (static_cast<size_t>(rpar) * NU + unit) * WPU * C;
+            if ((lane & 15) == 0) rb[wiu * C + (hi ? 1 : 0)] = v;
+            named_bar_sync(1 + unit, UT);
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                T sum = rb[c];
+#pragma unroll
+                for (int w = 1; w < WPU; ++w) sum += rb[w * C + c];
+                p[c] = sum;
+            }
+            rpar ^= 1;
+        } else {
 #pragma unroll
         for (int off = (TPC < 32 ? TPC : 32) / 2; off > 0; off >>= 1) {
 #pragma unroll
@@ -295,6 +316,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 p[c] = s;
             }
             rpar ^= 1;
+        }
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
