@@ -168,12 +168,27 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
     }
 }
 
-// S[blk][l][m] = sum over the splits of the Gram partials, upper tiles: one warp per
-// element, lane q adding splits q, q + 32, ... then a fixed butterfly (deterministic; a
-// thread-per-element loop over 128 splits had been latency-bound)
+// S[blk][l][m] = sum over the splits of the Gram partials, upper tiles, in a fixed order
+// (deterministic).  thread_per_elem: one thread per element walking the splits (coalesced
+// across threads; enough parallelism for large b); else one warp per element, lane q adding
+// splits q, q + 32, ... then a butterfly (small b: few elements, many splits).
 __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int nblk, int nsplit,
-                                      int full, float *__restrict__ S) {
+                                      int full, float *__restrict__ S, int thread_per_elem) {
     const int64_t bb = static_cast<int64_t>(b) * b;
+    if (thread_per_elem) {
+        for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+             idx < nblk * bb; idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t blk = idx / bb, e = idx % bb;
+            const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
+            float s = 0.f;
+            if (full || (l / 64) <= (m / 64)) {
+                const float *p = Sp + blk * nsplit * bb + e;
+                for (int q = 0; q < nsplit; ++q) s += p[q * bb];
+            }
+            S[idx] = s;
+        }
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -293,9 +308,16 @@ __global__ void __launch_bounds__(256) wy_tbuild_kernel(const float *__restrict_
         }
         __syncthreads();
     }
+    if (diag_only) {   // only the 32 x 32 diagonal blocks are read (wy_vrec_kernel)
+        for (int e = t; e < nb * 1024; e += 256) {
+            const int o = (e >> 10) * 32, l = o + ((e >> 5) & 31), m = o + (e & 31);
+            Tout[static_cast<int64_t>(l) * b + m] = m >= l ? tp(l, m) : 0.f;
+        }
+        return;
+    }
     for (int64_t e = t; e < bb; e += 256) {
         const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
-        Tout[e] = (m >= l && (!diag_only || l / 32 == m / 32)) ? tp(l, m) : 0.f;
+        Tout[e] = m >= l ? tp(l, m) : 0.f;
     }
 }
 
@@ -305,23 +327,25 @@ __global__ void __launch_bounds__(256) wy_tbuild_kernel(const float *__restrict_
 // 32 x 32 blocks T_cc are needed and the work is parallel over rows: a CTA owns 64 rows
 // of one block, keeps its V rows in SMEM and walks the chunks.  Output: bf16 hi/lo V
 // rows (Vt[hi: blk*n_pad + r][i], Vt[lo: lo_off + ...]).
+template <int RP>   // rows per thread: the CTA owns 32 * RP rows
 __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ Wf,
                                                       const float *__restrict__ Sg,
                                                       const float *__restrict__ Tg, int64_t n_pad,
                                                       int b, uint16_t *__restrict__ Vt,
                                                       int64_t lo_off) {
     extern __shared__ float vsm[];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+    constexpr int RW = 32 * RP;   // rows per CTA
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * RW;
     const int blk = blockIdx.y;
-    const int t = threadIdx.x, tx = t % 8, ty = t / 8;   // 8 x 32: 4 columns x 2 rows
+    const int t = threadIdx.x, tx = t % 8, ty = t / 8;   // 8 x 32: 4 columns x RP rows
     const int64_t bb = static_cast<int64_t>(b) * b;
     const float *S = Sg + blk * bb;
     const float *T = Tg + blk * bb;
     const float *W = Wf + static_cast<int64_t>(blk) * b * n_pad;
-    float *Vs = vsm;                    // 64 x (b + 1)
-    float *Sp = Vs + 64 * (b + 1);      // (b - 32) x 32 panel S[0:c, c:c+32]
+    float *Vs = vsm;                    // RW x (b + 1)
+    float *Sp = Vs + RW * (b + 1);      // (b - 32) x 32 panel S[0:c, c:c+32]
     float *Tc = Sp + (b - 32 > 0 ? (b - 32) * 32 : 32);   // 32 x 33
-    float *Zs = Tc + 32 * 33;           // 64 x 33
+    float *Zs = Tc + 32 * 33;           // RW x 33
     const int ld = b + 1;
     for (int c = 0; c < b; c += 32) {
         for (int e = t; e < c * 32; e += 256) Sp[e] = S[(e / 32) * b + c + (e % 32)];
@@ -331,30 +355,32 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
         }
         __syncthreads();
         // Z = W_c - V_{<c} S_{<c,c}   (64 x 32): thread rows ty*2.., columns tx*4..
-        float z[2][4];
+        float z[RP][4];
 #pragma unroll
-        for (int p = 0; p < 2; ++p)
+        for (int p = 0; p < RP; ++p)
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                z[p][q] = W[static_cast<int64_t>(c + tx * 4 + q) * n_pad + r0 + ty * 2 + p];
+                z[p][q] = W[static_cast<int64_t>(c + tx * 4 + q) * n_pad + r0 + ty * RP + p];
         for (int l = 0; l < c; ++l) {
-            const float v0 = Vs[(ty * 2) * ld + l], v1 = Vs[(ty * 2 + 1) * ld + l];
+            float vv[RP];
+#pragma unroll
+            for (int p = 0; p < RP; ++p) vv[p] = Vs[(ty * RP + p) * ld + l];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const float sv = Sp[l * 32 + tx * 4 + q];
-                z[0][q] = fmaf(-v0, sv, z[0][q]);
-                z[1][q] = fmaf(-v1, sv, z[1][q]);
+#pragma unroll
+                for (int p = 0; p < RP; ++p) z[p][q] = fmaf(-vv[p], sv, z[p][q]);
             }
         }
 #pragma unroll
-        for (int p = 0; p < 2; ++p)
+        for (int p = 0; p < RP; ++p)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) Zs[(ty * 2 + p) * 33 + tx * 4 + q] = z[p][q];
+            for (int q = 0; q < 4; ++q) Zs[(ty * RP + p) * 33 + tx * 4 + q] = z[p][q];
         __syncthreads();
         // V_c = Z T_cc  (T_cc upper triangular)
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            const int rr = ty * 2 + p;
+        for (int p = 0; p < RP; ++p) {
+            const int rr = ty * RP + p;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int j = tx * 4 + q;
@@ -366,7 +392,7 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
         __syncthreads();
     }
     // bf16 hi/lo rows out
-    for (int e = t; e < 64 * b; e += 256) {
+    for (int e = t; e < RW * b; e += 256) {
         const int rr = e / b, i = e % b;
         const float v = Vs[rr * ld + i];
         const uint16_t hv = f2bf(v);
@@ -1480,7 +1506,11 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         g_attr_err = cudaFuncSetAttribute(wy_project_kernel,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (g_attr_err == cudaSuccess)
-            g_attr_err = cudaFuncSetAttribute(wy_vrec_kernel,
+            g_attr_err = cudaFuncSetAttribute(wy_vrec_kernel<2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(vrec_smem(256)));
+        if (g_attr_err == cudaSuccess)
+            g_attr_err = cudaFuncSetAttribute(wy_vrec_kernel<1>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(vrec_smem(256)));
         if (g_attr_err == cudaSuccess)
@@ -1525,18 +1555,24 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                                                                        nullptr, 0, Sp);
         const int64_t ns = static_cast<int64_t>(m) * b * b;
         ++nlaunch, wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns * 32 + 255) / 256, sms * 16)),
-                                256, 0, stream>>>(Sp, b, m, p.nsplit, 0, S);
+                                256, 0, stream>>>(Sp, b, m, p.nsplit, 0, S, ns >= 32768 ? 1 : 0);
         if (sym) {   // P = W^T Lambda W of the last block (full)
             ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, p.gram_rows,
                                                                        m - 1, lam, 1, F(p.off_pp));
             ++nlaunch, wy_gram_reduce_kernel<<<std::max(1, std::min(sms * 16, (b * b * 32 + 255) / 256)), 256, 0, stream>>>(
-                F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p));
+                F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p), b * b >= 32768 ? 1 : 0);
         }
         ++nlaunch, wy_tbuild_kernel<<<m, 256, tbuild_smem(b), stream>>>(S, b, T, sym ? 0 : 1);
         if (!sym) {
             // V = W T per block, row-parallel from the diagonal T blocks (wy_vrec_kernel)
-            ++nlaunch, wy_vrec_kernel<<<dim3(static_cast<unsigned>(n_pad / 64), m), 256,
-                                        vrec_smem(b), stream>>>(Wf, S, T, n_pad, b, H(p.off_v), vlo);
+            // 32-row CTAs when 64-row ones would not fill two waves (one block of n = 4096:
+            // 64 CTAs on 148 SMs)
+            if (static_cast<int64_t>(n_pad / 64) * m < 2 * sms)
+                ++nlaunch, wy_vrec_kernel<1><<<dim3(static_cast<unsigned>(n_pad / 32), m), 256,
+                                               vrec_smem(b), stream>>>(Wf, S, T, n_pad, b, H(p.off_v), vlo);
+            else
+                ++nlaunch, wy_vrec_kernel<2><<<dim3(static_cast<unsigned>(n_pad / 64), m), 256,
+                                               vrec_smem(b), stream>>>(Wf, S, T, n_pad, b, H(p.off_v), vlo);
         }
         const dim3 gv(static_cast<unsigned>(n_pad / 64), b / 32);
         for (int k = 0; k < (sym ? m : 0); ++k) {
