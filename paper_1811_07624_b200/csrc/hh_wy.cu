@@ -1565,9 +1565,9 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         ++nlaunch, wy_tbuild_kernel<<<m, 256, tbuild_smem(b), stream>>>(S, b, T, sym ? 0 : 1);
         if (!sym) {
             // V = W T per block, row-parallel from the diagonal T blocks (wy_vrec_kernel)
-            // 32-row CTAs when 64-row ones would not fill two waves (one block of n = 4096:
-            // 64 CTAs on 148 SMs)
-            if (static_cast<int64_t>(n_pad / 64) * m < 2 * sms)
+            // 32-row CTAs when 64-row ones would not fill one wave (one block of n = 4096:
+            // 64 CTAs on 148 SMs; with 4 blocks the 64-row CTAs are faster: measured)
+            if (static_cast<int64_t>(n_pad / 64) * m < sms)
                 ++nlaunch, wy_vrec_kernel<1><<<dim3(static_cast<unsigned>(n_pad / 32), m), 256,
                                                vrec_smem(b), stream>>>(Wf, S, T, n_pad, b, H(p.off_v), vlo);
             else
