@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
     const int ti = blockIdx.x, tj = blockIdx.y;
     const int blk = blockIdx.z / nsplit, sp = blockIdx.z % nsplit;
     if (ti > tj && !full) return;
-    __shared__ float Ls[32][65], Ms[32][65];
+    __shared__ __align__(16) float Ls[32][68], Ms[32][68];   // rows 16-B aligned: float4 reads
     const int t = threadIdx.x, tx = t % 16, ty = t / 16;
     float acc[4][4] = {};
     const int64_t r0 = static_cast<int64_t>(sp) * rows;
@@ -142,12 +142,9 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
         __syncthreads();
 #pragma unroll 8
         for (int k = 0; k < 32; ++k) {
-            float a[4], m[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                a[q] = Ls[k][ty * 4 + q];
-                m[q] = Ms[k][tx * 4 + q];
-            }
+            const float4 a4 = *reinterpret_cast<const float4 *>(&Ls[k][ty * 4]);
+            const float4 m4 = *reinterpret_cast<const float4 *>(&Ms[k][tx * 4]);
+            const float a[4] = {a4.x, a4.y, a4.z, a4.w}, m[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
