@@ -378,13 +378,20 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
 #pragma unroll
         for (int p = 0; p < RP; ++p) {
             const int rr = ty * RP + p;
+            // the four columns' chains interleaved over a fully unrolled m (T_cc upper
+            // triangular: terms with m > j are predicated off)
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int j = tx * 4 + q;
-                float v = 0.f;
-                for (int m = 0; m <= j; ++m) v = fmaf(Zs[rr * 33 + m], Tc[m * 33 + j], v);
-                Vs[rr * ld + c + j] = v;
+            for (int m = 0; m < 32; ++m) {
+                const float zv = Zs[rr * 33 + m];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = tx * 4 + q;
+                    if (m <= j) v[q] = fmaf(zv, Tc[m * 33 + j], v[q]);
+                }
             }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Vs[rr * ld + c + tx * 4 + q] = v[q];
         }
         __syncthreads();
     }
