@@ -358,17 +358,33 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 z[p][q] = W[static_cast<int64_t>(c + tx * 4 + q) * n_pad + r0 + ty * RP + p];
-        for (int l = 0; l < c; ++l) {
-            float vv[RP];
+        // two partial sums per output (even / odd l): twice the independent FMA chains
+        float z2[RP][4];
 #pragma unroll
-            for (int p = 0; p < RP; ++p) vv[p] = Vs[(ty * RP + p) * ld + l];
+        for (int p = 0; p < RP; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) z2[p][q] = 0.f;
+        for (int l = 0; l < c; l += 2) {   // c is a multiple of 32
+            float va[RP], vb[RP];
+#pragma unroll
+            for (int p = 0; p < RP; ++p) {
+                va[p] = Vs[(ty * RP + p) * ld + l];
+                vb[p] = Vs[(ty * RP + p) * ld + l + 1];
+            }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float sv = Sp[l * 32 + tx * 4 + q];
+                const float sa = Sp[l * 32 + tx * 4 + q], sb = Sp[(l + 1) * 32 + tx * 4 + q];
 #pragma unroll
-                for (int p = 0; p < RP; ++p) z[p][q] = fmaf(-vv[p], sv, z[p][q]);
+                for (int p = 0; p < RP; ++p) {
+                    z[p][q] = fmaf(-va[p], sa, z[p][q]);
+                    z2[p][q] = fmaf(-vb[p], sb, z2[p][q]);
+                }
             }
         }
+#pragma unroll
+        for (int p = 0; p < RP; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) z[p][q] += z2[p][q];
 #pragma unroll
         for (int p = 0; p < RP; ++p)
 #pragma unroll
