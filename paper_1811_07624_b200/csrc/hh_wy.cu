@@ -339,25 +339,52 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
     const float *S = Sg + blk * bb;
     const float *T = Tg + blk * bb;
     const float *W = Wf + static_cast<int64_t>(blk) * b * n_pad;
+    const int spn = b - 32 > 0 ? (b - 32) * 32 : 32;
     float *Vs = vsm;                    // RW x (b + 1)
-    float *Sp = Vs + RW * (b + 1);      // (b - 32) x 32 panel S[0:c, c:c+32]
-    float *Tc = Sp + (b - 32 > 0 ? (b - 32) * 32 : 32);   // 32 x 33
-    float *Zs = Tc + 32 * 33;           // RW x 33
+    float *SpB = Vs + RW * (b + 1);     // 2 x (b - 32) x 32 panels S[0:c, c:c+32]
+    float *TcB = SpB + 2 * spn;         // 2 x 32 x 33
+    float *Zs = TcB + 2 * 32 * 33;      // RW x 33
     const int ld = b + 1;
-    for (int c = 0; c < b; c += 32) {
-        for (int e = t; e < c * 32; e += 256) Sp[e] = S[(e / 32) * b + c + (e % 32)];
+    // the next chunk's S panel and T_cc are copied asynchronously (cp.async) into the other
+    // buffer while this chunk computes, and its W values are prefetched into registers:
+    // the per-chunk global loads had been the exposed latency (long-scoreboard stalls)
+    auto issue = [&](int c, int buf) {
+        float *Sp = SpB + buf * spn, *Tc = TcB + buf * 32 * 33;
+        for (int e = t; e < c * 32; e += 256)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(Sp + e)),
+                         "l"(S + (e / 32) * b + c + (e % 32))
+                         : "memory");
         for (int e = t; e < 32 * 32; e += 256) {
             const int m = e / 32, j = e % 32;
-            Tc[m * 33 + j] = T[(c + m) * b + c + j];
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(Tc + m * 33 + j)),
+                         "l"(T + (c + m) * b + c + j)
+                         : "memory");
         }
-        __syncthreads();
-        // Z = W_c - V_{<c} S_{<c,c}   (64 x 32): thread rows ty*2.., columns tx*4..
-        float z[RP][4];
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float wn[RP][4];
+    auto load_w = [&](int c) {
 #pragma unroll
         for (int p = 0; p < RP; ++p)
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                z[p][q] = W[static_cast<int64_t>(c + tx * 4 + q) * n_pad + r0 + ty * RP + p];
+                wn[p][q] = W[static_cast<int64_t>(c + tx * 4 + q) * n_pad + r0 + ty * RP + p];
+    };
+    issue(0, 0);
+    load_w(0);
+    int buf = 0;
+    for (int c = 0; c < b; c += 32, buf ^= 1) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();   // this chunk's panel and T_cc landed; previous chunk done
+        if (c + 32 < b) issue(c + 32, buf ^ 1);
+        const float *Sp = SpB + buf * spn, *Tc = TcB + buf * 32 * 33;
+        // Z = W_c - V_{<c} S_{<c,c}   (RW x 32): thread rows ty*RP.., columns tx*4..
+        float z[RP][4];
+#pragma unroll
+        for (int p = 0; p < RP; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) z[p][q] = wn[p][q];
+        if (c + 32 < b) load_w(c + 32);
         // two partial sums per output (even / odd l): twice the independent FMA chains
         float z2[RP][4];
 #pragma unroll
@@ -423,8 +450,8 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
 }
 
 size_t vrec_smem(int b) {
-    return (static_cast<size_t>(64) * (b + 1) + static_cast<size_t>(std::max(b - 32, 1)) * 32 +
-            32 * 33 + 64 * 33) *
+    return (static_cast<size_t>(64) * (b + 1) + 2 * static_cast<size_t>(std::max(b - 32, 1)) * 32 +
+            2 * 32 * 33 + 64 * 33) *
            4;
 }
 
