@@ -94,9 +94,11 @@ typedef enum {
  * columns; reflector symmetry makes the transpose a reversal. */
 
 /* Path selection for hh_apply (fp32):
- *   HH_ALGO_AUTO  -- the measured crossover (DESIGN.md §5): K1 fused SIMT kernel for
+ *   HH_ALGO_AUTO  -- the measured crossover (DESIGN.md §4): K1 fused SIMT kernel for
  *                    small h, K5 compact-WY on the tensor cores for large h when a
- *                    workspace of hh_workspace_bytes(HH_CALL_APPLY, ...) is passed;
+ *                    workspace of hh_workspace_bytes(HH_CALL_APPLY, ...) is passed; the
+ *                    threshold depends on n and on the size n*N (12-19 for n >= 128 at
+ *                    n*N >= 2^27, 17-26 at >= 2^25, 32 below; never K5 for n < 128);
  *   HH_ALGO_FUSED -- always K1 (any dtype);
  *   HH_ALGO_WY    -- always K5 (fp32 only; HH_ERR_WORKSPACE without a workspace,
  *                    HH_ERR_UNSUPPORTED for fp64). */

@@ -23,15 +23,28 @@ thread_local LaunchInfo t_last;
 thread_local bool t_has_last = false;
 thread_local int t_algo = HH_ALGO_AUTO;
 
-// K1 (fused SIMT) vs K5 (compact-WY on tcgen05) crossover in h, fp32 only.
-// Measured on B200: below it the fused kernel's single HBM pass wins.
-int64_t wy_min_h(int64_t n) { return n >= 512 ? 32 : 1 << 30; }
+// K1 (fused SIMT) vs K5 (compact-WY on tcgen05) crossover in h, fp32 only, by n and by the
+// problem size E = n*N elements.  K1 is one HBM pass but its FMA work grows with h; K5 moves
+// ~1.5 passes and its cost is flat in h up to one block (b <= 32), plus a fixed cost of its
+// kernel chain (~55-100 us eager) that only large problems amortise.  Thresholds are the
+// first h where K5 won in the same-box sweep of profiles/r1/crossover_r1.txt:
+// E = 2^28 for the large band, E = 2^25 (the slowest point of its band) for the middle one.
+int64_t wy_min_h(int64_t n, int64_t N) {
+    if (n < 128) return int64_t(1) << 30;
+    const int i = n < 256 ? 0 : n < 512 ? 1 : n < 1024 ? 2 : n < 2048 ? 3 : n < 4096 ? 4 : 5;
+    static const int big[6] = {14, 12, 16, 19, 17, 13};   // E >= 2^27
+    static const int mid[6] = {20, 18, 22, 26, 22, 17};   // 2^25 <= E < 2^27
+    const int64_t E = n * N;
+    if (E >= (int64_t(1) << 27)) return big[i];
+    if (E >= (int64_t(1) << 25)) return mid[i];
+    return 32;   // small problems: K5's fixed cost dominates below h = 32
+}
 
 bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
     if (dtype != HH_F32 || !wy_supported(n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
-    return h >= wy_min_h(n);
+    return h >= wy_min_h(n, N);
 }
 
 // Symmetric apply: the SIMT kernel is FMA-bound from h ~ 11 (AI (8h+1)/8 flop/B vs the

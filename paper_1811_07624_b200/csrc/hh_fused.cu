@@ -80,7 +80,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     const void *fn = full ? v->fn_full : v->fn_ragged;
 
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+                                         static_cast<int>(maxs));
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, v->nt, smem);

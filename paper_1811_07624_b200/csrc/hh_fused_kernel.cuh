@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     constexpr int NU = NT / UT;              // units per CTA
     constexpr int WPU = UT / 32;             // warps per unit
     static_assert(NT % UT == 0, "block must hold whole units");
-    static_assert(NU <= 15, "named barrier ids");
+    static_assert(UT == 32 || NU <= 15, "named barrier ids");
 
     const int tid = threadIdx.x;
     const int unit = tid / UT;
