@@ -60,6 +60,23 @@ def test_workspace_query():
     assert b >= 3 * (64 << 20) + 10 * 1024 * 4
     with pytest.raises(hh.HHError):
         hhpkg.hh_workspace_bytes(7, 16, 1, 1, 0, 0)
+
+
+@pytest.mark.parametrize("n,h,N,wy", [
+    (1024, 10, 262144, False),                      # C2
+    (4096, 12, 65536, False), (4096, 13, 65536, True),   # C5 h=12 stays on K1
+    (2048, 16, 65536, False), (2048, 17, 65536, True),   # E = 2^27: large band
+    (2048, 28, 131072, True),                       # the old n>=512, h>=32 rule kept K1 here
+    (1024, 25, 32768, False), (1024, 26, 32768, True),   # E = 2^25: middle band
+    (1024, 31, 4096, False), (1024, 32, 4096, True),     # small problems: h >= 32
+    (128, 13, 1 << 21, False), (128, 14, 1 << 21, True),
+    (64, 512, 1 << 22, False),                      # n < 128: always K1
+])
+def test_auto_crossover(n, h, N, wy):
+    """HH_ALGO_AUTO's K1/K5 choice (hh_api.cu wy_min_h; thresholds from the same-box sweep in
+    profiles/r1/crossover_r1.txt): the apply workspace is non-zero exactly when K5 is chosen."""
+    ws = hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, n, h, N, 0, 0)
+    assert (ws > 0) == wy, (n, h, N, ws)
     with pytest.raises(hh.HHError):
         hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 0, 1, 1, 0, 0)
 
