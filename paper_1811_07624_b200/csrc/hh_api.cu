@@ -47,14 +47,25 @@ bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
     return h >= wy_min_h(n, N);
 }
 
-// Symmetric apply: the SIMT kernel is FMA-bound from h ~ 11 (AI (8h+1)/8 flop/B vs the
-// ridge 11.4); the tensor-core block program moves 1.5x the bytes of one fused pass, so
-// it wins from h ~ 16.
+// Symmetric apply: K2 does 2h reflectors per column and is FMA-bound from h ~ 5; the
+// tensor-core block program moves ~1.5 passes of X plus a fixed ~100 us (eager) for its kernel
+// chain.  Same-box sweep (profiles/r1/crossover_r1.txt, sym section), bands as in wy_min_h.
+int64_t wy_min_h_sym(int64_t n, int64_t N) {
+    if (n < 256) return int64_t(1) << 30;
+    const int i = n < 512 ? 0 : n < 1024 ? 1 : n < 2048 ? 2 : n < 4096 ? 3 : 4;
+    static const int big[5] = {7, 9, 11, 10, 8};      // E >= 2^27
+    static const int mid[5] = {13, 17, 19, 18, 15};   // 2^25 <= E < 2^27
+    const int64_t E = n * N;
+    if (E >= (int64_t(1) << 27)) return big[i];
+    if (E >= (int64_t(1) << 25)) return mid[i];
+    return 32;
+}
+
 bool use_wy_sym(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
     if (dtype != HH_F32 || !wy_supported(n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
-    return h >= 16 && n >= 256;
+    return h >= wy_min_h_sym(n, N);
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -135,3 +135,16 @@ def test_product_does_not_touch_oracle():
     L = hh.lib()
     assert not hasattr(L, "hh_ref_apply")
     ctypes.CDLL  # keep import used
+
+
+@pytest.mark.parametrize("n,h,N,wy", [
+    (2048, 32, 131072, True),                       # C3
+    (1024, 10, 262144, False), (1024, 11, 262144, True),  # E = 2^28
+    (512, 16, 65536, False), (512, 17, 65536, True),      # E = 2^25
+    (2048, 31, 2048, False), (2048, 32, 2048, True),      # small problems
+    (128, 64, 1 << 21, False),                      # n < 256: always K2
+])
+def test_auto_crossover_sym(n, h, N, wy):
+    """The same for the symmetric apply (hh_api.cu wy_min_h_sym)."""
+    ws = hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, n, h, N, 0, 0)
+    assert (ws > 0) == wy, (n, h, N, ws)
