@@ -142,7 +142,8 @@ hh_status hh_apply(hh_op op, int64_t n, int64_t h, const void *U, const void *X,
  *   scale by lambda, and a Q pass (u_h first).
  *   lambda: n values of dtype (the spectrum s-bar; any sign).
  *   workspace: DEVICE scratch of hh_workspace_bytes(HH_CALL_SYM, n, h, N, 0, dtype)
- *   (0 -> fused SIMT kernel).  For fp32 and h >= 16 (hh_algo AUTO) the block program
+ *   (0 -> fused SIMT kernel).  For fp32 and h past the measured crossover (hh_algo AUTO:
+ *   7-11 for n >= 256 at n*N >= 2^27, 13-19 at >= 2^25, 32 below) the block program
  *   runs on the tensor cores: blocks 1..m-1 as Q_k^T, the last block folded with
  *   diag(lambda) into one project/update pair (Y = Lambda X - [A1 A2][G; G_lambda]),
  *   then blocks m-1..1 as Q_k.
