@@ -7,7 +7,8 @@ namespace {
 // n in (512, 4096]: one 512-thread CTA per SM (16 warps, U staged once per SM) rather than two
 // 256-thread CTAs that each hold a copy of U -- the copy halved the occupancy from h = 11
 // (n = 1024) / h = 7 (n = 2048); same-box sweep: n = 2048, h = 12 0.634 -> 0.469 ms, C5 h=12
-// 0.553 -> 0.534 ms, C2 unchanged (profiles/r1/crossover_r1.txt)
+// 0.553 -> 0.534 ms, C2 unchanged (profiles/r1/crossover_r1.txt); n in (4096, 8192] likewise
+// (two 256-thread units): h = 4 / 8 / 12 0.529 / 1.093 / 1.510 -> 0.384 / 0.815 / 1.133 ms
 const FusedVariant kF32[] = {
     HH_FUSED_VAR(float, 8, 2, 1, 256, "f32_tpc8_ch2_c1"),      // n <= 64
     HH_FUSED_VAR(float, 8, 4, 1, 256, "f32_tpc8_ch4_c1"),      // n <= 128
@@ -16,7 +17,7 @@ const FusedVariant kF32[] = {
     HH_FUSED_VAR(float, 32, 8, 2, 512, "f32_tpc32_ch8_c2"),    // n <= 1024
     HH_FUSED_VAR(float, 64, 8, 2, 512, "f32_tpc64_ch8_c2"),    // n <= 2048
     HH_FUSED_VAR(float, 128, 8, 2, 512, "f32_tpc128_ch8_c2"),  // n <= 4096
-    HH_FUSED_VAR(float, 256, 8, 1, 256, "f32_tpc256_ch8_c1"),  // n <= 8192
+    HH_FUSED_VAR(float, 256, 8, 1, 512, "f32_tpc256_ch8_c1"),  // n <= 8192
 };
 }  // namespace
 
