@@ -31,9 +31,11 @@ thread_local int t_algo = HH_ALGO_AUTO;
 // E = 2^28 for the large band, E = 2^25 (the slowest point of its band) for the middle one.
 int64_t wy_min_h(int64_t n, int64_t N) {
     if (n < 128) return int64_t(1) << 30;
-    const int i = n < 256 ? 0 : n < 512 ? 1 : n < 1024 ? 2 : n < 2048 ? 3 : n < 4096 ? 4 : 5;
-    static const int big[6] = {14, 12, 16, 19, 17, 13};   // E >= 2^27
-    static const int mid[6] = {20, 18, 22, 26, 22, 17};   // 2^25 <= E < 2^27
+    // bands follow K1's variant table (measured at the top n of each band)
+    const int i = n <= 128 ? 0 : n <= 256 ? 1 : n <= 512 ? 2 : n <= 1024 ? 3 : n <= 2048 ? 4
+                : n <= 4096 ? 5 : 6;
+    static const int big[7] = {14, 12, 16, 19, 17, 13, 7};    // E >= 2^27
+    static const int mid[7] = {20, 18, 22, 26, 22, 17, 16};   // 2^25 <= E < 2^27
     const int64_t E = n * N;
     if (E >= (int64_t(1) << 27)) return big[i];
     if (E >= (int64_t(1) << 25)) return mid[i];
@@ -52,7 +54,7 @@ bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
 // chain.  Same-box sweep (profiles/r1/crossover_r1.txt, sym section), bands as in wy_min_h.
 int64_t wy_min_h_sym(int64_t n, int64_t N) {
     if (n < 256) return int64_t(1) << 30;
-    const int i = n < 512 ? 0 : n < 1024 ? 1 : n < 2048 ? 2 : n < 4096 ? 3 : 4;
+    const int i = n <= 256 ? 0 : n <= 512 ? 1 : n <= 1024 ? 2 : n <= 2048 ? 3 : 4;
     static const int big[5] = {7, 9, 11, 10, 8};      // E >= 2^27
     static const int mid[5] = {13, 17, 19, 18, 15};   // 2^25 <= E < 2^27
     const int64_t E = n * N;

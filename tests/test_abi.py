@@ -71,6 +71,8 @@ def test_workspace_query():
     (1024, 31, 4096, False), (1024, 32, 4096, True),     # small problems: h >= 32
     (128, 13, 1 << 21, False), (128, 14, 1 << 21, True),
     (64, 512, 1 << 22, False),                      # n < 128: always K1
+    (8192, 6, 32768, False), (8192, 7, 32768, True),
+    (8192, 15, 4096, False), (8192, 16, 4096, True),
 ])
 def test_auto_crossover(n, h, N, wy):
     """HH_ALGO_AUTO's K1/K5 choice (hh_api.cu wy_min_h; thresholds from the same-box sweep in
