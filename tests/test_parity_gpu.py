@@ -128,6 +128,10 @@ SHAPES = [  # (n, h, N, dtype) spanning every variant, full and ragged chunk cou
     (3000, 5, 64, "f32"), (4096, 12, 70, "f32"), (8192, 4, 20, "f32"), (6000, 40, 9, "f32"),
     (2, 1, 17, "f64"), (64, 6, 333, "f64"), (100, 10, 100, "f64"), (256, 16, 99, "f64"),
     (510, 8, 50, "f64"), (1024, 11, 40, "f64"), (2048, 6, 20, "f64"), (4096, 3, 9, "f64"),
+    # 512-thread variants (n in (512, 8192] fp32, (512, 4096] fp64) over several batches per
+    # unit, ragged n, and the chunked-U ring (n = 8192, h = 9: U does not fit next to X)
+    (1536, 13, 1001, "f32"), (5000, 9, 301, "f32"), (8192, 9, 150, "f32"), (1024, 21, 2000, "f32"),
+    (3000, 7, 517, "f64"), (4096, 5, 200, "f64"),
 ]
 
 
