@@ -205,22 +205,24 @@ def cpu_model():
 
 def time_oracle(c, op, target_s=10.0, max_cols=None):
     """Oracle (as it stands) on a bounded column / pair sample; returns (value GB/s,
-    units/s, seconds, sample description, threads)."""
+    units/s, seconds, sample description, threads, k, out) -- `out` is the oracle's result
+    for the first k units (all of them when the budget allows), reused for parity."""
     import oracle
     threads = oracle.num_threads()
     byts, flops, units = alg_cost(c)
     per_unit_bytes = byts / units
+    res = {}
 
     def run(k):
         t0 = time.perf_counter()
         if c.call == "knn":
-            oracle.knn(c.U, c.d, c.X, c.lam[:k], c.k)
+            res["out"] = oracle.knn(c.U, c.d, c.X, c.lam[:k], c.k)
         elif c.call == "mahalanobis":
-            oracle.mahalanobis(c.U, c.d, c.X, c.ia[:k], c.ib[:k])
+            res["out"] = oracle.mahalanobis(c.U, c.d, c.X, c.ia[:k], c.ib[:k])
         elif c.call == "sym":
-            oracle.sym_apply(c.U, c.lam, c.X[:k])
+            res["out"] = oracle.sym_apply(c.U, c.lam, c.X[:k])
         else:
-            oracle.apply(op, c.U, c.X[:k])   # apply_qr: the oracle's plain apply (same U)
+            res["out"] = oracle.apply(op, c.U, c.X[:k])   # apply_qr: the plain apply (same U)
         return time.perf_counter() - t0
 
     total = units
@@ -237,7 +239,44 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
         k = k2
     what = {"mahalanobis": "pairs", "knn": "queries"}.get(c.call, "columns")
     return (per_unit_bytes * k / dt / 1e9, k / dt, dt,
-            f"{k} of {total} {what} of {c.name} (fp64 oracle, {threads} threads)", threads)
+            f"{k} of {total} {what} of {c.name} (fp64 oracle, {threads} threads)", threads, k,
+            res["out"])
+
+
+def parity_of(c, k, ref, Y, dist_out, knn_out, dev):
+    """Parity of the GPU result against the oracle's output for the first k units (the
+    cpu_baseline run's own output): whole relative l2 error and the per-unit maximum, gated
+    like tests/test_fullsize_gpu.py."""
+    import torch
+    g = 1e-12 if c.dtype == "f64" else 2e-5 * math.sqrt(max(c.h, 1))
+    if c.call == "knn":
+        ri, rd = ref
+        gi_, gd_ = knn_out
+        got = gd_[:k].double().cpu().numpy()
+        e = float(np.linalg.norm(got - rd) / np.linalg.norm(rd))
+        return {"rel_l2_dist": e, "index_agreement": float((gi_[:k].cpu().numpy() == ri).mean()),
+                "gate": g, "sampled": int(k), "of": int(c.lam.shape[0]),
+                "pass": bool(e <= g)}
+    if c.call == "mahalanobis":
+        got = dist_out[:k].double().cpu().numpy()
+        e = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        pos = ref > 0
+        worst = float(np.max(np.abs(got[pos] - ref[pos]) / ref[pos]))
+        return {"rel_fro": e, "max_unit_rel": worst, "gate": g, "sampled": int(k),
+                "of": int(c.npairs), "pass": bool(e <= g and worst <= g)}
+    sd = sr = worst = 0.0
+    for j0 in range(0, k, 16384):
+        gg = Y[j0:min(k, j0 + 16384)].double().cpu().numpy()
+        rr = ref[j0:j0 + gg.shape[0]]
+        dcol = np.sqrt(((gg - rr) ** 2).sum(1))
+        rcol = np.sqrt((rr * rr).sum(1))
+        sd += float((dcol ** 2).sum())
+        sr += float((rcol ** 2).sum())
+        worst = max(worst, float(np.max(dcol / np.where(rcol > 0, rcol, 1.0))))
+    e = math.sqrt(sd / sr)
+    return {"rel_fro": e, "max_unit_rel": worst, "gate": g, "sampled": int(k), "of": int(c.N),
+            "finite": bool(torch.isfinite(Y).all().item()),
+            "pass": bool(e <= g and worst <= g and torch.isfinite(Y).all().item())}
 
 
 def run_reference(args):
@@ -252,7 +291,7 @@ def run_reference(args):
     _, _, units = alg_cost(c)
     byts, _, _ = alg_cost(c)
     # calibrate the sample size for ~budget seconds per step
-    _, ups, _, _, threads = time_oracle(c, op, target_s=min(2.0, budget))
+    _, ups, _, _, threads, _, _ = time_oracle(c, op, target_s=min(2.0, budget))
     k = int(max(1, min(units, ups * budget)))
     sub = workload_case(args.workload, N_override=None)
     per_unit_bytes = byts / units
@@ -332,6 +371,7 @@ def run_hh(args):
         wsb = hh.hh_workspace_bytes(hh.HH_CALL_KNN, c.n, c.h, c.N, Pq.shape[0], X.dtype)
         wsp = torch.empty(wsb, dtype=torch.uint8, device=dev)
         knn_out = {}
+        dist_out = None
 
         def step():
             knn_out["r"] = hh.hh_knn(U, d, X, Pq, c.k, workspace=wsp, stream=stream)
@@ -347,6 +387,7 @@ def run_hh(args):
         ia = torch.from_numpy(c.ia).to(dev)
         ib = torch.from_numpy(c.ib).to(dev)
         dist_out = torch.empty(c.npairs, dtype=X.dtype, device=dev)
+        knn_out = {}
         wsb = hh.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, c.n, c.h, c.N, c.npairs, X.dtype)
         wsp = torch.empty(wsb, dtype=torch.uint8, device=dev)
         step = lambda: hh.hh_mahalanobis(U, d, X, ia, ib, dist_out, workspace=wsp,  # noqa: E731
@@ -379,34 +420,6 @@ def run_hh(args):
     info = hh.last_launch_info()
     wy_path = str(info.get("variant", "")).startswith("wy_")
     launches = int(info.get("launches") or launches)   # the library's own count per step
-
-    # quick sampled parity against the oracle (rank 0; outside the timed region)
-    parity = None
-    if rank == 0 and not args.no_parity:
-        import oracle
-        if c.call == "knn":
-            idx = np.linspace(0, c.lam.shape[0] - 1, 64).astype(np.int64)
-            gi_, gd_ = knn_out["r"]
-            got = gd_[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
-            ri, ref = oracle.knn(c.U, c.d, c.X, c.lam[idx], c.k)
-            extra["knn_index_agreement"] = float(
-                (gi_[torch.from_numpy(idx).to(dev)].cpu().numpy() == ri).mean())
-        elif c.call in ("apply", "apply_qr"):
-            idx = np.linspace(0, c.N - 1, 256 if c.h < 2048 else 16).astype(np.int64)
-            got = Y[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
-            ref = oracle.apply(op, c.U, c.X[idx])
-        elif c.call == "sym":
-            idx = np.linspace(0, c.N - 1, 64).astype(np.int64)
-            got = Y[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
-            ref = oracle.sym_apply(c.U, c.lam, c.X[idx])
-        else:
-            idx = np.linspace(0, c.npairs - 1, 4096).astype(np.int64)
-            got = dist_out[torch.from_numpy(idx).to(dev)].double().cpu().numpy()
-            ref = oracle.mahalanobis(c.U, c.d, c.X, c.ia[idx], c.ib[idx])
-        e = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
-        parity = {"rel_fro": e, "gate": (1e-12 if c.dtype == "f64" else 2e-5 * math.sqrt(c.h)),
-                  "sampled": int(len(idx)), "pass": bool(e <= (1e-12 if c.dtype == "f64"
-                                                               else 2e-5 * math.sqrt(c.h)))}
 
     sampler = ClockSampler(dev.index if dev.index is not None else 0).start()
     time.sleep(0.3)
@@ -495,6 +508,23 @@ def run_hh(args):
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
                 "frac_of_8TBps": achieved / 8000.0,
                 "kernel": info.get("variant"), "launch": info}
+        # the algorithmic roofline is max(bytes / HBM peak, flops / pipe peak);
+        # the SIMT FP32 (FP64) pipe peak is #SM x 128 (64) FMA lanes x 2 x the maximum SM
+        # clock (R13).  When the flops floor is the larger one (C4's transform-once
+        # reading: 4.43 GFLOP vs 159 MB), the line reports the ALU bound.
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        fmax = float(peaks()[2].get("sm_max_mhz", 1965.0)) * 1e6 if peaks()[2] else 1.965e9
+        alu_peak = sms * (128 if c.dtype == "f32" else 64) * 2 * fmax / 1e12   # TFLOP/s
+        t_hbm_s, t_alu_s = byts / (hbm * 1e9), flops / (alu_peak * 1e12)
+        if t_alu_s > t_hbm_s and not wy_path and c.call != "knn":
+            roof = {"bound": "alu", "achieved": flops / (ms_step * 1e-3) / 1e12,
+                    "peak": alu_peak, "unit": "TFLOP/s",
+                    "frac": t_alu_s / (ms_step * 1e-3), "traffic": traffic,
+                    "peak_source": f"derived: {sms} SMs x {128 if c.dtype == 'f32' else 64} "
+                                   f"FMA lanes x 2 x {fmax / 1e6:.0f} MHz (DESIGN.md R13)",
+                    "hbm_frac": achieved / hbm, "hbm_floor_ms": 1e3 * t_hbm_s,
+                    "alu_floor_ms": 1e3 * t_alu_s,
+                    "kernel": info.get("variant"), "launch": info}
         if str(info.get("variant", "")).startswith("knn_"):
             pk = peaks()[2]
             tpeak = float(pk.get("bf16_tflops", 1590.0)) if pk else 1590.0
@@ -556,10 +586,18 @@ def run_hh(args):
                          "launch": info, "passes": npass,
                          "scope": "whole step (K4 prep + all K5 launches)"})
         cpu = None
-        if not args.no_cpu_baseline and ws == 1:
-            v, ups, secs, sample, thr = time_oracle(c, op, target_s=args.cpu_seconds)
-            cpu = {"value": v, "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": sample,
-                   "seconds": secs, "vectors_per_s": ups, "cpu": cpu_model()}
+        parity = None
+        if not (args.no_cpu_baseline and args.no_parity):
+            # the oracle as it stands on the host cores (cpu_baseline, rank 0 at N = 1), and
+            # the parity of this run's output against that same oracle output
+            v, ups, secs, sample, thr, k_or, ref = time_oracle(
+                c, op, target_s=args.cpu_seconds if not args.no_cpu_baseline else 2.0)
+            if not args.no_cpu_baseline and ws == 1:
+                cpu = {"value": v, "unit": "GB/s", "cores": thr, "kind": "oracle",
+                       "sample": sample, "seconds": secs, "vectors_per_s": ups, "cpu": cpu_model()}
+            if not args.no_parity:
+                parity = parity_of(c, k_or, ref, Y, dist_out if c.call == "mahalanobis" else None,
+                                   knn_out.get("r") if c.call == "knn" else None, dev)
         if not args.ncu and roof is not None:
             roof["same_run_copy_gbs"] = same_run_copy_gbs(dev)
         out = {

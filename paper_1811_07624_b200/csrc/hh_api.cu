@@ -43,7 +43,7 @@ int64_t wy_min_h(int64_t n, int64_t N) {
 }
 
 bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
-    if (dtype != HH_F32 || !wy_supported(n, h, N)) return false;
+    if (dtype != HH_F32 || !wy_supported(WY_APPLY_N, n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
     return h >= wy_min_h(n, N);
@@ -64,11 +64,21 @@ int64_t wy_min_h_sym(int64_t n, int64_t N) {
 }
 
 bool use_wy_sym(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
-    if (dtype != HH_F32 || !wy_supported(n, h, N)) return false;
+    if (dtype != HH_F32 || !wy_supported(WY_SYM, n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
     return h >= wy_min_h_sym(n, N);
 }
+
+// HH_ALGO_WY forces the tensor-core program: a shape it cannot run (fp64, n < 32, more than
+// kMaxPasses block passes, ...) is an error, never a silent switch to the SIMT kernel
+bool wy_forced_unsupported(int kind, hh_dtype dtype, int64_t n, int64_t h, int64_t N) {
+    return t_algo == HH_ALGO_WY && h > 0 && N > 0 &&
+           (dtype != HH_F32 || !wy_supported(kind, n, h, N));
+}
+
+// the bucketed Mahalanobis path indexes pairs and points with int32
+constexpr int64_t kMaxPairs = (int64_t(1) << 31) - 1;
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 size_t elem(hh_dtype dt) { return dt == HH_F32 ? 4 : 8; }
@@ -170,7 +180,8 @@ int hh_debug_wy_ts_min(int kw) { return wy_set_ts_min(kw); }
 hh_status hh_debug_wy_project(int op, int64_t n, int64_t h, const void *U, const void *X,
                               int64_t N, void *workspace, size_t workspace_bytes, int64_t *off,
                               hh_stream_t stream) {
-    if (!wy_supported(n, h, N) || !workspace || !off) return HH_ERR_INVALID_VALUE;
+    if (!wy_supported(op ? WY_APPLY_T : WY_APPLY_N, n, h, N) || !workspace || !off)
+        return HH_ERR_INVALID_VALUE;
     const WyPlan p = wy_plan(op ? WY_APPLY_T : WY_APPLY_N, n, h, N);
     if (workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
     off[0] = static_cast<int64_t>(p.off_gt);
@@ -214,6 +225,7 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
                                                             : 0;
             return HH_OK;
         case HH_CALL_MAHALANOBIS:
+            if (npairs >= kMaxPairs || N_or_M >= kMaxPairs) return HH_ERR_UNSUPPORTED;
             *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype)) +
                      bucket_ws_bytes(N_or_M, npairs);
             return HH_OK;
@@ -233,7 +245,10 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
             const size_t ub = round256(static_cast<size_t>(n) * static_cast<size_t>(h) * elem(dtype));
             const int64_t cols = host_chunk_cols(n, std::max<int64_t>(N_or_M, 1), dtype);
             const size_t slot = round256(static_cast<size_t>(cols) * n * elem(dtype));
-            *bytes = ub + kRing * slot;
+            // past the crossover each chunk runs the compact-WY program (its own scratch)
+            const size_t wyb = (h > 0 && use_wy(dtype, n, h, cols, t_algo))
+                                   ? round256(wy_plan(WY_APPLY_N, n, h, cols).bytes) : 0;
+            *bytes = ub + kRing * slot + wyb;
             return HH_OK;
         }
     }
@@ -261,6 +276,7 @@ static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const
     if (!aligned16(X) || !aligned16(Y)) return HH_ERR_UNSUPPORTED;
     if (dside && !dsign) return HH_ERR_INVALID_VALUE;
     if (dside && !aligned16(dsign)) return HH_ERR_UNSUPPORTED;
+    if (wy_forced_unsupported(WY_APPLY_N, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
     if (h > 0 && use_wy(dtype, n, h, N, t_algo)) {
         WyPlan p = wy_plan(op == HH_OP_T ? WY_APPLY_T : WY_APPLY_N, n, h, N);
         p.qr = qr;
@@ -327,6 +343,7 @@ static hh_status sym_impl(int64_t n, int64_t h, const void *U, const void *lambd
     if (!X || !Y || !lambda) return HH_ERR_INVALID_VALUE;
     if (!aligned16(X) || !aligned16(Y) || !aligned16(lambda)) return HH_ERR_UNSUPPORTED;
     if (dsign && !aligned16(dsign)) return HH_ERR_UNSUPPORTED;
+    if (wy_forced_unsupported(WY_SYM, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
     if (h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
         const WyPlan p = wy_plan(WY_SYM, n, h, N);
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
@@ -381,6 +398,7 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
                          hh_stream_t stream) {
     if (npairs < 0 || M < 0) return HH_ERR_INVALID_VALUE;
     if (npairs > 0 && M < 1) return HH_ERR_INVALID_VALUE;
+    if (npairs >= kMaxPairs || M >= kMaxPairs) return HH_ERR_UNSUPPORTED;
     hh_status st = check_common(n, h, U, M, dtype);
     if (st != HH_OK) return st;
     if (npairs == 0) return HH_OK;
@@ -516,6 +534,8 @@ hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host, cons
     char *ws = static_cast<char *>(workspace);
     char *Ud = ws;
     char *slots = ws + ub;
+    char *wyws = slots + kRing * slotB;
+    const size_t wyb = need - (ub + kRing * slotB);   // compact-WY scratch (0: fused path)
 
     cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
     cudaEvent_t start = nullptr, ev_in[kRing] = {}, ev_cp[kRing] = {}, ev_out[kRing] = {};
@@ -552,15 +572,11 @@ hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host, cons
                                 cudaMemcpyHostToDevice, sh));
             chk(cudaEventRecord(ev_in[r], sh));
             chk(cudaStreamWaitEvent(sc, ev_in[r], 0));
-            FusedArgs a{};
-            a.U = Ud;
-            a.X = slot;
-            a.Y = slot;
-            a.n = n;
-            a.h = h;
-            a.N = cc;
-            a.mode = op == HH_OP_N ? MODE_APPLY_N : MODE_APPLY_T;
-            if (e == cudaSuccess) kst = run_fused(a, dtype, sc);
+            // the same path selection as hh_apply on a device chunk (K1, or the compact-WY
+            // program past the crossover, with its scratch after the ring)
+            if (e == cudaSuccess)
+                kst = apply_impl(op, n, h, Ud, slot, slot, cc, dtype, wyb ? wyws : nullptr, wyb,
+                                 sc, nullptr, 0);
             chk(cudaEventRecord(ev_cp[r], sc));
             chk(cudaStreamWaitEvent(sd, ev_cp[r], 0));
             chk(cudaMemcpyAsync(static_cast<char *>(Y_host) + c0 * colB, slot, bytes,

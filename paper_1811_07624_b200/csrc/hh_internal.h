@@ -80,7 +80,7 @@ struct WyPlan {
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N);
 void wy_set_timeline(unsigned long long *buf);   // debug: per-role barrier wait cycles
 int wy_set_ts_min(int kw);                       // test: TS-mode update threshold (prev.)
-bool wy_supported(int64_t n, int64_t h, int64_t N);
+bool wy_supported(int kind, int64_t n, int64_t h, int64_t N);   // incl. the pass cap
 // Y = Q X / Q^T X / Q diag(lam) Q^T X by the compact-WY block program (fp32 in/out).
 // debug_stop_blocks >= 0: run the preparation and only the first projection (test hook).
 // dsign/dside: optional diagonal D (bit 0: right factor, D applied first; bit 1: left

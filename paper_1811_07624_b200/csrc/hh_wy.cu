@@ -41,6 +41,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "hh_internal.h"
 #include "hh_tc.cuh"
@@ -64,7 +65,8 @@ constexpr int kStage3Bytes = 16384;  // V hi/lo tile (128 rows x 32 bf16) x 2
 constexpr int kGresBytes = 131072;   // resident G hi/lo (128 x 256 bf16) x 2 at b = 256 (max)
 constexpr int kSmemMax = 232448;     // 227 KB opt-in per CTA
 constexpr int kKChunk1 = 8;          // K5a schedule unit: 8 K steps (256 rows of X)
-constexpr int kSlots1 = 256;         // K5a split-tile hand-off slots (>= the grid)
+constexpr int kSlots1 = 256;         // K5a split-tile hand-off pairs (>= the grid)
+constexpr int kMaxPasses = 128;      // block-program passes (h <= 32768 apply, 8192 sym)
 
 size_t al(size_t x) { return (x + 1023) & ~static_cast<size_t>(1023); }
 
@@ -759,67 +761,77 @@ __global__ void __launch_bounds__(480, 1)
         uint32_t aph = 0;
         uint16_t *Glo = Gt + N * b;
         const int jl = q * 32 + lane;
+        __shared__ int s_last;
         for_segments([&](int tile, int, int, bool head, bool tail) {
             mbar_wait(&bars->acc_full[a], aph);
             tc::fence_after_sync();
             const int64_t j = static_cast<int64_t>(tile) * kTileCols + jl;
-            if (tail) {
-                // wait for the next CTA's partial of this tile (it computed it first thing)
+            // A tile cut by a range boundary has two owners: this CTA's tail segment (its
+            // leading K chunks) and the next CTA's head segment (its trailing chunks).  The
+            // hand-off pair (slot pair + arrival counter) is indexed by the boundary: blockIdx
+            // for a tail, blockIdx - 1 for a head.  Each owner publishes its fp32 partial in
+            // its own slot and counts itself in; the second to arrive adds the other's partial
+            // (sum = leading + trailing in both cases: deterministic) and writes G.  Nobody
+            // waits, so the protocol needs no co-residency.
+            const bool split = head || tail;
+            const size_t hp = static_cast<size_t>(head ? blockIdx.x - 1 : blockIdx.x);
+            float *mine = part + (2 * hp + (head ? 1 : 0)) * kTileCols * b;
+            const float *other = part + (2 * hp + (head ? 0 : 1)) * kTileCols * b;
+            float v[32];
+            if (split) {
+                for (int c = 0; c < b / 32; ++c) {
+                    tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                      static_cast<uint32_t>(a * 256 + c * 32),
+                                  v);
+                    float *dst = mine + (static_cast<size_t>(c) * kTileCols + jl) * 32;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) st_cg4(dst + 4 * e, v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+                }
+                __threadfence();
+                named_bar_sync(1, 128);
                 if (jl == 0) {
-                    volatile int *f = flag + blockIdx.x;
-                    // the partner CTA is co-resident (grid <= SMs) and produces this first
-                    // thing; a missing hand-off is a bug: trap rather than hang
-                    for (uint32_t it = 0; *f == 0; ++it) {
-                        if (it > (1u << 24)) __trap();
-                        __nanosleep(256);
-                    }
+                    const int prev = atomicAdd(flag + hp, 1);
+                    s_last = prev == 1;
+                    if (prev == 1) flag[hp] = 0;   // both arrived: reset for the next launch
                     __threadfence();
                 }
                 named_bar_sync(1, 128);
             }
-            float *slot_w = part + (static_cast<size_t>(blockIdx.x) - 1) * kTileCols * b;   // head
-            const float *slot_r = part + static_cast<size_t>(blockIdx.x) * kTileCols * b;  // tail
-            for (int c = 0; c < b / 32; ++c) {
-                float v[32];
-                tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                                  static_cast<uint32_t>(a * 256 + c * 32),
-                              v);
-                if (head) {
-                    float *dst = slot_w + (static_cast<size_t>(c) * kTileCols + jl) * 32;
+            if (!split || s_last) {
+                for (int c = 0; c < b / 32; ++c) {
+                    if (split) {
+                        // leading + trailing, in that order whichever side finishes
+                        const float *lead = head ? other : mine;
+                        const float *trail = head ? mine : other;
+                        const float *s0 = lead + (static_cast<size_t>(c) * kTileCols + jl) * 32;
+                        const float *s1 = trail + (static_cast<size_t>(c) * kTileCols + jl) * 32;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) st_cg4(dst + 4 * e, v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-                    continue;
-                }
-                if (tail) {
-                    const float *src = slot_r + (static_cast<size_t>(c) * kTileCols + jl) * 32;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float4 pv = ld_cg4(src + 4 * e);
-                        v[4 * e] += pv.x;
-                        v[4 * e + 1] += pv.y;
-                        v[4 * e + 2] += pv.z;
-                        v[4 * e + 3] += pv.w;
+                        for (int e = 0; e < 8; ++e) {
+                            const float4 p0 = ld_cg4(s0 + 4 * e), p1 = ld_cg4(s1 + 4 * e);
+                            v[4 * e] = p0.x + p1.x;
+                            v[4 * e + 1] = p0.y + p1.y;
+                            v[4 * e + 2] = p0.z + p1.z;
+                            v[4 * e + 3] = p0.w + p1.w;
+                        }
+                    } else {
+                        tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                          static_cast<uint32_t>(a * 256 + c * 32),
+                                      v);
                     }
-                }
-                if (j < N) {
-                    uint32_t H[16], L[16];
+                    if (j < N) {
+                        uint32_t H[16], L[16];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
-                    uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
-                    uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
+                        for (int e = 0; e < 16; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
+                        uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
+                        uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
-                        gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
+                        for (int e = 0; e < 4; ++e) {
+                            gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
+                            gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
+                        }
                     }
                 }
             }
-            if (head) {
-                __threadfence();
-                named_bar_sync(1, 128);
-                if (jl == 0) atomicExch(flag + blockIdx.x - 1, 1);
-            }
-            if (tail && jl == 0) flag[blockIdx.x] = 0;   // ready for the next launch
             tc::fence_before_sync();
             tc::mbar_arrive(&bars->acc_empty[a]);
             if (++a == 2) {
@@ -1459,21 +1471,26 @@ size_t smem3(int kv) {
            static_cast<size_t>(nxs_for(kv)) * kXBoxBytes + sizeof(Bars3) + 1024;
 }
 
-std::once_flag g_attr_once;
-unsigned long long *g_timeline = nullptr;   // debug: hh_debug_wy_timeline
-cudaError_t g_attr_err = cudaSuccess;
+// per-device opt-in of the large dynamic shared memory (the attribute belongs to each
+// device's context): one flag and result per device
+constexpr int kMaxDevWy = 64;
+std::once_flag g_attr_once[kMaxDevWy];
+cudaError_t g_attr_err[kMaxDevWy];
+// debug / test hooks, per calling thread (like hh_set_algo): no process-global mutable state
+thread_local unsigned long long *t_timeline = nullptr;   // hh_debug_wy_timeline
+thread_local int t_ts_min = 256;                         // hh_debug_wy_ts_min
 
 }  // namespace
 
-void wy_set_timeline(unsigned long long *buf) { g_timeline = buf; }
+void wy_set_timeline(unsigned long long *buf) { t_timeline = buf; }
 
-// TS-mode update from this block width on (default 256; HH_WY_TS_MIN or the test hook
-// hh_debug_wy_ts_min override it)
-std::atomic<int> g_ts_min{[] {
-    const char *e = std::getenv("HH_WY_TS_MIN");
-    return e ? std::atoi(e) : 256;
-}()};
-int wy_set_ts_min(int kw) { return g_ts_min.exchange(kw); }
+// TS-mode update from this block width on (default 256; the test hook hh_debug_wy_ts_min
+// lowers it for the calling thread)
+int wy_set_ts_min(int kw) {
+    const int prev = t_ts_min;
+    t_ts_min = kw;
+    return prev;
+}
 
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     WyPlan p{};
@@ -1517,16 +1534,24 @@ WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     }
     const int kmax = kind == WY_SYM ? 2 * p.b : p.b;
     p.off_gt = take(static_cast<size_t>(std::max<int64_t>(N, 1)) * kmax * 2 * 2);
-    p.off_part = take(static_cast<size_t>(kSlots1) * kTileCols * kmax * 4);   // K5a hand-off
+    // K5a split-tile hand-off: a slot pair (leading / trailing partial) per CTA boundary
+    const int64_t ntl = (N + kTileCols - 1) / kTileCols;
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>({ntl, device_attr().sm_count, kSlots1}));
+    p.off_part = take(static_cast<size_t>(2 * pairs) * kTileCols * kmax * 4);
     p.off_flag = take(static_cast<size_t>(kSlots1) * 4);
     p.bytes = off;
     return p;
 }
 
-bool wy_supported(int64_t n, int64_t h, int64_t N) {
+bool wy_supported(int kind, int64_t n, int64_t h, int64_t N) {
     // TMA coordinates are int32; G rows are addressed as 2N
-    return n >= 32 && n % 4 == 0 && h >= 1 && N >= 1 && 2 * N < (int64_t(1) << 31) &&
-           n <= (int64_t(1) << 20);
+    if (!(n >= 32 && n % 4 == 0 && h >= 1 && N >= 1 && 2 * N < (int64_t(1) << 31) &&
+          n <= (int64_t(1) << 20)))
+        return false;
+    // the block program has at most kMaxPasses passes: m blocks (apply) or 2m - 1 (sym)
+    const int64_t bmax = kind == WY_SYM ? 128 : 256;
+    const int64_t m = (h + bmax - 1) / bmax;
+    return (kind == WY_SYM ? 2 * m - 1 : m) <= kMaxPasses;
 }
 
 namespace {
@@ -1549,31 +1574,30 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                       void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks,
                       const float *dsign, int dside) {
     if (!encoder()) return cudaErrorNotSupported;
-    std::call_once(g_attr_once, []() {
-        g_attr_err = cudaFuncSetAttribute(wy_project_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-        if (g_attr_err == cudaSuccess)
-            g_attr_err = cudaFuncSetAttribute(wy_vrec_kernel<2>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(vrec_smem(256)));
-        if (g_attr_err == cudaSuccess)
-            g_attr_err = cudaFuncSetAttribute(wy_vrec_kernel<1>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(vrec_smem(256)));
-        if (g_attr_err == cudaSuccess)
-            g_attr_err = cudaFuncSetAttribute(wy_tbuild_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(tbuild_smem(256)));
-        if (g_attr_err == cudaSuccess)
-            g_attr_err = cudaFuncSetAttribute(wy_update_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              kSmemMax);
-        if (g_attr_err == cudaSuccess)
-            g_attr_err = cudaFuncSetAttribute(wy_update_ts_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              kSmemMax);
+    if (!wy_supported(p.kind, p.n, p.h, p.N)) return cudaErrorNotSupported;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevWy) return cudaErrorInvalidDevice;
+    std::call_once(g_attr_once[dev], [dev]() {
+        cudaError_t &err = g_attr_err[dev];
+        err = cudaFuncSetAttribute(wy_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemMax);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_vrec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(vrec_smem(256)));
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_vrec_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(vrec_smem(256)));
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_tbuild_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(tbuild_smem(256)));
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemMax);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_update_ts_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
     });
-    if (g_attr_err != cudaSuccess) return g_attr_err;
+    if (g_attr_err[dev] != cudaSuccess) return g_attr_err[dev];
     const bool sym = p.kind == WY_SYM;
     if (sym && !lam) return cudaErrorInvalidValue;
     int nlaunch = 0;   // kernels enqueued by this call (reported through LaunchInfo)
@@ -1695,7 +1719,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     if (!ok) return cudaErrorNotSupported;
 
     // ---------------- the block program
-    Pass prog[2 * 64];
+    std::vector<Pass> prog(static_cast<size_t>(sym ? 2 * m - 1 : m));   // <= kMaxPasses
     int np = 0;
     auto blockpass = [&](int k, const CUtensorMap *mv) {
         Pass ps{k * b, b, &mWb, &mGb, mv, static_cast<int>(k * n_pad),
@@ -1739,7 +1763,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
 
     const int ntiles = static_cast<int>((N + kTileCols - 1) / kTileCols);
     const int grid = std::max(1, std::min(std::min(ntiles, sms), kSlots1));
-    // K5a hand-off flags start at zero (each tail resets its flag after use)
+    // K5a hand-off counters start at zero (the second arrival resets its counter)
     e = cudaMemsetAsync(w + p.off_flag, 0, static_cast<size_t>(kSlots1) * 4, stream);
     if (e != cudaSuccess) return e;
     const float *cur = X;
@@ -1756,11 +1780,11 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         const int grid3 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, sms)));
         // TS-mode update (G in TMEM) for the wide blocks: the resident G no longer competes
         // with the V and X rings for shared memory
-        if (ps.kw >= g_ts_min.load(std::memory_order_relaxed)) {
+        if (ps.kw >= t_ts_min) {
             ++nlaunch, wy_update_ts_kernel<<<grid3, 640, smem4(), stream>>>(
                 Gt, *ps.mV, (cur == X) ? mXb2 : mYb2, mYb2, ps.pre, ps.post, static_cast<int>(p.n),
                 static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
-                ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, g_timeline);
+                ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, t_timeline);
             cur = Y;
             continue;
         }
@@ -1768,7 +1792,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
             ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw),
-            g_timeline);
+            t_timeline);
         cur = Y;
     }
     if (info) {

@@ -124,9 +124,10 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream(stream) -> ctypes.c_void_p:
+def _stream(stream, device=None) -> ctypes.c_void_p:
+    """The given stream, else the current stream of the operands' device."""
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
 
 
@@ -141,6 +142,64 @@ def _dtype(t: torch.Tensor) -> int:
     if t.dtype not in _DT:
         raise ValueError(f"unsupported dtype {t.dtype}")
     return _DT[t.dtype]
+
+
+def _validate(X: torch.Tensor, xname: str = "X", U: Optional[torch.Tensor] = None,
+              same: dict = None, vecs: dict = None, host: bool = False) -> tuple:
+    """Check every operand against X before anything reaches libhh.so: X is a contiguous
+    2-D (N, n) float tensor; U is (h, n) (or empty) of X's dtype; every tensor in `same`
+    has X's shape and dtype; every tensor in `vecs` is n values of X's dtype; all of them
+    contiguous and on X's device (CUDA, or the host for hh_apply_host).  Returns (N, n, h)."""
+    if X.dim() != 2:
+        raise ValueError(f"{xname} must be 2-D (N, n), got shape {tuple(X.shape)}")
+    _dtype(X)
+    N, n = X.shape
+
+    def where(t, name):
+        if host:
+            if t.is_cuda:
+                raise ValueError(f"{name} must be a host tensor for hh_apply_host")
+            if not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+        else:
+            _dev(t, name)
+            if t.device != X.device:
+                raise ValueError(f"{name} is on {t.device}, {xname} on {X.device}")
+
+    where(X, xname)
+    h = 0
+    if U is not None and U.numel():
+        if U.dim() != 2 or U.shape[1] != n:
+            raise ValueError(f"U must be (h, {n}), got {tuple(U.shape)}")
+        if U.dtype != X.dtype:
+            raise ValueError(f"U dtype {U.dtype} != {xname} dtype {X.dtype}")
+        where(U, "U")
+        h = U.shape[0]
+    for name, t in (same or {}).items():
+        if tuple(t.shape) != (N, n) or t.dtype != X.dtype:
+            raise ValueError(f"{name} must be {(N, n)} {X.dtype}, got {tuple(t.shape)} {t.dtype}")
+        where(t, name)
+    for name, t in (vecs or {}).items():
+        if t.numel() != n or t.dtype != X.dtype:
+            raise ValueError(f"{name} must hold {n} values of {X.dtype}, got {t.numel()} {t.dtype}")
+        where(t, name)
+    return N, n, h
+
+
+def _workspace(call: int, n: int, h: int, N_or_M: int, npairs: int, like: torch.Tensor,
+               workspace: Optional[torch.Tensor]):
+    """(workspace tensor or None, bytes to pass): the query's size, allocated on `like`'s
+    device when not given or too small; a given workspace must be on that device."""
+    wsb = hh_workspace_bytes(call, n, h, N_or_M, npairs, like.dtype)
+    if not wsb:
+        return None, 0
+    if workspace is not None:
+        _dev(workspace, "workspace")
+        if workspace.device != like.device:
+            raise ValueError(f"workspace is on {workspace.device}, operands on {like.device}")
+    if workspace is None or workspace.numel() * workspace.element_size() < wsb:
+        workspace = torch.empty(wsb, dtype=torch.uint8, device=like.device)
+    return workspace, workspace.numel() * workspace.element_size()
 
 
 def hh_set_algo(algo: int) -> None:
@@ -193,20 +252,13 @@ def hh_apply(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor
 
     The workspace the selected path needs (hh_workspace_bytes) is allocated on the
     tensors' device when not given."""
-    _dev(X, "X")
-    N, n = X.shape
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
     if Y is None:
         Y = torch.empty_like(X)
-    _dev(Y, "Y")
-    wsb = hh_workspace_bytes(HH_CALL_APPLY, n, h, N, 0, X.dtype) if N else 0
-    if wsb and (workspace is None or workspace.numel() < wsb):
-        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
-    st = lib().hh_apply(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N, _dtype(X),
-                        _ptr(workspace) if wsb else None, workspace.numel() if wsb else 0,
-                        _stream(stream))
+    N, n, h = _validate(X, U=U, same={"Y": Y})
+    with torch.cuda.device(X.device):
+        ws, wsb = _workspace(HH_CALL_APPLY, n, h, N, 0, X, workspace) if N else (None, 0)
+        st = lib().hh_apply(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,
+                            _dtype(X), _ptr(ws), wsb, _stream(stream, X.device))
     _check(st, "hh_apply")
     return Y
 
@@ -216,21 +268,13 @@ def hh_sym_apply(U: torch.Tensor, lam: torch.Tensor, X: torch.Tensor,
                  stream=None) -> torch.Tensor:
     """Y = Q diag(lam) Q^T X (hh.h: hh_sym_apply); allocates the workspace the selected
     path needs when not given."""
-    _dev(X, "X")
-    _dev(lam, "lambda")
-    N, n = X.shape
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
     if Y is None:
         Y = torch.empty_like(X)
-    _dev(Y, "Y")
-    wsb = hh_workspace_bytes(HH_CALL_SYM, n, h, N, 0, X.dtype) if N else 0
-    if wsb and (workspace is None or workspace.numel() < wsb):
-        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
-    st = lib().hh_sym_apply(n, h, _ptr(U) if h else None, _ptr(lam), _ptr(X), _ptr(Y), N,
-                            _dtype(X), _ptr(workspace) if wsb else None,
-                            workspace.numel() if wsb else 0, _stream(stream))
+    N, n, h = _validate(X, U=U, same={"Y": Y}, vecs={"lambda": lam})
+    with torch.cuda.device(X.device):
+        ws, wsb = _workspace(HH_CALL_SYM, n, h, N, 0, X, workspace) if N else (None, 0)
+        st = lib().hh_sym_apply(n, h, _ptr(U) if h else None, _ptr(lam), _ptr(X), _ptr(Y), N,
+                                _dtype(X), _ptr(ws), wsb, _stream(stream, X.device))
     _check(st, "hh_sym_apply")
     return Y
 
@@ -240,21 +284,14 @@ def hh_apply_signed(op: int, side: int, U: torch.Tensor, d: torch.Tensor, X: tor
                     stream=None) -> torch.Tensor:
     """Y = D op(Q) X (side HH_SIDE_LEFT, Eq. 1) or op(Q) D X (HH_SIDE_RIGHT, Result 3)
     (hh.h: hh_apply_signed)."""
-    _dev(X, "X")
-    _dev(d, "d")
-    N, n = X.shape
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
     if Y is None:
         Y = torch.empty_like(X)
-    _dev(Y, "Y")
-    wsb = hh_workspace_bytes(HH_CALL_APPLY, n, h, N, 0, X.dtype) if N else 0
-    if wsb and (workspace is None or workspace.numel() < wsb):
-        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
-    st = lib().hh_apply_signed(int(op), int(side), n, h, _ptr(U) if h else None, _ptr(d), _ptr(X),
-                               _ptr(Y), N, _dtype(X), _ptr(workspace) if wsb else None,
-                               workspace.numel() if wsb else 0, _stream(stream))
+    N, n, h = _validate(X, U=U, same={"Y": Y}, vecs={"d": d})
+    with torch.cuda.device(X.device):
+        ws, wsb = _workspace(HH_CALL_APPLY, n, h, N, 0, X, workspace) if N else (None, 0)
+        st = lib().hh_apply_signed(int(op), int(side), n, h, _ptr(U) if h else None, _ptr(d),
+                                   _ptr(X), _ptr(Y), N, _dtype(X), _ptr(ws), wsb,
+                                   _stream(stream, X.device))
     _check(st, "hh_apply_signed")
     return Y
 
@@ -263,22 +300,14 @@ def hh_sym_apply_signed(U: torch.Tensor, d: torch.Tensor, lam: torch.Tensor, X: 
                         Y: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
                         stream=None) -> torch.Tensor:
     """Y = D Q diag(lam) Q^T D X (hh.h: hh_sym_apply_signed, eq:thesbar)."""
-    _dev(X, "X")
-    _dev(d, "d")
-    _dev(lam, "lambda")
-    N, n = X.shape
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
     if Y is None:
         Y = torch.empty_like(X)
-    _dev(Y, "Y")
-    wsb = hh_workspace_bytes(HH_CALL_SYM, n, h, N, 0, X.dtype) if N else 0
-    if wsb and (workspace is None or workspace.numel() < wsb):
-        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
-    st = lib().hh_sym_apply_signed(n, h, _ptr(U) if h else None, _ptr(d), _ptr(lam), _ptr(X),
-                                   _ptr(Y), N, _dtype(X), _ptr(workspace) if wsb else None,
-                                   workspace.numel() if wsb else 0, _stream(stream))
+    N, n, h = _validate(X, U=U, same={"Y": Y}, vecs={"d": d, "lambda": lam})
+    with torch.cuda.device(X.device):
+        ws, wsb = _workspace(HH_CALL_SYM, n, h, N, 0, X, workspace) if N else (None, 0)
+        st = lib().hh_sym_apply_signed(n, h, _ptr(U) if h else None, _ptr(d), _ptr(lam),
+                                       _ptr(X), _ptr(Y), N, _dtype(X), _ptr(ws), wsb,
+                                       _stream(stream, X.device))
     _check(st, "hh_sym_apply_signed")
     return Y
 
@@ -291,30 +320,25 @@ def hh_mahalanobis(U: torch.Tensor, d: torch.Tensor, P: torch.Tensor, ia: torch.
 
     By default a workspace is allocated for the transform-once path (K3a + K3b);
     `fused=True` passes NULL and runs the per-pair fused kernel (K3c)."""
-    _dev(P, "P")
-    _dev(d, "d")
-    _dev(ia, "ia")
-    _dev(ib, "ib")
-    if ia.dtype != torch.int32 or ib.dtype != torch.int32:
-        raise ValueError("ia, ib must be int32")
-    M, n = P.shape
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
+    M, n, h = _validate(P, "P", U=U, vecs={"d": d})
+    for t, nm in ((ia, "ia"), (ib, "ib")):
+        _dev(t, nm)
+        if t.dtype != torch.int32 or t.dim() != 1 or t.device != P.device:
+            raise ValueError(f"{nm} must be a 1-D int32 tensor on {P.device}")
+    if ia.numel() != ib.numel():
+        raise ValueError(f"ia ({ia.numel()}) and ib ({ib.numel()}) differ in length")
     npairs = ia.numel()
     if dist is None:
         dist = torch.empty(npairs, dtype=P.dtype, device=P.device)
     _dev(dist, "dist")
-    wsb = 0
-    if not fused:
-        wsb = hh_workspace_bytes(HH_CALL_MAHALANOBIS, n, h, M, npairs, P.dtype)
-        if workspace is None or workspace.numel() < wsb:
-            workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=P.device)
-        else:
-            wsb = workspace.numel()
-    st = lib().hh_mahalanobis(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P), M, _ptr(ia),
-                              _ptr(ib), npairs, _ptr(dist), _dtype(P),
-                              None if fused else _ptr(workspace), wsb, _stream(stream))
+    if dist.numel() != npairs or dist.dtype != P.dtype or dist.device != P.device:
+        raise ValueError(f"dist must hold {npairs} values of {P.dtype} on {P.device}")
+    with torch.cuda.device(P.device):
+        ws, wsb = (None, 0) if fused else _workspace(HH_CALL_MAHALANOBIS, n, h, M, npairs, P,
+                                                      workspace)
+        st = lib().hh_mahalanobis(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P), M, _ptr(ia),
+                                  _ptr(ib), npairs, _ptr(dist), _dtype(P), _ptr(ws), wsb,
+                                  _stream(stream, P.device))
     _check(st, "hh_mahalanobis")
     return dist
 
@@ -323,20 +347,13 @@ def hh_apply_qr(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Ten
                 workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """hh_apply for QR-structured reflectors (u_i[r] = 0 for r < i), skipping the zero
     prefix (hh.h: hh_apply_qr, NEXT-f2)."""
-    _dev(X, "X")
-    N, n = X.shape
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
     if Y is None:
         Y = torch.empty_like(X)
-    _dev(Y, "Y")
-    wsb = hh_workspace_bytes(HH_CALL_APPLY, n, h, N, 0, X.dtype) if N else 0
-    if wsb and (workspace is None or workspace.numel() < wsb):
-        workspace = torch.empty(wsb, dtype=torch.uint8, device=X.device)
-    st = lib().hh_apply_qr(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N, _dtype(X),
-                           _ptr(workspace) if wsb else None, workspace.numel() if wsb else 0,
-                           _stream(stream))
+    N, n, h = _validate(X, U=U, same={"Y": Y})
+    with torch.cuda.device(X.device):
+        ws, wsb = _workspace(HH_CALL_APPLY, n, h, N, 0, X, workspace) if N else (None, 0)
+        st = lib().hh_apply_qr(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,
+                               _dtype(X), _ptr(ws), wsb, _stream(stream, X.device))
     _check(st, "hh_apply_qr")
     return Y
 
@@ -345,18 +362,19 @@ def hh_congruence(op: int, U: torch.Tensor, M: torch.Tensor, out: Optional[torch
                   workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """op(Q) M_b op(Q)^T for M of shape (count, n, n), each M[b] a column-major n x n
     matrix (i.e. the math matrix is M[b].T) (hh.h: hh_congruence, NEXT-f4)."""
-    _dev(M, "M")
+    if M.dim() != 3 or M.shape[1] != M.shape[2]:
+        raise ValueError(f"M must be (count, n, n), got {tuple(M.shape)}")
     count, n, _ = M.shape
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
     if out is None:
         out = torch.empty_like(M)
-    wsb = hh_workspace_bytes(HH_CALL_CONGRUENCE, n, h, count, 0, M.dtype)
-    if workspace is None or workspace.numel() < wsb:
-        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=M.device)
-    st = lib().hh_congruence(int(op), n, h, _ptr(U) if h else None, _ptr(M), _ptr(out), count,
-                             _dtype(M), _ptr(workspace), workspace.numel(), _stream(stream))
+    if out.shape != M.shape or out.dtype != M.dtype:
+        raise ValueError(f"out must be {tuple(M.shape)} {M.dtype}")
+    _validate(M.view(count * n, n), "M", U=U, same={"out": out.view(count * n, n)})
+    h = U.shape[0] if U.numel() else 0
+    with torch.cuda.device(M.device):
+        ws, wsb = _workspace(HH_CALL_CONGRUENCE, n, h, count, 0, M, workspace)
+        st = lib().hh_congruence(int(op), n, h, _ptr(U) if h else None, _ptr(M), _ptr(out),
+                                 count, _dtype(M), _ptr(ws), wsb, _stream(stream, M.device))
     _check(st, "hh_congruence")
     return out
 
@@ -365,38 +383,37 @@ def hh_knn(U: torch.Tensor, d: torch.Tensor, P_ref: torch.Tensor, P_query: torch
            workspace: Optional[torch.Tensor] = None, stream=None):
     """k nearest references of every query under d_S = ||diag(sqrt d) Q^T (x_q - x_r)||^2
     (hh.h: hh_knn).  Returns (idx int32 (M_query, k), dist (M_query, k)), ascending."""
-    for t, nm in ((d, "d"), (P_ref, "P_ref"), (P_query, "P_query")):
-        _dev(t, nm)
-    Mr, n = P_ref.shape
+    Mr, n, h = _validate(P_ref, "P_ref", U=U, vecs={"d": d})
+    if P_query.dim() != 2 or P_query.shape[1] != n or P_query.dtype != P_ref.dtype:
+        raise ValueError(f"P_query must be (M_query, {n}) {P_ref.dtype}")
+    _dev(P_query, "P_query")
+    if P_query.device != P_ref.device:
+        raise ValueError(f"P_query is on {P_query.device}, P_ref on {P_ref.device}")
     Mq = P_query.shape[0]
-    h = U.shape[0] if U.numel() else 0
-    if h:
-        _dev(U, "U")
     idx = torch.empty(Mq, k, dtype=torch.int32, device=P_ref.device)
     dist = torch.empty(Mq, k, dtype=P_ref.dtype, device=P_ref.device)
-    wsb = hh_workspace_bytes(HH_CALL_KNN, n, h, Mr, Mq, P_ref.dtype)
-    if workspace is None or workspace.numel() < wsb:
-        workspace = torch.empty(wsb, dtype=torch.uint8, device=P_ref.device)
-    st = lib().hh_knn(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P_ref), Mr, _ptr(P_query), Mq,
-                      int(k), _ptr(idx), _ptr(dist), _dtype(P_ref), _ptr(workspace),
-                      workspace.numel(), _stream(stream))
+    with torch.cuda.device(P_ref.device):
+        ws, wsb = _workspace(HH_CALL_KNN, n, h, Mr, Mq, P_ref, workspace)
+        st = lib().hh_knn(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P_ref), Mr, _ptr(P_query),
+                          Mq, int(k), _ptr(idx), _ptr(dist), _dtype(P_ref), _ptr(ws), wsb,
+                          _stream(stream, P_ref.device))
     _check(st, "hh_knn")
     return idx, dist
 
 
 def hh_apply_host(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor] = None,
                   workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """hh_apply on HOST (CPU, ideally pinned) tensors; device workspace (hh.h: hh_apply_host)."""
-    if X.is_cuda or (U.numel() and U.is_cuda):
-        raise ValueError("hh_apply_host takes host tensors")
-    N, n = X.shape
-    h = U.shape[0] if U.numel() else 0
+    """hh_apply on HOST (CPU, ideally pinned) tensors; device workspace (hh.h: hh_apply_host).
+    The current CUDA device runs it unless `workspace` names another one."""
     if Y is None:
         Y = torch.empty_like(X, pin_memory=X.is_pinned())
-    wsb = hh_workspace_bytes(HH_CALL_APPLY_HOST, n, h, N, 0, X.dtype)
-    if workspace is None or workspace.numel() < wsb:
-        workspace = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-    st = lib().hh_apply_host(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,
-                             _dtype(X), _ptr(workspace), workspace.numel(), _stream(stream))
+    N, n, h = _validate(X, U=U, same={"Y": Y}, host=True)
+    device = workspace.device if workspace is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    with torch.cuda.device(device):
+        ws, wsb = _workspace(HH_CALL_APPLY_HOST, n, h, N, 0,
+                             torch.empty(0, dtype=X.dtype, device=device), workspace)
+        st = lib().hh_apply_host(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,
+                                 _dtype(X), _ptr(ws), wsb, _stream(stream, device))
     _check(st, "hh_apply_host")
     return Y

@@ -150,3 +150,52 @@ def test_auto_crossover_sym(n, h, N, wy):
     """The same for the symmetric apply (hh_api.cu wy_min_h_sym)."""
     ws = hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, n, h, N, 0, 0)
     assert (ws > 0) == wy, (n, h, N, ws)
+
+
+def test_wy_pass_cap_rejected_before_launch():
+    """The block program has at most 128 passes (hh_wy.cu kMaxPasses): h > 32768 (apply,
+    256-wide blocks) and h > 8192 (symmetric, 2m - 1 passes of 128-wide blocks) are refused
+    with HH_ERR_UNSUPPORTED when the tensor-core path is forced -- before any launch, so
+    nothing is written -- and AUTO keeps such shapes on the fused kernel (no scratch)."""
+    L = hh.lib()
+    A = 1 << 20
+    big = 1 << 40
+    with hhpkg.algo(hhpkg.HH_ALGO_WY):
+        assert L.hh_apply(0, 1024, 32769, A, A, A, 4, 0, A, big, None) == hh.HH_ERR_UNSUPPORTED
+        assert L.hh_apply(1, 1024, 40000, A, A, A, 4, 0, A, big, None) == hh.HH_ERR_UNSUPPORTED
+        assert L.hh_sym_apply(256, 8193, A, A, A, A, 4, 0, A, big, None) == hh.HH_ERR_UNSUPPORTED
+        assert L.hh_apply(0, 1024, 10, A, A, A, 4, 1, A, big, None) == hh.HH_ERR_UNSUPPORTED  # f64
+        assert L.hh_apply(0, 16, 10, A, A, A, 4, 0, A, big, None) == hh.HH_ERR_UNSUPPORTED    # n < 32
+        # the largest supported programs still get a (finite) scratch size
+        assert hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 1024, 32768, 4096, 0, 0) > 0
+        assert hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 256, 8192, 4096, 0, 0) > 0
+    assert hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 1024, 32769, 262144, 0, 0) == 0
+    assert hhpkg.hh_workspace_bytes(hh.HH_CALL_SYM, 256, 8193, 262144, 0, 0) == 0
+
+
+def test_mahalanobis_pair_count_limit():
+    """The bucketed gather indexes pairs and points with int32: npairs >= 2^31 - 1 (or M) is
+    HH_ERR_UNSUPPORTED in the workspace query and the call, before any launch."""
+    L = hh.lib()
+    A = 1 << 20
+    with pytest.raises(hh.HHError) as ei:
+        hhpkg.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, 16, 1, 5, 1 << 31, 0)
+    assert ei.value.status == hh.HH_ERR_UNSUPPORTED
+    assert L.hh_mahalanobis(16, 1, A, A, A, 5, A, A, 1 << 31, A, 0, A, 1 << 40, None) == \
+        hh.HH_ERR_UNSUPPORTED
+    assert L.hh_mahalanobis(16, 1, A, A, A, 5, A, A, (1 << 31) - 1, A, 0, None, 0, None) == \
+        hh.HH_ERR_UNSUPPORTED
+
+
+def test_debug_hooks_are_thread_local():
+    """The TS-mode test hook changes only the calling thread's setting (no process-global
+    mutable state in the library)."""
+    import threading
+    L = hh.lib()
+    prev = L.hh_debug_wy_ts_min(64)
+    seen = []
+    t = threading.Thread(target=lambda: seen.append(L.hh_debug_wy_ts_min(256)))
+    t.start()
+    t.join()
+    assert seen == [256]                      # the other thread still had the default
+    assert L.hh_debug_wy_ts_min(prev) == 64   # this thread's value was kept

@@ -98,3 +98,32 @@ def test_knn_errors():
     assert L.hh_knn(*args(300, 3)) == hh.hh.HH_ERR_UNSUPPORTED     # n > 256
     assert L.hh_knn(*args(64, 17)) == hh.hh.HH_ERR_UNSUPPORTED     # k > 16
     assert L.hh_knn(*args(64, 3, M=2)) == hh.hh.HH_ERR_INVALID_VALUE   # M_ref < k
+
+
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_knn_exact_ties(k):
+    """Reading R14 / hh.h "ties by the smaller reference index": duplicated references give
+    bit-identical transformed points and distances on the GPU too (same bytes, same
+    arithmetic), so the returned indices are unique and must equal the oracle's exactly.
+    The duplicates sit in different 256-reference tiles and in different reference splits
+    (the CTA range cut and the merge kernel), at the k-th place and inside the list."""
+    n, h, Mr, Mq = 40, 6, 6000, 64
+    U, d, Pr, _ = knn_case(n, h, Mr, 1, seed=3)
+    groups = [(10, 700, 2999, 5990), (5, 300), (4000, 4001, 255, 256)]
+    for grp in groups:
+        for r in grp[1:]:
+            Pr[r] = Pr[grp[0]]
+    g = gi.rng(402, k)
+    Pq = np.empty((Mq, n), dtype=np.float32)
+    for q in range(Mq):
+        base = groups[q % len(groups)][0]
+        Pq[q] = Pr[base] + (0.0 if q < 3 else 1e-3) * g.standard_normal(n).astype(np.float32)
+    idx, dist = hh.hh_knn(dev(U), dev(d), dev(Pr), dev(Pq), k)
+    idx, dist = idx.cpu().numpy(), dist.cpu().numpy()
+    ridx, _ = oracle.knn(U, d, Pr, Pq, k)
+    assert np.array_equal(idx, ridx), np.nonzero((idx != ridx).any(1))[0][:5]
+    for q in range(Mq):
+        grp = sorted(groups[q % len(groups)])
+        m = min(k, len(grp))
+        assert list(idx[q, :m]) == grp[:m]              # the tie group, ascending index
+        assert np.all(dist[q, :m] == dist[q, 0])        # bit-identical distances

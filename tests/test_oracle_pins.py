@@ -426,6 +426,41 @@ def test_knn_bruteforce_and_invariants():
         assert np.array_equal(ie[q], np.argsort(e, kind="stable")[:k])
 
 
+def test_knn_exact_ties_smaller_index_first():
+    """Reading R14 (hh.h: "ascending, ties by the smaller reference index"): duplicated
+    references give bit-identical distances, so the order among them is fixed by index
+    alone -- inside the returned list and at the k-th place.  References 4, 17 and 31 are
+    one point and 9, 25 another; a query next to point 4 must return [4, 17] for k = 2 (31
+    ties with 17 at the cut: the earlier index is kept) and [4, 17, 31] for k = 3, and a
+    query next to point 9 must return 9 before 25.  Expected orders come from the dense
+    quadratic form with numpy's stable sort, not from the oracle."""
+    g = gi.rng(909)
+    n, h, Mr = 16, 5, 40
+    U = unit_rows(g, h, n)
+    d = g.uniform(0.1, 10.0, n)
+    Pr = g.standard_normal((Mr, n))
+    Pr[17] = Pr[4]
+    Pr[31] = Pr[4]
+    Pr[25] = Pr[9]
+    Pq = np.vstack([Pr[4] + 1e-3 * g.standard_normal(n), Pr[9] + 1e-3 * g.standard_normal(n),
+                    Pr[4].copy()])
+    Q = dense_Q(U)
+    S = Q @ np.diag(d) @ Q.T
+    for k in (2, 3, 4):
+        idx, dist = oracle.knn(U, d, Pr, Pq, k)
+        for q in range(Pq.shape[0]):
+            diff = Pq[q] - Pr
+            dd = np.einsum("ij,jk,ik->i", diff, S, diff)
+            dd[[17, 31]] = dd[4]                 # identical inputs: identical distances
+            dd[25] = dd[9]
+            assert np.array_equal(idx[q], np.argsort(dd, kind="stable")[:k]), (k, q, idx[q])
+        assert list(idx[0, :2]) == [4, 17] and list(idx[1, :2]) == [9, 25]
+        assert dist[0, 0] == dist[0, 1]
+        if k >= 3:
+            assert idx[0, 2] == 31 and list(idx[2, :3]) == [4, 17, 31]
+            assert dist[2, 0] == dist[2, 1] == dist[2, 2] == 0.0
+
+
 
 # --------------------------------------------------------------------------- NEXT-f4
 def test_congruence_dense_and_shf_identity():
