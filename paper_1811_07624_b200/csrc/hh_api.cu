@@ -174,6 +174,11 @@ hh_status hh_debug_wy_timeline(void *device_buf) {
 // block width.  Returns the previous value.
 int hh_debug_wy_ts_min(int kw) { return wy_set_ts_min(kw); }
 
+// Test / A-B hook (not part of hh.h): the single-launch dataflow form of the block program
+// (K5f) on (default) or off for the calling thread, and its project-CTA count (0: default).
+// Returns the previous on/off.
+int hh_debug_wy_flow(int on, int project_ctas) { return wy_set_flow(on, project_ctas); }
+
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first
 // projection only, leaving G (bf16 hi/lo rows) and V in the workspace at the
 // offsets written to off[0..1] (G, V) and the block size b / count nblk to off[2..3].

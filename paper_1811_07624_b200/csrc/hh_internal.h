@@ -75,11 +75,17 @@ struct WyPlan {
     size_t off_wf = 0, off_wb = 0, off_sp = 0, off_s = 0, off_t = 0, off_v = 0, off_v2 = 0,
            off_asym = 0, off_vf = 0, off_vpf = 0, off_pp = 0, off_p = 0, off_m = 0, off_gt = 0,
            off_ld = 0, off_part = 0, off_flag = 0;
+    // K5f (single dataflow launch): G ring, partial slots, per-(pass, tile) counters
+    int np = 0, ntiles = 0, fD = 0, fnkc = 0, fkw = 0;
+    size_t off_ring = 0, off_fpart = 0, off_cnt = 0;
     size_t bytes = 0;
 };
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N);
 void wy_set_timeline(unsigned long long *buf);   // debug: per-role barrier wait cycles
 int wy_set_ts_min(int kw);                       // test: TS-mode update threshold (prev.)
+// test / A-B hook: K5f dataflow launch on (1, default) or off (0); project-CTA count
+// (0 = default); returns the previous on/off
+int wy_set_flow(int on, int project_ctas);
 bool wy_supported(int kind, int64_t n, int64_t h, int64_t N);   // incl. the pass cap
 // Y = Q X / Q^T X / Q diag(lam) Q^T X by the compact-WY block program (fp32 in/out).
 // debug_stop_blocks >= 0: run the preparation and only the first projection (test hook).

@@ -41,6 +41,8 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <memory>
+#include <new>
 #include <vector>
 
 #include "hh_internal.h"
@@ -546,6 +548,7 @@ struct Bars1 {
     uint64_t wfull[kStages1], cfull[kStages1], cempty[kStages1];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem;
+    int last;   // split-tile hand-off: this CTA arrived second (epilogue broadcast)
 };
 // ld/st of the split-tile hand-off (L2, bypassing L1: written by another CTA)
 __device__ __forceinline__ void st_cg4(float *p, float a, float b, float c, float d) {
@@ -761,7 +764,6 @@ __global__ void __launch_bounds__(480, 1)
         uint32_t aph = 0;
         uint16_t *Glo = Gt + N * b;
         const int jl = q * 32 + lane;
-        __shared__ int s_last;
         for_segments([&](int tile, int, int, bool head, bool tail) {
             mbar_wait(&bars->acc_full[a], aph);
             tc::fence_after_sync();
@@ -777,9 +779,30 @@ __global__ void __launch_bounds__(480, 1)
             const size_t hp = static_cast<size_t>(head ? blockIdx.x - 1 : blockIdx.x);
             float *mine = part + (2 * hp + (head ? 1 : 0)) * kTileCols * b;
             const float *other = part + (2 * hp + (head ? 0 : 1)) * kTileCols * b;
-            float v[32];
-            if (split) {
+            auto store_g = [&](int c, const float (&v)[32]) {
+                if (j >= N) return;
+                uint32_t H[16], L[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
+                uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
+                uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
+                    gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
+                }
+            };
+            if (!split) {
                 for (int c = 0; c < b / 32; ++c) {
+                    float v[32];
+                    tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
+                                      static_cast<uint32_t>(a * 256 + c * 32),
+                                  v);
+                    store_g(c, v);
+                }
+            } else {
+                for (int c = 0; c < b / 32; ++c) {
+                    float v[32];
                     tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
                                       static_cast<uint32_t>(a * 256 + c * 32),
                                   v);
@@ -791,20 +814,19 @@ __global__ void __launch_bounds__(480, 1)
                 named_bar_sync(1, 128);
                 if (jl == 0) {
                     const int prev = atomicAdd(flag + hp, 1);
-                    s_last = prev == 1;
+                    bars->last = prev == 1;
                     if (prev == 1) flag[hp] = 0;   // both arrived: reset for the next launch
                     __threadfence();
                 }
                 named_bar_sync(1, 128);
-            }
-            if (!split || s_last) {
-                for (int c = 0; c < b / 32; ++c) {
-                    if (split) {
-                        // leading + trailing, in that order whichever side finishes
-                        const float *lead = head ? other : mine;
-                        const float *trail = head ? mine : other;
+                if (bars->last) {
+                    // leading + trailing, in that order whichever side finishes
+                    const float *lead = head ? other : mine;
+                    const float *trail = head ? mine : other;
+                    for (int c = 0; c < b / 32; ++c) {
                         const float *s0 = lead + (static_cast<size_t>(c) * kTileCols + jl) * 32;
                         const float *s1 = trail + (static_cast<size_t>(c) * kTileCols + jl) * 32;
+                        float v[32];
 #pragma unroll
                         for (int e = 0; e < 8; ++e) {
                             const float4 p0 = ld_cg4(s0 + 4 * e), p1 = ld_cg4(s1 + 4 * e);
@@ -813,22 +835,7 @@ __global__ void __launch_bounds__(480, 1)
                             v[4 * e + 2] = p0.z + p1.z;
                             v[4 * e + 3] = p0.w + p1.w;
                         }
-                    } else {
-                        tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                                          static_cast<uint32_t>(a * 256 + c * 32),
-                                      v);
-                    }
-                    if (j < N) {
-                        uint32_t H[16], L[16];
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
-                        uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
-                        uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
-                            gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
-                        }
+                        store_g(c, v);
                     }
                 }
             }
@@ -1416,6 +1423,8 @@ __global__ void __launch_bounds__(640, 1)
     if (warp == 1) tc::tmem_free<512>(tbase);
 }
 
+#include "hh_wy_flow.cuh"
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
@@ -1479,6 +1488,19 @@ cudaError_t g_attr_err[kMaxDevWy];
 // debug / test hooks, per calling thread (like hh_set_algo): no process-global mutable state
 thread_local unsigned long long *t_timeline = nullptr;   // hh_debug_wy_timeline
 thread_local int t_ts_min = 256;                         // hh_debug_wy_ts_min
+thread_local int t_flow = 1;                             // hh_debug_wy_flow
+thread_local int t_flow_p = 0;                           // project CTAs (0: default)
+
+// K5f shape: K chunks per tile (project units) and the L2 window D (tiles in flight)
+void flow_shape(int64_t n, int kw, int np, int64_t ntiles, int *nkc, int *D) {
+    const int nk = static_cast<int>((n + 31) / 32);
+    const int target = kw >= 256 ? 32 : 16;               // K steps per project unit
+    *nkc = std::max(1, std::min(8, (nk + target / 2) / target));
+    const int64_t tile_bytes = static_cast<int64_t>(kTileCols) * n * 4;
+    const int64_t w = std::max<int64_t>(8, (int64_t(40) << 20) / tile_bytes);
+    *D = static_cast<int>(std::max<int64_t>(np, std::min<int64_t>({w, 64, std::max<int64_t>(ntiles, 1)})));
+    if (*D < np) *D = np;
+}
 
 }  // namespace
 
@@ -1489,6 +1511,13 @@ void wy_set_timeline(unsigned long long *buf) { t_timeline = buf; }
 int wy_set_ts_min(int kw) {
     const int prev = t_ts_min;
     t_ts_min = kw;
+    return prev;
+}
+
+int wy_set_flow(int on, int project_ctas) {
+    const int prev = t_flow;
+    t_flow = on;
+    t_flow_p = project_ctas;
     return prev;
 }
 
@@ -1539,6 +1568,14 @@ WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>({ntl, device_attr().sm_count, kSlots1}));
     p.off_part = take(static_cast<size_t>(2 * pairs) * kTileCols * kmax * 4);
     p.off_flag = take(static_cast<size_t>(kSlots1) * 4);
+    // K5f regions
+    p.np = kind == WY_SYM ? 2 * p.nblk - 1 : p.nblk;
+    p.ntiles = static_cast<int>(ntl);
+    p.fkw = kmax;
+    flow_shape(n, kmax, p.np, ntl, &p.fnkc, &p.fD);
+    p.off_ring = take(static_cast<size_t>(p.fD) * kTileCols * kmax * 2 * 2);
+    p.off_fpart = p.fnkc > 1 ? take(static_cast<size_t>(p.fD) * p.fnkc * kTileCols * kmax * 4) : off;
+    p.off_cnt = take(static_cast<size_t>(3) * p.np * std::max<int64_t>(ntl, 1) * 4);
     p.bytes = off;
     return p;
 }
@@ -1596,6 +1633,9 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(wy_update_ts_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemMax);
     });
     if (g_attr_err[dev] != cudaSuccess) return g_attr_err[dev];
     const bool sym = p.kind == WY_SYM;
@@ -1762,6 +1802,100 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     if (dsign && (dside & 2)) prog[np - 1].post = dsign;
 
     const int ntiles = static_cast<int>((N + kTileCols - 1) / kTileCols);
+
+    // ---------------- K5f: the whole program as one dataflow launch (hh_wy_flow.cuh) when
+    // every pass updates in the same mode (SS: G in shared memory, or TS: G in TMEM)
+    bool ss_all = true, ts_all = true;
+    for (int q = 0; q < np; ++q) {
+        if (prog[q].kw >= t_ts_min) ss_all = false;
+        else ts_all = false;
+    }
+    if (t_flow && debug_stop_blocks < 0 && Y && sms >= 2 && (ss_all || ts_all) && np == p.np) {
+        // ~10 KB of kernel parameters (maps + pass table): built on the heap, copied at launch
+        std::unique_ptr<FlowArgs> fap(new (std::nothrow) FlowArgs());
+        if (!fap) return cudaErrorMemoryAllocation;
+        FlowArgs &fa = *fap;
+        fa.mXp = mX;
+        fa.mYp = mY;
+        fa.mXu = ts_all ? mXb2 : mXb;
+        fa.mYu = ts_all ? mYb2 : mYb;
+        fa.mW[0] = mWb;
+        fa.mW[1] = sym ? mW2b : mWb;
+        fa.mV[0] = mV;
+        fa.mV[1] = sym ? mAs : mV;
+        fa.mV[2] = sym ? mV2 : mV;
+        fa.ring = H(p.off_ring);
+        fa.part = F(p.off_fpart);
+        int *cnt = reinterpret_cast<int *>(w + p.off_cnt);
+        const int64_t npt = static_cast<int64_t>(np) * ntiles;
+        fa.gcount = cnt;
+        fa.gready = cnt + npt;
+        fa.udone = cnt + 2 * npt;
+        fa.N = N;
+        fa.n = static_cast<int>(p.n);
+        fa.n_pad = static_cast<int>(n_pad);
+        fa.np = np;
+        fa.ntiles = ntiles;
+        fa.D = p.fD;
+        fa.nkc = p.fnkc;
+        fa.rseg = 4;
+        fa.kwmax = p.fkw;
+        fa.ts = ts_all ? 1 : 0;
+        fa.nraw = nraw_for(p.fkw);
+        fa.nxs = nxs_for(p.fkw);
+        fa.sms = sms;
+        fa.P = std::max(1, std::min(sms - 1, t_flow_p > 0 ? t_flow_p : sms / 2));
+        const int nrc = static_cast<int>(n_pad / kRowChunk);
+        for (int q = 0; q < np; ++q) {
+            const Pass &ps = prog[q];
+            FlowPass &f = fa.pass[q];
+            f.wrow = ps.wrow;
+            f.wrow_lo = static_cast<int>(R) + ps.wrow;
+            f.kw = ps.kw;
+            f.wmap = ps.mW == &mW2b ? 1 : 0;
+            f.vmap = ps.mV == &mV ? 0 : (ps.mV == &mAs ? 1 : 2);
+            f.vrow_hi = ps.vrow_hi;
+            f.vrow_lo = ps.vrow_lo;
+            f.ks0 = ps.row0 / 32;
+            f.rc0 = ps.row0 / kRowChunk;
+            // out of place, the first pass copies the rows a QR block does not touch
+            const bool copy_below = q == 0 && X != Y && ps.row0 >= kRowChunk;
+            f.xrc0 = copy_below ? 0 : f.rc0;
+            f.target = (nrc - f.xrc0) * 4;
+            f.dscale = ps.dscale;
+            f.pre = ps.pre;
+            f.post = ps.post;
+        }
+        if (!make_map(&fa.mG, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, fa.ring, p.fkw,
+                      static_cast<uint64_t>(2) * p.fD * kTileCols, 32, kTileCols,
+                      CU_TENSOR_MAP_SWIZZLE_64B))
+            return cudaErrorNotSupported;
+        e = cudaMemsetAsync(cnt, 0, static_cast<size_t>(3 * npt) * 4, stream);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(sms));
+        cfg.blockDim = dim3(640);
+        cfg.dynamicSmemBytes = kSmemMax;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;   // every CTA resident: waits always resolve
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ++nlaunch;
+        e = cudaLaunchKernelEx(&cfg, wy_flow_kernel, fa);
+        if (info) {
+            info->variant = sym ? "wy_sym_flow_bf16x3_tcgen05" : "wy_flow_bf16x3_tcgen05";
+            info->grid = sms;
+            info->block = 640;
+            info->smem = kSmemMax;
+            info->nchunks = np;
+            info->launches = nlaunch;
+        }
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+    }
+
     const int grid = std::max(1, std::min(std::min(ntiles, sms), kSlots1));
     // K5a hand-off counters start at zero (the second arrival resets its counter)
     e = cudaMemsetAsync(w + p.off_flag, 0, static_cast<size_t>(kSlots1) * 4, stream);

@@ -76,6 +76,9 @@ def lib() -> ctypes.CDLL:
         if hasattr(L, "hh_debug_wy_ts_min"):   # test hook (absent from older builds)
             L.hh_debug_wy_ts_min.argtypes = [i32]
             L.hh_debug_wy_ts_min.restype = i32
+        if hasattr(L, "hh_debug_wy_flow"):     # A/B hook: single-launch block program on/off
+            L.hh_debug_wy_flow.argtypes = [i32, i32]
+            L.hh_debug_wy_flow.restype = i32
         L.hh_status_string.argtypes = [i32]
         L.hh_status_string.restype = ctypes.c_char_p
         L.hh_version.restype = ctypes.c_char_p

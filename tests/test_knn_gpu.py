@@ -108,7 +108,7 @@ def test_knn_exact_ties(k):
     The duplicates sit in different 256-reference tiles and in different reference splits
     (the CTA range cut and the merge kernel), at the k-th place and inside the list."""
     n, h, Mr, Mq = 40, 6, 6000, 64
-    U, d, Pr, _ = knn_case(n, h, Mr, 1, seed=3)
+    U, d, Pr, _ = knn_case(n, h, Mr, 4, seed=3)
     groups = [(10, 700, 2999, 5990), (5, 300), (4000, 4001, 255, 256)]
     for grp in groups:
         for r in grp[1:]:
