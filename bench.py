@@ -497,17 +497,27 @@ def run_hh(args):
     if rank == 0:
         hbm, hbm_src, _ = peaks()
         achieved = byts / (ms_step * 1e-3) / 1e9
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        # ncu-measured DRAM bytes of one step of this workload (tools/traffic.py, committed
+        # under profiles/r2/): bench.py cannot run ncu itself
+        traffic, traffic_src = None, None
+        tf = os.path.join(ROOT, "profiles", "r2", "traffic_r2.json")
         if os.path.exists(tf):
             try:
-                traffic = json.load(open(tf)).get(c.name + ("" if c.call != "apply" else args.op))
-            except (ValueError, OSError):
+                tr = json.load(open(tf)).get(args.workload.upper().replace("H", "h") if
+                                             args.workload.upper().startswith("C5") else
+                                             args.workload.upper())
+                if tr:
+                    traffic = tr["dram_bytes_per_step"]
+                    traffic_src = {"per_step_bytes": tr["dram_bytes_per_step"],
+                                   "dominant_kernel": tr["dominant_kernel"],
+                                   "dominant_bytes_per_launch": tr["dominant_bytes_per_launch"],
+                                   "source": "profiles/r2/traffic_r2.json (" + tr["source"] + ")"}
+            except (ValueError, OSError, KeyError):
                 traffic = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
                 "frac_of_8TBps": achieved / 8000.0,
-                "kernel": info.get("variant"), "launch": info}
+                "kernel": info.get("variant"), "launch": info, "traffic_detail": traffic_src}
         # the algorithmic roofline is max(bytes / HBM peak, flops / pipe peak);
         # the SIMT FP32 (FP64) pipe peak is #SM x 128 (64) FMA lanes x 2 x the maximum SM
         # clock (R13).  When the flops floor is the larger one (C4's transform-once

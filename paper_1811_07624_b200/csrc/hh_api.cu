@@ -178,6 +178,10 @@ int hh_debug_wy_ts_min(int kw) { return wy_set_ts_min(kw); }
 // (K5f) on (default) or off for the calling thread, and its project-CTA count (0: default).
 // Returns the previous on/off.
 int hh_debug_wy_flow(int on, int project_ctas) { return wy_set_flow(on, project_ctas); }
+void hh_debug_wy_flow_knobs(const int *k, int cnt) { wy_set_flow_knobs(k, cnt); }
+void hh_debug_k1(int alt, int gridx) { k1_set_debug(alt, gridx); }
+int hh_debug_k1_stream(int on) { return k1_set_stream(on); }
+int hh_debug_wy_pdl(int on) { return wy_set_pdl(on); }
 
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first
 // projection only, leaving G (bf16 hi/lo rows) and V in the workspace at the

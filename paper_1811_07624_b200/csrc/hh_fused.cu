@@ -8,8 +8,20 @@
 namespace hh {
 namespace {
 
+// A/B knobs (hh_debug_k1, per calling thread): a forced alternative variant (-1: the table)
+// and a multiplier of the persistent grid (1: persistent)
+thread_local int t_k1_alt = -1;
+thread_local int t_k1_gridx = 1;
+thread_local int t_k1_stream = 0;   // K1s (hh_stream.cu) for fp32 n <= 1024: off until measured
+
 const FusedVariant *pick(int dtype, int64_t nv) {
     int cnt = 0;
+    if (dtype == 0 && t_k1_alt >= 0) {
+        const FusedVariant *alt = fused_alt_f32(&cnt);
+        if (t_k1_alt < cnt && static_cast<int64_t>(alt[t_k1_alt].tpc) * alt[t_k1_alt].ch >= nv)
+            return &alt[t_k1_alt];
+        cnt = 0;
+    }
     const FusedVariant *tab = dtype == 0 ? fused_table_f32(&cnt) : fused_table_f64(&cnt);
     for (int i = 0; i < cnt; ++i)
         if (static_cast<int64_t>(tab[i].tpc) * tab[i].ch >= nv) return &tab[i];
@@ -20,7 +32,19 @@ const FusedVariant *pick(int dtype, int64_t nv) {
 
 int64_t max_n(int dtype) { return dtype == 0 ? 8192 : 4096; }
 
+int k1_set_stream(int on) {
+    const int prev = t_k1_stream;
+    t_k1_stream = on;
+    return prev;
+}
+
+void k1_set_debug(int alt, int gridx) {
+    t_k1_alt = alt;
+    t_k1_gridx = gridx > 0 ? gridx : 1;
+}
+
 cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info) {
+    if (t_k1_stream && stream_supported(a, dtype)) return launch_stream(a, stream, info);
     const int E = dtype == 0 ? 4 : 2;
     const int s = dtype == 0 ? 4 : 8;
     const int64_t nv = a.n / E;
@@ -88,7 +112,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     if (occ < 1) return cudaErrorNotSupported;
     const int64_t ntiles = (a.N + UC - 1) / UC;
     const int64_t need = (ntiles + NU - 1) / NU;
-    const int64_t cap = static_cast<int64_t>(occ) * da.sm_count;
+    const int64_t cap = static_cast<int64_t>(occ) * da.sm_count * t_k1_gridx;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min(need, cap)));
     a.nbatches = static_cast<int>((ntiles + static_cast<int64_t>(grid) * NU - 1) /
                                   (static_cast<int64_t>(grid) * NU));

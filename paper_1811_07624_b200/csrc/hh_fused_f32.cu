@@ -19,7 +19,20 @@ const FusedVariant kF32[] = {
     HH_FUSED_VAR(float, 128, 8, 2, 512, "f32_tpc128_ch8_c2"),  // n <= 4096
     HH_FUSED_VAR(float, 256, 8, 1, 512, "f32_tpc256_ch8_c1"),  // n <= 8192
 };
+// alternatives for same-box A/B only (hh_debug_k1 forces one): two-warp column groups with
+// four columns each (half the u reads per column), 256-thread CTAs
+const FusedVariant kF32Alt[] = {
+    HH_FUSED_VAR(float, 64, 4, 4, 512, "f32_tpc64_ch4_c4_nt512"),
+    HH_FUSED_VAR(float, 64, 4, 2, 512, "f32_tpc64_ch4_c2_nt512"),
+    HH_FUSED_VAR(float, 32, 8, 2, 256, "f32_tpc32_ch8_c2_nt256"),
+    HH_FUSED_VAR(float, 128, 2, 4, 512, "f32_tpc128_ch2_c4_nt512"),
+};
 }  // namespace
+
+const FusedVariant *fused_alt_f32(int *count) {
+    *count = static_cast<int>(sizeof(kF32Alt) / sizeof(kF32Alt[0]));
+    return kF32Alt;
+}
 
 const FusedVariant *fused_table_f32(int *count) {
     *count = static_cast<int>(sizeof(kF32) / sizeof(kF32[0]));

@@ -555,5 +555,6 @@ struct FusedVariant {
 // tables (each defined in its own translation unit so the instantiations build in parallel)
 const FusedVariant *fused_table_f32(int *count);
 const FusedVariant *fused_table_f64(int *count);
+const FusedVariant *fused_alt_f32(int *count);   // A/B alternatives (hh_debug_k1)
 
 }  // namespace hh

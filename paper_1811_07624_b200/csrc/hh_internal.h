@@ -49,6 +49,13 @@ cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const in
                                    const int32_t *ib, int64_t npairs, void *dist, void *ws,
                                    int dtype, cudaStream_t stream, LaunchInfo *info);
 
+// A/B hook (hh_debug_k1): force an alternative fused variant (-1: none), grid multiplier.
+void k1_set_debug(int alt, int gridx);
+// K1s (hh_stream.cu): the non-persistent streaming form of K1 for fp32 n <= 1024
+bool stream_supported(const FusedArgs &a, int dtype);
+cudaError_t launch_stream(const FusedArgs &a, cudaStream_t stream, LaunchInfo *info);
+int k1_set_stream(int on);   // A/B hook (hh_debug_k1_stream): returns the previous setting
+
 // Largest n the vector kernels support for this dtype.
 int64_t max_n(int dtype);
 
@@ -76,7 +83,7 @@ struct WyPlan {
            off_asym = 0, off_vf = 0, off_vpf = 0, off_pp = 0, off_p = 0, off_m = 0, off_gt = 0,
            off_ld = 0, off_part = 0, off_flag = 0;
     // K5f (single dataflow launch): G ring, partial slots, per-(pass, tile) counters
-    int np = 0, ntiles = 0, fD = 0, fnkc = 0, fkw = 0;
+    int np = 0, ntiles = 0, fD = 0, fnkc = 0, fkw = 0, fG = 1;
     size_t off_ring = 0, off_fpart = 0, off_cnt = 0;
     size_t bytes = 0;
 };
@@ -86,6 +93,8 @@ int wy_set_ts_min(int kw);                       // test: TS-mode update thresho
 // test / A-B hook: K5f dataflow launch on (1, default) or off (0); project-CTA count
 // (0 = default); returns the previous on/off
 int wy_set_flow(int on, int project_ctas);
+void wy_set_flow_knobs(const int *k, int cnt);   // [on, P, nkc, rseg, D, G, pol]
+int wy_set_pdl(int on);                           // A/B hook: PDL launches on/off (prev.)
 bool wy_supported(int kind, int64_t n, int64_t h, int64_t N);   // incl. the pass cap
 // Y = Q X / Q^T X / Q diag(lam) Q^T X by the compact-WY block program (fp32 in/out).
 // debug_stop_blocks >= 0: run the preparation and only the first projection (test hook).

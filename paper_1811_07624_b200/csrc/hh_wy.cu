@@ -82,6 +82,15 @@ __device__ __forceinline__ float bf2f(uint16_t b) {
     return __uint_as_float(static_cast<uint32_t>(b) << 16);
 }
 
+// Programmatic dependent launch: every kernel of the program lets the next one launch at once
+// (its CTAs are placed as this grid's CTAs retire) and waits for the previous one's results
+// before touching them -- the launch latency and setup of each dependent kernel overlap the
+// tail of its predecessor (no effect when a kernel is launched without the attribute).
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ K4: preparation
 // Wf[i][r] (fp32, h_pad x n_pad) = u_i[r] (product order of R1, zero padded).
 // Wb = bf16 split, R = h_pad + extra rows: [hi rows 0..R) [lo rows R..2R), ld = n_pad.
@@ -91,6 +100,8 @@ __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h
                                int64_t n_pad, const float *__restrict__ lam, int lam_blk, int b,
                                int extra, int reverse, float *__restrict__ Wf,
                                uint16_t *__restrict__ Wb) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t R = h_pad + extra;
     const int64_t total = R * n_pad;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -113,6 +124,8 @@ __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h
 // out[r] = a[r] * b[r] (the symmetric block's pre-scale Lambda D for a two-sided D)
 __global__ void wy_vmul_kernel(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
                                float *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();
     for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
          r += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[r] = a[r] * b[r];
@@ -126,6 +139,8 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
                                                       int b, int nsplit, int rows, int blk0,
                                                       const float *__restrict__ wt, int full,
                                                       float *__restrict__ Sp) {
+    pdl_trigger();
+    pdl_wait();
     const int ti = blockIdx.x, tj = blockIdx.y;
     const int blk = blockIdx.z / nsplit, sp = blockIdx.z % nsplit;
     if (ti > tj && !full) return;
@@ -175,6 +190,8 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
 // splits q, q + 32, ... then a butterfly (small b: few elements, many splits).
 __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int nblk, int nsplit,
                                       int full, float *__restrict__ S, int thread_per_elem) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t bb = static_cast<int64_t>(b) * b;
     if (thread_per_elem) {
         for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -214,6 +231,8 @@ __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int n
 // 2 = [c,c+32)):  T[0:c, c:c+32] = -T[0:c,0:c] * (S[0:c, c:c+32] * T[c:c+32, c:c+32]).
 __global__ void __launch_bounds__(256) wy_tbuild_kernel(const float *__restrict__ Sg, int b,
                                                           float *__restrict__ Tg, int diag_only) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ float tsm[];
     const int blk = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -334,6 +353,8 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
                                                       const float *__restrict__ Tg, int64_t n_pad,
                                                       int b, uint16_t *__restrict__ Vt,
                                                       int64_t lo_off) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ float vsm[];
     constexpr int RW = 32 * RP;   // rows per CTA
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * RW;
@@ -470,6 +491,8 @@ __global__ void __launch_bounds__(256) wy_rowgemm_kernel(
     int K, const float *__restrict__ C, int64_t ldc, const float *__restrict__ alpha,
     int64_t alpha_n, float sgn, float *__restrict__ Of, uint16_t *__restrict__ Ob, int64_t ldo,
     int64_t lo_off) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t r0 = blockIdx.x * 64;
     const int c0 = blockIdx.y * 32;
     __shared__ float As[32][65], Bs[32][33];
@@ -631,6 +654,8 @@ __global__ void __launch_bounds__(480, 1)
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = bars->tmem;
+    pdl_trigger();
+    pdl_wait();   // the previous kernel's results (after this CTA's setup)
 
     if (warp == 0) {
         if (lane == 0) {
@@ -936,6 +961,8 @@ __global__ void __launch_bounds__(640, 1)
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = bars->tmem;
+    pdl_trigger();
+    pdl_wait();   // the previous kernel's results (after this CTA's setup)
 
     if (warp == 0) {
         if (lane == 0) {
@@ -1225,6 +1252,8 @@ __global__ void __launch_bounds__(640, 1)
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = bars->tmem;
+    pdl_trigger();
+    pdl_wait();   // the previous kernel's results (after this CTA's setup)
 
     if (warp == 0) {
         if (lane == 0) {
@@ -1488,20 +1517,26 @@ cudaError_t g_attr_err[kMaxDevWy];
 // debug / test hooks, per calling thread (like hh_set_algo): no process-global mutable state
 thread_local unsigned long long *t_timeline = nullptr;   // hh_debug_wy_timeline
 thread_local int t_ts_min = 256;                         // hh_debug_wy_ts_min
-thread_local int t_flow = 1;                             // hh_debug_wy_flow
-thread_local int t_flow_p = 0;                           // project CTAs (0: default)
+// K5f knobs (hh_debug_wy_flow*): on/off, project CTAs, K chunks per tile, row chunks per
+// update entry, L2 window (tiles), tiles per wavefront group, L2 policy bits; 0 = default
+struct FlowKnobs {
+    int on = 0, P = 0, nkc = 0, rseg = 0, D = 0, G = 0, pol = 3;   // K5f measured slower: opt-in
+};
+thread_local FlowKnobs t_fk;
 
-// K5f shape: K chunks per tile (project units) and the L2 window D (tiles in flight)
-void flow_shape(int64_t n, int kw, int np, int64_t ntiles, int *nkc, int *D) {
+// K5f shape: K chunks per tile (project units), tiles per wavefront group G, L2 window D
+void flow_shape(int64_t n, int kw, int np, int64_t ntiles, int *nkc, int *D, int *G) {
     const int nk = static_cast<int>((n + 31) / 32);
     const int target = kw >= 256 ? 32 : 16;               // K steps per project unit
-    *nkc = std::max(1, std::min(8, (nk + target / 2) / target));
+    *nkc = t_fk.nkc > 0 ? t_fk.nkc : std::max(1, std::min(8, (nk + target / 2) / target));
+    *G = t_fk.G > 0 ? t_fk.G : (np > 1 ? 4 : 1);
     const int64_t tile_bytes = static_cast<int64_t>(kTileCols) * n * 4;
-    const int64_t w = std::max<int64_t>(8, (int64_t(40) << 20) / tile_bytes);
-    *D = static_cast<int>(std::max<int64_t>(np, std::min<int64_t>({w, 64, std::max<int64_t>(ntiles, 1)})));
-    if (*D < np) *D = np;
+    const int64_t w = t_fk.D > 0 ? t_fk.D
+                                 : std::max<int64_t>(8, std::min<int64_t>(64, (int64_t(40) << 20) / tile_bytes));
+    // deadlock freedom needs the window to span np wavefront groups (hh_wy_flow.cuh)
+    *D = static_cast<int>(std::max<int64_t>(static_cast<int64_t>(np) * *G,
+                                            std::min<int64_t>(w, std::max<int64_t>(ntiles, 1))));
 }
-
 }  // namespace
 
 void wy_set_timeline(unsigned long long *buf) { t_timeline = buf; }
@@ -1515,10 +1550,17 @@ int wy_set_ts_min(int kw) {
 }
 
 int wy_set_flow(int on, int project_ctas) {
-    const int prev = t_flow;
-    t_flow = on;
-    t_flow_p = project_ctas;
+    const int prev = t_fk.on;
+    t_fk.on = on;
+    t_fk.P = project_ctas;
     return prev;
+}
+
+void wy_set_flow_knobs(const int *k, int cnt) {
+    FlowKnobs f;
+    int *dst[7] = {&f.on, &f.P, &f.nkc, &f.rseg, &f.D, &f.G, &f.pol};
+    for (int i = 0; i < cnt && i < 7; ++i) *dst[i] = k[i];
+    t_fk = f;
 }
 
 WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
@@ -1572,7 +1614,7 @@ WyPlan wy_plan(int kind, int64_t n, int64_t h, int64_t N) {
     p.np = kind == WY_SYM ? 2 * p.nblk - 1 : p.nblk;
     p.ntiles = static_cast<int>(ntl);
     p.fkw = kmax;
-    flow_shape(n, kmax, p.np, ntl, &p.fnkc, &p.fD);
+    flow_shape(n, kmax, p.np, ntl, &p.fnkc, &p.fD, &p.fG);
     p.off_ring = take(static_cast<size_t>(p.fD) * kTileCols * kmax * 2 * 2);
     p.off_fpart = p.fnkc > 1 ? take(static_cast<size_t>(p.fD) * p.fnkc * kTileCols * kmax * 4) : off;
     p.off_cnt = take(static_cast<size_t>(3) * p.np * std::max<int64_t>(ntl, 1) * 4);
@@ -1606,6 +1648,33 @@ struct Pass {
 };
 
 }  // namespace
+
+namespace {
+thread_local int t_pdl = 1;   // A/B hook (hh_debug_wy_pdl)
+// every kernel of the block program is launched with programmatic stream serialization (PDL):
+// see pdl_trigger / pdl_wait
+template <typename... K, typename... A>
+cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       A &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = t_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+}  // namespace
+
+int wy_set_pdl(int on) {
+    const int prev = t_pdl;
+    t_pdl = on;
+    return prev;
+}
 
 cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const float *X, float *Y,
                       void *ws, cudaStream_t stream, LaunchInfo *info, int debug_stop_blocks,
@@ -1641,6 +1710,10 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     const bool sym = p.kind == WY_SYM;
     if (sym && !lam) return cudaErrorInvalidValue;
     int nlaunch = 0;   // kernels enqueued by this call (reported through LaunchInfo)
+    cudaError_t lerr = cudaSuccess;   // the first launch error
+    auto note = [&](cudaError_t le) {
+        if (le != cudaSuccess && lerr == cudaSuccess) lerr = le;
+    };
     char *w = static_cast<char *>(ws);
     auto F = [&](size_t o) { return reinterpret_cast<float *>(w + o); };
     auto H = [&](size_t o) { return reinterpret_cast<uint16_t *>(w + o); };
@@ -1651,6 +1724,13 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     const int64_t n_pad = p.n_pad, R = p.h_pad + p.extra;
     const int64_t vlo = static_cast<int64_t>(m) * n_pad * b;           // lo offset in a V array
 
+    // K5a hand-off counters start at zero (the second arrival resets its counter); done first
+    // so that the kernels of the program follow each other directly (PDL)
+    {
+        const cudaError_t me = cudaMemsetAsync(w + p.off_flag, 0, static_cast<size_t>(kSlots1) * 4, stream);
+        if (me != cudaSuccess) return me;
+    }
+
     // ---------------- K4: pack + Gram + T + V (and the symmetric block's operands)
     {
         const int64_t tot = R * n_pad;
@@ -1659,31 +1739,31 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         // product of symmetric reflectors reverses it); the symmetric program keeps the
         // natural order and uses T and T^T explicitly
         const int rev = p.kind == WY_APPLY_T ? 1 : 0;
-        ++nlaunch, wy_pack_kernel<<<g, 256, 0, stream>>>(U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b,
-                                                         p.extra, rev, Wf, Wb);
+        ++nlaunch, note(pdl_launch(wy_pack_kernel, g, 256, 0, stream, U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b,
+                                                         p.extra, rev, Wf, Wb));
         const int tb = (b + 63) / 64;
-        ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, m * p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, p.gram_rows, 0,
-                                                                       nullptr, 0, Sp);
+        ++nlaunch, note(pdl_launch(wy_gram_kernel, dim3(tb, tb, m * p.nsplit), 256, 0, stream, Wf, n_pad, b, p.nsplit, p.gram_rows, 0,
+                                                                       nullptr, 0, Sp));
         const int64_t ns = static_cast<int64_t>(m) * b * b;
-        ++nlaunch, wy_gram_reduce_kernel<<<static_cast<int>(std::min<int64_t>((ns * 32 + 255) / 256, sms * 16)),
-                                256, 0, stream>>>(Sp, b, m, p.nsplit, 0, S, ns >= 32768 ? 1 : 0);
+        ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, static_cast<int>(std::min<int64_t>((ns * 32 + 255) / 256, sms * 16)),
+                                256, 0, stream, Sp, b, m, p.nsplit, 0, S, ns >= 32768 ? 1 : 0));
         if (sym) {   // P = W^T Lambda W of the last block (full)
-            ++nlaunch, wy_gram_kernel<<<dim3(tb, tb, p.nsplit), 256, 0, stream>>>(Wf, n_pad, b, p.nsplit, p.gram_rows,
-                                                                       m - 1, lam, 1, F(p.off_pp));
-            ++nlaunch, wy_gram_reduce_kernel<<<std::max(1, std::min(sms * 16, (b * b * 32 + 255) / 256)), 256, 0, stream>>>(
-                F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p), b * b >= 32768 ? 1 : 0);
+            ++nlaunch, note(pdl_launch(wy_gram_kernel, dim3(tb, tb, p.nsplit), 256, 0, stream, Wf, n_pad, b, p.nsplit, p.gram_rows,
+                                                                       m - 1, lam, 1, F(p.off_pp)));
+            ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, std::max(1, std::min(sms * 16, (b * b * 32 + 255) / 256)), 256, 0, stream, 
+                F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p), b * b >= 32768 ? 1 : 0));
         }
-        ++nlaunch, wy_tbuild_kernel<<<m, 256, tbuild_smem(b), stream>>>(S, b, T, sym ? 0 : 1);
+        ++nlaunch, note(pdl_launch(wy_tbuild_kernel, m, 256, tbuild_smem(b), stream, S, b, T, sym ? 0 : 1));
         if (!sym) {
             // V = W T per block, row-parallel from the diagonal T blocks (wy_vrec_kernel)
             // 32-row CTAs when 64-row ones would not fill one wave (one block of n = 4096:
             // 64 CTAs on 148 SMs; with 4 blocks the 64-row CTAs are faster: measured)
             if (static_cast<int64_t>(n_pad / 64) * m < sms)
-                ++nlaunch, wy_vrec_kernel<1><<<dim3(static_cast<unsigned>(n_pad / 32), m), 256,
-                                               vrec_smem(b), stream>>>(Wf, S, T, n_pad, b, H(p.off_v), vlo);
+                ++nlaunch, note(pdl_launch(wy_vrec_kernel<1>, dim3(static_cast<unsigned>(n_pad / 32), m), 256,
+                                               vrec_smem(b), stream, Wf, S, T, n_pad, b, H(p.off_v), vlo));
             else
-                ++nlaunch, wy_vrec_kernel<2><<<dim3(static_cast<unsigned>(n_pad / 64), m), 256,
-                                               vrec_smem(b), stream>>>(Wf, S, T, n_pad, b, H(p.off_v), vlo);
+                ++nlaunch, note(pdl_launch(wy_vrec_kernel<2>, dim3(static_cast<unsigned>(n_pad / 64), m), 256,
+                                               vrec_smem(b), stream, Wf, S, T, n_pad, b, H(p.off_v), vlo));
         }
         const dim3 gv(static_cast<unsigned>(n_pad / 64), b / 32);
         for (int k = 0; k < (sym ? m : 0); ++k) {
@@ -1694,36 +1774,36 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
             uint16_t *Vn = H(p.off_v2);
             uint16_t *Vt = H(p.off_v);
             if (!last_sym) {
-                ++nlaunch, wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<true, false>, gv, 256, 0, stream, 
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
-                    Vn + static_cast<int64_t>(k) * n_pad * b, b, vlo);
-                ++nlaunch, wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
+                    Vn + static_cast<int64_t>(k) * n_pad * b, b, vlo));
+                ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<true, true>, gv, 256, 0, stream, 
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
-                    Vt + static_cast<int64_t>(k) * n_pad * b, b, vlo);
+                    Vt + static_cast<int64_t>(k) * n_pad * b, b, vlo));
             } else {
                 // A2 = W T (bf16 into columns [b, 2b) of Asym, fp32 copy Vf); V' = W T^T;
                 // M = P T^T; A1 = Lambda V' - V M (columns [0, b)).  DESIGN.md §4.
                 uint16_t *As = H(p.off_asym);
                 const int64_t alo = n_pad * 2 * b;
-                ++nlaunch, wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<true, false>, gv, 256, 0, stream, 
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_vf),
-                    nullptr, b, 0);
-                ++nlaunch, wy_rowgemm_kernel<true, false><<<gv, 256, 0, stream>>>(
+                    nullptr, b, 0));
+                ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<true, false>, gv, 256, 0, stream, 
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr, As + b,
-                    2 * b, alo);
-                ++nlaunch, wy_rowgemm_kernel<true, true><<<gv, 256, 0, stream>>>(
+                    2 * b, alo));
+                ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<true, true>, gv, 256, 0, stream, 
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_vpf),
-                    nullptr, b, 0);
-                ++nlaunch, wy_rowgemm_kernel<false, true><<<dim3((b + 63) / 64, b / 32), 256, 0, stream>>>(
+                    nullptr, b, 0));
+                ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<false, true>, dim3((b + 63) / 64, b / 32), 256, 0, stream, 
                     b, F(p.off_p), b, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, F(p.off_m), nullptr,
-                    b, 0);
-                ++nlaunch, wy_rowgemm_kernel<false, false><<<gv, 256, 0, stream>>>(
+                    b, 0));
+                ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<false, false>, gv, 256, 0, stream, 
                     n_pad, F(p.off_vf), b, F(p.off_m), b, b, F(p.off_vpf), b, lam, p.n, -1.f,
-                    nullptr, As, 2 * b, alo);
+                    nullptr, As, 2 * b, alo));
             }
         }
     }
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = lerr != cudaSuccess ? lerr : cudaGetLastError();
     if (e != cudaSuccess) return e;
 
     // ---------------- tensor maps
@@ -1792,8 +1872,8 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         f.dscale = dsign;
         if (f.pre) {   // first pass is the symmetric block: pre-scale Lambda D
             float *ld = F(p.off_ld);
-            ++nlaunch, wy_vmul_kernel<<<std::max(1, static_cast<int>((p.n + 255) / 256)), 256, 0, stream>>>(
-                f.pre, dsign, p.n, ld);
+            ++nlaunch, note(pdl_launch(wy_vmul_kernel, std::max(1, static_cast<int>((p.n + 255) / 256)), 256, 0, stream, 
+                f.pre, dsign, p.n, ld));
             f.pre = ld;
         } else {
             f.pre = dsign;
@@ -1810,7 +1890,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         if (prog[q].kw >= t_ts_min) ss_all = false;
         else ts_all = false;
     }
-    if (t_flow && debug_stop_blocks < 0 && Y && sms >= 2 && (ss_all || ts_all) && np == p.np) {
+    if (t_fk.on && debug_stop_blocks < 0 && Y && sms >= 2 && (ss_all || ts_all) && np == p.np) {
         // ~10 KB of kernel parameters (maps + pass table): built on the heap, copied at launch
         std::unique_ptr<FlowArgs> fap(new (std::nothrow) FlowArgs());
         if (!fap) return cudaErrorMemoryAllocation;
@@ -1838,13 +1918,16 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         fa.ntiles = ntiles;
         fa.D = p.fD;
         fa.nkc = p.fnkc;
-        fa.rseg = 4;
+        fa.rseg = t_fk.rseg > 0 ? t_fk.rseg : 4;
+        fa.G = p.fG;
+        fa.pol = t_fk.pol;
+        fa.tl = t_timeline;
         fa.kwmax = p.fkw;
         fa.ts = ts_all ? 1 : 0;
         fa.nraw = nraw_for(p.fkw);
         fa.nxs = nxs_for(p.fkw);
         fa.sms = sms;
-        fa.P = std::max(1, std::min(sms - 1, t_flow_p > 0 ? t_flow_p : sms / 2));
+        fa.P = std::max(1, std::min(sms - 1, t_fk.P > 0 ? t_fk.P : sms / 2));
         const int nrc = static_cast<int>(n_pad / kRowChunk);
         for (int q = 0; q < np; ++q) {
             const Pass &ps = prog[q];
@@ -1897,17 +1980,14 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     }
 
     const int grid = std::max(1, std::min(std::min(ntiles, sms), kSlots1));
-    // K5a hand-off counters start at zero (the second arrival resets its counter)
-    e = cudaMemsetAsync(w + p.off_flag, 0, static_cast<size_t>(kSlots1) * 4, stream);
-    if (e != cudaSuccess) return e;
     const float *cur = X;
     for (int q = 0; q < np; ++q) {
         const Pass &ps = prog[q];
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
-        ++nlaunch, wy_project_kernel<<<grid, 480, smem1(ps.kw), stream>>>(
+        ++nlaunch, note(pdl_launch(wy_project_kernel, grid, 480, smem1(ps.kw), stream, 
             mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
             ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw), F(p.off_part),
-            reinterpret_cast<int *>(w + p.off_flag));
+            reinterpret_cast<int *>(w + p.off_flag)));
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
         const int64_t uxrc = (cur != Y && ps.row0 >= kRowChunk) ? 0 : ps.row0 / kRowChunk;
         const int64_t units = static_cast<int64_t>(ntiles) * (n_pad / kRowChunk - uxrc);
@@ -1915,18 +1995,18 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         // TS-mode update (G in TMEM) for the wide blocks: the resident G no longer competes
         // with the V and X rings for shared memory
         if (ps.kw >= t_ts_min) {
-            ++nlaunch, wy_update_ts_kernel<<<grid3, 640, smem4(), stream>>>(
+            ++nlaunch, note(pdl_launch(wy_update_ts_kernel, grid3, 640, smem4(), stream, 
                 Gt, *ps.mV, (cur == X) ? mXb2 : mYb2, mYb2, ps.pre, ps.post, static_cast<int>(p.n),
                 static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
-                ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, t_timeline);
+                ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, t_timeline));
             cur = Y;
             continue;
         }
-        ++nlaunch, wy_update_kernel<<<grid3, 640, smem3(ps.kw), stream>>>(
+        ++nlaunch, note(pdl_launch(wy_update_kernel, grid3, 640, smem3(ps.kw), stream, 
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
             ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw),
-            t_timeline);
+            t_timeline));
         cur = Y;
     }
     if (info) {
@@ -1937,7 +2017,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         info->nchunks = np;
         info->launches = nlaunch;
     }
-    return cudaGetLastError();
+    return lerr != cudaSuccess ? lerr : cudaGetLastError();
 }
 
 }  // namespace hh

@@ -45,8 +45,22 @@ struct FlowArgs {
     float *part;            // partials [D][nkc][kwmax/32][128][32]
     int *gcount, *gready, *udone;   // [np][ntiles]
     int64_t N;
-    int n, n_pad, np, ntiles, D, P, nkc, rseg, kwmax, ts, nraw, nxs, sms;
+    int n, n_pad, np, ntiles, D, P, nkc, rseg, kwmax, ts, nraw, nxs, sms, G;
+    int pol;                     // L2 policy bits (A/B): 1 project evict_last, 2 update evict_first
+    unsigned long long *tl;      // debug: per-CTA role timeline (hh_debug_wy_timeline), or NULL
     FlowPass pass[kFlowMaxPasses];
+};
+
+// debug timeline: per CTA 16 counters (cycles unless noted), written once at the end
+enum : int {
+    TL_ROLE = 0, TL_TOTAL, TL_PDEP, TL_PRING, TL_MMA_IN, TL_MMA_ACC, TL_EPI_ACC, TL_EPI_RED,
+    TL_EPI_X, TL_UNITS, TL_CV_IN, TL_CV_OUT, TL_EPI_BUSY, TL_UDEP, TL_13, TL_14
+};
+struct FlowTimer {
+    unsigned long long acc = 0;
+    unsigned long long t0 = 0;
+    __device__ __forceinline__ void start(bool on) { if (on) t0 = clock64(); }
+    __device__ __forceinline__ void stop(bool on) { if (on) acc += clock64() - t0; }
 };
 
 // ---------------------------------------------------------------- flags
@@ -94,18 +108,31 @@ __device__ __forceinline__ void tma_store_2d_hint(const void *tmap, const void *
 struct FlowCursor {
     int q, t, sub;
     int64_t pidx;   // pair index (end: np * ntiles)
+    // pairs in the order: s = q + t / G ascending, then q descending, then t ascending
+    // (tile groups of G tiles move through the passes as a wavefront)
+    int G, ng;
     __device__ __forceinline__ void next_pair(int np, int ntiles) {
         ++pidx;
-        if (q > 0 && t + 1 < ntiles) {
-            --q;
+        const int g = t / G;
+        const int tl = t - g * G;
+        const int gsz = min(G, ntiles - g * G);
+        if (tl + 1 < gsz) {
             ++t;
             return;
         }
-        const int s = q + t + 1;
-        q = s < np - 1 ? s : np - 1;
-        t = s - q;
+        const int s = q + g;
+        if (q > 0 && g + 1 < ng) {   // next group of the same diagonal, one pass lower
+            --q;
+            t = (g + 1) * G;
+            return;
+        }
+        const int s1 = s + 1;
+        q = s1 < np - 1 ? s1 : np - 1;
+        t = (s1 - q) * G;
     }
-    __device__ __forceinline__ void init(int first, int per, int np, int ntiles) {
+    __device__ __forceinline__ void init(int first, int per, int np, int ntiles, int G_) {
+        G = G_;
+        ng = (ntiles + G - 1) / G;
         q = 0;
         t = 0;
         pidx = 0;
@@ -131,7 +158,7 @@ template <typename Fn>
 __device__ __forceinline__ void flow_for_units(const FlowArgs &A, int first, int step, int per,
                                                Fn &&fn) {
     FlowCursor c;
-    c.init(first, per, A.np, A.ntiles);
+    c.init(first, per, A.np, A.ntiles, A.G);
     while (c.valid(A.np, A.ntiles)) {
         fn(c.q, c.t, c.sub);
         c.advance(step, per, A.np, A.ntiles);
@@ -163,6 +190,10 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int first = blockIdx.x, step = A.P, per = A.nkc;
+    const bool dbg = A.tl != nullptr;
+    unsigned long long *tl = dbg ? A.tl + static_cast<int64_t>(blockIdx.x) * 16 : nullptr;
+    FlowTimer t_a, t_b, t_c;
+    unsigned long long nunits = 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < nraw; ++s) {
             mbar_init(&bars->rfull[s], 1);
@@ -189,7 +220,8 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
         if (lane == 0) {
             tc::prefetch_tmap(&A.mXp);
             tc::prefetch_tmap(&A.mYp);
-            const uint64_t pol = policy_evict_last();   // re-read by the update role from L2
+            // re-read by the update role from L2
+            const uint64_t pol = (A.pol & 1) ? policy_evict_last() : policy_evict_normal();
             int s = 0;
             uint32_t ph = 0;
             flow_for_units(A, first, step, per, [&](int q, int t, int kc) {
@@ -199,14 +231,18 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
                 if (klo >= khi) return;
                 // dependencies: the previous pass of this tile has stored all its rows, or
                 // (first pass) tile t - D has left the program (the L2 window)
+                t_a.start(dbg);
                 if (q > 0)
                     flow_wait(A.udone + static_cast<int64_t>(q - 1) * A.ntiles + t, A.pass[q - 1].target);
                 else if (t >= A.D)
                     flow_wait(A.udone + static_cast<int64_t>(A.np - 1) * A.ntiles + (t - A.D),
                               A.pass[A.np - 1].target);
+                t_a.stop(dbg);
                 const CUtensorMap *m = q == 0 ? &A.mXp : &A.mYp;
                 for (int ks = klo; ks < khi; ++ks) {
+                    t_b.start(dbg);
                     mbar_wait(&bars->rempty[s], ph ^ 1u);
+                    t_b.stop(dbg);
                     mbar_arrive_expect_tx(&bars->rfull[s], static_cast<uint32_t>(kRawBytes));
                     tc::tma_load_2d_hint(rawX(s), m, ks * 32, t * kTileCols, &bars->rfull[s], pol);
                     if (++s == nraw) {
@@ -215,6 +251,10 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
                     }
                 }
             });
+            if (dbg) {
+                tl[TL_PDEP] = t_a.acc;
+                tl[TL_PRING] = t_b.acc;
+            }
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -247,12 +287,16 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
             int klo, khi;
             flow_krange(A, ps, kc, klo, khi);
             const uint32_t idesc = tc::idesc_bf16(128, ps.kw);
+            t_b.start(dbg);
             mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+            t_b.stop(dbg);
             tc::fence_after_sync();
             const uint32_t d = tbase + static_cast<uint32_t>(a * 256);
             for (int ks = klo; ks < khi; ++ks) {
+                t_a.start(dbg);
                 mbar_wait(&bars->wfull[s], ph);
                 mbar_wait(&bars->cfull[s], ph);
+                t_a.stop(dbg);
                 tc::fence_after_sync();
                 const uint32_t xh = smem_u32(Xhi(s)), xl = smem_u32(Xlo(s));
                 const uint32_t wh = smem_u32(Whi(s)), wl = smem_u32(Wlo(s, ps.kw));
@@ -277,6 +321,10 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
             }
         });
         __syncwarp();
+        if (dbg && lane == 0) {
+            tl[TL_MMA_IN] = t_a.acc;
+            tl[TL_MMA_ACC] = t_b.acc;
+        }
     } else if (warp < 11) {
         // converters: 256 threads, 4 float4 each per K step (fp32 X tile -> bf16 hi/lo)
         const int ct = threadIdx.x - 96;
@@ -287,7 +335,9 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
             int klo, khi;
             flow_krange(A, ps, kc, klo, khi);
             for (int ks = klo; ks < khi; ++ks) {
+                t_a.start(dbg);
                 mbar_wait(&bars->rfull[rs], rph);
+                t_a.stop(dbg);
                 const uint32_t raw = smem_u32(rawX(rs));
                 float4 v[4];
 #pragma unroll
@@ -305,7 +355,9 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
                         }
                     }
                 }
+                t_b.start(dbg);
                 mbar_wait(&bars->cempty[cs], cph ^ 1u);
+                t_b.stop(dbg);
                 const uint32_t xh = smem_u32(Xhi(cs)), xl = smem_u32(Xlo(cs));
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
@@ -331,6 +383,10 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
                 }
             }
         });
+        if (dbg && ct == 0) {
+            tl[TL_CV_IN] = t_a.acc;
+            tl[TL_CV_OUT] = t_b.acc;
+        }
     } else if (warp < 15) {
         // epilogue: TMEM lane quarter qd = warp % 4 = columns j of the tile
         const int qd = warp & 3;
@@ -346,7 +402,11 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
             const bool empty = klo >= khi;
             const int slot = t % A.D;
             const int nsl = ps.kw / 16;   // 16-column groups of G
+            t_a.start(dbg);
             mbar_wait(&bars->acc_full[a], aph);
+            t_a.stop(dbg);
+            ++nunits;
+            t_c.start(dbg);
             tc::fence_after_sync();
             uint16_t *gh = A.ring + (static_cast<int64_t>(slot) * kTileCols + jl) * kwmax;
             uint16_t *gl = A.ring + (lo_rows + static_cast<int64_t>(slot) * kTileCols + jl) * kwmax;
@@ -403,6 +463,7 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
                 }
                 named_bar_sync(1, 128);
                 if (bars->last) {
+                    t_b.start(dbg);
                     // the last of the tile's nkc units: G = sum of the partials in kc order
                     const float *p0 = A.part + (static_cast<int64_t>(slot) * nkc * (kwmax / 16) * kTileCols) * 16;
                     const int64_t pstride = static_cast<int64_t>(kwmax / 16) * kTileCols * 16;
@@ -426,13 +487,21 @@ __device__ __forceinline__ void flow_project(const FlowArgs &A, unsigned char *s
                     __threadfence();
                     named_bar_sync(1, 128);
                     if (jl == 0) st_release(gflag, 1);
+                    t_b.stop(dbg);
                 }
             }
+            t_c.stop(dbg);
             if (++a == 2) {
                 a = 0;
                 aph ^= 1u;
             }
         });
+        if (dbg && jl == 0) {
+            tl[TL_EPI_ACC] = t_a.acc;
+            tl[TL_EPI_RED] = t_b.acc;
+            tl[TL_EPI_BUSY] = t_c.acc;
+            tl[TL_UNITS] = nunits;
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -476,6 +545,10 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int first = blockIdx.x - A.P, step = gridDim.x - A.P;
+    const bool dbg = A.tl != nullptr;
+    unsigned long long *tl = dbg ? A.tl + static_cast<int64_t>(blockIdx.x) * 16 : nullptr;
+    FlowTimer t_a, t_b;
+    unsigned long long nunits = 0;
     const int per = (A.n_pad / kRowChunk + A.rseg - 1) / A.rseg;
     const int64_t lo_rows = static_cast<int64_t>(A.D) * kTileCols;
     if (threadIdx.x == 0) {
@@ -513,8 +586,12 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
                 flow_rows(A, ps, seg, rlo, rhi, mlo);
                 if (mlo >= rhi) return;   // copy-only (or empty) entry: no G, no V
                 const int nslab = ps.kw / 32;
+                t_a.start(dbg);
                 flow_wait(A.gready + static_cast<int64_t>(q) * A.ntiles + t, 1);
+                t_a.stop(dbg);
+                t_b.start(dbg);
                 mbar_wait(&bars->gempty, gph ^ 1u);
+                t_b.stop(dbg);
                 mbar_arrive_expect_tx(&bars->gfull, static_cast<uint32_t>(nslab) * 16384u);
                 const int slot = t % A.D;
                 for (int c = 0; c < nslab; ++c) {
@@ -526,7 +603,9 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
                 const CUtensorMap *mv = &A.mV[ps.vmap];
                 for (int rc = mlo; rc < rhi; ++rc) {
                     for (int c = 0; c < nslab; ++c) {
+                        t_b.start(dbg);
                         mbar_wait(&bars->empty[s], ph ^ 1u);
+                        t_b.stop(dbg);
                         mbar_arrive_expect_tx(&bars->full[s], static_cast<uint32_t>(kStage3Bytes));
                         tc::tma_load_2d(Vhi(s), mv, c * 32, ps.vrow_hi + rc * kRowChunk, &bars->full[s]);
                         tc::tma_load_2d(Vlo(s), mv, c * 32, ps.vrow_lo + rc * kRowChunk, &bars->full[s]);
@@ -537,6 +616,10 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
                     }
                 }
             });
+            if (dbg) {
+                tl[TL_PDEP] = t_a.acc;
+                tl[TL_PRING] = t_b.acc;
+            }
         }
     } else if (warp == 1) {
         const uint32_t idesc = tc::idesc_bf16(kRowChunk, kTileCols);
@@ -549,15 +632,21 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
             flow_rows(A, ps, seg, rlo, rhi, mlo);
             if (mlo >= rhi) return;
             const int nslab = ps.kw / 32;
+            t_a.start(dbg);
             mbar_wait(&bars->gfull, gph);
+            t_a.stop(dbg);
             gph ^= 1u;
             tc::fence_after_sync();
             for (int rc = mlo; rc < rhi; ++rc) {
+                t_b.start(dbg);
                 mbar_wait(&bars->acc_empty[a], aph ^ 1u);
+                t_b.stop(dbg);
                 tc::fence_after_sync();
                 const uint32_t d = tbase + static_cast<uint32_t>(a * kTileCols);
                 for (int c = 0; c < nslab; ++c) {
+                    t_a.start(dbg);
                     mbar_wait(&bars->full[s], ph);
+                    t_a.stop(dbg);
                     tc::fence_after_sync();
                     const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
 #pragma unroll
@@ -584,11 +673,15 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
             tc::mma_commit_w(&bars->gempty);
         });
         __syncwarp();
+        if (dbg && lane == 0) {
+            tl[TL_MMA_IN] = t_a.acc;
+            tl[TL_MMA_ACC] = t_b.acc;
+        }
     } else if (warp == 2) {
         if (lane == 0) {
             tc::prefetch_tmap(&A.mXu);
             tc::prefetch_tmap(&A.mYu);
-            const uint64_t pol = policy_evict_first();   // the last read of these rows
+            const uint64_t pol = (A.pol & 2) ? policy_evict_first() : policy_evict_normal();
             int s = 0;
             uint32_t ph = 0;
             flow_for_units(A, first, step, per, [&](int q, int t, int seg) {
@@ -597,11 +690,15 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
                 flow_rows(A, ps, seg, rlo, rhi, mlo);
                 if (rlo >= rhi) return;
                 // the tile's G is ready, hence its projection (and the previous pass) is done
+                t_a.start(dbg);
                 flow_wait(A.gready + static_cast<int64_t>(q) * A.ntiles + t, 1);
+                t_a.stop(dbg);
                 const CUtensorMap *m = q == 0 ? &A.mXu : &A.mYu;
                 for (int rc = rlo; rc < rhi; ++rc) {
                     for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb) {
+                        t_b.start(dbg);
                         mbar_wait(&bars->xempty[s], ph ^ 1u);
+                        t_b.stop(dbg);
                         mbar_arrive_expect_tx(&bars->xfull[s], static_cast<uint32_t>(kXBoxBytes));
                         tc::tma_load_2d_hint(Xs(s), m, rc * kRowChunk, t * kTileCols + cb * kXBoxCols,
                                              &bars->xfull[s], pol);
@@ -612,6 +709,10 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
                     }
                 }
             });
+            if (dbg) {
+                tl[TL_UDEP] = t_a.acc;
+                tl[TL_CV_OUT] = t_b.acc;
+            }
         }
     } else if (warp >= 4) {
         const int qd = warp & 3, grp = (warp - 4) >> 2;
@@ -628,8 +729,11 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
             flow_rows(A, ps, seg, rlo, rhi, mlo);
             for (int rc = rlo; rc < rhi; ++rc, seq += kBoxes) {
                 const bool mma_rc = rc >= mlo;
+                ++nunits;
                 if (mma_rc) {
+                    t_a.start(dbg);
                     mbar_wait(&bars->acc_full[a], aph);
+                    t_a.stop(dbg);
                     tc::fence_after_sync();
                 }
                 const int r = rc * kRowChunk + r_in;
@@ -640,7 +744,9 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
                     const int cb = grp + 4 * k;
                     const int64_t sq = seq + cb;
                     const int s = static_cast<int>(sq % nxs);
+                    t_b.start(dbg);
                     mbar_wait(&bars->xfull[s], static_cast<uint32_t>((sq / nxs) & 1));
+                    t_b.stop(dbg);
                     const uint32_t xs = smem_u32(Xs(s)) + static_cast<uint32_t>(r_in) * 4u;
                     float v[16];
                     if (mma_rc) {
@@ -677,6 +783,11 @@ __device__ __forceinline__ void flow_update_ss(const FlowArgs &A, unsigned char 
             }
         });
         if (storer) tc::bulk_wait0();
+        if (dbg && warp == 4 && lane == 0) {
+            tl[TL_EPI_ACC] = t_a.acc;
+            tl[TL_EPI_X] = t_b.acc;
+            tl[TL_UNITS] = nunits;
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -793,7 +904,7 @@ __device__ __forceinline__ void flow_update_ts(const FlowArgs &A, unsigned char 
         if (lane == 0) {
             tc::prefetch_tmap(&A.mXu);
             tc::prefetch_tmap(&A.mYu);
-            const uint64_t pol = policy_evict_first();
+            const uint64_t pol = (A.pol & 2) ? policy_evict_first() : policy_evict_normal();
             int s = 0;
             uint32_t ph = 0;
             flow_for_units(A, first, step, per, [&](int q, int t, int seg) {
@@ -919,10 +1030,15 @@ __global__ void __launch_bounds__(640, 1) wy_flow_kernel(const __grid_constant__
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const unsigned long long t0 = clock64();
     if (static_cast<int>(blockIdx.x) < A.P)
         flow_project(A, smem);
     else if (A.ts)
         flow_update_ts(A, smem);
     else
         flow_update_ss(A, smem);
+    if (A.tl && threadIdx.x == 0) {
+        A.tl[static_cast<int64_t>(blockIdx.x) * 16 + TL_ROLE] = static_cast<int>(blockIdx.x) < A.P ? 0 : 1;
+        A.tl[static_cast<int64_t>(blockIdx.x) * 16 + TL_TOTAL] = clock64() - t0;
+    }
 }

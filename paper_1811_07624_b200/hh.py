@@ -79,6 +79,18 @@ def lib() -> ctypes.CDLL:
         if hasattr(L, "hh_debug_wy_flow"):     # A/B hook: single-launch block program on/off
             L.hh_debug_wy_flow.argtypes = [i32, i32]
             L.hh_debug_wy_flow.restype = i32
+            L.hh_debug_wy_flow_knobs.argtypes = [ctypes.POINTER(ctypes.c_int), i32]
+            L.hh_debug_wy_flow_knobs.restype = None
+        if hasattr(L, "hh_debug_k1"):
+            L.hh_debug_k1.argtypes = [i32, i32]
+            L.hh_debug_k1.restype = None
+            L.hh_debug_k1_stream.argtypes = [i32]
+            L.hh_debug_k1_stream.restype = i32
+            L.hh_debug_wy_pdl.argtypes = [i32]
+            L.hh_debug_wy_pdl.restype = i32
+        if hasattr(L, "hh_debug_wy_timeline"):
+            L.hh_debug_wy_timeline.argtypes = [p]
+            L.hh_debug_wy_timeline.restype = i32
         L.hh_status_string.argtypes = [i32]
         L.hh_status_string.restype = ctypes.c_char_p
         L.hh_version.restype = ctypes.c_char_p

@@ -218,3 +218,29 @@ def test_wy_ts_many_tiles(ts_everywhere, op):
     c = gi.make_case("apply", 512, 64, 40000, "f32", seed=31)
     got = wy(op, c.U, c.X)
     assert_parity(got, oracle.apply(op, c.U, c.X), "f32", 64, f"WY-TS many tiles op{op}")
+
+
+@pytest.fixture
+def flow_on():
+    """The single-launch dataflow form of the block program (K5f, opt-in: measured slower
+    than the two-kernel program) for this test."""
+    L = hh.hh.lib()
+    prev = L.hh_debug_wy_flow(1, 0)
+    yield
+    L.hh_debug_wy_flow(prev, 0)
+
+
+@pytest.mark.parametrize("call,n,h,N,op", [("apply", 512, 64, 40000, 0), ("apply", 512, 64, 40000, 1),
+                                           ("apply", 4096, 64, 2000, 0), ("apply", 1024, 300, 3000, 1),
+                                           ("apply", 4096, 1024, 700, 0), ("sym", 2048, 32, 5000, 0),
+                                           ("sym", 512, 100, 3000, 0), ("apply", 100, 50, 129, 1)])
+def test_wy_flow_parity(flow_on, call, n, h, N, op):
+    c = gi.make_case(call, n, h, N, "f32", seed=5)
+    if call == "sym":
+        got = wy_sym(c.U, c.lam, c.X)
+        ref = oracle.sym_apply(c.U, c.lam, c.X)
+    else:
+        got = wy(op, c.U, c.X)
+        ref = oracle.apply(op, c.U, c.X)
+    assert "flow" in hh.last_launch_info()["variant"], hh.last_launch_info()
+    assert_parity(got, ref, "f32", h, f"K5f {call} n{n} h{h} N{N} op{op}")
