@@ -23,19 +23,20 @@ thread_local LaunchInfo t_last;
 thread_local bool t_has_last = false;
 thread_local int t_algo = HH_ALGO_AUTO;
 
-// K1 (fused SIMT) vs K5 (compact-WY on tcgen05) crossover in h, fp32 only, by n and by the
-// problem size E = n*N elements.  K1 is one HBM pass but its FMA work grows with h; K5 moves
-// ~1.5 passes and its cost is flat in h up to one block (b <= 32), plus a fixed cost of its
-// kernel chain (~55-100 us eager) that only large problems amortise.  Thresholds are the
-// first h where K5 won in the same-box sweep of profiles/r1/crossover_r1.txt:
-// E = 2^28 for the large band, E = 2^25 (the slowest point of its band) for the middle one.
+// K1 (fused SIMT; K1s for fp32 n <= 512, hh_stream.cu) vs K5 (compact-WY on tcgen05) crossover
+// in h, fp32 only, by n and by the problem size E = n*N elements.  K1 is one HBM pass but its
+// FMA work grows with h; K5 moves ~1.5 passes and its cost is flat in h up to one block
+// (b <= 32), plus a fixed cost of its kernel chain that only large problems amortise.
+// Thresholds are the first h where K5 won in same-box sweeps: n <= 512 against K1s
+// (profiles/r2/crossover_r2.txt, round 2: K1s moved them up by 2-10), n > 512 against K1
+// (profiles/r1/crossover_r1.txt); E = 2^28 for the large band, 2^25 for the middle one.
 int64_t wy_min_h(int64_t n, int64_t N) {
     if (n < 128) return int64_t(1) << 30;
     // bands follow K1's variant table (measured at the top n of each band)
     const int i = n <= 128 ? 0 : n <= 256 ? 1 : n <= 512 ? 2 : n <= 1024 ? 3 : n <= 2048 ? 4
                 : n <= 4096 ? 5 : 6;
-    static const int big[7] = {14, 12, 16, 19, 17, 13, 7};    // E >= 2^27
-    static const int mid[7] = {20, 18, 22, 26, 22, 17, 16};   // 2^25 <= E < 2^27
+    static const int big[7] = {24, 20, 18, 19, 17, 13, 7};    // E >= 2^27
+    static const int mid[7] = {28, 25, 23, 26, 22, 17, 16};   // 2^25 <= E < 2^27
     const int64_t E = n * N;
     if (E >= (int64_t(1) << 27)) return big[i];
     if (E >= (int64_t(1) << 25)) return mid[i];
@@ -50,13 +51,14 @@ bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
 }
 
 // Symmetric apply: K2 does 2h reflectors per column and is FMA-bound from h ~ 5; the
-// tensor-core block program moves ~1.5 passes of X plus a fixed ~100 us (eager) for its kernel
-// chain.  Same-box sweep (profiles/r1/crossover_r1.txt, sym section), bands as in wy_min_h.
+// tensor-core block program moves ~1.5 passes of X plus a fixed cost for its kernel chain.
+// Same-box sweeps: n <= 512 against the streaming K2 (profiles/r2/crossover_r2.txt, E = 2^28;
+// the middle band raised by the same margin), n > 512 against K2 (profiles/r1/crossover_r1.txt).
 int64_t wy_min_h_sym(int64_t n, int64_t N) {
-    if (n < 256) return int64_t(1) << 30;
-    const int i = n <= 256 ? 0 : n <= 512 ? 1 : n <= 1024 ? 2 : n <= 2048 ? 3 : 4;
-    static const int big[5] = {7, 9, 11, 10, 8};      // E >= 2^27
-    static const int mid[5] = {13, 17, 19, 18, 15};   // 2^25 <= E < 2^27
+    if (n < 128) return int64_t(1) << 30;
+    const int i = n <= 128 ? 0 : n <= 256 ? 1 : n <= 512 ? 2 : n <= 1024 ? 3 : n <= 2048 ? 4 : 5;
+    static const int big[6] = {16, 13, 10, 11, 10, 8};       // E >= 2^27
+    static const int mid[6] = {24, 19, 18, 19, 18, 15};      // 2^25 <= E < 2^27
     const int64_t E = n * N;
     if (E >= (int64_t(1) << 27)) return big[i];
     if (E >= (int64_t(1) << 25)) return mid[i];

@@ -12,7 +12,7 @@ namespace {
 // and a multiplier of the persistent grid (1: persistent)
 thread_local int t_k1_alt = -1;
 thread_local int t_k1_gridx = 1;
-thread_local int t_k1_stream = 0;   // K1s (hh_stream.cu) for fp32 n <= 1024: off until measured
+thread_local int t_k1_stream = -1;   // K1s (hh_stream.cu): -1 measured policy, 0 never, 1 always
 
 const FusedVariant *pick(int dtype, int64_t nv) {
     int cnt = 0;
@@ -44,7 +44,8 @@ void k1_set_debug(int alt, int gridx) {
 }
 
 cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info) {
-    if (t_k1_stream && stream_supported(a, dtype)) return launch_stream(a, stream, info);
+    if (t_k1_stream != 0 && stream_supported(a, dtype) && (t_k1_stream == 1 || stream_preferred(a)))
+        return launch_stream(a, stream, info);
     const int E = dtype == 0 ? 4 : 2;
     const int s = dtype == 0 ? 4 : 8;
     const int64_t nv = a.n / E;

@@ -53,8 +53,9 @@ cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const in
 void k1_set_debug(int alt, int gridx);
 // K1s (hh_stream.cu): the non-persistent streaming form of K1 for fp32 n <= 1024
 bool stream_supported(const FusedArgs &a, int dtype);
+bool stream_preferred(const FusedArgs &a);   // the measured K1 / K1s policy
 cudaError_t launch_stream(const FusedArgs &a, cudaStream_t stream, LaunchInfo *info);
-int k1_set_stream(int on);   // A/B hook (hh_debug_k1_stream): returns the previous setting
+int k1_set_stream(int on);   // A/B hook (hh_debug_k1_stream): -1 auto, 0 K1, 1 K1s; previous
 
 // Largest n the vector kernels support for this dtype.
 int64_t max_n(int dtype);

@@ -184,6 +184,9 @@ struct StreamVariant {
 #define HH_STREAM_VAR(TPC, CH, C, NT, NAME) \
     StreamVariant { reinterpret_cast<const void *>(&hh_stream_kernel<TPC, CH, C, NT>), TPC, CH, C, NT, NAME }
 const StreamVariant kStream[] = {
+    HH_STREAM_VAR(4, 1, 4, 128, "f32s_tpc4_ch1_c4"),     // n <= 16
+    HH_STREAM_VAR(4, 2, 4, 128, "f32s_tpc4_ch2_c4"),     // n <= 32
+    HH_STREAM_VAR(8, 2, 4, 128, "f32s_tpc8_ch2_c4"),     // n <= 64
     HH_STREAM_VAR(8, 4, 2, 128, "f32s_tpc8_ch4_c2"),     // n <= 128
     HH_STREAM_VAR(16, 4, 2, 128, "f32s_tpc16_ch4_c2"),   // n <= 256
     HH_STREAM_VAR(32, 4, 2, 128, "f32s_tpc32_ch4_c2"),   // n <= 512
@@ -223,6 +226,17 @@ bool stream_supported(const FusedArgs &a, int dtype) {
     return dtype == 0 && a.n <= 1024 && a.n % 4 == 0 &&
            (a.mode == MODE_APPLY_N || a.mode == MODE_APPLY_T || a.mode == MODE_SYM ||
             a.mode == MODE_TRANSFORM);
+}
+
+// When K1s replaces K1 (same-box grid n x h at 1 GiB, profiles/r2/k1s_grid_r2.txt): K1s is
+// 5-39 % faster for n <= 512 at every h measured (2..32) and for n in (512, 1024] outside
+// h = 9..11, where the persistent staged K1 is 1-2 % faster (C2: n = 1024, h = 10); U must stay
+// L1-resident next to nothing else (h n 4 <= 128 KB).
+bool stream_preferred(const FusedArgs &a) {
+    const int64_t ub = a.h * a.n * 4;
+    if (ub > (int64_t(128) << 10)) return false;
+    if (a.n > 512 && a.h >= 9 && a.h <= 11) return false;
+    return true;
 }
 
 }  // namespace hh

@@ -69,7 +69,10 @@ def test_workspace_query():
     (2048, 28, 131072, True),                       # the old n>=512, h>=32 rule kept K1 here
     (1024, 25, 32768, False), (1024, 26, 32768, True),   # E = 2^25: middle band
     (1024, 31, 4096, False), (1024, 32, 4096, True),     # small problems: h >= 32
-    (128, 13, 1 << 21, False), (128, 14, 1 << 21, True),
+    (128, 23, 1 << 21, False), (128, 24, 1 << 21, True),   # n <= 512: against K1s (r2)
+    (256, 19, 1 << 20, False), (256, 20, 1 << 20, True),
+    (512, 17, 1 << 19, False), (512, 18, 1 << 19, True),
+    (512, 22, 1 << 16, False), (512, 23, 1 << 16, True),
     (64, 512, 1 << 22, False),                      # n < 128: always K1
     (8192, 6, 32768, False), (8192, 7, 32768, True),
     (8192, 15, 4096, False), (8192, 16, 4096, True),
@@ -142,9 +145,11 @@ def test_product_does_not_touch_oracle():
 @pytest.mark.parametrize("n,h,N,wy", [
     (2048, 32, 131072, True),                       # C3
     (1024, 10, 262144, False), (1024, 11, 262144, True),  # E = 2^28
-    (512, 16, 65536, False), (512, 17, 65536, True),      # E = 2^25
+    (1024, 18, 32768, False), (1024, 19, 32768, True),    # E = 2^25
     (2048, 31, 2048, False), (2048, 32, 2048, True),      # small problems
-    (128, 64, 1 << 21, False),                      # n < 256: always K2
+    (128, 15, 1 << 21, False), (128, 16, 1 << 21, True),  # n <= 512: against K1s (r2)
+    (256, 12, 1 << 20, False), (256, 13, 1 << 20, True),
+    (64, 64, 1 << 22, False),                       # n < 128: always K2
 ])
 def test_auto_crossover_sym(n, h, N, wy):
     """The same for the symmetric apply (hh_api.cu wy_min_h_sym)."""

@@ -260,3 +260,47 @@ def test_binding_validates_operands():
     assert_parity(hh.hh_apply(0, U, X).cpu().numpy(), oracle.apply(0, U.cpu().numpy(),
                                                                      X.cpu().numpy()),
                   "f32", 3, "valid call")
+
+
+@pytest.fixture(params=[0, 1], ids=["K1", "K1s"])
+def k1_kind(request):
+    """Force the persistent staged K1 (0) or the non-persistent streaming K1s (1) for fp32
+    n <= 1024 (hh_stream.cu); the default picks by the measured policy."""
+    L = hh.hh.lib()
+    prev = L.hh_debug_k1_stream(request.param)
+    yield request.param
+    L.hh_debug_k1_stream(prev)
+
+
+K1S_SHAPES = [(4, 3, 37), (16, 5, 1001), (32, 4, 999), (64, 6, 1000), (100, 7, 2339), (128, 9, 513),
+              (200, 24, 777), (256, 9, 513), (384, 17, 300), (512, 9, 1000), (1000, 12, 250),
+              (1024, 10, 3001), (1024, 40, 257)]
+
+
+@pytest.mark.parametrize("n,h,N", K1S_SHAPES)
+def test_k1_and_k1s(k1_kind, n, h, N):
+    """Both fused kernels on every fp32 shape class they serve: both ops, the symmetric form,
+    the D factor on both sides, the transform-once of Mahalanobis, exact alias."""
+    c = gi.make_case("sym", n, h, N, "f32", seed=41)
+    d = gi.sign_diag(gi.rng(41, n), n, "f32")
+    for op in (0, 1):
+        with hh.algo(hh.HH_ALGO_FUSED):
+            got = run_apply(op, c.U, c.X)
+            want = "f32s_" if k1_kind else "f32_"
+            assert hh.last_launch_info()["variant"].startswith(want), hh.last_launch_info()
+        assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"{c.name} op{op}")
+    with hh.algo(hh.HH_ALGO_FUSED):
+        got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", h, f"{c.name} sym")
+    for side in (0, 1):
+        with hh.algo(hh.HH_ALGO_FUSED):
+            got = hh.hh_apply_signed(1, side, dev(c.U), dev(d), dev(c.X)).cpu().numpy()
+        assert_parity(got, oracle.apply_signed(1, side, c.U, d, c.X), "f32", h, f"signed {side}")
+    m = gi.make_case("mahalanobis", n, h, max(N // 4, 2), "f32", seed=42, npairs=3000)
+    got = hh.hh_mahalanobis(dev(m.U), dev(m.d), dev(m.X), dev(m.ia), dev(m.ib)).cpu().numpy()
+    assert_parity(got, oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib), "f32", h, "mahalanobis")
+    X = dev(c.X)
+    with hh.algo(hh.HH_ALGO_FUSED):
+        hh.hh_apply(0, dev(c.U), X, Y=X)
+    torch.cuda.synchronize()
+    assert_parity(X.cpu().numpy(), oracle.apply(0, c.U, c.X), "f32", h, "alias")
