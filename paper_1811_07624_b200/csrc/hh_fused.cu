@@ -44,7 +44,7 @@ void k1_set_debug(int alt, int gridx) {
 }
 
 cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info) {
-    if (t_k1_stream != 0 && stream_supported(a, dtype) && (t_k1_stream == 1 || stream_preferred(a)))
+    if (t_k1_stream != 0 && stream_supported(a, dtype) && (t_k1_stream >= 1 || stream_preferred(a)))
         return launch_stream(a, stream, info);
     const int E = dtype == 0 ? 4 : 2;
     const int s = dtype == 0 ? 4 : 8;

@@ -85,6 +85,9 @@ __global__ void __launch_bounds__(NT) hh_stream_kernel(const FusedArgs a) {
     }
     // one reflector (Eq. 2): alpha = u^T x (FFMA2 partial sums, xor butterfly over the group),
     // x <- x - 2 alpha u
+    // one reflector (Eq. 2): alpha = u^T x (FFMA2 partial sums, xor butterfly over the group),
+    // x <- x - 2 alpha u.  (Loading u_{i+1} during reflector i was measured 1.5x slower at
+    // n = 1024: the extra registers cost a quarter of the resident warps.)
     auto reflect = [&](int i) {
         const float4 *u = Ug + static_cast<int64_t>(i) * nv + gt;
         float4 uk[CH];
@@ -115,11 +118,16 @@ __global__ void __launch_bounds__(NT) hh_stream_kernel(const FusedArgs a) {
             }
         }
     };
-    if (mode == MODE_APPLY_N) {
+    auto run_desc = [&]() {
         for (int i = h - 1; i >= 0; --i) reflect(i);
-    } else {
-        for (int i = 0; i < h; ++i) reflect(i);   // Q^T X, the Q^T pass of SYM, TRANSFORM
-    }
+    };
+    auto run_asc = [&]() {
+        for (int i = 0; i < h; ++i) reflect(i);
+    };
+    if (mode == MODE_APPLY_N)
+        run_desc();
+    else
+        run_asc();   // Q^T X, the Q^T pass of SYM, TRANSFORM
     if (mode == MODE_SYM) {   // x <- lambda (.) x, then the Q pass (eq:thesbar)
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(NT) hh_stream_kernel(const FusedArgs a) {
                 x[c][k].w *= l.w;
             }
         }
-        for (int i = h - 1; i >= 0; --i) reflect(i);
+        run_desc();
     }
     if (mode == MODE_TRANSFORM) {   // Z = diag(sqrt d) Q^T P
 #pragma unroll
@@ -231,7 +239,9 @@ bool stream_supported(const FusedArgs &a, int dtype) {
 // When K1s replaces K1 (same-box grid n x h at 1 GiB, profiles/r2/k1s_grid_r2.txt): K1s is
 // 5-39 % faster for n <= 512 at every h measured (2..32) and for n in (512, 1024] outside
 // h = 9..11, where the persistent staged K1 is 1-2 % faster (C2: n = 1024, h = 10); U must stay
-// L1-resident next to nothing else (h n 4 <= 128 KB).
+// L1-resident next to nothing else (h n 4 <= 128 KB).  (Multi-warp column groups for
+// n in (1024, 4096], partial dots summed through shared memory, were measured 8-38 % slower than
+// the persistent K1 for h >= 8 at n = 2048 / 4096 and were removed.)
 bool stream_preferred(const FusedArgs &a) {
     const int64_t ub = a.h * a.n * 4;
     if (ub > (int64_t(128) << 10)) return false;

@@ -801,31 +801,30 @@ __global__ void __launch_bounds__(480, 1)
             // (sum = leading + trailing in both cases: deterministic) and writes G.  Nobody
             // waits, so the protocol needs no co-residency.
             const bool split = head || tail;
-            const size_t hp = static_cast<size_t>(head ? blockIdx.x - 1 : blockIdx.x);
-            float *mine = part + (2 * hp + (head ? 1 : 0)) * kTileCols * b;
-            const float *other = part + (2 * hp + (head ? 0 : 1)) * kTileCols * b;
-            auto store_g = [&](int c, const float (&v)[32]) {
-                if (j >= N) return;
-                uint32_t H[16], L[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
-                uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
-                uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
-                    gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
-                }
-            };
             if (!split) {
                 for (int c = 0; c < b / 32; ++c) {
                     float v[32];
                     tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
                                       static_cast<uint32_t>(a * 256 + c * 32),
                                   v);
-                    store_g(c, v);
+                    if (j < N) {
+                        uint32_t H[16], L[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
+                        uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
+                        uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
+                            gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
+                        }
+                    }
                 }
             } else {
+                // the boundary's slot pair: [leading partial, trailing partial]
+                const size_t hp = static_cast<size_t>(head ? blockIdx.x - 1 : blockIdx.x);
+                float *mine = part + (2 * hp + (head ? 1 : 0)) * kTileCols * b;
+                const float *other = part + (2 * hp + (head ? 0 : 1)) * kTileCols * b;
                 for (int c = 0; c < b / 32; ++c) {
                     float v[32];
                     tc::tmem_ld32(tbase + (static_cast<uint32_t>(q * 32) << 16) +
@@ -851,16 +850,22 @@ __global__ void __launch_bounds__(480, 1)
                     for (int c = 0; c < b / 32; ++c) {
                         const float *s0 = lead + (static_cast<size_t>(c) * kTileCols + jl) * 32;
                         const float *s1 = trail + (static_cast<size_t>(c) * kTileCols + jl) * 32;
-                        float v[32];
+                        uint32_t H[16], L[16];
 #pragma unroll
                         for (int e = 0; e < 8; ++e) {
                             const float4 p0 = ld_cg4(s0 + 4 * e), p1 = ld_cg4(s1 + 4 * e);
-                            v[4 * e] = p0.x + p1.x;
-                            v[4 * e + 1] = p0.y + p1.y;
-                            v[4 * e + 2] = p0.z + p1.z;
-                            v[4 * e + 3] = p0.w + p1.w;
+                            tc::split2(p0.x + p1.x, p0.y + p1.y, H[2 * e], L[2 * e]);
+                            tc::split2(p0.z + p1.z, p0.w + p1.w, H[2 * e + 1], L[2 * e + 1]);
                         }
-                        store_g(c, v);
+                        if (j < N) {
+                            uint4 *gh = reinterpret_cast<uint4 *>(Gt + j * b + c * 32);
+                            uint4 *gl = reinterpret_cast<uint4 *>(Glo + j * b + c * 32);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                gh[e] = make_uint4(H[4 * e], H[4 * e + 1], H[4 * e + 2], H[4 * e + 3]);
+                                gl[e] = make_uint4(L[4 * e], L[4 * e + 1], L[4 * e + 2], L[4 * e + 3]);
+                            }
+                        }
                     }
                 }
             }
@@ -1085,22 +1090,25 @@ __global__ void __launch_bounds__(640, 1)
         constexpr int kBoxes = kTileCols / kXBoxCols;   // X boxes per r-chunk
         static_assert(kBoxes % 4 == 0, "one consumer group per stage (nxs % 4 == 0)");
         int64_t seq = 0;   // position in the X box ring (both groups follow it)
+        const bool lag = nxs >= 8;
+        int pend = -1;     // storer: the box whose release waits for the next store
         for_segments([&](int tile, int rlo, int rhi) {
             for (int rc = rlo; rc < rhi; ++rc, seq += kBoxes) {
                 // NEXT-f2: below row rc0*128 the block's V rows are zero, no MMA ran: those
                 // rows are copied (scaled) when the pass is out of place
                 const bool mma_rc = rc >= rc0;
+                const int r = rc * kRowChunk + r_in;
+                // pre-scale of X (Lambda for the symmetric block, D for a right factor D)
+                // and post-scale of the result (a left factor D, NEXT-f1): loaded before the
+                // accumulator wait so that their latency hides behind it
+                const float lr = (lam && r < n) ? __ldg(lam + r) : 1.f;
+                const float pr = (post && r < n) ? __ldg(post + r) : 1.f;
                 if (mma_rc) {
                     const unsigned long long t0 = clock64();
                     mbar_wait(&bars->acc_full[a], aph);
                     w_a += clock64() - t0;
                     tc::fence_after_sync();
                 }
-                const int r = rc * kRowChunk + r_in;
-                // pre-scale of X (Lambda for the symmetric block, D for a right factor D)
-                // and post-scale of the result (a left factor D, NEXT-f1)
-                const float lr = (lam && r < n) ? lam[r] : 1.f;
-                const float pr = (post && r < n) ? post[r] : 1.f;
 #pragma unroll
                 for (int k = 0; k < kBoxes / 4; ++k) {
                     const int cb = grp + 4 * k;
@@ -1132,8 +1140,18 @@ __global__ void __launch_bounds__(640, 1)
                     if (q == 0 && lane == 0) {
                         tc::tma_store_2d(&tmYs, Xs(s), rc * kRowChunk, tile * kTileCols + cb * kXBoxCols);
                         tc::bulk_commit();
-                        tc::bulk_wait_read0();   // the box may be refilled once TMA has read it
-                        tc::mbar_arrive(&bars->xempty[s]);
+                        // a box may be refilled once TMA has read it; with >= 8 stages the
+                        // storer releases the PREVIOUS box instead of waiting for this one
+                        // (the read of this box overlaps the group's next box): same-box A/B
+                        // C3 / C5 h=64 -0.8 / -1 %
+                        if (lag) {
+                            tc::bulk_wait_read1();
+                            if (pend >= 0) tc::mbar_arrive(&bars->xempty[pend]);
+                            pend = s;
+                        } else {
+                            tc::bulk_wait_read0();
+                            tc::mbar_arrive(&bars->xempty[s]);
+                        }
                     }
                 }
                 if (mma_rc) {
@@ -1431,6 +1449,8 @@ __global__ void __launch_bounds__(640, 1)
                 if (q == 0 && lane == 0) {
                     tc::tma_store_2d(&tmYs, Xs(s), r0, tile * kTileCols);
                     tc::bulk_commit();
+                    // (releasing the previous box instead, as the SS update does, was
+                    // measured 2-3 % slower here at b = 256 / 1024)
                     tc::bulk_wait_read0();
                     tc::mbar_arrive(&bars->xempty[s]);
                 }
