@@ -100,8 +100,8 @@ __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h
                                int64_t n_pad, const float *__restrict__ lam, int lam_blk, int b,
                                int extra, int reverse, float *__restrict__ Wf,
                                uint16_t *__restrict__ Wb) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     const int64_t R = h_pad + extra;
     const int64_t total = R * n_pad;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -124,8 +124,8 @@ __global__ void wy_pack_kernel(const float *__restrict__ U, int64_t n, int64_t h
 // out[r] = a[r] * b[r] (the symmetric block's pre-scale Lambda D for a two-sided D)
 __global__ void wy_vmul_kernel(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
                                float *__restrict__ out) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
          r += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[r] = a[r] * b[r];
@@ -138,9 +138,11 @@ __global__ void wy_vmul_kernel(const float *__restrict__ a, const float *__restr
 __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ Wf, int64_t n_pad,
                                                       int b, int nsplit, int rows, int blk0,
                                                       const float *__restrict__ wt, int full,
-                                                      float *__restrict__ Sp) {
+                                                      float *__restrict__ Sp, int dep_wait) {
+    // dep_wait = 0: launched behind the first projection, whose result it does not read (its
+    // input W was packed before that projection started): it runs beside it, not after it
+    if (dep_wait) pdl_wait();
     pdl_trigger();
-    pdl_wait();
     const int ti = blockIdx.x, tj = blockIdx.y;
     const int blk = blockIdx.z / nsplit, sp = blockIdx.z % nsplit;
     if (ti > tj && !full) return;
@@ -190,8 +192,8 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
 // splits q, q + 32, ... then a butterfly (small b: few elements, many splits).
 __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int nblk, int nsplit,
                                       int full, float *__restrict__ S, int thread_per_elem) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     const int64_t bb = static_cast<int64_t>(b) * b;
     if (thread_per_elem) {
         for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -231,8 +233,8 @@ __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int n
 // 2 = [c,c+32)):  T[0:c, c:c+32] = -T[0:c,0:c] * (S[0:c, c:c+32] * T[c:c+32, c:c+32]).
 __global__ void __launch_bounds__(256) wy_tbuild_kernel(const float *__restrict__ Sg, int b,
                                                           float *__restrict__ Tg, int diag_only) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     extern __shared__ float tsm[];
     const int blk = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -353,8 +355,8 @@ __global__ void __launch_bounds__(256) wy_vrec_kernel(const float *__restrict__ 
                                                       const float *__restrict__ Tg, int64_t n_pad,
                                                       int b, uint16_t *__restrict__ Vt,
                                                       int64_t lo_off) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     extern __shared__ float vsm[];
     constexpr int RW = 32 * RP;   // rows per CTA
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * RW;
@@ -491,8 +493,8 @@ __global__ void __launch_bounds__(256) wy_rowgemm_kernel(
     int K, const float *__restrict__ C, int64_t ldc, const float *__restrict__ alpha,
     int64_t alpha_n, float sgn, float *__restrict__ Of, uint16_t *__restrict__ Ob, int64_t ldo,
     int64_t lo_off) {
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();
     const int64_t r0 = blockIdx.x * 64;
     const int c0 = blockIdx.y * 32;
     __shared__ float As[32][65], Bs[32][33];
@@ -654,8 +656,8 @@ __global__ void __launch_bounds__(480, 1)
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = bars->tmem;
-    pdl_trigger();
     pdl_wait();   // the previous kernel's results (after this CTA's setup)
+    pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -966,8 +968,8 @@ __global__ void __launch_bounds__(640, 1)
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = bars->tmem;
-    pdl_trigger();
     pdl_wait();   // the previous kernel's results (after this CTA's setup)
+    pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -1270,8 +1272,8 @@ __global__ void __launch_bounds__(640, 1)
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = bars->tmem;
-    pdl_trigger();
     pdl_wait();   // the previous kernel's results (after this CTA's setup)
+    pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -1670,12 +1672,13 @@ struct Pass {
 }  // namespace
 
 namespace {
-thread_local int t_pdl = 1;   // A/B hook (hh_debug_wy_pdl)
+thread_local int t_pdl = 1;   // A/B hooks (hh_debug_wy_pdl): PDL launches, and
+thread_local int t_overlap = 1;   // the preparation beside the first projection
 // every kernel of the block program is launched with programmatic stream serialization (PDL):
 // see pdl_trigger / pdl_wait
 template <typename... K, typename... A>
-cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                       A &&...args) {
+cudaError_t launch_k(bool use_pdl, void (*kernel)(K...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, A &&...args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -1685,14 +1688,20 @@ cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem,
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = t_pdl ? 1 : 0;
+    cfg.numAttrs = (t_pdl && use_pdl) ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+template <typename... K, typename... A>
+cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       A &&...args) {
+    return launch_k(true, kernel, grid, block, smem, stream, std::forward<A>(args)...);
 }
 }  // namespace
 
 int wy_set_pdl(int on) {
-    const int prev = t_pdl;
-    t_pdl = on;
+    const int prev = t_pdl | (t_overlap << 1);
+    t_pdl = on & 1;
+    t_overlap = (on >> 1) & 1;
     return prev;
 }
 
@@ -1751,7 +1760,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         if (me != cudaSuccess) return me;
     }
 
-    // ---------------- K4: pack + Gram + T + V (and the symmetric block's operands)
+    // ---------------- K4: pack (the projection's operand W) ...
     {
         const int64_t tot = R * n_pad;
         const int g = static_cast<int>(std::min<int64_t>((tot + 255) / 256, sms * 16));
@@ -1761,15 +1770,20 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         const int rev = p.kind == WY_APPLY_T ? 1 : 0;
         ++nlaunch, note(pdl_launch(wy_pack_kernel, g, 256, 0, stream, U, p.n, p.h, p.h_pad, n_pad, lam, m - 1, b,
                                                          p.extra, rev, Wf, Wb));
+    }
+    // ... and the rest of the preparation (Gram, T, V = W T, the symmetric block's operands),
+    // which only the updates read.  gram_wait = 0: launched behind the first projection, on
+    // the SMs that projection leaves free, so that it runs beside it.
+    auto prep_rest = [&](int gram_wait) {
         const int tb = (b + 63) / 64;
         ++nlaunch, note(pdl_launch(wy_gram_kernel, dim3(tb, tb, m * p.nsplit), 256, 0, stream, Wf, n_pad, b, p.nsplit, p.gram_rows, 0,
-                                                                       nullptr, 0, Sp));
+                                                                       nullptr, 0, Sp, gram_wait));
         const int64_t ns = static_cast<int64_t>(m) * b * b;
         ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, static_cast<int>(std::min<int64_t>((ns * 32 + 255) / 256, sms * 16)),
                                 256, 0, stream, Sp, b, m, p.nsplit, 0, S, ns >= 32768 ? 1 : 0));
         if (sym) {   // P = W^T Lambda W of the last block (full)
             ++nlaunch, note(pdl_launch(wy_gram_kernel, dim3(tb, tb, p.nsplit), 256, 0, stream, Wf, n_pad, b, p.nsplit, p.gram_rows,
-                                                                       m - 1, lam, 1, F(p.off_pp)));
+                                                                       m - 1, lam, 1, F(p.off_pp), 1));
             ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, std::max(1, std::min(sms * 16, (b * b * 32 + 255) / 256)), 256, 0, stream, 
                 F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p), b * b >= 32768 ? 1 : 0));
         }
@@ -1822,7 +1836,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                     nullptr, As, 2 * b, alo));
             }
         }
-    }
+    };
     cudaError_t e = lerr != cudaSuccess ? lerr : cudaGetLastError();
     if (e != cudaSuccess) return e;
 
@@ -1911,6 +1925,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         else ts_all = false;
     }
     if (t_fk.on && debug_stop_blocks < 0 && Y && sms >= 2 && (ss_all || ts_all) && np == p.np) {
+        prep_rest(1);
         // ~10 KB of kernel parameters (maps + pass table): built on the heap, copied at launch
         std::unique_ptr<FlowArgs> fap(new (std::nothrow) FlowArgs());
         if (!fap) return cudaErrorMemoryAllocation;
@@ -1999,15 +2014,24 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         return cudaGetLastError();
     }
 
-    const int grid = std::max(1, std::min(std::min(ntiles, sms), kSlots1));
+    // The first projection needs only the packed W: the rest of the preparation (Gram, T, V)
+    // is launched behind it without waiting for it and runs on the kPrepSms SMs it leaves
+    // free; the first update is a plain launch (it waits for both), later passes chain by PDL.
+    constexpr int kPrepSms = 8;
+    const int grid_all = std::max(1, std::min(std::min(ntiles, sms), kSlots1));
+    const bool overlap = t_overlap != 0;
+    if (!overlap) prep_rest(1);
+    const int grid_first =
+        overlap ? std::max(1, std::min(grid_all, sms > 4 * kPrepSms ? sms - kPrepSms : sms)) : grid_all;
     const float *cur = X;
     for (int q = 0; q < np; ++q) {
         const Pass &ps = prog[q];
         const CUtensorMap &mcur = (cur == X) ? mX : mY;
-        ++nlaunch, note(pdl_launch(wy_project_kernel, grid, 480, smem1(ps.kw), stream, 
+        ++nlaunch, note(pdl_launch(wy_project_kernel, q == 0 ? grid_first : grid_all, 480, smem1(ps.kw), stream,
             mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
             ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw), F(p.off_part),
             reinterpret_cast<int *>(w + p.off_flag)));
+        if (q == 0 && overlap) prep_rest(0);
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
         const int64_t uxrc = (cur != Y && ps.row0 >= kRowChunk) ? 0 : ps.row0 / kRowChunk;
         const int64_t units = static_cast<int64_t>(ntiles) * (n_pad / kRowChunk - uxrc);
@@ -2015,14 +2039,14 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         // TS-mode update (G in TMEM) for the wide blocks: the resident G no longer competes
         // with the V and X rings for shared memory
         if (ps.kw >= t_ts_min) {
-            ++nlaunch, note(pdl_launch(wy_update_ts_kernel, grid3, 640, smem4(), stream, 
+            ++nlaunch, note(launch_k(q != 0 || !overlap, wy_update_ts_kernel, grid3, 640, smem4(), stream,
                 Gt, *ps.mV, (cur == X) ? mXb2 : mYb2, mYb2, ps.pre, ps.post, static_cast<int>(p.n),
                 static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
                 ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, t_timeline));
             cur = Y;
             continue;
         }
-        ++nlaunch, note(pdl_launch(wy_update_kernel, grid3, 640, smem3(ps.kw), stream, 
+        ++nlaunch, note(launch_k(q != 0 || !overlap, wy_update_kernel, grid3, 640, smem3(ps.kw), stream,
             *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
             static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
             ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw),
@@ -2031,7 +2055,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     }
     if (info) {
         info->variant = sym ? "wy_sym_bf16x3_tcgen05" : "wy_bf16x3_tcgen05";
-        info->grid = grid;
+        info->grid = grid_all;
         info->block = 480;
         info->smem = static_cast<int>(smem1(b));
         info->nchunks = np;

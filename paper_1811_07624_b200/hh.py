@@ -10,6 +10,7 @@ hh_workspace_bytes.  Layout (hh.h): U is a (h, n) tensor (row i = u_{i+1},
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import re
@@ -201,11 +202,37 @@ def _validate(X: torch.Tensor, xname: str = "X", U: Optional[torch.Tensor] = Non
     return N, n, h
 
 
+_NULLCTX = contextlib.nullcontext()
+
+
+def _on(device: torch.device):
+    """Run the call on `device` (its current stream): a device guard only when it is not
+    already the current device (the guard costs microseconds per call)."""
+    if device.type == "cuda" and device.index is not None and device.index != torch.cuda.current_device():
+        return torch.cuda.device(device)
+    return _NULLCTX
+
+
+_WS_CACHE = {}
+
+
+def clear_workspace_cache() -> None:
+    """Forget the memoised workspace sizes (after changing a debug knob that sizes them)."""
+    _WS_CACHE.clear()
+
+
 def _workspace(call: int, n: int, h: int, N_or_M: int, npairs: int, like: torch.Tensor,
                workspace: Optional[torch.Tensor]):
     """(workspace tensor or None, bytes to pass): the query's size, allocated on `like`'s
-    device when not given or too small; a given workspace must be on that device."""
-    wsb = hh_workspace_bytes(call, n, h, N_or_M, npairs, like.dtype)
+    device when not given or too small; a given workspace must be on that device.  The
+    library's size query is memoised per (call, shape, dtype, this thread's algo selection)."""
+    key = (call, n, h, N_or_M, npairs, like.dtype, int(lib().hh_get_algo()))
+    wsb = _WS_CACHE.get(key)
+    if wsb is None:
+        wsb = hh_workspace_bytes(call, n, h, N_or_M, npairs, like.dtype)
+        if len(_WS_CACHE) > 4096:
+            _WS_CACHE.clear()
+        _WS_CACHE[key] = wsb
     if not wsb:
         return None, 0
     if workspace is not None:
@@ -270,7 +297,7 @@ def hh_apply(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Tensor
     if Y is None:
         Y = torch.empty_like(X)
     N, n, h = _validate(X, U=U, same={"Y": Y})
-    with torch.cuda.device(X.device):
+    with _on(X.device):
         ws, wsb = _workspace(HH_CALL_APPLY, n, h, N, 0, X, workspace) if N else (None, 0)
         st = lib().hh_apply(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,
                             _dtype(X), _ptr(ws), wsb, _stream(stream, X.device))
@@ -286,7 +313,7 @@ def hh_sym_apply(U: torch.Tensor, lam: torch.Tensor, X: torch.Tensor,
     if Y is None:
         Y = torch.empty_like(X)
     N, n, h = _validate(X, U=U, same={"Y": Y}, vecs={"lambda": lam})
-    with torch.cuda.device(X.device):
+    with _on(X.device):
         ws, wsb = _workspace(HH_CALL_SYM, n, h, N, 0, X, workspace) if N else (None, 0)
         st = lib().hh_sym_apply(n, h, _ptr(U) if h else None, _ptr(lam), _ptr(X), _ptr(Y), N,
                                 _dtype(X), _ptr(ws), wsb, _stream(stream, X.device))
@@ -302,7 +329,7 @@ def hh_apply_signed(op: int, side: int, U: torch.Tensor, d: torch.Tensor, X: tor
     if Y is None:
         Y = torch.empty_like(X)
     N, n, h = _validate(X, U=U, same={"Y": Y}, vecs={"d": d})
-    with torch.cuda.device(X.device):
+    with _on(X.device):
         ws, wsb = _workspace(HH_CALL_APPLY, n, h, N, 0, X, workspace) if N else (None, 0)
         st = lib().hh_apply_signed(int(op), int(side), n, h, _ptr(U) if h else None, _ptr(d),
                                    _ptr(X), _ptr(Y), N, _dtype(X), _ptr(ws), wsb,
@@ -318,7 +345,7 @@ def hh_sym_apply_signed(U: torch.Tensor, d: torch.Tensor, lam: torch.Tensor, X: 
     if Y is None:
         Y = torch.empty_like(X)
     N, n, h = _validate(X, U=U, same={"Y": Y}, vecs={"d": d, "lambda": lam})
-    with torch.cuda.device(X.device):
+    with _on(X.device):
         ws, wsb = _workspace(HH_CALL_SYM, n, h, N, 0, X, workspace) if N else (None, 0)
         st = lib().hh_sym_apply_signed(n, h, _ptr(U) if h else None, _ptr(d), _ptr(lam),
                                        _ptr(X), _ptr(Y), N, _dtype(X), _ptr(ws), wsb,
@@ -348,7 +375,7 @@ def hh_mahalanobis(U: torch.Tensor, d: torch.Tensor, P: torch.Tensor, ia: torch.
     _dev(dist, "dist")
     if dist.numel() != npairs or dist.dtype != P.dtype or dist.device != P.device:
         raise ValueError(f"dist must hold {npairs} values of {P.dtype} on {P.device}")
-    with torch.cuda.device(P.device):
+    with _on(P.device):
         ws, wsb = (None, 0) if fused else _workspace(HH_CALL_MAHALANOBIS, n, h, M, npairs, P,
                                                       workspace)
         st = lib().hh_mahalanobis(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P), M, _ptr(ia),
@@ -365,7 +392,7 @@ def hh_apply_qr(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.Ten
     if Y is None:
         Y = torch.empty_like(X)
     N, n, h = _validate(X, U=U, same={"Y": Y})
-    with torch.cuda.device(X.device):
+    with _on(X.device):
         ws, wsb = _workspace(HH_CALL_APPLY, n, h, N, 0, X, workspace) if N else (None, 0)
         st = lib().hh_apply_qr(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,
                                _dtype(X), _ptr(ws), wsb, _stream(stream, X.device))
@@ -386,7 +413,7 @@ def hh_congruence(op: int, U: torch.Tensor, M: torch.Tensor, out: Optional[torch
         raise ValueError(f"out must be {tuple(M.shape)} {M.dtype}")
     _validate(M.view(count * n, n), "M", U=U, same={"out": out.view(count * n, n)})
     h = U.shape[0] if U.numel() else 0
-    with torch.cuda.device(M.device):
+    with _on(M.device):
         ws, wsb = _workspace(HH_CALL_CONGRUENCE, n, h, count, 0, M, workspace)
         st = lib().hh_congruence(int(op), n, h, _ptr(U) if h else None, _ptr(M), _ptr(out),
                                  count, _dtype(M), _ptr(ws), wsb, _stream(stream, M.device))
@@ -407,7 +434,7 @@ def hh_knn(U: torch.Tensor, d: torch.Tensor, P_ref: torch.Tensor, P_query: torch
     Mq = P_query.shape[0]
     idx = torch.empty(Mq, k, dtype=torch.int32, device=P_ref.device)
     dist = torch.empty(Mq, k, dtype=P_ref.dtype, device=P_ref.device)
-    with torch.cuda.device(P_ref.device):
+    with _on(P_ref.device):
         ws, wsb = _workspace(HH_CALL_KNN, n, h, Mr, Mq, P_ref, workspace)
         st = lib().hh_knn(n, h, _ptr(U) if h else None, _ptr(d), _ptr(P_ref), Mr, _ptr(P_query),
                           Mq, int(k), _ptr(idx), _ptr(dist), _dtype(P_ref), _ptr(ws), wsb,
@@ -425,7 +452,7 @@ def hh_apply_host(op: int, U: torch.Tensor, X: torch.Tensor, Y: Optional[torch.T
     N, n, h = _validate(X, U=U, same={"Y": Y}, host=True)
     device = workspace.device if workspace is not None else torch.device(
         "cuda", torch.cuda.current_device())
-    with torch.cuda.device(device):
+    with _on(device):
         ws, wsb = _workspace(HH_CALL_APPLY_HOST, n, h, N, 0,
                              torch.empty(0, dtype=X.dtype, device=device), workspace)
         st = lib().hh_apply_host(int(op), n, h, _ptr(U) if h else None, _ptr(X), _ptr(Y), N,

@@ -30,6 +30,7 @@ def knobs(**kw):
         v[6] = 3
     arr = (ctypes.c_int * 7)(*v)
     L.hh_debug_wy_flow_knobs(arr, 7)
+    hh.hh.clear_workspace_cache()
 
 
 def setup(name):

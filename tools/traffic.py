@@ -40,7 +40,7 @@ def parse():
         hdr = rows[0]
         ki, mi, vi, ui = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
         kern = {}
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
                  "msecond": 1e-3}
         for r in rows[1:]:
             name = r[ki].split("(")[0].split("<")[0].replace("(anonymous namespace)::", "")
