@@ -2019,7 +2019,10 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     // free; the first update is a plain launch (it waits for both), later passes chain by PDL.
     constexpr int kPrepSms = 8;
     const int grid_all = std::max(1, std::min(std::min(ntiles, sms), kSlots1));
-    const bool overlap = t_overlap != 0;
+    // (same box, tools/prep_ab.py: -4 % at h = 1024 (4 blocks), -1 % at h = 256; +0.4-0.5 % on
+    // the one-block b <= 64 programs C3 / C5 h=64, whose short preparation does not pay for the
+    // projection's 8 SMs)
+    const bool overlap = t_overlap != 0 && (m > 1 || b >= 128);
     if (!overlap) prep_rest(1);
     const int grid_first =
         overlap ? std::max(1, std::min(grid_all, sms > 4 * kPrepSms ? sms - kPrepSms : sms)) : grid_all;
