@@ -52,6 +52,14 @@ def workload_case(name: str, N_override=None):
         return gi.make_config(5, h=int(name[3:]), N=N_override)
     if name == "KNN":   # NEXT-f3, Table-I-shaped (MNIST after PCA) synthetic stand-in
         return gi.make_knn_case()
+    if name == "CONG":   # NEXT-f4: SHF congruences op(Q) M op(Q)^T, 64 matrices of n = 512, h = 18
+        n, h, cnt = 512, 18, 64   # h = ceil(2 log2 n): the middle of Table I's h range
+        g = gi.rng(600, n, h, cnt)
+        c = gi.make_case("apply", n, h, 1, "f32", seed=60)
+        c.U = gi.unit_reflectors(g, h, n, "f32")
+        c.X = gi.gaussian_columns(g, cnt * n, n, "f32")     # (count * n, n) == count n x n matrices
+        c.N, c.call, c.name, c.count = cnt * n, "congruence", "CONG", cnt
+        return c
     if name.startswith("QR"):   # NEXT-f2: n=4096, h = n-1 partial-QR reflectors (C5's X)
         h = int(name[2:]) if len(name) > 2 else 4095
         c = gi.make_config(5, h=min(h, 1024), N=N_override)
@@ -69,6 +77,10 @@ def alg_cost(c, op_count=1):
         byts = (c.N + Mq) * c.n * s + Mq * c.k * 8           # points read once + results
         flops = 4 * c.h * c.n * (c.N + Mq) + 2 * c.n * c.N * Mq   # transform once + dots
         return byts, flops, Mq
+    if c.call == "congruence":   # op(Q) M op(Q)^T: M read once, written once; 2 x 4hn per column
+        byts = 2 * c.count * c.n * c.n * s
+        flops = 2 * 4 * c.h * c.n * c.n * c.count
+        return byts, flops, c.count
     if c.call == "mahalanobis":
         P = c.npairs
         byts = c.N * c.n * s + 2 * P * 4 + P * s          # points once + indices + dist
@@ -217,6 +229,8 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
         t0 = time.perf_counter()
         if c.call == "knn":
             res["out"] = oracle.knn(c.U, c.d, c.X, c.lam[:k], c.k)
+        elif c.call == "congruence":
+            res["out"] = oracle.congruence(op, c.U, c.X[:k * c.n].reshape(k, c.n, c.n))
         elif c.call == "mahalanobis":
             res["out"] = oracle.mahalanobis(c.U, c.d, c.X, c.ia[:k], c.ib[:k])
         elif c.call == "sym":
@@ -226,7 +240,7 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
         return time.perf_counter() - t0
 
     total = units
-    k = min(total, {"mahalanobis": 2048, "knn": 4}.get(c.call, 256))
+    k = min(total, {"mahalanobis": 2048, "knn": 4, "congruence": 1}.get(c.call, 256))
     dt = run(k)
     while dt < 0.5 and k < total:
         k = min(total, k * 4)
@@ -237,7 +251,7 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
     if k2 != k:
         dt = run(k2)
         k = k2
-    what = {"mahalanobis": "pairs", "knn": "queries"}.get(c.call, "columns")
+    what = {"mahalanobis": "pairs", "knn": "queries", "congruence": "matrices"}.get(c.call, "columns")
     return (per_unit_bytes * k / dt / 1e9, k / dt, dt,
             f"{k} of {total} {what} of {c.name} (fp64 oracle, {threads} threads)", threads, k,
             res["out"])
@@ -257,6 +271,10 @@ def parity_of(c, k, ref, Y, dist_out, knn_out, dev):
         return {"rel_l2_dist": e, "index_agreement": float((gi_[:k].cpu().numpy() == ri).mean()),
                 "gate": g, "sampled": int(k), "of": int(c.lam.shape[0]),
                 "pass": bool(e <= g)}
+    if c.call == "congruence":
+        got = Y[:k * c.n].double().cpu().numpy().reshape(ref.shape)
+        e = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        return {"rel_fro": e, "gate": g, "sampled": int(k), "of": int(c.count), "pass": bool(e <= g)}
     if c.call == "mahalanobis":
         got = dist_out[:k].double().cpu().numpy()
         e = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
@@ -300,6 +318,8 @@ def run_reference(args):
         t0 = time.perf_counter()
         if c.call == "knn":
             oracle.knn(sub.U, sub.d, sub.X, sub.lam[:k], sub.k)
+        elif c.call == "congruence":
+            oracle.congruence(op, sub.U, sub.X[:k * sub.n].reshape(k, sub.n, sub.n))
         elif c.call == "mahalanobis":
             oracle.mahalanobis(sub.U, sub.d, sub.X, sub.ia[:k], sub.ib[:k])
         elif c.call == "sym":
@@ -311,7 +331,7 @@ def run_reference(args):
             times.append(dt)
     tot = sum(times)
     value = per_unit_bytes * k * steps / tot / 1e9
-    what = {"mahalanobis": "pairs", "knn": "queries"}.get(c.call, "columns")
+    what = {"mahalanobis": "pairs", "knn": "queries", "congruence": "matrices"}.get(c.call, "columns")
     sample = f"{k} of {units} {what} of {c.name} per step (fp64 oracle, {threads} threads)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
@@ -336,6 +356,8 @@ def config_of(c, args):
          > 256 << 20 else "L2-resident inputs (warm L2, labelled)"}
     if c.call == "mahalanobis":
         d["npairs"] = c.npairs
+    if c.call == "congruence":
+        d.update({"count": c.count, "op": args.op, "form": "op(Q) M op(Q)^T (eq:ak / eq:bk, P:297-304)"})
     if c.call == "knn":
         d.update({"M_ref": c.N, "M_query": int(c.lam.shape[0]), "k": c.k,
                   "stand_in_for": "Table I MNIST after PCA (P:670), iid N(0,1)"})
@@ -393,6 +415,13 @@ def run_hh(args):
         step = lambda: hh.hh_mahalanobis(U, d, X, ia, ib, dist_out, workspace=wsp,  # noqa: E731
                                          stream=stream)
         launches = 2
+    elif c.call == "congruence":
+        M = X.view(c.count, c.n, c.n)
+        Mo = Y.view(c.count, c.n, c.n)
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_CONGRUENCE, c.n, c.h, c.count, 0, X.dtype)
+        wsp = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        step = lambda: hh.hh_congruence(op, U, M, Mo, workspace=wsp, stream=stream)  # noqa: E731
+        launches = 4
     elif c.call == "apply_qr":
         wsb = hh.hh_workspace_bytes(hh.HH_CALL_APPLY, c.n, c.h, c.N, 0, X.dtype)
         wsp = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)

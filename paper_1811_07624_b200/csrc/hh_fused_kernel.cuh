@@ -25,6 +25,7 @@
 //     TPC > 32), so every thread of the group holds the identical alpha.
 #pragma once
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -68,6 +69,14 @@ __device__ __forceinline__ void vfma(double2 &acc, const double2 &u, const doubl
     acc.y = fma(u.y, x.y, acc.y);
 }
 __device__ __forceinline__ float vsum(const float4 &a) { return (a.x + a.y) + (a.z + a.w); }
+// two IEEE fp32 adds in one instruction (FADD2): d = a + b elementwise
+__device__ __forceinline__ void fadd2(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 A, B, D;\n\t"
+        "mov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\t"
+        "add.rn.f32x2 D, A, B;\n\tmov.b64 {%0, %1}, D;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
 __device__ __forceinline__ double vsum(const double2 &a) { return a.x + a.y; }
 // x <- x - s * u
 __device__ __forceinline__ void vaxpy(float4 &x, float s, const float4 &u) {
@@ -265,6 +274,26 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             if constexpr (kKeepU) return uk[k];
             else return ub[gt + TPC * k];
         };
+        // fp32, two columns per single-warp group: the partial sums and the butterfly use
+        // packed FADD2 (two IEEE adds per instruction) -- fewer issue slots on the serial chain
+        constexpr bool kPair = std::is_same<T, float>::value && C == 2 && TPC <= 32;
+        if constexpr (kPair) {
+            V acc0, acc1;
+            vzero(acc0);
+            vzero(acc1);
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                if (valid_k(k)) {
+                    const V uk0 = uget(k);
+                    vfma(acc0, uk0, x[0][k]);
+                    vfma(acc1, uk0, x[1][k]);
+                }
+            }
+            float a0, a1, b0, b1;
+            fadd2(a0, a1, acc0.x, acc0.y, acc0.z, acc0.w);   // (x + z, y + w)
+            fadd2(b0, b1, acc1.x, acc1.y, acc1.z, acc1.w);
+            fadd2(p[0], p[1], a0, b0, a1, b1);
+        } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             V acc;
@@ -274,6 +303,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 if (valid_k(k)) vfma(acc, uget(k), x[c][k]);
             }
             p[c] = vsum(acc);
+        }
         }
         if constexpr (TPC > 32 && C == 2) {
             // two columns over a multi-warp group: reduce-scatter in the warp (the first step
@@ -295,6 +325,13 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 p[c] = sum;
             }
             rpar ^= 1;
+        } else if constexpr (kPair) {
+#pragma unroll
+            for (int off = TPC / 2; off > 0; off >>= 1) {
+                const float t0 = __shfl_xor_sync(0xffffffffu, p[0], off);
+                const float t1 = __shfl_xor_sync(0xffffffffu, p[1], off);
+                fadd2(p[0], p[1], p[0], p[1], t0, t1);
+            }
         } else {
 #pragma unroll
         for (int off = (TPC < 32 ? TPC : 32) / 2; off > 0; off >>= 1) {
@@ -318,6 +355,18 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             rpar ^= 1;
         }
         }
+        if constexpr (kPair) {
+            float s0, s1;
+            fadd2(s0, s1, p[0], p[1], p[0], p[1]);   // 2 alpha for both columns at once
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                if (valid_k(k)) {
+                    const V uk0 = uget(k);
+                    vaxpy(x[0][k], s0, uk0);
+                    vaxpy(x[1][k], s1, uk0);
+                }
+            }
+        } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const T s = p[c] + p[c];
@@ -326,15 +375,29 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 if (valid_k(k)) vaxpy(x[c][k], s, uget(k));
             }
         }
+        }
     };
     // reflectors [r0, r1) of the chunk resident at `base` (first row = chunk_lo)
     // (NEXT-f2: the fused kernel applies QR-structured reflectors in full -- it serves
     // small h, where the zero prefixes are a negligible share; K5 skips them.)
     auto run_range = [&](const V *base, int chunk_lo, int r0, int r1, bool desc) {
-        if (desc) {
-            for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+        constexpr bool kPairLoop = std::is_same<T, float>::value && C == 2 && TPC <= 32;
+        if constexpr (kPairLoop) {
+            // two reflectors per loop trip: the loop bookkeeping is ~10 of the ~100 issue slots
+            // of a reflector here, and this kernel is issue-bound (C2 0.358 -> 0.353 ms, A/B)
+            if (desc) {
+#pragma unroll 2
+                for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+            } else {
+#pragma unroll 2
+                for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+            }
         } else {
-            for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+            if (desc) {
+                for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+            } else {
+                for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+            }
         }
     };
     auto scale_vec = [&]() {

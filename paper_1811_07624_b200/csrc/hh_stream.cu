@@ -46,6 +46,15 @@ __device__ __forceinline__ void ffma2s(float &d0, float &d1, float a0, float a1,
         : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
 
+// d0 += b0, d1 += b1 in one FADD2
+__device__ __forceinline__ void fadd2s(float &d0, float &d1, float b0, float b1) {
+    asm("{\n\t.reg .b64 A, B;\n\t"
+        "mov.b64 A, {%0, %1};\n\tmov.b64 B, {%2, %3};\n\t"
+        "add.rn.f32x2 A, A, B;\n\tmov.b64 {%0, %1}, A;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(b0), "f"(b1));
+}
+
 template <int TPC, int CH, int C, int NT>
 __global__ void __launch_bounds__(NT) hh_stream_kernel(const FusedArgs a) {
     constexpr int GPC = NT / TPC;   // column groups per CTA
@@ -102,12 +111,20 @@ __global__ void __launch_bounds__(NT) hh_stream_kernel(const FusedArgs a) {
                 ffma2s(s0, s1, uk[k].x, uk[k].y, x[c][k].x, x[c][k].y);
                 ffma2s(s2, s3, uk[k].z, uk[k].w, x[c][k].z, x[c][k].w);
             }
-            p[c] = (s0 + s1) + (s2 + s3);
+            fadd2s(s0, s1, s2, s3);   // (s0 + s2, s1 + s3)
+            p[c] = s0 + s1;
         }
+        // column pairs share packed FADD2s in the butterfly (two IEEE adds per instruction)
 #pragma unroll
-        for (int off = TPC / 2; off > 0; off >>= 1)
+        for (int off = TPC / 2; off > 0; off >>= 1) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) p[c] += __shfl_xor_sync(0xffffffffu, p[c], off);
+            for (int c = 0; c + 1 < C; c += 2) {
+                const float t0 = __shfl_xor_sync(0xffffffffu, p[c], off);
+                const float t1 = __shfl_xor_sync(0xffffffffu, p[c + 1], off);
+                fadd2s(p[c], p[c + 1], t0, t1);
+            }
+            if constexpr (C % 2) p[C - 1] += __shfl_xor_sync(0xffffffffu, p[C - 1], off);
+        }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const float s = -(p[c] + p[c]);

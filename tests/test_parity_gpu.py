@@ -304,3 +304,15 @@ def test_k1_and_k1s(k1_kind, n, h, N):
         hh.hh_apply(0, dev(c.U), X, Y=X)
     torch.cuda.synchronize()
     assert_parity(X.cpu().numpy(), oracle.apply(0, c.U, c.X), "f32", h, "alias")
+
+
+def test_apply_host_takes_the_wy_path():
+    """hh_apply_host past the crossover runs the compact-WY program on each device chunk
+    (it had always run K1) and matches the oracle."""
+    c = gi.make_case("apply", 1024, 64, 40000, "f32", seed=43)
+    X = torch.from_numpy(c.X).pin_memory()
+    U = torch.from_numpy(c.U)
+    for op in (0, 1):
+        Y = hh.hh_apply_host(op, U, X)
+        assert hh.last_launch_info()["variant"].startswith("wy_"), hh.last_launch_info()
+        assert_parity(Y.numpy(), oracle.apply(op, c.U, c.X), "f32", 64, f"host WY op{op}")
