@@ -136,9 +136,11 @@ __global__ void __launch_bounds__(NT) hh_stream_kernel(const FusedArgs a) {
         }
     };
     auto run_desc = [&]() {
+#pragma unroll 2
         for (int i = h - 1; i >= 0; --i) reflect(i);
     };
     auto run_asc = [&]() {
+#pragma unroll 2
         for (int i = 0; i < h; ++i) reflect(i);
     };
     if (mode == MODE_APPLY_N)
