@@ -900,7 +900,6 @@ struct Bars3 {
     uint64_t xfull[kXStages], xempty[kXStages];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem;
-    int progress;   // direct epilogue: row chunks finished (read by the L2 prefetcher)
 };
 
 __global__ void __launch_bounds__(640, 1)
@@ -1169,243 +1168,6 @@ __global__ void __launch_bounds__(640, 1)
         });
     }
     if (warp >= 4 && (warp & 3) == 0 && lane == 0) tc::bulk_wait0();
-    if (dbg && lane == 0) {
-        // [0] kernel cycles  [1,2] V producer: empty waits  [3,4] MMA: full waits, acc_empty
-        // waits  [5,6] X producer: xempty waits  [7,8] epilogue warp 4: acc_full, xfull waits
-        const unsigned long long tot = clock64() - t_k0;
-        if (warp == 0) { tl[0] = tot; tl[1] = w_a; }
-        if (warp == 1) { tl[3] = w_a; tl[4] = w_b; }
-        if (warp == 2) { tl[5] = w_a; }
-        if (warp == 4) { tl[7] = w_a; tl[8] = w_b; }
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 1) tc::tmem_free<256>(tbase);
-}
-
-__global__ void __launch_bounds__(640, 1)
-    wy_update_direct_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmV,
-                     const __grid_constant__ CUtensorMap tmXb,
-                     const __grid_constant__ CUtensorMap tmYs, float *Y,
-                     const float *__restrict__ lam, const float *__restrict__ post, int n,
-                     int n_pad, int64_t N, int b, int vrow_hi, int vrow_lo, int ntiles, int rc0,
-                     int copy_below, int nxs, unsigned long long *tl, const float *Xsrc) {
-    // tl (debug, CTA 0 only): per-role cycles spent waiting on each barrier (see
-    // hh_debug_wy_timeline); NULL in production
-    const bool dbg = tl != nullptr && blockIdx.x == 0;
-    unsigned long long t_k0 = clock64(), w_a = 0, w_b = 0;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    const int nslab = b / 32;
-    unsigned char *Ghi = smem;                       // nslab x 8 KB (128 columns x 32 K)
-    unsigned char *Glo = smem + nslab * 8192;
-    unsigned char *stg = smem + nslab * 16384;        // G hi/lo take nslab x 16 KB
-    Bars3 *bars = reinterpret_cast<Bars3 *>(stg + kStages3 * kStage3Bytes);   // no X ring
-    auto Vhi = [&](int s) { return stg + s * kStage3Bytes; };
-    auto Vlo = [&](int s) { return stg + s * kStage3Bytes + 8192; };
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nrc = n_pad / kRowChunk;
-    // balanced schedule: the (tile, row chunk) units, tile-major, are split into equal
-    // contiguous ranges per CTA (512 tiles over 148 SMs would otherwise leave a 4th-tile
-    // tail on some SMs); every role walks the same segments [rlo, rhi) of each tile.
-    // Rows below rc0 are copy-only (no MMA) and exist only when copy_below.
-    const int xrc0 = copy_below ? 0 : rc0;
-    const int64_t per = nrc - xrc0;
-    const int64_t utot = static_cast<int64_t>(ntiles) * per;
-    const int64_t ubeg = utot * blockIdx.x / gridDim.x, uend = utot * (blockIdx.x + 1) / gridDim.x;
-    auto for_segments = [&](auto &&fn) {
-        for (int64_t u = ubeg; u < uend;) {
-            const int tile = static_cast<int>(u / per);
-            const int64_t t0 = static_cast<int64_t>(tile) * per;
-            const int rlo = xrc0 + static_cast<int>(u - t0);
-            const int rhi = xrc0 + static_cast<int>(uend - t0 < per ? uend - t0 : per);
-            fn(tile, rlo, rhi);
-            u = t0 + per;
-        }
-    };
-    if (threadIdx.x == 0) {
-        mbar_init(&bars->gfull, 1);
-        mbar_init(&bars->gempty, 1);
-        for (int s = 0; s < kStages3; ++s) {
-            mbar_init(&bars->full[s], 1);
-            mbar_init(&bars->empty[s], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&bars->acc_full[a], 1);
-            mbar_init(&bars->acc_empty[a], 512);
-        }
-        bars->progress = 0;
-        fence_mbar_init();
-    }
-    if (warp == 1) tc::tmem_alloc<256>(&bars->tmem);
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tbase = bars->tmem;
-    pdl_wait();   // the previous kernel's results (after this CTA's setup)
-    pdl_trigger();
-
-    if (warp == 0) {
-        if (lane == 0) {
-            tc::prefetch_tmap(&tmG);
-            tc::prefetch_tmap(&tmV);
-            int s = 0;
-            uint32_t ph = 0, gph = 0;
-            for_segments([&](int tile, int rlo, int rhi) {
-                const int mlo = rlo > rc0 ? rlo : rc0;
-                if (mlo >= rhi) return;   // copy-only segment: no G, no V
-                mbar_wait(&bars->gempty, gph ^ 1u);
-                mbar_arrive_expect_tx(&bars->gfull, static_cast<uint32_t>(nslab) * 16384u);
-                for (int c = 0; c < nslab; ++c) {
-                    tc::tma_load_2d(Ghi + c * 8192, &tmG, c * 32, tile * kTileCols, &bars->gfull);
-                    tc::tma_load_2d(Glo + c * 8192, &tmG, c * 32,
-                                    static_cast<int>(N) + tile * kTileCols, &bars->gfull);
-                }
-                gph ^= 1u;
-                for (int rc = mlo; rc < rhi; ++rc) {
-                    for (int c = 0; c < nslab; ++c) {
-                        const unsigned long long t0 = clock64();
-                        mbar_wait(&bars->empty[s], ph ^ 1u);
-                        w_a += clock64() - t0;
-                        mbar_arrive_expect_tx(&bars->full[s], static_cast<uint32_t>(kStage3Bytes));
-                        tc::tma_load_2d(Vhi(s), &tmV, c * 32, vrow_hi + rc * kRowChunk, &bars->full[s]);
-                        tc::tma_load_2d(Vlo(s), &tmV, c * 32, vrow_lo + rc * kRowChunk, &bars->full[s]);
-                        if (++s == kStages3) {
-                            s = 0;
-                            ph ^= 1u;
-                        }
-                    }
-                }
-            });
-        }
-    } else if (warp == 1) {
-        const uint32_t idesc = tc::idesc_bf16(kRowChunk, kTileCols);
-        int s = 0, a = 0;
-        uint32_t ph = 0, aph = 0, gph = 0;
-        const uint32_t gh0 = smem_u32(Ghi), gl0 = smem_u32(Glo);
-        for_segments([&](int tile, int rlo, int rhi) {
-            const int mlo = rlo > rc0 ? rlo : rc0;
-            if (mlo >= rhi) return;
-            mbar_wait(&bars->gfull, gph);
-            gph ^= 1u;
-            tc::fence_after_sync();
-            for (int rc = mlo; rc < rhi; ++rc) {
-                const unsigned long long t1 = clock64();
-                mbar_wait(&bars->acc_empty[a], aph ^ 1u);
-                w_b += clock64() - t1;
-                tc::fence_after_sync();
-                const uint32_t d = tbase + static_cast<uint32_t>(a * kTileCols);
-                for (int c = 0; c < nslab; ++c) {
-                    const unsigned long long t0 = clock64();
-                    mbar_wait(&bars->full[s], ph);
-                    w_a += clock64() - t0;
-                    tc::fence_after_sync();
-                    const uint32_t vh = smem_u32(Vhi(s)), vl = smem_u32(Vlo(s));
-#pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) {
-                        const uint64_t ah = tc::sdesc_sw64(vh + kk * 32), alo = tc::sdesc_sw64(vl + kk * 32);
-                        const uint64_t bh = tc::sdesc_sw64(gh0 + c * 8192 + kk * 32);
-                        const uint64_t blo = tc::sdesc_sw64(gl0 + c * 8192 + kk * 32);
-                        tc::mma_bf16_w(d, ah, bh, idesc, (c | kk) != 0);
-                        tc::mma_bf16_w(d, ah, blo, idesc, 1u);
-                        tc::mma_bf16_w(d, alo, bh, idesc, 1u);
-                    }
-                    tc::mma_commit_w(&bars->empty[s]);
-                    if (++s == kStages3) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
-                }
-                tc::mma_commit_w(&bars->acc_full[a]);
-                if (++a == 2) {
-                    a = 0;
-                    aph ^= 1u;
-                }
-            }
-            tc::mma_commit_w(&bars->gempty);
-        });
-        __syncwarp();
-    } else if (warp == 2) {
-        // X is read by the epilogue straight from global memory; this warp pulls each row
-        // chunk's X rows into L2 up to kAhead chunks before the epilogue gets there (TMA
-        // prefetch, no shared memory)
-        if (lane == 0) {
-            constexpr int kAhead = 3;
-            tc::prefetch_tmap(&tmXb);
-            int u = 0;
-            for_segments([&](int tile, int rlo, int rhi) {
-                for (int rc = rlo; rc < rhi; ++rc, ++u) {
-                    const unsigned long long t0 = clock64();
-                    while (u > *reinterpret_cast<volatile int *>(&bars->progress) + kAhead) __nanosleep(100);
-                    w_a += clock64() - t0;
-                    for (int cb = 0; cb < kTileCols / kXBoxCols; ++cb)
-                        tc::tma_prefetch_2d(&tmXb, rc * kRowChunk, tile * kTileCols + cb * kXBoxCols);
-                }
-            });
-        }
-    } else if (warp >= 4) {
-        // 16 epilogue warps: 4 lane quarters (32 rows each) x 4 column groups; group g owns
-        // columns [16 g, 16 g + 16) and [64 + 16 g, 64 + 16 g + 16) of each tile.  A thread
-        // (one row) loads its 32 X values straight from global memory (a warp reads 128
-        // consecutive bytes of one column per load), drains the accumulator and stores Y the
-        // same way: no shared-memory X boxes, no cross-warp barrier
-        const int q = warp & 3, grp = (warp - 4) >> 2;
-        const int r_in = q * 32 + lane;
-        int a = 0;
-        uint32_t aph = 0;
-        for_segments([&](int tile, int rlo, int rhi) {
-            for (int rc = rlo; rc < rhi; ++rc) {
-                const bool mma_rc = rc >= rc0;
-                const int r = rc * kRowChunk + r_in;
-                const bool rv = r < n;
-                const float lr = (lam && rv) ? __ldg(lam + r) : 1.f;
-                const float pr = (post && rv) ? __ldg(post + r) : 1.f;
-                float xv[2][kXBoxCols];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-#pragma unroll
-                    for (int e = 0; e < kXBoxCols; ++e) {
-                        const int64_t j = static_cast<int64_t>(tile) * kTileCols + (grp + 4 * k) * kXBoxCols + e;
-                        xv[k][e] = (rv && j < N) ? __ldcs(Xsrc + j * n + r) : 0.f;
-                    }
-                }
-                if (mma_rc) {
-                    const unsigned long long t0 = clock64();
-                    mbar_wait(&bars->acc_full[a], aph);
-                    w_a += clock64() - t0;
-                    tc::fence_after_sync();
-                }
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    float v[kXBoxCols];
-                    if (mma_rc) {
-                        tc::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) +
-                                          static_cast<uint32_t>(a * kTileCols + (grp + 4 * k) * kXBoxCols),
-                                      v);
-                        if (k == 1) {   // both halves read: the accumulator is free
-                            tc::fence_before_sync();
-                            tc::mbar_arrive(&bars->acc_empty[a]);
-                            if (++a == 2) {
-                                a = 0;
-                                aph ^= 1u;
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < kXBoxCols; ++e) v[e] = 0.f;
-                    }
-#pragma unroll
-                    for (int e = 0; e < kXBoxCols; ++e) {
-                        const int64_t j = static_cast<int64_t>(tile) * kTileCols + (grp + 4 * k) * kXBoxCols + e;
-                        if (rv && j < N) __stcs(Y + j * n + r, pr * fmaf(lr, xv[k][e], -v[e]));
-                    }
-                }
-                if (warp == 4 && lane == 0) *reinterpret_cast<volatile int *>(&bars->progress) += 1;
-            }
-        });
-    }
     if (dbg && lane == 0) {
         // [0] kernel cycles  [1,2] V producer: empty waits  [3,4] MMA: full waits, acc_empty
         // waits  [5,6] X producer: xempty waits  [7,8] epilogue warp 4: acc_full, xfull waits
@@ -1912,7 +1674,6 @@ struct Pass {
 namespace {
 thread_local int t_pdl = 1;   // A/B hooks (hh_debug_wy_pdl): PDL launches, and
 thread_local int t_overlap = 1;   // the preparation beside the first projection
-thread_local int t_direct = 0;    // K5b epilogue straight from / to global memory (A/B)
 // every kernel of the block program is launched with programmatic stream serialization (PDL):
 // see pdl_trigger / pdl_wait
 template <typename... K, typename... A>
@@ -1938,10 +1699,9 @@ cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem,
 }  // namespace
 
 int wy_set_pdl(int on) {
-    const int prev = t_pdl | (t_overlap << 1) | (t_direct << 2);
+    const int prev = t_pdl | (t_overlap << 1);
     t_pdl = on & 1;
     t_overlap = (on >> 1) & 1;
-    t_direct = (on >> 2) & 1;
     return prev;
 }
 
@@ -1974,9 +1734,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(wy_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemMax);
-        if (err == cudaSuccess)
-            err = cudaFuncSetAttribute(wy_update_direct_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+
     });
     if (g_attr_err[dev] != cudaSuccess) return g_attr_err[dev];
     const bool sym = p.kind == WY_SYM;
@@ -2289,17 +2047,6 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                 Gt, *ps.mV, (cur == X) ? mXb2 : mYb2, mYb2, ps.pre, ps.post, static_cast<int>(p.n),
                 static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
                 ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, t_timeline));
-            cur = Y;
-            continue;
-        }
-        if (t_direct) {
-            const size_t sm3d = static_cast<size_t>(ps.kw / 32) * 16384 +
-                                static_cast<size_t>(kStages3) * kStage3Bytes + sizeof(Bars3) + 1024;
-            ++nlaunch, note(launch_k(q != 0 || !overlap, wy_update_direct_kernel, grid3, 640, sm3d, stream,
-                *ps.mG, *ps.mV, (cur == X) ? mXb : mYb, mYb, Y, ps.pre, ps.post, static_cast<int>(p.n),
-                static_cast<int>(n_pad), N, ps.kw, ps.vrow_hi, ps.vrow_lo, ntiles,
-                ps.row0 / kRowChunk, (cur != Y && ps.row0 >= kRowChunk) ? 1 : 0, nxs_for(ps.kw),
-                t_timeline, cur));
             cur = Y;
             continue;
         }
