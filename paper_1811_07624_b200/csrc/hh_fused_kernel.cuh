@@ -277,7 +277,9 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         // fp32, two columns per single-warp group: the partial sums and the butterfly use
         // packed FADD2 (two IEEE adds per instruction) -- fewer issue slots on the serial chain
         constexpr bool kPair = std::is_same<T, float>::value && C == 2 && TPC <= 32;
-        if constexpr (kPair) {
+        // the packed partial sums and 2-alpha also serve the multi-warp two-column groups
+        constexpr bool kPairSum = std::is_same<T, float>::value && C == 2;
+        if constexpr (kPairSum) {
             V acc0, acc1;
             vzero(acc0);
             vzero(acc1);
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             rpar ^= 1;
         }
         }
-        if constexpr (kPair) {
+        if constexpr (kPairSum) {
             float s0, s1;
             fadd2(s0, s1, p[0], p[1], p[0], p[1]);   // 2 alpha for both columns at once
 #pragma unroll
