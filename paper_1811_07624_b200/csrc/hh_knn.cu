@@ -388,8 +388,11 @@ __global__ void knn_merge_kernel(const float *__restrict__ pd, const int32_t *__
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
-std::once_flag g_enc_once, g_knn_attr_once;
-cudaError_t g_knn_attr_err = cudaSuccess;
+std::once_flag g_enc_once;
+// the large dynamic shared-memory opt-in belongs to each device's context: once per device
+constexpr int kKnnMaxDev = 64;
+std::once_flag g_knn_attr_once[kKnnMaxDev];
+cudaError_t g_knn_attr_err[kKnnMaxDev];
 
 bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer, uint32_t rows) {
     std::call_once(g_enc_once, []() {
@@ -476,18 +479,19 @@ bool knn_supported(int64_t n, int64_t Mr, int64_t Mq, int k) {
 cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float *d,
                        const float *Pr, const float *Pq, int32_t *nn_idx, float *nn_dist, void *ws,
                        cudaStream_t stream, LaunchInfo *info) {
-    std::call_once(g_knn_attr_once, []() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kKnnMaxDev) return cudaErrorInvalidDevice;
+    std::call_once(g_knn_attr_once[dev], [dev]() {
         const int sm = static_cast<int>(kKnnSmemMax);
-        g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel<4>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        if (g_knn_attr_err == cudaSuccess)
-            g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel<8>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        if (g_knn_attr_err == cudaSuccess)
-            g_knn_attr_err = cudaFuncSetAttribute(knn_topk_kernel<kKnnMaxK>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        cudaError_t &err = g_knn_attr_err[dev];
+        err = cudaFuncSetAttribute(knn_topk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(knn_topk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(knn_topk_kernel<kKnnMaxK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     });
-    if (g_knn_attr_err != cudaSuccess) return g_knn_attr_err;
+    if (g_knn_attr_err[dev] != cudaSuccess) return g_knn_attr_err[dev];
     char *w = static_cast<char *>(ws);
     float *Zr = reinterpret_cast<float *>(w + p.off_zr);
     float *Zq = reinterpret_cast<float *>(w + p.off_zq);
