@@ -319,29 +319,14 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             T *rb = red + (static_cast<size_t>(rpar) * NU + unit) * WPU * C;
             if ((lane & 15) == 0) rb[wiu * C + (hi ? 1 : 0)] = v;
             named_bar_sync(1 + unit, UT);
-            if constexpr (kPairSum && WPU % 2 == 0) {
-                // the warps' [col 0, col 1] pairs as 128-bit loads, summed pairwise with FADD2
-                // in warp order (w = 0, 1, ... as the scalar loop)
-                const float4 *r4 = reinterpret_cast<const float4 *>(rb);
-                float4 v0 = r4[0];
-                float s0 = v0.x, s1 = v0.y;
-                fadd2(s0, s1, s0, s1, v0.z, v0.w);
-#pragma unroll
-                for (int w2 = 1; w2 < WPU / 2; ++w2) {
-                    const float4 vw = r4[w2];
-                    fadd2(s0, s1, s0, s1, vw.x, vw.y);
-                    fadd2(s0, s1, s0, s1, vw.z, vw.w);
-                }
-                p[0] = s0;
-                p[1] = s1;
-            } else {
+            // (128-bit loads of the warps' pairs summed with FADD2 were measured 6 % slower
+            // here: the extra live registers spill at n = 4096)
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 T sum = rb[c];
 #pragma unroll
                 for (int w = 1; w < WPU; ++w) sum += rb[w * C + c];
                 p[c] = sum;
-            }
             }
             rpar ^= 1;
         } else if constexpr (kPair) {
