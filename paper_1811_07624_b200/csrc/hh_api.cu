@@ -483,6 +483,15 @@ hh_status hh_congruence(hh_op op, int64_t n, int64_t h, const void *U, const voi
     const size_t awsb = need - 2 * mb;
     const int64_t NC = n * count;
     const int dt = dtype == HH_F32 ? 0 : 1;
+    if (h > 0 && row_apply_supported(n, h, dt)) {
+        // two passes: T1 = op(Q) M (columns), M_out = T1 op(Q)^T (rows, K7)
+        st = apply_impl(op, n, h, U, M, T1, NC, dtype, awsb ? aws : nullptr, awsb, stream, nullptr, 0);
+        if (st != HH_OK) return st;
+        if (map_err(launch_row_apply(T1, Mout, U, n, h, count, op == HH_OP_N ? 0 : 1, stream)) != HH_OK)
+            return HH_ERR_CUDA;
+        if (t_has_last) t_last.launches += 1;
+        return HH_OK;
+    }
     // (op(Q) (op(Q) M)^T)^T = op(Q) M op(Q)^T
     st = apply_impl(op, n, h, U, M, T1, NC, dtype, awsb ? aws : nullptr, awsb, stream, nullptr, 0);
     if (st != HH_OK) return st;

@@ -9,6 +9,12 @@
 // op(Q) again, and a transpose back:  (op(Q) (op(Q) M)^T)^T = op(Q) M op(Q)^T.
 // The applies are the library's K1 / K5 kernels; the transpose is a 32 x 32
 // shared-memory tiled kernel (one read and one write of each matrix).
+//
+// Round 2 (fp32, n <= 1024, small h): the row side runs as ONE kernel, K7 below, so the
+// congruence is two passes over the batch instead of four:  T = op(Q) M  (columns, the apply
+// path), then  M_out = T op(Q)^T,  whose rows are the vectors op(Q) t_r: row r of a product
+// with op(Q)^T on the right is op(Q) applied to row r (the same reflectors, in the
+// same order as op).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,7 +45,100 @@ __global__ void __launch_bounds__(256) batched_transpose_kernel(const T *__restr
     }
 }
 
+// K7: every row of a column-major n x n matrix through op(Q) -- out = A op(Q)^T.  A CTA stages
+// 32 rows of one matrix in shared memory (each column's 32 rows are one coalesced 128-B read,
+// written transposed into row vectors with a padded pitch), each warp applies the h
+// reflectors to its rows two at a time with the row elements in registers (lane l owns
+// elements l + 32 k; dot by FMA partials and an xor butterfly, then x -= 2 alpha u, u read
+// through L1), and the rows leave with coalesced column writes.
+template <int CH>
+__global__ void __launch_bounds__(256) row_apply_kernel(const float *__restrict__ A, float *__restrict__ B,
+                                                        const float *__restrict__ U, int n, int h, int op) {
+    extern __shared__ float S[];   // 32 rows x (n + 1)
+    const int64_t base = static_cast<int64_t>(blockIdx.y) * n * n;
+    const int r0 = blockIdx.x * 32;
+    const int ld = n + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < 32 * n; e += 256) {
+        const int i = e & 31, c = e >> 5;
+        S[i * ld + c] = (r0 + i < n) ? A[base + static_cast<int64_t>(c) * n + r0 + i] : 0.f;
+    }
+    __syncthreads();
+    auto valid = [&](int k) { return lane + 32 * k < n; };
+#pragma unroll 1
+    for (int pr = 0; pr < 2; ++pr) {
+        const int i0 = warp * 4 + pr * 2;   // rows i0, i0 + 1 of the slab
+        float x[2][CH];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int k = 0; k < CH; ++k) x[c][k] = valid(k) ? S[(i0 + c) * ld + lane + 32 * k] : 0.f;
+        for (int t = 0; t < h; ++t) {
+            const int i = op == 0 ? h - 1 - t : t;   // op N: u_h first; op T: u_1 first (R1)
+            const float *u = U + static_cast<int64_t>(i) * n + lane;
+            float uk[CH];
+#pragma unroll
+            for (int k = 0; k < CH; ++k) uk[k] = valid(k) ? __ldg(u + 32 * k) : 0.f;
+            float p0a = 0.f, p0b = 0.f, p1a = 0.f, p1b = 0.f;
+#pragma unroll
+            for (int k = 0; k < CH; k += 2) {
+                p0a = fmaf(uk[k], x[0][k], p0a);
+                p1a = fmaf(uk[k], x[1][k], p1a);
+                if (k + 1 < CH) {
+                    p0b = fmaf(uk[k + 1], x[0][k + 1], p0b);
+                    p1b = fmaf(uk[k + 1], x[1][k + 1], p1b);
+                }
+            }
+            float p0 = p0a + p0b, p1 = p1a + p1b;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                p0 += __shfl_xor_sync(0xffffffffu, p0, off);
+                p1 += __shfl_xor_sync(0xffffffffu, p1, off);
+            }
+            const float s0 = -(p0 + p0), s1 = -(p1 + p1);
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                x[0][k] = fmaf(s0, uk[k], x[0][k]);
+                x[1][k] = fmaf(s1, uk[k], x[1][k]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int k = 0; k < CH; ++k)
+                if (valid(k)) S[(i0 + c) * ld + lane + 32 * k] = x[c][k];
+    }
+    __syncthreads();
+    for (int e = tid; e < 32 * n; e += 256) {
+        const int i = e & 31, c = e >> 5;
+        if (r0 + i < n) B[base + static_cast<int64_t>(c) * n + r0 + i] = S[i * ld + c];
+    }
+}
+
 }  // namespace
+
+bool row_apply_supported(int64_t n, int64_t h, int dtype) {
+    return dtype == 0 && n >= 4 && n <= 1024 && n % 4 == 0 && h <= 256;
+}
+
+cudaError_t launch_row_apply(const void *A, void *B, const void *U, int64_t n, int64_t h,
+                             int64_t count, int op, cudaStream_t stream) {
+    const size_t smem = static_cast<size_t>(32) * (n + 1) * 4;
+    const dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>(count));
+    auto go = [&](auto kernel) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kernel<<<grid, 256, smem, stream>>>(static_cast<const float *>(A), static_cast<float *>(B),
+                                            static_cast<const float *>(U), static_cast<int>(n),
+                                            static_cast<int>(h), op);
+        return cudaGetLastError();
+    };
+    if (n <= 128) return go(row_apply_kernel<4>);
+    if (n <= 256) return go(row_apply_kernel<8>);
+    if (n <= 512) return go(row_apply_kernel<16>);
+    return go(row_apply_kernel<32>);
+}
 
 cudaError_t launch_transpose(const void *A, void *B, int64_t n, int64_t count, int dtype,
                              cudaStream_t stream) {

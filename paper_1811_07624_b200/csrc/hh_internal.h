@@ -129,4 +129,8 @@ namespace hh {
 // NEXT-f4 (hh_cong.cu): B_b = A_b^T for `count` column-major n x n matrices.
 cudaError_t launch_transpose(const void *A, void *B, int64_t n, int64_t count, int dtype,
                              cudaStream_t stream);
+// K7: out_b = A_b op(Q)^T (every row through op(Q)) for fp32 n <= 1024
+bool row_apply_supported(int64_t n, int64_t h, int dtype);
+cudaError_t launch_row_apply(const void *A, void *B, const void *U, int64_t n, int64_t h,
+                             int64_t count, int op, cudaStream_t stream);
 }  // namespace hh

@@ -18,6 +18,9 @@
 namespace hh {
 namespace {
 
+// X through the non-coherent path, bypassing L1: every element is read exactly once, by the
+// thread that later writes the same element of Y -- so an exact alias Y == X (allowed by the
+// ABI) never lets a load observe a store of another thread
 __device__ __forceinline__ float4 ld_na4(const float4 *p) {
     float4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"

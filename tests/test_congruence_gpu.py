@@ -47,3 +47,21 @@ def test_congruence_alias_and_shf_blocks():
     s = np.diag(g.standard_normal(n)).astype(np.float32)[None]
     got = hh.hh_congruence(0, dev(U[k:]), dev(s)).cpu().numpy()
     assert_parity(got, oracle.congruence(0, U[k:], s), "f32", h - k, "B_k")
+
+
+@pytest.mark.parametrize("n,h,count", [(300, 9, 5), (1000, 5, 2), (96, 12, 3), (4, 3, 7),
+                                       (1024, 18, 2), (256, 64, 3)])
+def test_congruence_row_kernel(n, h, count):
+    """fp32 n <= 1024: the column apply followed by the row kernel K7 (every row of
+    op(Q) M through op(Q)) -- ragged row slabs, both ops, and M_out aliasing M."""
+    g = gi.rng(602, n, h, count)
+    U = gi.unit_reflectors(g, h, n, "f32")
+    M = g.standard_normal((count, n, n)).astype(np.float32)
+    for op in (0, 1):
+        ref = oracle.congruence(op, U, M)
+        got = hh.hh_congruence(op, dev(U), dev(M)).cpu().numpy()
+        assert_parity(got, ref, "f32", h, f"K7 n{n} h{h} op{op}")
+        Mt = dev(M)
+        hh.hh_congruence(op, dev(U), Mt, out=Mt)
+        torch.cuda.synchronize()
+        assert_parity(Mt.cpu().numpy(), ref, "f32", h, f"K7 alias n{n} op{op}")
