@@ -51,6 +51,22 @@ __global__ void __launch_bounds__(256) batched_transpose_kernel(const T *__restr
 // reflectors to its rows two at a time with the row elements in registers (lane l owns
 // elements l + 32 k; dot by FMA partials and an xor butterfly, then x -= 2 alpha u, u read
 // through L1), and the rows leave with coalesced column writes.
+// d += a * b elementwise over a pair (FFMA2), d += b (FADD2): two IEEE fp32 operations each
+__device__ __forceinline__ void ffma2_rows(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 A, B, D;\n\t"
+        "mov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\tmov.b64 D, {%0, %1};\n\t"
+        "fma.rn.f32x2 D, A, B, D;\n\tmov.b64 {%0, %1}, D;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void fadd2_rows(float &d0, float &d1, float b0, float b1) {
+    asm("{\n\t.reg .b64 A, B;\n\t"
+        "mov.b64 A, {%0, %1};\n\tmov.b64 B, {%2, %3};\n\t"
+        "add.rn.f32x2 A, A, B;\n\tmov.b64 {%0, %1}, A;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(b0), "f"(b1));
+}
+
 template <int CH>
 __global__ void __launch_bounds__(256) row_apply_kernel(const float *__restrict__ A, float *__restrict__ B,
                                                         const float *__restrict__ U, int n, int h, int op) {
@@ -68,39 +84,43 @@ __global__ void __launch_bounds__(256) row_apply_kernel(const float *__restrict_
 #pragma unroll 1
     for (int pr = 0; pr < 2; ++pr) {
         const int i0 = warp * 4 + pr * 2;   // rows i0, i0 + 1 of the slab
-        float x[2][CH];
+        // the two rows' elements packed as pairs: every FMA of the dot and the update is one
+        // FFMA2 for both rows (u_k broadcast), the butterfly one FADD2 per step
+        float x0[CH], x1[CH];
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int k = 0; k < CH; ++k) x[c][k] = valid(k) ? S[(i0 + c) * ld + lane + 32 * k] : 0.f;
+        for (int k = 0; k < CH; ++k) {
+            x0[k] = valid(k) ? S[i0 * ld + lane + 32 * k] : 0.f;
+            x1[k] = valid(k) ? S[(i0 + 1) * ld + lane + 32 * k] : 0.f;
+        }
         for (int t = 0; t < h; ++t) {
             const int i = op == 0 ? h - 1 - t : t;   // op N: u_h first; op T: u_1 first (R1)
             const float *u = U + static_cast<int64_t>(i) * n + lane;
             float uk[CH];
 #pragma unroll
             for (int k = 0; k < CH; ++k) uk[k] = valid(k) ? __ldg(u + 32 * k) : 0.f;
-            float p0a = 0.f, p0b = 0.f, p1a = 0.f, p1b = 0.f;
+            float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f;
 #pragma unroll
             for (int k = 0; k < CH; k += 2) {
-                p0a = fmaf(uk[k], x[0][k], p0a);
-                p1a = fmaf(uk[k], x[1][k], p1a);
-                if (k + 1 < CH) {
-                    p0b = fmaf(uk[k + 1], x[0][k + 1], p0b);
-                    p1b = fmaf(uk[k + 1], x[1][k + 1], p1b);
-                }
+                ffma2_rows(pa0, pa1, uk[k], uk[k], x0[k], x1[k]);
+                if (k + 1 < CH) ffma2_rows(pb0, pb1, uk[k + 1], uk[k + 1], x0[k + 1], x1[k + 1]);
             }
-            float p0 = p0a + p0b, p1 = p1a + p1b;
+            float p0 = pa0, p1 = pa1;
+            fadd2_rows(p0, p1, pb0, pb1);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
-                p0 += __shfl_xor_sync(0xffffffffu, p0, off);
-                p1 += __shfl_xor_sync(0xffffffffu, p1, off);
+                const float t0 = __shfl_xor_sync(0xffffffffu, p0, off);
+                const float t1 = __shfl_xor_sync(0xffffffffu, p1, off);
+                fadd2_rows(p0, p1, t0, t1);
             }
             const float s0 = -(p0 + p0), s1 = -(p1 + p1);
 #pragma unroll
-            for (int k = 0; k < CH; ++k) {
-                x[0][k] = fmaf(s0, uk[k], x[0][k]);
-                x[1][k] = fmaf(s1, uk[k], x[1][k]);
-            }
+            for (int k = 0; k < CH; ++k) ffma2_rows(x0[k], x1[k], s0, s1, uk[k], uk[k]);
+        }
+        float x[2][CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            x[0][k] = x0[k];
+            x[1][k] = x1[k];
         }
 #pragma unroll
         for (int c = 0; c < 2; ++c)
