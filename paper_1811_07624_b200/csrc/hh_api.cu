@@ -183,6 +183,8 @@ int hh_debug_wy_flow(int on, int project_ctas) { return wy_set_flow(on, project_
 void hh_debug_wy_flow_knobs(const int *k, int cnt) { wy_set_flow_knobs(k, cnt); }
 void hh_debug_k1(int alt, int gridx) { k1_set_debug(alt, gridx); }
 int hh_debug_k1_stream(int on) { return k1_set_stream(on); }
+int hh_debug_k1_prefetch(int dist) { return k1_set_prefetch(dist); }
+int hh_debug_k1_tmem(int on) { return k1_set_tmem(on); }
 int hh_debug_wy_pdl(int on) { return wy_set_pdl(on); }
 
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first

@@ -12,7 +12,22 @@ namespace {
 // and a multiplier of the persistent grid (1: persistent)
 thread_local int t_k1_alt = -1;
 thread_local int t_k1_gridx = 1;
-thread_local int t_k1_stream = -1;   // K1s (hh_stream.cu): -1 measured policy, 0 never, 1 always
+thread_local int t_k1_stream = -1;
+thread_local int t_k1_pf = 0;       // unstaged K1: L2 prefetch distance in batches (0: off;
+                                    // measured slower at n = 4096, tools/k1_pf_ab.py)
+thread_local int t_k1_tmem = -1;    // K1t (reflectors in TMEM): -1 policy, 0 never, 1 when eligible   // K1s (hh_stream.cu): -1 measured policy, 0 never, 1 always
+
+// K1t policy (reflectors in TMEM), from a same-box A/B (tools/k1t_ab.py,
+// profiles/r2/k1t_ab_r2.txt; outputs bit-identical): multi-warp groups (n > 1024) always --
+// n = 4096, h = 8 / 12 / 16: 404 / 542 / 880 -> 338 / 439 / 535 us, n = 2048, h = 12 / 16:
+// 461 / 602 -> 381 / 487 us; one-warp groups (n <= 1024) from h = 12 (n = 1024, h = 16:
+// 499 -> 430 us, but h = 10: 350 -> 380 us: the tcgen05.ld wait sits on the reflector's
+// serial chain where the shared-memory loads pipelined with the FMAs); never for the two-CTA
+// (256-thread) variants (n = 512, h = 10: 448 -> 609 us; K1s serves those shapes)
+bool k1t_preferred(const FusedVariant *v, int64_t h) {
+    if (v->nt <= 256) return false;
+    return v->tpc > 32 || h >= 12;
+}
 
 const FusedVariant *pick(int dtype, int64_t nv) {
     int cnt = 0;
@@ -31,6 +46,18 @@ const FusedVariant *pick(int dtype, int64_t nv) {
 }  // namespace
 
 int64_t max_n(int dtype) { return dtype == 0 ? 8192 : 4096; }
+
+int k1_set_prefetch(int dist) {
+    const int prev = t_k1_pf;
+    t_k1_pf = dist < 0 ? 0 : dist;
+    return prev;
+}
+
+int k1_set_tmem(int on) {
+    const int prev = t_k1_tmem;
+    t_k1_tmem = on;
+    return prev;
+}
 
 int k1_set_stream(int on) {
     const int prev = t_k1_stream;
@@ -60,9 +87,17 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     const int WPU = UT / 32;
     const size_t colB = static_cast<size_t>(a.n) * s;
     const size_t red = v->tpc > 32 ? static_cast<size_t>(2) * NU * WPU * v->c * s : 0;
-    const size_t bars = 8 * static_cast<size_t>(2 + NU);
+    const size_t bars = 8 * static_cast<size_t>(2 + NU) + 8;   // + the K1t TMEM address slot
     const size_t maxs = static_cast<size_t>(da.max_smem_optin);
     const int64_t h = a.h;
+
+    // K1t: the reflectors in TMEM (4 CH columns each; a CTA per SM may take all 512 columns,
+    // two CTAs 256 each) -- fp32 variants built with the TMEM form, U resident, no gathers
+    int tcols = 32;
+    while (tcols < h * 4 * v->ch) tcols *= 2;
+    const bool tm_ok = v->fn_tm_full != nullptr && a.mode != MODE_PAIR && h > 0 &&
+                       tcols <= (v->nt <= 256 ? 256 : 512);
+    const bool utm = tm_ok && (t_k1_tmem == 1 || (t_k1_tmem < 0 && k1t_preferred(v, h)));
 
     // Shared-memory plan, in order of preference: (1) staged column tiles + resident U,
     // (2) resident U with columns loaded straight into registers (a chunked U would be
@@ -73,7 +108,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     const size_t ub = static_cast<size_t>(h) * colB;
     int stage = 0, R = 0, nc = 1;
     size_t smem = 0;
-    if (h == 0) {
+    if (h == 0 || utm) {   // (K1t: no U in shared memory, R = 0)
         stage = pair ? 0 : 1;
         smem = (stage ? xs_st : 0) + red + bars;
     } else if (!pair && ub + xs_st + red + bars <= maxs) {
@@ -102,7 +137,9 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     a.R = R;
     a.nchunks = nc;
     a.stage_x = stage;
-    const void *fn = full ? v->fn_full : v->fn_ragged;
+    a.l2pf = t_k1_pf;
+    a.tcols = utm ? tcols : 0;
+    const void *fn = utm ? (full ? v->fn_tm_full : v->fn_tm_ragged) : (full ? v->fn_full : v->fn_ragged);
 
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(maxs));
@@ -121,7 +158,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     void *args[] = {&a};
     e = cudaLaunchKernel(fn, dim3(grid), dim3(v->nt), args, smem, stream);
     if (info) {
-        info->variant = v->name;
+        info->variant = utm ? v->name_tm : v->name;
         info->grid = grid;
         info->block = v->nt;
         info->smem = static_cast<int>(smem);

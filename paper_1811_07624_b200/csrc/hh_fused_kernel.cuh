@@ -32,6 +32,7 @@
 
 #include "hh_internal.h"
 #include "hh_ptx.cuh"
+#include "hh_tc.cuh"
 
 namespace hh {
 
@@ -137,6 +138,54 @@ template <typename V>
 __device__ __forceinline__ V ldg_v(const V *p) {
     return __ldg(p);
 }
+
+// TMEM-resident reflectors (K1t): this thread's NC consecutive 32-bit columns of its lane
+// (warp: its lane quarter), 32x32b shape; NC = 8 / 16 / 32
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) {
+    if constexpr (NC == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                       "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr)
+                     : "memory");
+    } else if constexpr (NC == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+            "%11, %12, %13, %14, %15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr)
+            : "memory");
+    } else {
+        static_assert(NC == 32, "8, 16 or 32 columns");
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+            "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+            "%28, %29, %30, %31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+              "=r"(r[31])
+            : "r"(taddr)
+            : "memory");
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc_n(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_n(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+                 : "memory");
+}
 // ---------------------------------------------------------------------------------
 // Kernel template
 //   T   element type       TPC threads per column group      CH vector chunks / thread
@@ -144,8 +193,19 @@ __device__ __forceinline__ V ldg_v(const V *p) {
 // ---------------------------------------------------------------------------------
 // (NT <= 256: two CTAs per SM, so at most 128 registers -- pinned explicitly, ptxas's own
 // choice drifts with unrelated code changes and halves the occupancy of the C2 kernel)
-template <typename T, int TPC, int CH, int C, int NT, bool FULL>
+//
+// UTM ("K1t", fp32, TPC dividing 128): the reflectors live in TMEM instead of shared memory.
+// TMEM lane L holds the u chunks of group thread gt = L mod TPC (replicated over the lane
+// quarters when TPC < 128, since a warp reads only its own quarter), reflector i at columns
+// [4 CH i, 4 CH (i + 1)); each reflect() reads its 4 CH values with one tcgen05.ld.  The
+// per-reflector u reads leave the shared-memory pipe (measured TMEM read rate 340+ B/clk/SM
+// against 128 for ld.shared, tools/micro/tmem_ld_rate.cu), and shared memory is free for
+// staging column tiles even when U is large (n = 4096, h = 12: 192 KB).
+template <typename T, int TPC, int CH, int C, int NT, bool FULL, bool UTM = false>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const FusedArgs a) {
+    static_assert(!UTM || (std::is_same<T, float>::value && 128 % TPC == 0 && TPC >= 32),
+                  "TMEM reflectors: fp32, TPC in {32, 64, 128}");
+    constexpr int UCOLS = 4 * CH;   // TMEM columns per reflector (UTM)
     using V = typename VT<T>::V;
     constexpr int E = VT<T>::E;
     constexpr int UT = TPC > 32 ? TPC : 32;  // threads per scheduling unit
@@ -234,10 +294,44 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     }
     if (ut == 0) mbar_init(&xbar[unit], 1);
     fence_mbar_init();
+    // the TMEM address slot follows the barriers in dynamic shared memory (a static __shared__
+    // variable would push the opt-in dynamic size the launcher requests over the limit)
+    uint32_t &s_tmem = *reinterpret_cast<uint32_t *>(bars + 2 + NU);
+    uint32_t tlane = 0;   // this thread's TMEM lane address (UTM)
+    if constexpr (UTM) {
+        const int warp = tid >> 5;
+        if (warp == 0) tmem_alloc_n(&s_tmem, static_cast<uint32_t>(a.tcols));
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        tlane = s_tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        if (warp < 4) {
+            // warp q fills lane quarter q: lane 32 q + l holds the chunks of gt = (32 q + l) mod TPC
+            const int g2 = (warp * 32 + lane) % TPC;
+            for (int i = 0; i < h; ++i) {
+#pragma unroll
+                for (int k = 0; k < CH; k += 2) {
+                    float4 u0 = make_float4(0.f, 0.f, 0.f, 0.f), u1 = u0;
+                    if (FULL || g2 + TPC * k < nv)
+                        u0 = __ldg(reinterpret_cast<const float4 *>(a.U) + static_cast<size_t>(i) * nv + g2 + TPC * k);
+                    if (FULL || g2 + TPC * (k + 1) < nv)
+                        u1 = __ldg(reinterpret_cast<const float4 *>(a.U) + static_cast<size_t>(i) * nv + g2 + TPC * (k + 1));
+                    tc::tmem_st8(tlane + static_cast<uint32_t>(i * UCOLS + 4 * k),
+                                 make_uint4(__float_as_uint(u0.x), __float_as_uint(u0.y),
+                                            __float_as_uint(u0.z), __float_as_uint(u0.w)),
+                                 make_uint4(__float_as_uint(u1.x), __float_as_uint(u1.y),
+                                            __float_as_uint(u1.z), __float_as_uint(u1.w)));
+                }
+            }
+            tc::tmem_wait_st();
+        }
+        tc::fence_before_sync();
+    }
     __syncthreads();
+    if constexpr (UTM) tc::fence_after_sync();
 
     // prologue: U (resident, or the first two chunk visits) and each unit's first tile
-    if (tid == 0 && h > 0) {
+    if (!UTM && tid == 0 && h > 0) {
         if (nc == 1) {
             issue_u(0, 0);
         } else {
@@ -251,19 +345,28 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     uint32_t xphase = 0;
     int rpar = 0;       // reduction-buffer parity (TPC > 32)
     int64_t g = 0;      // chunk-visit counter (nc > 1)
-    bool u_ready = (h == 0) || (nc > 1);
+    bool u_ready = UTM || (h == 0) || (nc > 1);
 
     auto valid_k = [&](int k) -> bool { return FULL || (gt + TPC * k < nv); };
 
     // one reflector: x <- x - 2 (u^T x) u   for the C columns of this group
-    auto reflect = [&](const V *ub) {
+    auto reflect = [&](const V *ub, int ui) {
         T p[C];
         // multi-warp groups: keep the u chunk in registers across the cross-warp
         // reduction (a shared-memory store + barrier the compiler cannot see through),
         // so u is read from shared memory once per reflector, not twice
-        constexpr bool kKeepU = TPC > 32;
+        constexpr bool kKeepU = TPC > 32 || UTM;
         V uk[kKeepU ? CH : 1];
-        if constexpr (kKeepU) {
+        if constexpr (UTM) {
+            uint32_t r[UCOLS];
+            tmem_ld_cols<UCOLS>(tlane + static_cast<uint32_t>(ui * UCOLS), r);
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                if constexpr (std::is_same<T, float>::value)
+                    uk[k] = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                        __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+            }
+        } else if constexpr (kKeepU) {
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
                 if (valid_k(k)) uk[k] = ub[gt + TPC * k];
@@ -391,16 +494,16 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             // of a reflector here, and this kernel is issue-bound (C2 0.358 -> 0.353 ms, A/B)
             if (desc) {
 #pragma unroll 2
-                for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+                for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv, i);
             } else {
 #pragma unroll 2
-                for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+                for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv, i);
             }
         } else {
             if (desc) {
-                for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+                for (int i = r1 - 1; i >= r0; --i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv, i);
             } else {
-                for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv);
+                for (int i = r0; i < r1; ++i) reflect(base + static_cast<size_t>(i - chunk_lo) * nv, i);
             }
         }
     };
@@ -419,6 +522,21 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         const int64_t t = tile_of(b);
         const bool tv = t < ntiles;
         const int64_t col0 = t * UC + static_cast<int64_t>(grp) * C;
+
+        // unstaged columns (U fills shared memory, e.g. n = 4096, h = 12): pull the unit's tile
+        // l2pf batches ahead into L2 with one bulk prefetch, so the register loads of that
+        // batch are served at L2 latency while this one computes
+        if (!stage && mode != MODE_PAIR && a.l2pf > 0 && ut == 0) {
+            const int64_t tp = tile_of(b + a.l2pf);
+            if (b + a.l2pf < nb && tp < ntiles) {
+                const int64_t c0 = tp * UC;
+                const int64_t cols = min(static_cast<int64_t>(UC), a.N - c0);
+                const uint32_t bytes = static_cast<uint32_t>(cols * nv * sizeof(V));
+                const char *src = reinterpret_cast<const char *>(Xg + c0 * nv);
+                for (uint32_t off = 0; off < bytes; off += 32768u)
+                    bulk_prefetch_l2(src + off, min(32768u, bytes - off));
+            }
+        }
 
         // ---- 1. columns -> registers
         if (tv) {
@@ -600,6 +718,11 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             }
         }
     }
+    if constexpr (UTM) {
+        tc::fence_before_sync();
+        __syncthreads();
+        if ((tid >> 5) == 0) tmem_dealloc_n(s_tmem, static_cast<uint32_t>(a.tcols));
+    }
 }
 
 // One instantiated shape of the kernel: TPC threads per column, CH vector chunks per
@@ -607,16 +730,28 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
 struct FusedVariant {
     const void *fn_full;        // nv == TPC*CH exactly
     const void *fn_ragged;
+    const void *fn_tm_full;     // K1t (reflectors in TMEM), or nullptr
+    const void *fn_tm_ragged;
     int tpc, ch, c, nt;
     int elem;  // bytes
     const char *name;
+    const char *name_tm;   // K1t form's name
 };
 
 #define HH_FUSED_VAR(T, TPC, CH, C, NT, NAME)                                           \
     FusedVariant {                                                                      \
         reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true>),      \
             reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false>), \
-            TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME                                  \
+            nullptr, nullptr, TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME, NAME   \
+    }
+// the same shape with a K1t (TMEM reflector) form
+#define HH_FUSED_VAR_TM(T, TPC, CH, C, NT, NAME)                                          \
+    FusedVariant {                                                                        \
+        reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true>),        \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false>),   \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true, true>), \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, true>), \
+            TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME, NAME "_tmem"                  \
     }
 
 // tables (each defined in its own translation unit so the instantiations build in parallel)

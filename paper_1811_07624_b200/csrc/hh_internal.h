@@ -30,6 +30,8 @@ struct FusedArgs {
     const void *dsign;  // NEXT-f1: the diagonal D of Eq. 1 (n values) or NULL
     int dside;          // bit 0: x <- D x before the reflectors, bit 1: y <- D y after
     int qr;             // NEXT-f2: u_i[r] = 0 for r < i (partial-QR reflectors)
+    int l2pf;           // unstaged columns: prefetch the tile this many batches ahead into L2
+    int tcols;          // K1t: TMEM columns allocated per CTA (power of 2 >= 32)
 };
 
 struct LaunchInfo {
@@ -55,6 +57,8 @@ void k1_set_debug(int alt, int gridx);
 bool stream_supported(const FusedArgs &a, int dtype);
 bool stream_preferred(const FusedArgs &a);   // the measured K1 / K1s policy
 cudaError_t launch_stream(const FusedArgs &a, cudaStream_t stream, LaunchInfo *info);
+int k1_set_prefetch(int dist);
+int k1_set_tmem(int on);   // A/B hook (hh_debug_k1_tmem): -1 policy, 0 never, 1 when eligible; previous   // A/B hook (hh_debug_k1_prefetch): L2 prefetch distance; previous
 int k1_set_stream(int on);   // A/B hook (hh_debug_k1_stream): -1 auto, 0 K1, 1 K1s; previous
 
 // Largest n the vector kernels support for this dtype.

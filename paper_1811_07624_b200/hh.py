@@ -87,6 +87,10 @@ def lib() -> ctypes.CDLL:
             L.hh_debug_k1.restype = None
             L.hh_debug_k1_stream.argtypes = [i32]
             L.hh_debug_k1_stream.restype = i32
+            L.hh_debug_k1_prefetch.argtypes = [i32]
+            L.hh_debug_k1_prefetch.restype = i32
+            L.hh_debug_k1_tmem.argtypes = [i32]
+            L.hh_debug_k1_tmem.restype = i32
             L.hh_debug_wy_pdl.argtypes = [i32]
             L.hh_debug_wy_pdl.restype = i32
         if hasattr(L, "hh_debug_wy_timeline"):

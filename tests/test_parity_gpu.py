@@ -316,3 +316,69 @@ def test_apply_host_takes_the_wy_path():
         Y = hh.hh_apply_host(op, U, X)
         assert hh.last_launch_info()["variant"].startswith("wy_"), hh.last_launch_info()
         assert_parity(Y.numpy(), oracle.apply(op, c.U, c.X), "f32", 64, f"host WY op{op}")
+
+
+@pytest.fixture(params=[0, 1], ids=["u-smem", "u-tmem"])
+def k1_tmem(request):
+    """Force K1 with the reflectors in shared memory (0) or in TMEM (1, K1t) -- the default
+    picks by the measured policy (hh_fused.cu: k1t_preferred); K1s off so K1 runs."""
+    L = hh.hh.lib()
+    prev_s = L.hh_debug_k1_stream(0)
+    prev_t = L.hh_debug_k1_tmem(request.param)
+    yield request.param
+    L.hh_debug_k1_tmem(prev_t)
+    L.hh_debug_k1_stream(prev_s)
+
+
+# every K1 variant built with a TMEM form (TPC = 32 at 256 / 512 threads, 64, 128), full and
+# ragged n, up to the largest h whose reflectors fit the CTA's TMEM columns
+K1T_SHAPES = [(300, 7, 333), (512, 16, 400), (780, 11, 259), (1024, 16, 1000), (1500, 13, 300),
+              (2048, 16, 700), (3000, 9, 150), (4096, 12, 300), (4096, 16, 160)]
+
+
+@pytest.mark.parametrize("n,h,N", K1T_SHAPES)
+def test_k1_tmem_reflectors(k1_tmem, n, h, N):
+    """K1t (reflectors in TMEM) against the oracle: both ops, the symmetric form, D on both
+    sides, the Mahalanobis transform-once, exact alias."""
+    c = gi.make_case("sym", n, h, N, "f32", seed=45)
+    d = gi.sign_diag(gi.rng(45, n), n, "f32")
+    for op in (0, 1):
+        with hh.algo(hh.HH_ALGO_FUSED):
+            got = run_apply(op, c.U, c.X)
+            v = hh.last_launch_info()["variant"]
+        assert v.endswith("_tmem") == bool(k1_tmem), v
+        assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"{c.name} op{op}")
+    with hh.algo(hh.HH_ALGO_FUSED):
+        got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", 2 * h, f"{c.name} sym")
+    for side in (0, 1):
+        with hh.algo(hh.HH_ALGO_FUSED):
+            got = hh.hh_apply_signed(0, side, dev(c.U), dev(d), dev(c.X)).cpu().numpy()
+        assert_parity(got, oracle.apply_signed(0, side, c.U, d, c.X), "f32", h, f"signed {side}")
+    m = gi.make_case("mahalanobis", n, h, max(N // 4, 2), "f32", seed=46, npairs=2000)
+    got = hh.hh_mahalanobis(dev(m.U), dev(m.d), dev(m.X), dev(m.ia), dev(m.ib)).cpu().numpy()
+    assert_parity(got, oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib), "f32", h, "mahalanobis")
+    X = dev(c.X)
+    with hh.algo(hh.HH_ALGO_FUSED):
+        hh.hh_apply(1, dev(c.U), X, Y=X)
+    torch.cuda.synchronize()
+    assert_parity(X.cpu().numpy(), oracle.apply(1, c.U, c.X), "f32", h, "alias")
+
+
+def test_k1t_policy():
+    """The default picks K1t where the A/B measured it faster (hh_fused.cu: k1t_preferred)."""
+    g = torch.Generator().manual_seed(3)
+    for n, h, want in ((4096, 12, True), (2048, 9, True), (1024, 16, True), (1024, 10, False),
+                       (1024, 40, False)):
+        U = torch.randn(h, n, generator=g, dtype=torch.float64)
+        U = (U / U.norm(dim=1, keepdim=True)).float().cuda()
+        X = torch.randn(64, n, generator=g).cuda()
+        L = hh.hh.lib()
+        prev = L.hh_debug_k1_stream(0)
+        try:
+            with hh.algo(hh.HH_ALGO_FUSED):
+                hh.hh_apply(0, U, X)
+            v = hh.last_launch_info()["variant"]
+        finally:
+            L.hh_debug_k1_stream(prev)
+        assert v.endswith("_tmem") == want, (n, h, v)
