@@ -185,6 +185,7 @@ void hh_debug_k1(int alt, int gridx) { k1_set_debug(alt, gridx); }
 int hh_debug_k1_stream(int on) { return k1_set_stream(on); }
 int hh_debug_k1_prefetch(int dist) { return k1_set_prefetch(dist); }
 int hh_debug_k1_tmem(int on) { return k1_set_tmem(on); }
+int hh_debug_k1_blocked(int on) { return k1_set_blocked(on); }
 int hh_debug_wy_pdl(int on) { return wy_set_pdl(on); }
 
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first

@@ -15,7 +15,9 @@ thread_local int t_k1_gridx = 1;
 thread_local int t_k1_stream = -1;
 thread_local int t_k1_pf = 0;       // unstaged K1: L2 prefetch distance in batches (0: off;
                                     // measured slower at n = 4096, tools/k1_pf_ab.py)
-thread_local int t_k1_tmem = -1;    // K1t (reflectors in TMEM): -1 policy, 0 never, 1 when eligible   // K1s (hh_stream.cu): -1 measured policy, 0 never, 1 always
+thread_local int t_k1_tmem = -1;    // K1t (reflectors in TMEM): -1 policy, 0 never, 1 when eligible
+thread_local int t_k1_blk = -1;     // K1w (K1t in blocks of kb reflectors): -1 policy, 0 never,
+                                    // 1 when the variant has the form and K1t runs
 
 // K1t policy (reflectors in TMEM), from a same-box A/B (tools/k1t_ab.py,
 // profiles/r2/k1t_ab_r2.txt; outputs bit-identical): multi-warp groups (n > 1024) always --
@@ -59,6 +61,21 @@ int k1_set_tmem(int on) {
     return prev;
 }
 
+int k1_set_blocked(int on) {
+    const int prev = t_k1_blk;
+    t_k1_blk = on;
+    return prev;
+}
+
+// K1w policy, from a same-box A/B (tools/k1w_ab.py, profiles/r2/k1w_ab_r2.txt): blocks of 4
+// reflectors for multi-warp groups from h = 12 -- n = 4096, h = 12 / 16: 431-441 / 560 ->
+// 421-437 / 548-550 us, n = 2048, h = 12 / 16: 392-424 / 530-571 -> 383-415 / 516-552 us;
+// at h = 8 / 10 and for one-warp groups (n <= 1024) the second TMEM read of each u costs
+// more than the saved per-reflector exchanges; block sizes 2 and 8 measured slower
+bool k1w_preferred(const FusedVariant *v, int64_t h) {
+    return v->tpc > 32 && h >= 12;
+}
+
 int k1_set_stream(int on) {
     const int prev = t_k1_stream;
     t_k1_stream = on;
@@ -86,8 +103,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     const int NU = v->nt / UT;
     const int WPU = UT / 32;
     const size_t colB = static_cast<size_t>(a.n) * s;
-    const size_t red = v->tpc > 32 ? static_cast<size_t>(2) * NU * WPU * v->c * s : 0;
-    const size_t bars = 8 * static_cast<size_t>(2 + NU) + 8;   // + the K1t TMEM address slot
+    const size_t bars0 = 8 * static_cast<size_t>(2 + NU) + 8;   // + the K1t TMEM address slot
     const size_t maxs = static_cast<size_t>(da.max_smem_optin);
     const int64_t h = a.h;
 
@@ -98,6 +114,12 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     const bool tm_ok = v->fn_tm_full != nullptr && a.mode != MODE_PAIR && h > 0 &&
                        tcols <= (v->nt <= 256 ? 256 : 512);
     const bool utm = tm_ok && (t_k1_tmem == 1 || (t_k1_tmem < 0 && k1t_preferred(v, h)));
+    // K1w: the blocked form of K1t (its h x h Gram and per-pair partials follow the barriers)
+    const bool ublk = utm && v->fn_tb_full != nullptr &&
+                      (t_k1_blk == 1 || (t_k1_blk < 0 && k1w_preferred(v, h)));
+    const int kv = ublk ? v->kb * v->c : v->c;
+    const size_t red = v->tpc > 32 ? static_cast<size_t>(2) * NU * WPU * kv * s : 0;
+    const size_t bars = bars0 + (ublk ? 4 * static_cast<size_t>(h * h + (h * (h + 1) / 2) * (v->tpc / 32)) : 0);
 
     // Shared-memory plan, in order of preference: (1) staged column tiles + resident U,
     // (2) resident U with columns loaded straight into registers (a chunked U would be
@@ -139,7 +161,8 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     a.stage_x = stage;
     a.l2pf = t_k1_pf;
     a.tcols = utm ? tcols : 0;
-    const void *fn = utm ? (full ? v->fn_tm_full : v->fn_tm_ragged) : (full ? v->fn_full : v->fn_ragged);
+    const void *fn = ublk ? (full ? v->fn_tb_full : v->fn_tb_ragged)
+                     : utm ? (full ? v->fn_tm_full : v->fn_tm_ragged) : (full ? v->fn_full : v->fn_ragged);
 
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(maxs));
@@ -158,7 +181,7 @@ cudaError_t launch_fused(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo
     void *args[] = {&a};
     e = cudaLaunchKernel(fn, dim3(grid), dim3(v->nt), args, smem, stream);
     if (info) {
-        info->variant = utm ? v->name_tm : v->name;
+        info->variant = ublk ? v->name_tb : utm ? v->name_tm : v->name;
         info->grid = grid;
         info->block = v->nt;
         info->smem = static_cast<int>(smem);

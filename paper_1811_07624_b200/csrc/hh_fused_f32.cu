@@ -14,9 +14,9 @@ const FusedVariant kF32[] = {
     HH_FUSED_VAR(float, 8, 4, 1, 256, "f32_tpc8_ch4_c1"),      // n <= 128
     HH_FUSED_VAR(float, 16, 4, 1, 256, "f32_tpc16_ch4_c1"),    // n <= 256
     HH_FUSED_VAR_TM(float, 32, 4, 2, 256, "f32_tpc32_ch4_c2"),    // n <= 512
-    HH_FUSED_VAR_TM(float, 32, 8, 2, 512, "f32_tpc32_ch8_c2"),    // n <= 1024
-    HH_FUSED_VAR_TM(float, 64, 8, 2, 512, "f32_tpc64_ch8_c2"),    // n <= 2048
-    HH_FUSED_VAR_TM(float, 128, 8, 2, 512, "f32_tpc128_ch8_c2"),  // n <= 4096
+    HH_FUSED_VAR_TB(float, 32, 8, 2, 512, "f32_tpc32_ch8_c2", 4),    // n <= 1024
+    HH_FUSED_VAR_TB(float, 64, 8, 2, 512, "f32_tpc64_ch8_c2", 4),    // n <= 2048
+    HH_FUSED_VAR_TB(float, 128, 8, 2, 512, "f32_tpc128_ch8_c2", 4),  // n <= 4096
     HH_FUSED_VAR(float, 256, 8, 1, 512, "f32_tpc256_ch8_c1"),  // n <= 8192
 };
 // alternatives for same-box A/B only (hh_debug_k1 forces one): two-warp column groups with
@@ -26,6 +26,10 @@ const FusedVariant kF32Alt[] = {
     HH_FUSED_VAR(float, 64, 4, 2, 512, "f32_tpc64_ch4_c2_nt512"),
     HH_FUSED_VAR(float, 32, 8, 2, 256, "f32_tpc32_ch8_c2_nt256"),
     HH_FUSED_VAR(float, 128, 2, 4, 512, "f32_tpc128_ch2_c4_nt512"),
+    HH_FUSED_VAR_TB(float, 128, 8, 2, 512, "f32_tpc128_ch8_c2", 2),   // K1w block sizes
+    HH_FUSED_VAR_TB(float, 128, 8, 2, 512, "f32_tpc128_ch8_c2", 8),
+    HH_FUSED_VAR_TB(float, 64, 8, 2, 512, "f32_tpc64_ch8_c2", 2),
+    HH_FUSED_VAR_TB(float, 64, 8, 2, 512, "f32_tpc64_ch8_c2", 8),
 };
 }  // namespace
 

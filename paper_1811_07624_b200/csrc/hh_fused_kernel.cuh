@@ -201,10 +201,23 @@ __device__ __forceinline__ void tmem_dealloc_n(uint32_t taddr, uint32_t ncols) {
 // per-reflector u reads leave the shared-memory pipe (measured TMEM read rate 340+ B/clk/SM
 // against 128 for ld.shared, tools/micro/tmem_ld_rate.cu), and shared memory is free for
 // staging column tiles even when U is large (n = 4096, h = 12: 192 KB).
-template <typename T, int TPC, int CH, int C, int NT, bool FULL, bool UTM = false>
+//
+// KB > 1 ("K1w", with UTM): the reflectors are applied in blocks of KB.  For a block
+// i_1 .. i_m (application order), u_{i_t}^T x^{(t-1)} = u_{i_t}^T x - 2 sum_{s<t} alpha_s
+// (u_{i_s}^T u_{i_t}), so all m dot products are taken against the block's input x, reduced
+// across the column group together (one reduce-scatter, one cross-warp exchange), the alphas
+// follow from the m x m Gram entries by forward substitution, and x <- x - 2 sum_t alpha_t u_t.
+// Same FMAs as the sequential form (the compact-WY identity of Eq. 2 for a block); the
+// per-reflector serial chain (dot -> reduction -> barrier -> update) becomes one per block, at
+// the price of a second TMEM read of each u.  The Gram G = U^T U (h x h, fp32) is formed once per
+// CTA from the TMEM-resident reflectors (fixed-order sums: identical in every CTA).
+template <typename T, int TPC, int CH, int C, int NT, bool FULL, bool UTM = false, int KB = 1>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const FusedArgs a) {
     static_assert(!UTM || (std::is_same<T, float>::value && 128 % TPC == 0 && TPC >= 32),
                   "TMEM reflectors: fp32, TPC in {32, 64, 128}");
+    static_assert(KB == 1 || (UTM && (KB * C == 4 || KB * C == 8 || KB * C == 16)),
+                  "blocked reflectors: TMEM form, KB * C in {4, 8, 16}");
+    constexpr int KV = KB > 1 ? KB * C : C;   // values per cross-lane reduction
     constexpr int UCOLS = 4 * CH;   // TMEM columns per reflector (UTM)
     using V = typename VT<T>::V;
     constexpr int E = VT<T>::E;
@@ -237,7 +250,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     V *Us = reinterpret_cast<V *>(smem);
     V *Xs = Us + static_cast<size_t>(nbuf) * R * nv;
     T *red = reinterpret_cast<T *>(Xs + (stage ? static_cast<size_t>(NU) * UC * nv : 0));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(red + (TPC > 32 ? 2 * NU * WPU * C : 0));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(red + (TPC > 32 ? 2 * NU * WPU * KV : 0));
     uint64_t *ubar = bars;      // [2]
     uint64_t *xbar = bars + 2;  // [NU]
 
@@ -329,6 +342,51 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     }
     __syncthreads();
     if constexpr (UTM) tc::fence_after_sync();
+    // K1w: the Gram G[i][j] = u_i^T u_j from the TMEM-resident chunks.  A "set" of TPC / 32
+    // warps covers every chunk position once; the sets split the pairs i <= j, each warp
+    // reduces its partial in the warp and parks it, then the partials of a pair are added in
+    // warp order (deterministic, the same bits in every CTA).
+    float *gram = reinterpret_cast<float *>(bars + 2 + NU + 1);   // h x h, then partials
+    if constexpr (KB > 1) {
+        constexpr int S = TPC / 32;          // warps per set
+        constexpr int NSET = NT / TPC;
+        const int warp = tid >> 5;
+        const int set = warp / S, ws = warp % S;
+        const int npair = h * (h + 1) / 2;
+        float *gpart = gram + h * h;         // [npair][S]
+        for (int pidx = set; pidx < npair; pidx += NSET) {
+            int i = 0, rem = pidx;
+            while (rem >= h - i) {
+                rem -= h - i;
+                ++i;
+            }
+            const int j = i + rem;
+            uint32_t ri[UCOLS], rj[UCOLS];
+            tmem_ld_cols<UCOLS>(tlane + static_cast<uint32_t>(i * UCOLS), ri);
+            tmem_ld_cols<UCOLS>(tlane + static_cast<uint32_t>(j * UCOLS), rj);
+            float acc = 0.f;
+#pragma unroll
+            for (int e = 0; e < UCOLS; ++e) acc = fmaf(__uint_as_float(ri[e]), __uint_as_float(rj[e]), acc);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) gpart[pidx * S + ws] = acc;
+        }
+        __syncthreads();
+        for (int pidx = tid; pidx < npair; pidx += NT) {
+            int i = 0, rem = pidx;
+            while (rem >= h - i) {
+                rem -= h - i;
+                ++i;
+            }
+            const int j = i + rem;
+            float g = gpart[pidx * S];
+#pragma unroll
+            for (int w = 1; w < S; ++w) g += gpart[pidx * S + w];
+            gram[i * h + j] = g;
+            gram[j * h + i] = g;
+        }
+        __syncthreads();
+    }
 
     // prologue: U (resident, or the first two chunk visits) and each unit's first tile
     if (!UTM && tid == 0 && h > 0) {
@@ -484,6 +542,109 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         }
         }
     };
+    // K1w: reflectors [r0, r1) in blocks of KB (application order descending for desc)
+    auto run_blocked = [&](int r0, int r1, bool desc) {
+        if constexpr (KB > 1) {
+            const int mt = r1 - r0;
+            for (int s0 = 0; s0 < mt; s0 += KB) {
+                const int m = min(KB, mt - s0);
+                int idx[KB];
+#pragma unroll
+                for (int t = 0; t < KB; ++t) idx[t] = desc ? r1 - 1 - (s0 + t) : r0 + s0 + t;
+                // (a) the m dot products against the block's input x
+                float v[KV];
+#pragma unroll
+                for (int t = 0; t < KB; ++t) {
+                    if (t < m) {
+                        uint32_t r[UCOLS];
+                        tmem_ld_cols<UCOLS>(tlane + static_cast<uint32_t>(idx[t] * UCOLS), r);
+                        float4 acc[C];
+#pragma unroll
+                        for (int c = 0; c < C; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int k = 0; k < CH; ++k) {
+                            if (valid_k(k)) {
+                                const float4 uk0 = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                                               __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+#pragma unroll
+                                for (int c = 0; c < C; ++c) vfma(acc[c], uk0, x[c][k]);
+                            }
+                        }
+#pragma unroll
+                        for (int c = 0; c < C; ++c) v[t * C + c] = vsum(acc[c]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < C; ++c) v[t * C + c] = 0.f;
+                    }
+                }
+                // (b) reduce the KV values over the group: reduce-scatter in the warp (lane l
+                // ends with value index = its top log2(KV) bits), then across the group's warps
+                constexpr int LV = KV == 4 ? 2 : (KV == 8 ? 3 : 4);
+#pragma unroll
+                for (int st = 0; st < 5; ++st) {
+                    const int off = 16 >> st;
+                    if (st < LV) {
+                        const bool up = (lane & off) != 0;
+                        const int half = KV >> (st + 1);
+#pragma unroll
+                        for (int j = 0; j < half; ++j) {
+                            const float send = up ? v[j] : v[j + half];
+                            const float keep = up ? v[j + half] : v[j];
+                            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                        }
+                    } else {
+                        v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+                    }
+                }
+                float p[KV];
+                if constexpr (TPC > 32) {
+                    float *rb = red + (static_cast<size_t>(rpar) * NU + unit) * WPU * KV;
+                    if ((lane & ((32 >> LV) - 1)) == 0) rb[(lane >> (5 - LV)) * WPU + wiu] = v[0];
+                    named_bar_sync(1 + unit, UT);
+#pragma unroll
+                    for (int w = 0; w < KV; ++w) {
+                        float sum = rb[w * WPU];
+#pragma unroll
+                        for (int q = 1; q < WPU; ++q) sum += rb[w * WPU + q];
+                        p[w] = sum;
+                    }
+                    rpar ^= 1;
+                } else {
+#pragma unroll
+                    for (int w = 0; w < KV; ++w) p[w] = __shfl_sync(0xffffffffu, v[0], w << (5 - LV));
+                }
+                // (c) forward substitution: alpha_t = p_t - 2 sum_{s<t} G[i_s][i_t] alpha_s
+#pragma unroll
+                for (int t = 1; t < KB; ++t) {
+                    if (t < m) {
+#pragma unroll
+                        for (int s2 = 0; s2 < t; ++s2) {
+                            const float g2 = -2.f * gram[idx[s2] * h + idx[t]];
+#pragma unroll
+                            for (int c = 0; c < C; ++c) p[t * C + c] = fmaf(g2, p[s2 * C + c], p[t * C + c]);
+                        }
+                    }
+                }
+                // (d) x <- x - 2 sum_t alpha_t u_t
+#pragma unroll
+                for (int t = 0; t < KB; ++t) {
+                    if (t < m) {
+                        uint32_t r[UCOLS];
+                        tmem_ld_cols<UCOLS>(tlane + static_cast<uint32_t>(idx[t] * UCOLS), r);
+#pragma unroll
+                        for (int k = 0; k < CH; ++k) {
+                            if (valid_k(k)) {
+                                const float4 uk0 = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                                               __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+#pragma unroll
+                                for (int c = 0; c < C; ++c) vaxpy(x[c][k], 2.f * p[t * C + c], uk0);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    };
     // reflectors [r0, r1) of the chunk resident at `base` (first row = chunk_lo)
     // (NEXT-f2: the fused kernel applies QR-structured reflectors in full -- it serves
     // small h, where the zero prefixes are a negligible share; K5 skips them.)
@@ -523,10 +684,12 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         const bool tv = t < ntiles;
         const int64_t col0 = t * UC + static_cast<int64_t>(grp) * C;
 
-        // unstaged columns (U fills shared memory, e.g. n = 4096, h = 12): pull the unit's tile
-        // l2pf batches ahead into L2 with one bulk prefetch, so the register loads of that
-        // batch are served at L2 latency while this one computes
-        if (!stage && mode != MODE_PAIR && a.l2pf > 0 && ut == 0) {
+        // pull the unit's tile l2pf batches ahead into L2 with one bulk prefetch, so the
+        // register loads (unstaged) or the slot copy (staged) of that batch are served at L2
+        // latency while this one computes (measured slower for unstaged n = 4096)
+        // (staged columns: the next tile is already on its way into the slot; l2pf >= 2
+        // reaches further ahead)
+        if (mode != MODE_PAIR && a.l2pf > (stage ? 1 : 0) && ut == 0) {
             const int64_t tp = tile_of(b + a.l2pf);
             if (b + a.l2pf < nb && tp < ntiles) {
                 const int64_t c0 = tp * UC;
@@ -612,7 +775,17 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 u_ready = true;
             }
             if (tv) {
-                if (mode == MODE_APPLY_N) {
+                if constexpr (KB > 1) {
+                    if (mode == MODE_APPLY_N) {
+                        run_blocked(0, h, true);
+                    } else if (mode == MODE_SYM) {
+                        run_blocked(0, h, false);
+                        scale_vec();
+                        run_blocked(0, h, true);
+                    } else {
+                        run_blocked(0, h, false);
+                    }
+                } else if (mode == MODE_APPLY_N) {
                     run_range(Us, 0, 0, h, true);
                 } else if (mode == MODE_SYM) {
                     run_range(Us, 0, 0, h, false);
@@ -736,6 +909,10 @@ struct FusedVariant {
     int elem;  // bytes
     const char *name;
     const char *name_tm;   // K1t form's name
+    const void *fn_tb_full = nullptr;    // K1w (TMEM reflectors in blocks of kb), or nullptr
+    const void *fn_tb_ragged = nullptr;
+    int kb = 1;
+    const char *name_tb = nullptr;
 };
 
 #define HH_FUSED_VAR(T, TPC, CH, C, NT, NAME)                                           \
@@ -752,6 +929,18 @@ struct FusedVariant {
             reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true, true>), \
             reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, true>), \
             TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME, NAME "_tmem"                  \
+    }
+// ... and a K1w (blocked TMEM reflectors, KB per block) form
+#define HH_FUSED_VAR_TB(T, TPC, CH, C, NT, NAME, KB)                                       \
+    FusedVariant {                                                                        \
+        reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true>),        \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false>),   \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true, true>), \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, true>), \
+            TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME, NAME "_tmem",                 \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, true, true, KB>), \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, true, KB>), \
+            KB, NAME "_tmem_kb" #KB                                                        \
     }
 
 // tables (each defined in its own translation unit so the instantiations build in parallel)

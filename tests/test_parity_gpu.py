@@ -318,14 +318,17 @@ def test_apply_host_takes_the_wy_path():
         assert_parity(Y.numpy(), oracle.apply(op, c.U, c.X), "f32", 64, f"host WY op{op}")
 
 
-@pytest.fixture(params=[0, 1], ids=["u-smem", "u-tmem"])
+@pytest.fixture(params=[0, 1, 2], ids=["u-smem", "u-tmem", "u-tmem-blocked"])
 def k1_tmem(request):
-    """Force K1 with the reflectors in shared memory (0) or in TMEM (1, K1t) -- the default
-    picks by the measured policy (hh_fused.cu: k1t_preferred); K1s off so K1 runs."""
+    """Force K1 with the reflectors in shared memory (0), in TMEM (1, K1t) or in TMEM applied in
+    blocks (2, K1w) -- the default picks by the measured policy (hh_fused.cu: k1t_preferred,
+    k1w_preferred); K1s off so K1 runs."""
     L = hh.hh.lib()
     prev_s = L.hh_debug_k1_stream(0)
-    prev_t = L.hh_debug_k1_tmem(request.param)
+    prev_t = L.hh_debug_k1_tmem(1 if request.param else 0)
+    prev_b = L.hh_debug_k1_blocked(1 if request.param == 2 else 0)
     yield request.param
+    L.hh_debug_k1_blocked(prev_b)
     L.hh_debug_k1_tmem(prev_t)
     L.hh_debug_k1_stream(prev_s)
 
@@ -333,7 +336,8 @@ def k1_tmem(request):
 # every K1 variant built with a TMEM form (TPC = 32 at 256 / 512 threads, 64, 128), full and
 # ragged n, up to the largest h whose reflectors fit the CTA's TMEM columns
 K1T_SHAPES = [(300, 7, 333), (512, 16, 400), (780, 11, 259), (1024, 16, 1000), (1500, 13, 300),
-              (2048, 16, 700), (3000, 9, 150), (4096, 12, 300), (4096, 16, 160)]
+              (2048, 16, 700), (3000, 9, 150), (4096, 12, 300), (4096, 16, 160), (1024, 3, 77),
+              (2048, 5, 90), (4000, 1, 50)]
 
 
 @pytest.mark.parametrize("n,h,N", K1T_SHAPES)
@@ -346,7 +350,9 @@ def test_k1_tmem_reflectors(k1_tmem, n, h, N):
         with hh.algo(hh.HH_ALGO_FUSED):
             got = run_apply(op, c.U, c.X)
             v = hh.last_launch_info()["variant"]
-        assert v.endswith("_tmem") == bool(k1_tmem), v
+        assert ("_tmem" in v) == bool(k1_tmem), v
+        if n > 512:   # (the 256-thread n <= 512 variant has no blocked form)
+            assert ("_kb" in v) == (k1_tmem == 2), v
         assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"{c.name} op{op}")
     with hh.algo(hh.HH_ALGO_FUSED):
         got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
@@ -366,10 +372,12 @@ def test_k1_tmem_reflectors(k1_tmem, n, h, N):
 
 
 def test_k1t_policy():
-    """The default picks K1t where the A/B measured it faster (hh_fused.cu: k1t_preferred)."""
+    """The default picks K1t where the A/B measured it faster (hh_fused.cu: k1t_preferred), in
+    blocks of four reflectors (K1w) for multi-warp groups from h = 12 (k1w_preferred)."""
     g = torch.Generator().manual_seed(3)
-    for n, h, want in ((4096, 12, True), (2048, 9, True), (1024, 16, True), (1024, 10, False),
-                       (1024, 40, False)):
+    for n, h, want, blk in ((4096, 12, True, True), (2048, 9, True, False), (2048, 16, True, True),
+                            (1024, 16, True, False), (1024, 10, False, False),
+                            (1024, 40, False, False)):
         U = torch.randn(h, n, generator=g, dtype=torch.float64)
         U = (U / U.norm(dim=1, keepdim=True)).float().cuda()
         X = torch.randn(64, n, generator=g).cuda()
@@ -381,4 +389,5 @@ def test_k1t_policy():
             v = hh.last_launch_info()["variant"]
         finally:
             L.hh_debug_k1_stream(prev)
-        assert v.endswith("_tmem") == want, (n, h, v)
+        assert ("_tmem" in v) == want, (n, h, v)
+        assert v.endswith("_kb4") == blk, (n, h, v)

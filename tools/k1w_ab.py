@@ -1,7 +1,7 @@
-"""Same-box A/B of K1 with the reflectors in shared memory vs in TMEM (K1t,
-hh_debug_k1_tmem), K1t in blocks of reflectors (K1w, hh_debug_k1_blocked), plus K1s where it
-applies; K1 / K1t / K1s outputs must be bit-identical, K1w's differ by rounding only.
-usage (GPU box): python tools/k1t_ab.py [n:h[:op],...]"""
+"""Same-box A/B of K1t (TMEM reflectors) against its blocked form K1w at block sizes 2 / 4 / 8
+(hh_debug_k1_blocked, the kb2 / kb8 forms through hh_debug_k1's alternative table) and the
+staged-path L2 prefetch two tiles ahead (hh_debug_k1_prefetch).
+usage (GPU box): python tools/k1w_ab.py [n:h[:op],...]"""
 import os
 import sys
 
@@ -12,7 +12,8 @@ import torch  # noqa: E402
 import paper_1811_07624_b200 as hh  # noqa: E402
 
 L = hh.hh.lib()
-DEFAULT = "1024:10,1024:10:1,4096:12,4096:8,4096:16,2048:12,2048:16,1024:16,1000:10,512:10,256:8,4096:12:2"
+DEFAULT = "4096:12,4096:8,4096:10,4096:16,2048:12,2048:10,2048:16"
+ALT = {(4096, 2): 4, (4096, 8): 5, (2048, 2): 6, (2048, 8): 7}   # kF32Alt indices
 spec = sys.argv[1] if len(sys.argv) > 1 else DEFAULT
 g = torch.Generator(device="cuda").manual_seed(1)
 for item in spec.split(","):
@@ -22,50 +23,40 @@ for item in spec.split(","):
     U = torch.randn(h, n, device="cuda", generator=g, dtype=torch.float64)
     U = (U / U.norm(dim=1, keepdim=True)).float()
     X = torch.randn(N, n, device="cuda", generator=g)
-    lam = torch.rand(n, device="cuda", generator=g)
     Y = torch.empty_like(X)
     byts = 2 * N * n * 4
-
-    def call():
-        if op == 2:
-            hh.hh_sym_apply(U, lam, X, Y)
-        else:
-            hh.hh_apply(op, U, X, Y)
 
     def run(reps=20):
         with hh.algo(hh.HH_ALGO_FUSED):
             for _ in range(3):
-                call()
+                hh.hh_apply(op, U, X, Y)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(reps):
-                call()
+                hh.hh_apply(op, U, X, Y)
             e1.record()
             torch.cuda.synchronize()
             return e0.elapsed_time(e1) / reps, hh.last_launch_info()
 
     L.hh_debug_k1_stream(0)
-    L.hh_debug_k1_tmem(0)
+    L.hh_debug_k1_tmem(1)
     L.hh_debug_k1_blocked(0)
     run(2)
     ref = Y.clone()
+    cfgs = [("K1t", 0, -1, 0), ("K1w kb4", 1, -1, 0), ("K1w kb2", 1, ALT.get((n, 2), -1), 0),
+            ("K1w kb8", 1, ALT.get((n, 8), -1), 0), ("K1t pf2", 0, -1, 2), ("K1w kb4 pf2", 1, -1, 2)]
     for rep in range(2):
-        for name, st, tm, bk in (("K1 smem-u", 0, 0, 0), ("K1t tmem-u", 0, 1, 0), ("K1w blocked", 0, 1, 1),
-                                 ("K1s", 1, 0, 0)):
-            if st == 1 and n > 1024:
-                continue
-            L.hh_debug_k1_stream(st)
-            L.hh_debug_k1_tmem(tm)
+        for name, bk, alt, pf in cfgs:
             L.hh_debug_k1_blocked(bk)
-            try:
-                ms, info = run()
-            except Exception as e:  # noqa: BLE001
-                print(f"n={n} h={h} op={op} {name}: {e}", flush=True)
-                continue
+            L.hh_debug_k1(alt, 1)
+            L.hh_debug_k1_prefetch(pf)
+            ms, info = run()
             d = ((Y - ref).norm() / ref.norm()).item()
-            print(f"n={n:5d} h={h:3d} op={op} {name:11s} {info.get('variant', '?'):26s} {ms * 1e3:7.1f} us "
+            print(f"n={n:5d} h={h:3d} op={op} {name:12s} {info.get('variant', '?'):30s} {ms * 1e3:7.1f} us "
                   f"{byts / ms / 1e6:6.0f} GB/s  reldiff {d:.1e}", flush=True)
+    L.hh_debug_k1(-1, 1)
+    L.hh_debug_k1_prefetch(0)
     L.hh_debug_k1_stream(-1)
     L.hh_debug_k1_tmem(-1)
     L.hh_debug_k1_blocked(-1)
