@@ -129,6 +129,39 @@ constexpr int kRing = 3;
 
 }  // namespace
 
+// hh_mahalanobis's second stream (the pair sort beside the transform): created once per
+// calling thread and device, with its fork / join events; the hook hh_debug_mahal_fork turns
+// the overlap off for A/B (the sort then runs on the caller's stream)
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    bool tried = false;
+    ~SideStream() {
+        // (at thread exit; errors ignored -- the context may already be gone)
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
+        if (s) cudaStreamDestroy(s);
+    }
+};
+thread_local SideStream t_side[kMaxDev];
+thread_local int t_mahal_fork = 1;
+
+SideStream *side_stream() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+    SideStream &ss = t_side[dev];
+    if (!ss.tried) {
+        ss.tried = true;
+        if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            ss.s = nullptr;
+        }
+    }
+    return ss.s ? &ss : nullptr;
+}
+
 const DevAttr &device_attr() {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -186,6 +219,11 @@ int hh_debug_k1_stream(int on) { return k1_set_stream(on); }
 int hh_debug_k1_prefetch(int dist) { return k1_set_prefetch(dist); }
 int hh_debug_k1_tmem(int on) { return k1_set_tmem(on); }
 int hh_debug_k1_blocked(int on) { return k1_set_blocked(on); }
+int hh_debug_mahal_fork(int on) {
+    const int prev = t_mahal_fork;
+    t_mahal_fork = on;
+    return prev;
+}
 int hh_debug_wy_pdl(int on) { return wy_set_pdl(on); }
 
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first
@@ -424,6 +462,23 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
     if (workspace) {
         if (workspace_bytes < need) return HH_ERR_WORKSPACE;
         if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+        // The counting sort of the pairs needs only ia: it runs on a second stream beside
+        // K3a (fork / join through events, so the call stays stream-ordered and graph-
+        // capturable), and the gather waits for both.
+        const size_t zb = round256(static_cast<size_t>(n) * static_cast<size_t>(M) * elem(dtype));
+        void *bws = static_cast<char *>(workspace) + zb;
+        SideStream *side = t_mahal_fork ? side_stream() : nullptr;
+        cudaError_t e = cudaSuccess;
+        if (side) {
+            e = cudaEventRecord(side->fork, stream);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(side->s, side->fork, 0);
+            if (e == cudaSuccess) e = launch_bucket_sort(M, ia, npairs, bws, side->s);
+            if (e == cudaSuccess) e = cudaEventRecord(side->join, side->s);
+            if (e != cudaSuccess) return map_err(e);
+        } else {
+            e = launch_bucket_sort(M, ia, npairs, bws, stream);
+            if (e != cudaSuccess) return map_err(e);
+        }
         // K3a: Z = diag(sqrt d) Q^T P  (transform each point once)
         FusedArgs a{};
         a.U = U;
@@ -435,13 +490,15 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
         a.N = M;
         a.mode = MODE_TRANSFORM;
         st = run_fused(a, dtype, stream);
+        if (side) {   // join (also when K3a failed: the side stream's work stays ordered)
+            e = cudaStreamWaitEvent(stream, side->join, 0);
+            if (e != cudaSuccess) return map_err(e);
+        }
         if (st != HH_OK) return st;
         // K3b: dist[j] = ||Z[:,ia[j]] - Z[:,ib[j]]||^2, pairs bucketed by ia on device
         LaunchInfo info;
-        const size_t zb = round256(static_cast<size_t>(n) * static_cast<size_t>(M) * elem(dtype));
-        cudaError_t e = launch_gather_bucketed(workspace, n, M, ia, ib, npairs, dist,
-                                               static_cast<char *>(workspace) + zb,
-                                               dtype == HH_F32 ? 0 : 1, stream, &info);
+        e = launch_bucket_gather(workspace, n, M, ib, npairs, dist, bws, dtype == HH_F32 ? 0 : 1,
+                                 stream, &info);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (info.variant) {
             info.launches += 1;   // + K3a

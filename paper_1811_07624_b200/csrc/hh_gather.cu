@@ -234,28 +234,54 @@ size_t bucket_ws_bytes(int64_t M, int64_t npairs) {
            r(static_cast<size_t>(npairs) * 4) + r(static_cast<size_t>((M + kScanPer - 1) / kScanPer) * 4);
 }
 
+namespace {
+struct BucketWs {
+    int32_t *cnt, *cur, *off, *perm, *tot;
+};
+BucketWs bucket_ws(void *ws, int64_t M, int64_t npairs) {
+    auto r = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+    char *w = static_cast<char *>(ws);
+    BucketWs b;
+    b.cnt = reinterpret_cast<int32_t *>(w);
+    b.cur = reinterpret_cast<int32_t *>(w + r(static_cast<size_t>(M) * 4));
+    b.off = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4));
+    b.perm = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4) +
+                                         r(static_cast<size_t>(M + 1) * 4));
+    b.tot = b.perm + r(static_cast<size_t>(npairs) * 4) / 4;   // per-CTA scan totals
+    return b;
+}
+}  // namespace
+
+cudaError_t launch_bucket_sort(int64_t M, const int32_t *ia, int64_t npairs, void *ws,
+                               cudaStream_t stream) {
+    const BucketWs b = bucket_ws(ws, M, npairs);
+    const int sms = device_attr().sm_count;
+    cudaError_t e = cudaMemsetAsync(b.cnt, 0, static_cast<size_t>(M) * 4, stream);
+    if (e != cudaSuccess) return e;
+    const int g = static_cast<int>(std::min<int64_t>((npairs + 255) / 256, sms * 8));
+    bucket_hist_kernel<<<g, 256, 0, stream>>>(ia, npairs, b.cnt);
+    const int nsb = static_cast<int>((M + kScanPer - 1) / kScanPer);
+    bucket_scan_local_kernel<<<nsb, 1024, 0, stream>>>(b.cnt, M, b.off, b.tot);
+    bucket_scan_add_kernel<<<nsb, 1024, 0, stream>>>(b.tot, M, b.off, b.cur);
+    bucket_scatter_kernel<<<g, 256, 0, stream>>>(ia, npairs, b.cur, b.perm);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const int32_t *ia,
                                    const int32_t *ib, int64_t npairs, void *dist, void *ws,
                                    int dtype, cudaStream_t stream, LaunchInfo *info) {
-    auto r = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
-    char *w = static_cast<char *>(ws);
-    int32_t *cnt = reinterpret_cast<int32_t *>(w);
-    int32_t *cur = reinterpret_cast<int32_t *>(w + r(static_cast<size_t>(M) * 4));
-    int32_t *off = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4));
-    int32_t *perm = reinterpret_cast<int32_t *>(w + 2 * r(static_cast<size_t>(M) * 4) +
-                                                r(static_cast<size_t>(M + 1) * 4));
-    int32_t *tot = perm + r(static_cast<size_t>(npairs) * 4) / 4;   // per-CTA scan totals
+    cudaError_t e = launch_bucket_sort(M, ia, npairs, ws, stream);
+    if (e != cudaSuccess) return e;
+    return launch_bucket_gather(Z, n, M, ib, npairs, dist, ws, dtype, stream, info);
+}
+
+cudaError_t launch_bucket_gather(const void *Z, int64_t n, int64_t M, const int32_t *ib,
+                                 int64_t npairs, void *dist, void *ws, int dtype,
+                                 cudaStream_t stream, LaunchInfo *info) {
+    const BucketWs b = bucket_ws(ws, M, npairs);
+    int32_t *off = b.off, *perm = b.perm;
     const int sms = device_attr().sm_count;
-    cudaError_t e = cudaMemsetAsync(cnt, 0, static_cast<size_t>(M) * 4, stream);
-    if (e != cudaSuccess) return e;
-    const int g = static_cast<int>(std::min<int64_t>((npairs + 255) / 256, sms * 8));
-    bucket_hist_kernel<<<g, 256, 0, stream>>>(ia, npairs, cnt);
-    const int nsb = static_cast<int>((M + kScanPer - 1) / kScanPer);
-    bucket_scan_local_kernel<<<nsb, 1024, 0, stream>>>(cnt, M, off, tot);
-    bucket_scan_add_kernel<<<nsb, 1024, 0, stream>>>(tot, M, off, cur);
-    bucket_scatter_kernel<<<g, 256, 0, stream>>>(ia, npairs, cur, perm);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
 
     const int E = dtype == 0 ? 4 : 2;
     const int64_t nv = n / E;

@@ -50,6 +50,14 @@ size_t bucket_ws_bytes(int64_t M, int64_t npairs);
 cudaError_t launch_gather_bucketed(const void *Z, int64_t n, int64_t M, const int32_t *ia,
                                    const int32_t *ib, int64_t npairs, void *dist, void *ws,
                                    int dtype, cudaStream_t stream, LaunchInfo *info);
+// ... the same in two halves: the counting sort of the pairs by ia (memset, histogram, scan,
+// scatter: needs only ia) and the gather (needs the sort and Z), so that the sort can run on a
+// second stream beside the transform K3a
+cudaError_t launch_bucket_sort(int64_t M, const int32_t *ia, int64_t npairs, void *ws,
+                               cudaStream_t stream);
+cudaError_t launch_bucket_gather(const void *Z, int64_t n, int64_t M, const int32_t *ib,
+                                 int64_t npairs, void *dist, void *ws, int dtype,
+                                 cudaStream_t stream, LaunchInfo *info);
 
 // A/B hook (hh_debug_k1): force an alternative fused variant (-1: none), grid multiplier.
 void k1_set_debug(int alt, int gridx);

@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
             L.hh_debug_k1_tmem.restype = i32
             L.hh_debug_k1_blocked.argtypes = [i32]
             L.hh_debug_k1_blocked.restype = i32
+            L.hh_debug_mahal_fork.argtypes = [i32]
+            L.hh_debug_mahal_fork.restype = i32
             L.hh_debug_wy_pdl.argtypes = [i32]
             L.hh_debug_wy_pdl.restype = i32
         if hasattr(L, "hh_debug_wy_timeline"):
