@@ -135,16 +135,28 @@ __global__ void wy_vmul_kernel(const float *__restrict__ a, const float *__restr
 // of n_pad (wt = 1 or lambda), blocks blk0.., upper 64x64 tiles only unless `full`
 // (the reduction over splits is done in fixed order by wy_gram_reduce_kernel:
 // deterministic).
+// With Pp != NULL the z slices from pz on compute, in the same launch, the partials of
+// P = W^T Lambda W of block pblk (full, wt = plam) into Pp[split] (the symmetric program).
 __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ Wf, int64_t n_pad,
                                                       int b, int nsplit, int rows, int blk0,
                                                       const float *__restrict__ wt, int full,
-                                                      float *__restrict__ Sp, int dep_wait) {
+                                                      float *__restrict__ Sp, int dep_wait, int pz,
+                                                      int pblk, const float *__restrict__ plam,
+                                                      float *__restrict__ Pp) {
     // dep_wait = 0: launched behind the first projection, whose result it does not read (its
     // input W was packed before that projection started): it runs beside it, not after it
     if (dep_wait) pdl_wait();
     pdl_trigger();
     const int ti = blockIdx.x, tj = blockIdx.y;
-    const int blk = blockIdx.z / nsplit, sp = blockIdx.z % nsplit;
+    int blk = blockIdx.z / nsplit, sp = blockIdx.z % nsplit;
+    float *out = Sp + (static_cast<int64_t>(blk) * nsplit + sp) * b * b;
+    if (Pp && static_cast<int>(blockIdx.z) >= pz) {
+        sp = blockIdx.z - pz;
+        blk = pblk - blk0;
+        wt = plam;
+        full = 1;
+        out = Pp + static_cast<int64_t>(sp) * b * b;
+    }
     if (ti > tj && !full) return;
     __shared__ __align__(16) float Ls[32][68], Ms[32][68];   // rows 16-B aligned: float4 reads
     const int t = threadIdx.x, tx = t % 16, ty = t / 16;
@@ -173,7 +185,6 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
         }
         __syncthreads();
     }
-    float *out = Sp + (static_cast<int64_t>(blk) * nsplit + sp) * b * b;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const int l = ti * 64 + ty * 4 + p;
@@ -190,39 +201,58 @@ __global__ void __launch_bounds__(256) wy_gram_kernel(const float *__restrict__ 
 // (deterministic).  thread_per_elem: one thread per element walking the splits (coalesced
 // across threads; enough parallelism for large b); else one warp per element, lane q adding
 // splits q, q + 32, ... then a butterfly (small b: few elements, many splits).
+// With Pp != NULL one more b x b matrix follows the nblk blocks: P = sum of the Pp partials
+// (full), written to P.
 __global__ void wy_gram_reduce_kernel(const float *__restrict__ Sp, int b, int nblk, int nsplit,
-                                      int full, float *__restrict__ S, int thread_per_elem) {
+                                      int full, float *__restrict__ S, int thread_per_elem,
+                                      const float *__restrict__ Pp, float *__restrict__ P) {
     pdl_wait();
     pdl_trigger();
     const int64_t bb = static_cast<int64_t>(b) * b;
-    if (thread_per_elem) {
-        for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-             idx < nblk * bb; idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t tot = nblk * bb + (Pp ? bb : 0);
+    // element idx: (source partials, full?, destination)
+    auto src = [&](int64_t idx, const float *&p, bool &f, float *&dst) {
+        if (idx >= nblk * bb) {
+            const int64_t e = idx - nblk * bb;
+            p = Pp + e;
+            f = true;
+            dst = P + e;
+        } else {
             const int64_t blk = idx / bb, e = idx % bb;
             const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
+            p = Sp + blk * nsplit * bb + e;
+            f = full || (l / 64) <= (m / 64);
+            dst = S + idx;
+        }
+    };
+    if (thread_per_elem) {
+        for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+             idx < tot; idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const float *p;
+            bool f;
+            float *dst;
+            src(idx, p, f, dst);
             float s = 0.f;
-            if (full || (l / 64) <= (m / 64)) {
-                const float *p = Sp + blk * nsplit * bb + e;
+            if (f)
                 for (int q = 0; q < nsplit; ++q) s += p[q * bb];
-            }
-            S[idx] = s;
+            *dst = s;
         }
         return;
     }
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t idx = w0; idx < nblk * bb; idx += nw) {
-        const int64_t blk = idx / bb, e = idx % bb;
-        const int l = static_cast<int>(e / b), m = static_cast<int>(e % b);
+    for (int64_t idx = w0; idx < tot; idx += nw) {
+        const float *p;
+        bool f;
+        float *dst;
+        src(idx, p, f, dst);
         float s = 0.f;
-        if (full || (l / 64) <= (m / 64)) {
-            const float *p = Sp + blk * nsplit * bb + e;
+        if (f)
             for (int q = lane; q < nsplit; q += 32) s += p[q * bb];
-        }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) S[idx] = s;
+        if (lane == 0) *dst = s;
     }
 }
 
@@ -561,6 +591,81 @@ __global__ void __launch_bounds__(256) wy_rowgemm_kernel(
             *reinterpret_cast<uint2 *>(Ob + o) = H;
             *reinterpret_cast<uint2 *>(Ob + lo_off + o) = L;
         }
+    }
+}
+
+// The symmetric program's folded block (b <= 64) in one launch instead of five rowgemms
+// (DESIGN.md §4): a CTA owns 64 rows r and computes, from T and P = W^T Lambda W,
+//   M = P T^T (redundantly per CTA: b^3 FMAs),  V = W T,  V' = W T^T   (its 64 rows),
+//   A1 = Lambda V' - V M,  A2 = V,
+// and writes A = [A1, A2] as bf16 hi/lo rows (As[r][0:b) = A1, As[r][b:2b) = A2).
+constexpr int kSymRows = 64;
+size_t symrows_smem(int b) {
+    return static_cast<size_t>(4) * (2 * b * (b + 1) + b * kSymRows + 2 * kSymRows * (b + 1));
+}
+__global__ void __launch_bounds__(256) wy_sym_rows_kernel(const float *__restrict__ Wk,
+                                                          const float *__restrict__ Tk,
+                                                          const float *__restrict__ P,
+                                                          const float *__restrict__ lam, int64_t n,
+                                                          int64_t n_pad, int b,
+                                                          uint16_t *__restrict__ As, int64_t alo) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ float ssm[];
+    const int ldb = b + 1;
+    float *Ts = ssm;                       // b x (b + 1): T
+    float *Ms = Ts + b * ldb;              // b x (b + 1): P, then M = P T^T
+    float *Ws = Ms + b * ldb;              // b x 64: W[l][rr]
+    float *Vs = Ws + b * kSymRows;         // 64 x (b + 1): V = W T
+    float *Vp = Vs + kSymRows * ldb;       // 64 x (b + 1): V' = W T^T
+    const int t = threadIdx.x;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kSymRows;
+    for (int e = t; e < b * b; e += 256) {
+        Ts[(e / b) * ldb + e % b] = Tk[e];
+        Ms[(e / b) * ldb + e % b] = P[e];
+    }
+    for (int e = t; e < b * kSymRows; e += 256) {
+        const int l = e / kSymRows, rr = e % kSymRows;
+        Ws[e] = Wk[static_cast<int64_t>(l) * n_pad + r0 + rr];
+    }
+    __syncthreads();
+    // V and V' (64 x b each) and M = P T^T (b x b, into registers first: Ms holds P)
+    float macc[16];
+    int mcnt = 0;
+    for (int e = t; e < b * b; e += 256, ++mcnt) {
+        const int i = e / b, j = e % b;
+        float a = 0.f;
+        for (int l = 0; l < b; ++l) a = fmaf(Ms[i * ldb + l], Ts[j * ldb + l], a);
+        macc[mcnt] = a;
+    }
+    for (int e = t; e < kSymRows * b; e += 256) {
+        const int rr = e / b, c = e % b;
+        float v = 0.f, vp = 0.f;
+        for (int l = 0; l < b; ++l) {
+            const float w = Ws[l * kSymRows + rr];
+            v = fmaf(w, Ts[l * ldb + c], v);
+            vp = fmaf(w, Ts[c * ldb + l], vp);
+        }
+        Vs[rr * ldb + c] = v;
+        Vp[rr * ldb + c] = vp;
+    }
+    __syncthreads();
+    mcnt = 0;
+    for (int e = t; e < b * b; e += 256, ++mcnt) Ms[(e / b) * ldb + e % b] = macc[mcnt];
+    __syncthreads();
+    const int64_t lda = 2 * static_cast<int64_t>(b);
+    for (int e = t; e < kSymRows * b; e += 256) {
+        const int rr = e / b, c = e % b;
+        const int64_t r = r0 + rr;
+        float acc = 0.f;
+        for (int l = 0; l < b; ++l) acc = fmaf(Vs[rr * ldb + l], Ms[l * ldb + c], acc);
+        const float a1 = fmaf(r < n ? lam[r] : 0.f, Vp[rr * ldb + c], -acc);
+        const float a2 = Vs[rr * ldb + c];
+        const uint16_t h1 = f2bf(a1), h2 = f2bf(a2);
+        As[r * lda + c] = h1;
+        As[alo + r * lda + c] = f2bf(a1 - bf2f(h1));
+        As[r * lda + b + c] = h2;
+        As[alo + r * lda + b + c] = f2bf(a2 - bf2f(h2));
     }
 }
 
@@ -1539,6 +1644,8 @@ cudaError_t g_attr_err[kMaxDevWy];
 // debug / test hooks, per calling thread (like hh_set_algo): no process-global mutable state
 thread_local unsigned long long *t_timeline = nullptr;   // hh_debug_wy_timeline
 thread_local int t_ts_min = 256;                         // hh_debug_wy_ts_min
+thread_local int t_symfuse = 3;   // hh_debug_wy_symfuse: bit 0 the folded block's operands in one
+                                  // launch, bit 1 S and P in one Gram + one reduction launch
 // K5f knobs (hh_debug_wy_flow*): on/off, project CTAs, K chunks per tile, row chunks per
 // update entry, L2 window (tiles), tiles per wavefront group, L2 policy bits; 0 = default
 struct FlowKnobs {
@@ -1698,6 +1805,12 @@ cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem,
 }
 }  // namespace
 
+int wy_set_symfuse(int on) {
+    const int prev = t_symfuse;
+    t_symfuse = on;
+    return prev;
+}
+
 int wy_set_pdl(int on) {
     const int prev = t_pdl | (t_overlap << 1);
     t_pdl = on & 1;
@@ -1716,6 +1829,9 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         cudaError_t &err = g_attr_err[dev];
         err = cudaFuncSetAttribute(wy_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kSmemMax);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_sym_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(symrows_smem(64)));
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(wy_vrec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(vrec_smem(256)));
@@ -1777,16 +1893,35 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     // the SMs that projection leaves free, so that it runs beside it.
     auto prep_rest = [&](int gram_wait) {
         const int tb = (b + 63) / 64;
+        // (fused only when the preparation runs alone, i.e. before the first projection: beside
+        // it -- multi-block programs -- the larger fused launches measured slower)
+        if (sym && (t_symfuse & 2) && gram_wait) {
+            // S (every block) and P = W^T Lambda W of the last block (full) in one Gram launch
+            // and one reduction launch
+            const int pz = m * p.nsplit;
+            ++nlaunch, note(pdl_launch(wy_gram_kernel, dim3(tb, tb, pz + p.nsplit), 256, 0, stream, Wf, n_pad, b,
+                                       p.nsplit, p.gram_rows, 0, nullptr, 0, Sp, gram_wait, pz, m - 1, lam,
+                                       F(p.off_pp)));
+            const int64_t ns = static_cast<int64_t>(m + 1) * b * b;
+            ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, static_cast<int>(std::min<int64_t>((ns * 32 + 255) / 256, sms * 16)),
+                                       256, 0, stream, Sp, b, m, p.nsplit, 0, S, ns >= 32768 ? 1 : 0,
+                                       static_cast<const float *>(F(p.off_pp)), F(p.off_p)));
+        } else {
         ++nlaunch, note(pdl_launch(wy_gram_kernel, dim3(tb, tb, m * p.nsplit), 256, 0, stream, Wf, n_pad, b, p.nsplit, p.gram_rows, 0,
-                                                                       nullptr, 0, Sp, gram_wait));
+                                   nullptr, 0, Sp, gram_wait, 0, 0, static_cast<const float *>(nullptr),
+                                   static_cast<float *>(nullptr)));
         const int64_t ns = static_cast<int64_t>(m) * b * b;
         ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, static_cast<int>(std::min<int64_t>((ns * 32 + 255) / 256, sms * 16)),
-                                256, 0, stream, Sp, b, m, p.nsplit, 0, S, ns >= 32768 ? 1 : 0));
+                                256, 0, stream, Sp, b, m, p.nsplit, 0, S, ns >= 32768 ? 1 : 0,
+                                static_cast<const float *>(nullptr), static_cast<float *>(nullptr)));
         if (sym) {   // P = W^T Lambda W of the last block (full)
             ++nlaunch, note(pdl_launch(wy_gram_kernel, dim3(tb, tb, p.nsplit), 256, 0, stream, Wf, n_pad, b, p.nsplit, p.gram_rows,
-                                                                       m - 1, lam, 1, F(p.off_pp), 1));
-            ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, std::max(1, std::min(sms * 16, (b * b * 32 + 255) / 256)), 256, 0, stream, 
-                F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p), b * b >= 32768 ? 1 : 0));
+                                       m - 1, lam, 1, F(p.off_pp), 1, 0, 0, static_cast<const float *>(nullptr),
+                                       static_cast<float *>(nullptr)));
+            ++nlaunch, note(pdl_launch(wy_gram_reduce_kernel, std::max(1, std::min(sms * 16, (b * b * 32 + 255) / 256)), 256, 0, stream,
+                F(p.off_pp), b, 1, p.nsplit, 1, F(p.off_p), b * b >= 32768 ? 1 : 0,
+                static_cast<const float *>(nullptr), static_cast<float *>(nullptr)));
+        }
         }
         ++nlaunch, note(pdl_launch(wy_tbuild_kernel, m, 256, tbuild_smem(b), stream, S, b, T, sym ? 0 : 1));
         if (!sym) {
@@ -1815,6 +1950,11 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
                 ++nlaunch, note(pdl_launch(wy_rowgemm_kernel<true, true>, gv, 256, 0, stream, 
                     n_pad, Wk, n_pad, Tk, b, b, nullptr, 0, nullptr, 0, 1.f, nullptr,
                     Vt + static_cast<int64_t>(k) * n_pad * b, b, vlo));
+            } else if (b <= 64 && (t_symfuse & 1) && gram_wait) {
+                // the folded block's operands in one launch (wy_sym_rows_kernel)
+                ++nlaunch, note(pdl_launch(wy_sym_rows_kernel, static_cast<int>(n_pad / kSymRows), 256,
+                    symrows_smem(b), stream, Wk, Tk, F(p.off_p), lam, p.n, n_pad, b, H(p.off_asym),
+                    n_pad * 2 * b));
             } else {
                 // A2 = W T (bf16 into columns [b, 2b) of Asym, fp32 copy Vf); V' = W T^T;
                 // M = P T^T; A1 = Lambda V' - V M (columns [0, b)).  DESIGN.md §4.
