@@ -57,6 +57,8 @@ def lib():
         L.hh_ref_knn.restype = i32
         L.hh_ref_congruence.argtypes = [i32, i64, i64, p, p, p, i64]
         L.hh_ref_congruence.restype = i32
+        L.hh_ref_shf_cost.argtypes = [i64, p, p, p, i64, p, p]
+        L.hh_ref_shf_cost.restype = i32
         L.hh_ref_sym_apply_signed.restype = i32
         L.hh_ref_num_threads.restype = i32
         L.hh_ref_set_threads.argtypes = [i32]
@@ -179,3 +181,20 @@ def congruence(op: int, U, M) -> np.ndarray:
     if rc:
         raise ValueError(f"hh_ref_congruence rc={rc}")
     return out
+
+
+def shf_cost(A, B, Uc, grad: bool = True):
+    """(cost (K,), grad (K, n) or None): the SHF objective C(u_k) of one reflector and its
+    gradient for candidates Uc of shape (K, n) (hh_ref.c: hh_ref_shf_cost, eq:theRk,
+    eq:gradient, NEXT-f4).  A, B: symmetric (n, n)."""
+    A, B, Uc = _f64(A), _f64(B), _f64(Uc)
+    n = A.shape[0]
+    Uc = Uc.reshape(-1, n) if np.size(Uc) else np.zeros((0, n))
+    K = Uc.shape[0]
+    cost = np.empty(K, dtype=np.float64)
+    g = np.empty((K, n), dtype=np.float64) if grad else None
+    rc = lib().hh_ref_shf_cost(n, _ptr(A), _ptr(B), _ptr(Uc), K, _ptr(cost),
+                               _ptr(g) if grad else None)
+    if rc:
+        raise ValueError(f"hh_ref_shf_cost rc={rc}")
+    return cost, g

@@ -280,6 +280,60 @@ int hh_ref_congruence(int op, int64_t n, int64_t h, const double *U, const doubl
     return rc;
 }
 
+/* NEXT-f4: the SHF objective of one reflector and its gradient for K
+ * candidate vectors u_k (Uc: n x K column-major, u_k = Uc + k*n), A and B symmetric n x n:
+ *   C(u)      = u^T (A B + B A) u - 2 tr(A u u^T B u u^T)                   eq:theRk
+ *   tr(A u u^T B u u^T) = (u^T A u)(u^T B u)                               (cyclic trace)
+ *   grad C(u) = 2 (A B + B A) u - 4 ((u^T A u) B + (u^T B u) A) u           eq:gradient
+ * Literally: the matrix A B + B A is formed once (plain triple loop), then each candidate
+ * takes its quadratic forms and matrix-vector products one by one.  grad may be NULL. */
+int hh_ref_shf_cost(int64_t n, const double *A, const double *B, const double *Uc, int64_t K,
+                    double *cost, double *grad) {
+    if (n < 1 || K < 0) return 1;
+    const size_t nn = (size_t)n * (size_t)n;
+    double *Mab = (double *)malloc(sizeof(double) * nn);
+    if (!Mab) return 2;
+    /* Mab = A B + B A (entry (i, j); A, B symmetric so either storage order) */
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (int64_t l = 0; l < n; ++l) s += A[i * n + l] * B[l * n + j];
+            for (int64_t l = 0; l < n; ++l) s += B[i * n + l] * A[l * n + j];
+            Mab[i * n + j] = s;
+        }
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < K; ++k) {
+        const double *u = Uc + (size_t)k * (size_t)n;
+        double q = 0.0, qa = 0.0, qb = 0.0;   /* u^T Mab u, u^T A u, u^T B u */
+        for (int64_t i = 0; i < n; ++i) {
+            double mi = 0.0, ai = 0.0, bi = 0.0;
+            for (int64_t j = 0; j < n; ++j) {
+                mi += Mab[i * n + j] * u[j];
+                ai += A[i * n + j] * u[j];
+                bi += B[i * n + j] * u[j];
+            }
+            q += u[i] * mi;
+            qa += u[i] * ai;
+            qb += u[i] * bi;
+        }
+        cost[k] = q - 2.0 * (qa * qb);
+        if (grad) {
+            double *g = grad + (size_t)k * (size_t)n;
+            for (int64_t i = 0; i < n; ++i) {
+                double mi = 0.0, ci = 0.0;
+                for (int64_t j = 0; j < n; ++j) {
+                    mi += Mab[i * n + j] * u[j];
+                    ci += (qa * B[i * n + j] + qb * A[i * n + j]) * u[j];
+                }
+                g[i] = 2.0 * mi - 4.0 * ci;
+            }
+        }
+    }
+    free(Mab);
+    return 0;
+}
+
 int hh_ref_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

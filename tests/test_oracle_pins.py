@@ -489,3 +489,76 @@ def test_congruence_dense_and_shf_identity():
         lhs = np.linalg.norm(S - Sbar)
         rhs = np.linalg.norm(Ak - Hk @ Bk @ Hk)
         assert abs(lhs - rhs) < 1e-12 * max(1.0, lhs)
+
+
+# ---------------------------------------------------------------- NEXT-f4: C(u), grad C(u)
+def _sym_pair(g, n):
+    A = g.standard_normal((n, n))
+    B = g.standard_normal((n, n))
+    return A + A.T, B + B.T
+
+
+def test_shf_cost_objective_identity():
+    """eq:objectivefunctionS3: for unit u and H = I - 2 u u^T,
+    ||A - H B H||_F^2 = ||A||_F^2 + ||B||_F^2 - 2 tr(A B) + 4 C(u) -- the paper's own expansion,
+    computed densely here; a wrong sign, factor or dropped term of C fails it."""
+    g = np.random.default_rng(71)
+    for n in (3, 8, 33):
+        A, B = _sym_pair(g, n)
+        U = g.standard_normal((6, n))
+        U /= np.linalg.norm(U, axis=1, keepdims=True)
+        cost, _ = oracle.shf_cost(A, B, U, grad=False)
+        for k, u in enumerate(U):
+            H = dense_reflector(u)
+            lhs = np.linalg.norm(A - H @ B @ H) ** 2
+            rhs = np.linalg.norm(A) ** 2 + np.linalg.norm(B) ** 2 - 2 * np.trace(A @ B) + 4 * cost[k]
+            assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(lhs)), (n, k, lhs, rhs)
+
+
+def test_shf_gradient_finite_differences():
+    """eq:gradient against central differences of the oracle's own C (fp64),
+    for arbitrary (not unit) u: the gradient formula is that of the unconstrained C."""
+    g = np.random.default_rng(72)
+    n = 11
+    A, B = _sym_pair(g, n)
+    U = g.standard_normal((4, n))
+    _, G = oracle.shf_cost(A, B, U)
+    eps = 1e-6
+    for k in range(U.shape[0]):
+        fd = np.empty(n)
+        for i in range(n):
+            up, um = U[k].copy(), U[k].copy()
+            up[i] += eps
+            um[i] -= eps
+            fd[i] = (oracle.shf_cost(A, B, up[None], grad=False)[0][0] -
+                     oracle.shf_cost(A, B, um[None], grad=False)[0][0]) / (2 * eps)
+        assert np.allclose(G[k], fd, rtol=1e-6, atol=1e-6 * np.abs(G[k]).max()), (k, G[k], fd)
+
+
+def test_shf_cost_shared_eigenvector():
+    """Closed form: if A v = a v and B v = b v (unit v) then C(v) = 2ab - 2ab = 0 and
+    grad C(v) = 4ab v - 8ab v = -4ab v (eq:theRk, eq:gradient)."""
+    g = np.random.default_rng(73)
+    n = 9
+    Qm, _ = np.linalg.qr(g.standard_normal((n, n)))
+    ea, eb = g.standard_normal(n), g.standard_normal(n)
+    A = Qm @ np.diag(ea) @ Qm.T
+    B = Qm @ np.diag(eb) @ Qm.T
+    A, B = (A + A.T) / 2, (B + B.T) / 2
+    cost, G = oracle.shf_cost(A, B, Qm.T)
+    for k in range(n):
+        assert abs(cost[k]) < 1e-12 * (1 + abs(ea[k] * eb[k])), (k, cost[k])
+        assert np.allclose(G[k], -4 * ea[k] * eb[k] * Qm[:, k], atol=1e-11), k
+
+
+def test_shf_cost_swap_and_scale():
+    """C is symmetric in (A, B); C(u; sA, B) = s C(u; A, B) (both terms are linear in A)."""
+    g = np.random.default_rng(74)
+    n = 7
+    A, B = _sym_pair(g, n)
+    U = g.standard_normal((5, n))
+    c1, g1 = oracle.shf_cost(A, B, U)
+    c2, g2 = oracle.shf_cost(B, A, U)
+    c3, g3 = oracle.shf_cost(2.5 * A, B, U)
+    assert np.allclose(c1, c2, rtol=1e-12, atol=1e-12) and np.allclose(g1, g2, rtol=1e-12, atol=1e-11)
+    assert np.allclose(c3, 2.5 * c1, rtol=1e-12, atol=1e-11) and np.allclose(g3, 2.5 * g1, rtol=1e-12, atol=1e-10)
