@@ -2,7 +2,7 @@
 """Benchmark of the Householder-product apply hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {hh,reference}]
-                    [--workload C2|C1|C3|C4|C5h12|C5h64|C5h256|C5h1024] [--op N|T]
+                    [--workload C2|C1|C3|C4|C5h12|C5h64|C5h256|C5h1024|KNN|CONG|QR4095|SHF] [--op N|T]
 
 Default workload = BASELINE.json configs[1] (the metric's config): Y = H1...Hh X,
 fp32, n=1024, h=10, N=262144 columns (1 GiB in, 1 GiB out; larger than the 126 MB
@@ -60,6 +60,17 @@ def workload_case(name: str, N_override=None):
         c.X = gi.gaussian_columns(g, cnt * n, n, "f32")     # (count * n, n) == count n x n matrices
         c.N, c.call, c.name, c.count = cnt * n, "congruence", "CONG", cnt
         return c
+    if name == "SHF":   # NEXT-f4: C(u) and grad C for 256 candidates of one (A_k, B_k), n = 1024
+        n, K = 1024, 256
+        g = gi.rng(610, n, K)
+        c = gi.make_case("apply", n, 1, 1, "f32", seed=61)
+        A = g.standard_normal((n, n))
+        B = g.standard_normal((n, n))
+        c.X = ((A + A.T) / 2).astype(np.float32)          # A_k (symmetric)
+        c.d = ((B + B.T) / 2).astype(np.float32)          # B_k (symmetric)
+        c.U = gi.unit_reflectors(g, K, n, "f32")          # the candidates u (K, n)
+        c.N, c.h, c.call, c.name, c.K = K, 0, "shf", "SHF", K
+        return c
     if name.startswith("QR"):   # NEXT-f2: n=4096, h = n-1 partial-QR reflectors (C5's X)
         h = int(name[2:]) if len(name) > 2 else 4095
         c = gi.make_config(5, h=min(h, 1024), N=N_override)
@@ -77,6 +88,10 @@ def alg_cost(c, op_count=1):
         byts = (c.N + Mq) * c.n * s + Mq * c.k * 8           # points read once + results
         flops = 4 * c.h * c.n * (c.N + Mq) + 2 * c.n * c.N * Mq   # transform once + dots
         return byts, flops, Mq
+    if c.call == "shf":   # A, B, the candidates read once; C and grad C written; 8 n^2 K flops
+        byts = (2 * c.n * c.n + 2 * c.n * c.K + c.K) * s
+        flops = 8 * c.n * c.n * c.K
+        return byts, flops, c.K
     if c.call == "congruence":   # op(Q) M op(Q)^T: M read once, written once; 2 x 4hn per column
         byts = 2 * c.count * c.n * c.n * s
         flops = 2 * 4 * c.h * c.n * c.n * c.count
@@ -229,6 +244,8 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
         t0 = time.perf_counter()
         if c.call == "knn":
             res["out"] = oracle.knn(c.U, c.d, c.X, c.lam[:k], c.k)
+        elif c.call == "shf":
+            res["out"] = oracle.shf_cost(c.X, c.d, c.U[:k])
         elif c.call == "congruence":
             res["out"] = oracle.congruence(op, c.U, c.X[:k * c.n].reshape(k, c.n, c.n))
         elif c.call == "mahalanobis":
@@ -240,7 +257,7 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
         return time.perf_counter() - t0
 
     total = units
-    k = min(total, {"mahalanobis": 2048, "knn": 4, "congruence": 1}.get(c.call, 256))
+    k = min(total, {"mahalanobis": 2048, "knn": 4, "congruence": 1, "shf": 64}.get(c.call, 256))
     dt = run(k)
     while dt < 0.5 and k < total:
         k = min(total, k * 4)
@@ -251,7 +268,8 @@ def time_oracle(c, op, target_s=10.0, max_cols=None):
     if k2 != k:
         dt = run(k2)
         k = k2
-    what = {"mahalanobis": "pairs", "knn": "queries", "congruence": "matrices"}.get(c.call, "columns")
+    what = {"mahalanobis": "pairs", "knn": "queries", "congruence": "matrices",
+            "shf": "candidates"}.get(c.call, "columns")
     return (per_unit_bytes * k / dt / 1e9, k / dt, dt,
             f"{k} of {total} {what} of {c.name} (fp64 oracle, {threads} threads)", threads, k,
             res["out"])
@@ -271,6 +289,19 @@ def parity_of(c, k, ref, Y, dist_out, knn_out, dev):
         return {"rel_l2_dist": e, "index_agreement": float((gi_[:k].cpu().numpy() == ri).mean()),
                 "gate": g, "sampled": int(k), "of": int(c.lam.shape[0]),
                 "pass": bool(e <= g)}
+    if c.call == "shf":   # reading R21: each candidate against the size of its terms
+        cost, grad = knn_out
+        c_ref, g_ref = ref
+        A64, B64, U64 = (x.astype(np.float64) for x in (c.X, c.d, c.U[:k]))
+        a, b = U64 @ A64, U64 @ B64
+        al, be = np.sum(U64 * a, 1), np.sum(U64 * b, 1)
+        na, nb = np.linalg.norm(a, axis=1), np.linalg.norm(b, axis=1)
+        g = 1e-6 * math.sqrt(c.n)
+        ec = np.abs(cost[:k].double().cpu().numpy() - c_ref) / (2 * na * nb + 2 * np.abs(al * be))
+        sg = 2 * (np.linalg.norm(A64) * nb + np.linalg.norm(B64) * na) + 4 * (np.abs(al) * nb + np.abs(be) * na)
+        eg = np.linalg.norm(grad[:k].double().cpu().numpy() - g_ref, axis=1) / sg
+        return {"max_rel_cost": float(ec.max()), "max_rel_grad": float(eg.max()), "gate": g,
+                "sampled": int(k), "of": int(c.K), "pass": bool(ec.max() <= g and eg.max() <= g)}
     if c.call == "congruence":
         got = Y[:k * c.n].double().cpu().numpy().reshape(ref.shape)
         e = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
@@ -318,6 +349,8 @@ def run_reference(args):
         t0 = time.perf_counter()
         if c.call == "knn":
             oracle.knn(sub.U, sub.d, sub.X, sub.lam[:k], sub.k)
+        elif c.call == "shf":
+            oracle.shf_cost(sub.X, sub.d, sub.U[:k])
         elif c.call == "congruence":
             oracle.congruence(op, sub.U, sub.X[:k * sub.n].reshape(k, sub.n, sub.n))
         elif c.call == "mahalanobis":
@@ -331,7 +364,8 @@ def run_reference(args):
             times.append(dt)
     tot = sum(times)
     value = per_unit_bytes * k * steps / tot / 1e9
-    what = {"mahalanobis": "pairs", "knn": "queries", "congruence": "matrices"}.get(c.call, "columns")
+    what = {"mahalanobis": "pairs", "knn": "queries", "congruence": "matrices",
+            "shf": "candidates"}.get(c.call, "columns")
     sample = f"{k} of {units} {what} of {c.name} per step (fp64 oracle, {threads} threads)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
@@ -358,6 +392,9 @@ def config_of(c, args):
         d["npairs"] = c.npairs
     if c.call == "congruence":
         d.update({"count": c.count, "op": args.op, "form": "op(Q) M op(Q)^T (eq:ak / eq:bk, P:297-304)"})
+    if c.call == "shf":
+        d.update({"K": c.K, "form": "C(u) and grad C(u) of one reflector (eq:theRk, eq:gradient, "
+                                    "P:316-377), A, B symmetric"})
     if c.call == "knn":
         d.update({"M_ref": c.N, "M_query": int(c.lam.shape[0]), "k": c.k,
                   "stand_in_for": "Table I MNIST after PCA (P:670), iid N(0,1)"})
@@ -415,6 +452,18 @@ def run_hh(args):
         step = lambda: hh.hh_mahalanobis(U, d, X, ia, ib, dist_out, workspace=wsp,  # noqa: E731
                                          stream=stream)
         launches = 2
+    elif c.call == "shf":
+        A = X
+        B = torch.from_numpy(c.d).to(dev)
+        cost = torch.empty(c.K, dtype=X.dtype, device=dev)
+        gout = torch.empty_like(U)
+        wsb = hh.hh_workspace_bytes(hh.HH_CALL_SHF, c.n, 0, c.K, 0, X.dtype)
+        wsp = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        knn_out = {"r": (cost, gout)}
+        dist_out = None
+        step = lambda: hh.hh_shf_cost(A, B, U, cost=cost, grad_out=gout, workspace=wsp,  # noqa: E731
+                                      stream=stream)
+        launches = 4
     elif c.call == "congruence":
         M = X.view(c.count, c.n, c.n)
         Mo = Y.view(c.count, c.n, c.n)
@@ -649,7 +698,7 @@ def run_hh(args):
                        "sample": sample, "seconds": secs, "vectors_per_s": ups, "cpu": cpu_model()}
             if not args.no_parity:
                 parity = parity_of(c, k_or, ref, Y, dist_out if c.call == "mahalanobis" else None,
-                                   knn_out.get("r") if c.call == "knn" else None, dev)
+                                   knn_out.get("r") if c.call in ("knn", "shf") else None, dev)
         if not args.ncu and roof is not None:
             roof["same_run_copy_gbs"] = same_run_copy_gbs(dev)
         out = {

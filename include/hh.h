@@ -118,7 +118,8 @@ typedef enum {
     HH_CALL_MAHALANOBIS = 2,
     HH_CALL_APPLY_HOST = 3,
     HH_CALL_KNN = 4,
-    HH_CALL_CONGRUENCE = 5
+    HH_CALL_CONGRUENCE = 5,
+    HH_CALL_SHF = 6
 } hh_call;
 
 /*
@@ -236,6 +237,28 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d,
 hh_status hh_congruence(hh_op op, int64_t n, int64_t h, const void *U, const void *M, void *Mout,
                         int64_t count, hh_dtype dtype, void *workspace, size_t workspace_bytes,
                         hh_stream_t stream);
+
+/*
+ * hh_shf_cost -- the SHF fitting objective of one reflector and its gradient for K
+ *   candidate vectors u_k (NEXT-f4):
+ *     cost[k]   = C(u_k) = u^T (A B + B A) u - 2 tr(A u u^T B u u^T)       (eq:theRk)
+ *               = 2 (A u)^T (B u) - 2 (u^T A u)(u^T B u)                    (A, B symmetric)
+ *     grad[:,k] = 2 (A B + B A) u - 4 ((u^T A u) B + (u^T B u) A) u        (eq:gradient)
+ *   the per-candidate quantities of the SHF step: the gamma sweep of eq:combine and the
+ *   gradient iteration eq:iterate evaluate C (and grad C) at many u for one (A_k, B_k).
+ *   A, B: n x n SYMMETRIC (DEVICE; symmetry is a documented, unvalidated precondition --
+ *   either storage order then reads the same), Uc: n x K column-major (u_k at Uc + k n),
+ *   cost: K values, grad: n x K column-major or NULL (cost only).  u need not be unit.
+ *   Computed as [A u | B u] for all k (one batched contraction), per-candidate dots, and
+ *   (with grad) A (B u) + B (A u) with the -4 (.) terms fused; A B + B A is never formed.
+ *   fp32 or fp64 on the FMA pipe.  workspace (DEVICE) >=
+ *   hh_workspace_bytes(HH_CALL_SHF, n, 0, K, 0, dtype) (a = A u and b = B u for every
+ *   candidate, the split-K partial products of the contraction, a few per-candidate scalars).  Errors: HH_ERR_INVALID_VALUE (n < 1, K < 0, NULL operands, bad dtype),
+ *   HH_ERR_WORKSPACE (too small), HH_ERR_UNSUPPORTED (operands not aligned to the dtype).
+ */
+hh_status hh_shf_cost(int64_t n, const void *A, const void *B, const void *Uc, int64_t K,
+                      void *cost, void *grad, hh_dtype dtype, void *workspace,
+                      size_t workspace_bytes, hh_stream_t stream);
 
 /*
  * hh_knn -- test-time k nearest neighbours under the learned metric (NEXT-f3):

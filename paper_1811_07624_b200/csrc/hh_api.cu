@@ -291,6 +291,9 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
             *bytes = 2 * mb + aw;
             return HH_OK;
         }
+        case HH_CALL_SHF:   /* N_or_M = K candidates */
+            *bytes = shf_ws_bytes(n, N_or_M, dtype == HH_F32 ? 0 : 1);
+            return HH_OK;
         case HH_CALL_KNN:   /* N_or_M = M_ref, npairs = M_query; k = h is not needed: max */
             *bytes = knn_plan(n, N_or_M, npairs, 16, device_attr().sm_count).bytes;
             return HH_OK;
@@ -521,6 +524,27 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
     a.N = npairs;
     a.mode = MODE_PAIR;
     return run_fused(a, dtype, stream);
+}
+
+hh_status hh_shf_cost(int64_t n, const void *A, const void *B, const void *Uc, int64_t K,
+                      void *cost, void *grad, hh_dtype dtype, void *workspace,
+                      size_t workspace_bytes, hh_stream_t stream) {
+    if (n < 1 || K < 0 || !dtype_ok(dtype)) return HH_ERR_INVALID_VALUE;
+    if (K == 0) return HH_OK;
+    if (!A || !B || !Uc || !cost || !workspace) return HH_ERR_INVALID_VALUE;
+    const size_t s = elem(dtype);
+    for (const void *q : {A, B, Uc, static_cast<const void *>(cost), static_cast<const void *>(grad),
+                          static_cast<const void *>(workspace)})
+        if (reinterpret_cast<uintptr_t>(q) % s != 0) return HH_ERR_UNSUPPORTED;
+    if (workspace_bytes < shf_ws_bytes(n, K, dtype == HH_F32 ? 0 : 1)) return HH_ERR_WORKSPACE;
+    LaunchInfo info;
+    cudaError_t e = launch_shf(n, A, B, Uc, K, cost, grad, dtype == HH_F32 ? 0 : 1, workspace,
+                               static_cast<cudaStream_t>(stream), &info);
+    if (e == cudaSuccess) {
+        t_last = info;
+        t_has_last = true;
+    }
+    return map_err(e);
 }
 
 hh_status hh_congruence(hh_op op, int64_t n, int64_t h, const void *U, const void *M, void *Mout,

@@ -70,6 +70,11 @@ int k1_set_tmem(int on);      // A/B hook (hh_debug_k1_tmem): -1 policy, 0 never
 int k1_set_blocked(int on);   // A/B hook (hh_debug_k1_blocked): K1w -1 policy, 0 never, 1 when K1t runs; previous
 int k1_set_stream(int on);   // A/B hook (hh_debug_k1_stream): -1 auto, 0 K1, 1 K1s; previous
 
+// K8 (hh_shf.cu): the SHF objective C(u) and its gradient for K candidates (NEXT-f4)
+size_t shf_ws_bytes(int64_t n, int64_t K, int dtype);
+cudaError_t launch_shf(int64_t n, const void *A, const void *B, const void *Uc, int64_t K, void *cost,
+                       void *grad, int dtype, void *ws, cudaStream_t stream, LaunchInfo *info);
+
 // Largest n the vector kernels support for this dtype.
 int64_t max_n(int dtype);
 

@@ -26,7 +26,7 @@ HH_OK, HH_ERR_INVALID_VALUE, HH_ERR_UNSUPPORTED, HH_ERR_WORKSPACE, HH_ERR_CUDA =
 HH_F32, HH_F64 = 0, 1
 HH_OP_N, HH_OP_T = 0, 1
 HH_CALL_APPLY, HH_CALL_SYM, HH_CALL_MAHALANOBIS, HH_CALL_APPLY_HOST, HH_CALL_KNN, \
-    HH_CALL_CONGRUENCE = range(6)
+    HH_CALL_CONGRUENCE, HH_CALL_SHF = range(7)
 HH_ALGO_AUTO, HH_ALGO_FUSED, HH_ALGO_WY = range(3)
 HH_SIDE_LEFT, HH_SIDE_RIGHT = range(2)
 
@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
         L.hh_apply_qr.restype = i32
         L.hh_congruence.argtypes = [i32, i64, i64, p, p, p, i64, i32, p, sz, p]
         L.hh_congruence.restype = i32
+        L.hh_shf_cost.argtypes = [i64, p, p, p, i64, p, p, i32, p, sz, p]
+        L.hh_shf_cost.restype = i32
         L.hh_knn.argtypes = [i64, i64, p, p, p, i64, p, i64, i32, p, p, i32, p, sz, p]
         L.hh_knn.restype = i32
         L.hh_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
@@ -429,6 +431,41 @@ def hh_congruence(op: int, U: torch.Tensor, M: torch.Tensor, out: Optional[torch
                                  count, _dtype(M), _ptr(ws), wsb, _stream(stream, M.device))
     _check(st, "hh_congruence")
     return out
+
+
+def hh_shf_cost(A: torch.Tensor, B: torch.Tensor, Uc: torch.Tensor, grad: bool = True,
+                cost: Optional[torch.Tensor] = None, grad_out: Optional[torch.Tensor] = None,
+                workspace: Optional[torch.Tensor] = None, stream=None):
+    """(cost (K,), grad (K, n) or None): the SHF objective C(u_k) of one reflector and its
+    gradient for the candidates Uc of shape (K, n), A and B symmetric (n, n)
+    (hh.h: hh_shf_cost, eq:theRk / eq:gradient, NEXT-f4)."""
+    for t, nm in ((A, "A"), (B, "B"), (Uc, "Uc")):
+        _dev(t, nm)
+    if A.dim() != 2 or A.shape[0] != A.shape[1] or A.dtype not in _DT:
+        raise ValueError(f"A must be a square fp32/fp64 matrix, got {tuple(A.shape)} {A.dtype}")
+    n = A.shape[0]
+    if B.shape != A.shape or B.dtype != A.dtype or B.device != A.device:
+        raise ValueError(f"B must match A ({tuple(A.shape)} {A.dtype} on {A.device})")
+    if Uc.dim() != 2 or Uc.shape[1] != n or Uc.dtype != A.dtype or Uc.device != A.device:
+        raise ValueError(f"Uc must be (K, {n}) {A.dtype} on {A.device}")
+    K = Uc.shape[0]
+    if cost is None:
+        cost = torch.empty(K, dtype=A.dtype, device=A.device)
+    if grad and grad_out is None:
+        grad_out = torch.empty_like(Uc)
+    for t, nm, shp in ((cost, "cost", (K,)), (grad_out if grad else None, "grad_out", tuple(Uc.shape))):
+        if t is None:
+            continue
+        _dev(t, nm)
+        if tuple(t.shape) != shp or t.dtype != A.dtype or t.device != A.device:
+            raise ValueError(f"{nm} must be {shp} {A.dtype} on {A.device}")
+    with _on(A.device):
+        ws, wsb = _workspace(HH_CALL_SHF, n, 0, K, 0, A, workspace) if K else (None, 0)
+        st = lib().hh_shf_cost(n, _ptr(A), _ptr(B), _ptr(Uc), K, _ptr(cost),
+                               _ptr(grad_out) if grad else None, _DT[A.dtype], _ptr(ws), wsb,
+                               _stream(stream, A.device))
+    _check(st, "hh_shf_cost")
+    return cost, (grad_out if grad else None)
 
 
 def hh_knn(U: torch.Tensor, d: torch.Tensor, P_ref: torch.Tensor, P_query: torch.Tensor, k: int,

@@ -4,7 +4,7 @@
 tag=${1:-sweep}; shift
 mkdir -p gpurun_out
 out=gpurun_out/${tag}_sweep.jsonl; : > $out
-for w in C1 C2 C3 C4 C5h12 C5h64 C5h256 C5h1024 KNN QR4095 CONG; do
+for w in C1 C2 C3 C4 C5h12 C5h64 C5h256 C5h1024 KNN QR4095 CONG SHF; do
   steps=50; [ $w = C5h1024 ] && steps=20; [ $w = QR4095 ] && steps=5
   timeout 600 python bench.py --workload $w --steps $steps --warmup 3 --no-e2e --cpu-seconds 3 "$@" >> $out 2>> gpurun_out/${tag}_sweep.err
   echo "$w rc=$?" >> gpurun_out/${tag}_sweep.err
