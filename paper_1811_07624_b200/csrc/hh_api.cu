@@ -162,6 +162,13 @@ SideStream *side_stream() {
     return ss.s ? &ss : nullptr;
 }
 
+void drop_side_stream() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return;
+    t_side[dev] = SideStream{};   // (the old handles are abandoned, not destroyed: they are stale)
+    t_side[dev].tried = true;     // and not re-created in this thread
+}
+
 const DevAttr &device_attr() {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -478,6 +485,15 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
             if (e == cudaSuccess) e = cudaStreamWaitEvent(side->s, side->fork, 0);
             if (e == cudaSuccess) e = launch_bucket_sort(M, ia, npairs, bws, side->s);
             if (e == cudaSuccess) e = cudaEventRecord(side->join, side->s);
+            if (e != cudaSuccess && e != cudaErrorStreamCaptureUnsupported &&
+                e != cudaErrorStreamCaptureInvalidated) {
+                // a stale cached stream (e.g. after a device reset): forget it and sort on the
+                // caller's stream instead
+                cudaGetLastError();
+                drop_side_stream();
+                side = nullptr;
+                e = launch_bucket_sort(M, ia, npairs, bws, stream);
+            }
             if (e != cudaSuccess) return map_err(e);
         } else {
             e = launch_bucket_sort(M, ia, npairs, bws, stream);

@@ -123,7 +123,7 @@ __device__ __forceinline__ void ffma2(float &d0, float &d1, float a, float b0, f
         : "+f"(d0), "+f"(d1)
         : "f"(a), "f"(b0), "f"(b1));
 }
-__global__ void __launch_bounds__(128) shf_gemm_f32_kernel(int64_t n, int64_t K, const float *__restrict__ A,
+__global__ void __launch_bounds__(128, 2) shf_gemm_f32_kernel(int64_t n, int64_t K, const float *__restrict__ A,
                                                            const float *__restrict__ B, const float *__restrict__ Uc,
                                                            const float *__restrict__ Ya, const float *__restrict__ Yb,
                                                            float *__restrict__ part, int grad_mode) {
@@ -136,32 +136,37 @@ __global__ void __launch_bounds__(128) shf_gemm_f32_kernel(int64_t n, int64_t K,
     const int64_t k0 = static_cast<int64_t>(blockIdx.y) * kFN;
     const int64_t js = static_cast<int64_t>(blockIdx.z) * kSlice;
     const int64_t je = js + kSlice < Jtot ? js + kSlice : Jtot;
-    auto mval = [&](int64_t i, int64_t j) -> float {
-        if (i >= Mrows || j >= je) return 0.f;
-        if (!grad_mode) return i < n ? A[j * n + i] : B[j * n + (i - n)];
-        return j < n ? A[j * n + i] : B[(j - n) * n + i];
-    };
-    auto rval = [&](int64_t j, int64_t k) -> float {
-        if (k >= K || j >= je) return 0.f;
-        if (!grad_mode) return Uc[k * n + j];
-        return j < n ? Yb[k * n + j] : Ya[k * n + (j - n)];
-    };
     float acc[8][8];
 #pragma unroll
     for (int p = 0; p < 8; ++p)
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[p][q] = 0.f;
-    float mreg[16], rreg[8];   // next step: 2048 M and 1024 R values over 128 threads
+    // next step's tiles: this thread loads M row i0 + t (16 contraction rows) and the R
+    // values (j0 + t % 16, k0 + t / 16 + 8 e) -- one row pointer each, no per-element branches
+    // beyond the bounds
+    float mreg[16], rreg[8];
+    const int64_t irow = i0 + t;
+    const bool irow_ok = irow < Mrows;
+    const float *mbase = grad_mode ? A + irow : (irow < n ? A + irow : B + (irow - n));
+    const int64_t kq = k0 + t / 16;
+    const int jr0 = t % 16;
     auto fetch = [&](int64_t j0) {
 #pragma unroll
         for (int e16 = 0; e16 < 16; ++e16) {
-            const int e = t + 128 * e16;
-            mreg[e16] = mval(i0 + e % kFM, j0 + e / kFM);
+            const int64_t j = j0 + e16;
+            float v = 0.f;
+            if (irow_ok && j < je)
+                v = (grad_mode && j >= n) ? B[(j - n) * n + irow] : mbase[j * n];
+            mreg[e16] = v;
         }
+        const int64_t j = j0 + jr0;
 #pragma unroll
         for (int e8 = 0; e8 < 8; ++e8) {
-            const int e = t + 128 * e8;
-            rreg[e8] = rval(j0 + e % kBK, k0 + e / kBK);
+            const int64_t k = kq + 8 * e8;
+            float v = 0.f;
+            if (k < K && j < je)
+                v = !grad_mode ? Uc[k * n + j] : (j < n ? Yb[k * n + j] : Ya[k * n + (j - n)]);
+            rreg[e8] = v;
         }
     };
     fetch(js);

@@ -595,11 +595,11 @@ __global__ void __launch_bounds__(256) wy_rowgemm_kernel(
 }
 
 // The symmetric program's folded block (b <= 64) in one launch instead of five rowgemms
-// (DESIGN.md §4): a CTA owns 64 rows r and computes, from T and P = W^T Lambda W,
-//   M = P T^T (redundantly per CTA: b^3 FMAs),  V = W T,  V' = W T^T   (its 64 rows),
+// (DESIGN.md §4): a CTA owns kSymRows rows r and computes, from T and P = W^T Lambda W,
+//   M = P T^T (redundantly per CTA: b^3 FMAs),  V = W T,  V' = W T^T   (its rows),
 //   A1 = Lambda V' - V M,  A2 = V,
 // and writes A = [A1, A2] as bf16 hi/lo rows (As[r][0:b) = A1, As[r][b:2b) = A2).
-constexpr int kSymRows = 64;
+constexpr int kSymRows = 16;   // rows per CTA: 128 CTAs at n = 2048 (64-row CTAs: 32 CTAs, 22.8 us under ncu)
 size_t symrows_smem(int b) {
     return static_cast<size_t>(4) * (2 * b * (b + 1) + b * kSymRows + 2 * kSymRows * (b + 1));
 }
@@ -615,9 +615,9 @@ __global__ void __launch_bounds__(256) wy_sym_rows_kernel(const float *__restric
     const int ldb = b + 1;
     float *Ts = ssm;                       // b x (b + 1): T
     float *Ms = Ts + b * ldb;              // b x (b + 1): P, then M = P T^T
-    float *Ws = Ms + b * ldb;              // b x 64: W[l][rr]
-    float *Vs = Ws + b * kSymRows;         // 64 x (b + 1): V = W T
-    float *Vp = Vs + kSymRows * ldb;       // 64 x (b + 1): V' = W T^T
+    float *Ws = Ms + b * ldb;              // b x kSymRows: W[l][rr]
+    float *Vs = Ws + b * kSymRows;         // kSymRows x (b + 1): V = W T
+    float *Vp = Vs + kSymRows * ldb;       // kSymRows x (b + 1): V' = W T^T
     const int t = threadIdx.x;
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kSymRows;
     for (int e = t; e < b * b; e += 256) {

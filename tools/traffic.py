@@ -69,7 +69,10 @@ def parse():
                   "source": f"ncu --metrics {METRICS} --clock-control none, bench.py --workload {w} "
                             f"--steps 2 --warmup 3 --ncu ({STEPS} steps), {os.path.basename(path)}"}
     dst = os.path.join(ROOT, "profiles", "r2", "traffic_r2.json")
-    json.dump(out, open(dst, "w"), indent=1, sort_keys=True)
+    # merge: workloads not re-captured keep their earlier entries
+    merged = json.load(open(dst)) if os.path.exists(dst) else {}
+    merged.update(out)
+    json.dump(merged, open(dst, "w"), indent=1, sort_keys=True)
     for w, d in out.items():
         print(f"{w:10s} {d['dram_bytes_per_step'] / 1e9:7.3f} GB/step  top {d['dominant_kernel']} "
               f"{d['kernels'][d['dominant_kernel']]['ncu_time_share']:.2f}")
