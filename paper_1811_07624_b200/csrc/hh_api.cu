@@ -233,6 +233,7 @@ int hh_debug_mahal_fork(int on) {
 }
 int hh_debug_wy_pdl(int on) { return wy_set_pdl(on); }
 int hh_debug_wy_symfuse(int on) { return wy_set_symfuse(on); }
+int hh_debug_wy_tsa(int on) { return wy_set_tsa(on); }
 
 // Test hook (not part of hh.h): runs the compact-WY preparation and the first
 // projection only, leaving G (bf16 hi/lo rows) and V in the workspace at the

@@ -114,6 +114,7 @@ int wy_set_ts_min(int kw);                       // test: TS-mode update thresho
 int wy_set_flow(int on, int project_ctas);
 void wy_set_flow_knobs(const int *k, int cnt);   // [on, P, nkc, rseg, D, G, pol]
 int wy_set_pdl(int on);   // A/B hook: bit 0 PDL launches, bit 1 prep beside the first projection
+int wy_set_tsa(int on);       // A/B hook: K5a converts X into TMEM (b <= 128); previous
 int wy_set_symfuse(int on);   // A/B hook: the symmetric folded block's operands in one launch
 bool wy_supported(int kind, int64_t n, int64_t h, int64_t N);   // incl. the pass cap
 // Y = Q X / Q^T X / Q diag(lam) Q^T X by the compact-WY block program (fp32 in/out).

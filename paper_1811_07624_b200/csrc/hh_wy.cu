@@ -694,6 +694,13 @@ __device__ __forceinline__ float4 ld_cg4(const float *p) {
     return v;
 }
 
+// TSA (b <= 128): the converters write X hi/lo straight into TMEM (tcgen05.st; each thread
+// owns one column of the tile = one TMEM lane and 16 of the k-step's 32 rows, read from a
+// SWIZZLE_128B raw box without bank conflicts) and the MMA takes A from TMEM: the converted X
+// never touches shared memory (its stores and the MMA's A reads were ~40 of the ~92 KB of
+// shared-memory traffic per k-step at b = 64).  TMEM: accumulators at 0 / 256,
+// the three A stages at 128 + 32 s (hi 16 columns, lo 16).
+template <bool TSA>
 __global__ void __launch_bounds__(480, 1)
     wy_project_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                       uint16_t *__restrict__ Gt, int n, int64_t N, int b, int wrow_hi, int wrow_lo,
@@ -816,11 +823,18 @@ __global__ void __launch_bounds__(480, 1)
                 const uint32_t wh = smem_u32(Whi(s)), wl = smem_u32(Wlo(s));
 #pragma unroll
                 for (int kk = 0; kk < 2; ++kk) {
-                    const uint64_t ah = tc::sdesc_sw64(xh + kk * 32), alo = tc::sdesc_sw64(xl + kk * 32);
                     const uint64_t bh = tc::sdesc_sw64(wh + kk * 32), blo = tc::sdesc_sw64(wl + kk * 32);
-                    tc::mma_bf16_w(d, ah, bh, idesc, (ks != klo || kk != 0) ? 1u : 0u);
-                    tc::mma_bf16_w(d, ah, blo, idesc, 1u);
-                    tc::mma_bf16_w(d, alo, bh, idesc, 1u);
+                    if constexpr (TSA) {
+                        const uint32_t ta = tbase + 128u + static_cast<uint32_t>(s * 32 + kk * 8);
+                        tc::mma_bf16_ts_w(d, ta, bh, idesc, (ks != klo || kk != 0) ? 1u : 0u);
+                        tc::mma_bf16_ts_w(d, ta, blo, idesc, 1u);
+                        tc::mma_bf16_ts_w(d, ta + 16u, bh, idesc, 1u);
+                    } else {
+                        const uint64_t ah = tc::sdesc_sw64(xh + kk * 32), alo = tc::sdesc_sw64(xl + kk * 32);
+                        tc::mma_bf16_w(d, ah, bh, idesc, (ks != klo || kk != 0) ? 1u : 0u);
+                        tc::mma_bf16_w(d, ah, blo, idesc, 1u);
+                        tc::mma_bf16_w(d, alo, bh, idesc, 1u);
+                    }
                 }
                 tc::mma_commit_w(&bars->cempty[s]);
                 if (++s == kStages1) {
@@ -835,6 +849,58 @@ __global__ void __launch_bounds__(480, 1)
             }
         });
         __syncwarp();
+    } else if (TSA && warp < 11) {
+        // converters (TSA): warp w owns TMEM lane quarter w % 4 (tile columns 32 (w % 4) + lane)
+        // and rows 16 hf .. 16 hf + 15 of each k-step (hf = 0 for warps 3-6, 1 for 7-10)
+        const int q = warp & 3, hf = (warp - 3) >> 2;
+        const int col = q * 32 + lane;
+        const uint32_t tl = tbase + (static_cast<uint32_t>(q * 32) << 16);
+        int rs = 0, cs = 0;
+        uint32_t rph = 0, cph = 0;
+        for_segments([&](int, int klo, int khi, bool, bool) {
+            for (int ks = klo; ks < khi; ++ks) {
+                mbar_wait(&bars->rfull[rs], rph);
+                // SWIZZLE_128B raw box: column col's 16-B chunk j at col * 128 + ((j ^ (col & 7)) << 4)
+                const uint32_t raw = smem_u32(rawX(rs)) + static_cast<uint32_t>(col) * 128u;
+                float v[16];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const uint32_t j = static_cast<uint32_t>(4 * hf + jj);
+                    const float4 f = tc::lds128(raw + ((j ^ static_cast<uint32_t>(col & 7)) << 4));
+                    v[4 * jj] = f.x;
+                    v[4 * jj + 1] = f.y;
+                    v[4 * jj + 2] = f.z;
+                    v[4 * jj + 3] = f.w;
+                }
+                if (dscale) {   // NEXT-f1 right factor: project D X (rows uniform over the warp)
+                    const int r0 = ks * 32 + 16 * hf;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (r0 + e < n) v[e] *= __ldg(dscale + r0 + e);
+                }
+                fence_proxy_async_smem();
+                tc::mbar_arrive(&bars->rempty[rs]);
+                uint32_t H[8], L[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
+                mbar_wait(&bars->cempty[cs], cph ^ 1u);
+                tc::fence_after_sync();
+                const uint32_t ta = tl + 128u + static_cast<uint32_t>(cs * 32 + hf * 8);
+                tc::tmem_st8(ta, make_uint4(H[0], H[1], H[2], H[3]), make_uint4(H[4], H[5], H[6], H[7]));
+                tc::tmem_st8(ta + 16u, make_uint4(L[0], L[1], L[2], L[3]), make_uint4(L[4], L[5], L[6], L[7]));
+                tc::tmem_wait_st();
+                tc::fence_before_sync();
+                tc::mbar_arrive(&bars->cfull[cs]);
+                if (++rs == nraw) {
+                    rs = 0;
+                    rph ^= 1u;
+                }
+                if (++cs == kStages1) {
+                    cs = 0;
+                    cph ^= 1u;
+                }
+            }
+        });
     } else if (warp < 11) {
         // converters: 256 threads, 4 float4 each per k-step
         const int ct = threadIdx.x - 96;
@@ -1644,6 +1710,8 @@ cudaError_t g_attr_err[kMaxDevWy];
 // debug / test hooks, per calling thread (like hh_set_algo): no process-global mutable state
 thread_local unsigned long long *t_timeline = nullptr;   // hh_debug_wy_timeline
 thread_local int t_ts_min = 256;                         // hh_debug_wy_ts_min
+thread_local int t_tsa = 1;   // hh_debug_wy_tsa: K5a converts X into TMEM (b <= 128); same-box A/B
+                              // (tools/wy_tsa_ab.py): bit-identical, C3 -2 % min / -6 % median, C5 h=64 -1 / -2 %
 thread_local int t_symfuse = 3;   // hh_debug_wy_symfuse: bit 0 the folded block's operands in one
                                   // launch, bit 1 S and P in one Gram + one reduction launch
 // K5f knobs (hh_debug_wy_flow*): on/off, project CTAs, K chunks per tile, row chunks per
@@ -1805,6 +1873,12 @@ cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem,
 }
 }  // namespace
 
+int wy_set_tsa(int on) {
+    const int prev = t_tsa;
+    t_tsa = on;
+    return prev;
+}
+
 int wy_set_symfuse(int on) {
     const int prev = t_symfuse;
     t_symfuse = on;
@@ -1827,7 +1901,10 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevWy) return cudaErrorInvalidDevice;
     std::call_once(g_attr_once[dev], [dev]() {
         cudaError_t &err = g_attr_err[dev];
-        err = cudaFuncSetAttribute(wy_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        err = cudaFuncSetAttribute(wy_project_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemMax);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(wy_project_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kSmemMax);
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(wy_sym_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2170,8 +2247,12 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
     const float *cur = X;
     for (int q = 0; q < np; ++q) {
         const Pass &ps = prog[q];
-        const CUtensorMap &mcur = (cur == X) ? mX : mY;
-        ++nlaunch, note(pdl_launch(wy_project_kernel, q == 0 ? grid_first : grid_all, 480, smem1(ps.kw), stream,
+        // K5a with X converted into TMEM (b <= 128) reads the raw tiles through the
+        // SWIZZLE_128B map of the same box; the shared-memory form otherwise
+        const bool tsa = ps.kw <= 128 && t_tsa;
+        const CUtensorMap &mcur = tsa ? ((cur == X) ? mXb2 : mYb2) : ((cur == X) ? mX : mY);
+        auto k5a = tsa ? wy_project_kernel<true> : wy_project_kernel<false>;
+        ++nlaunch, note(pdl_launch(k5a, q == 0 ? grid_first : grid_all, 480, smem1(ps.kw), stream,
             mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
             ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw), F(p.off_part),
             reinterpret_cast<int *>(w + p.off_flag)));

@@ -101,6 +101,8 @@ def lib() -> ctypes.CDLL:
             L.hh_debug_wy_pdl.restype = i32
             L.hh_debug_wy_symfuse.argtypes = [i32]
             L.hh_debug_wy_symfuse.restype = i32
+            L.hh_debug_wy_tsa.argtypes = [i32]
+            L.hh_debug_wy_tsa.restype = i32
         if hasattr(L, "hh_debug_wy_timeline"):
             L.hh_debug_wy_timeline.argtypes = [p]
             L.hh_debug_wy_timeline.restype = i32

@@ -244,3 +244,27 @@ def test_wy_flow_parity(flow_on, call, n, h, N, op):
         ref = oracle.apply(op, c.U, c.X)
     assert "flow" in hh.last_launch_info()["variant"], hh.last_launch_info()
     assert_parity(got, ref, "f32", h, f"K5f {call} n{n} h{h} N{N} op{op}")
+
+
+@pytest.mark.parametrize("tsa", [0, 1])
+@pytest.mark.parametrize("n,h,N", [(1024, 64, 40000), (1000, 40, 3001), (2048, 33, 20000), (512, 128, 9000)])
+def test_wy_project_tmem_a_bit_identical(tsa, n, h, N):
+    """K5a with X converted into TMEM (the default for blocks of <= 128) and the shared-memory
+    form (hh_debug_wy_tsa 0) give bit-identical results: same bf16 splits, same MMA order --
+    both ops, the symmetric program and a right D factor; and both match the oracle."""
+    c = gi.make_case("sym", n, h, N, "f32", seed=3)
+    d = gi.sign_diag(gi.rng(3, n), n, "f32")
+    L = hh.hh.lib()
+    outs = {}
+    for on in (1 - tsa, tsa):
+        prev = L.hh_debug_wy_tsa(on)
+        try:
+            with hh.algo(hh.HH_ALGO_WY):
+                outs[on] = [hh.hh_apply(op, dev(c.U), dev(c.X)) for op in (0, 1)] + [
+                    hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)),
+                    hh.hh_apply_signed(0, 1, dev(c.U), dev(d), dev(c.X))]
+        finally:
+            L.hh_debug_wy_tsa(prev)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    assert_parity(outs[tsa][2].cpu().numpy(), oracle.sym_apply(c.U, c.lam, c.X), "f32", 2 * h, "sym")
