@@ -711,14 +711,14 @@ __global__ void __launch_bounds__(480, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     // ring sizes depend on b: a conversion stage holds X hi/lo (16 KB) and the W hi/lo
     // tiles (128 b bytes); the rest of the 227 KB is a deep raw-X ring (nraw stages)
-    const int cvb = 16384 + 128 * b;
+    const int cvb = (TSA ? 0 : 16384) + 128 * b;   // (TSA: X hi/lo live in TMEM, W only)
     unsigned char *conv = smem + nraw * kRawBytes;
     Bars1 *bars = reinterpret_cast<Bars1 *>(conv + kStages1 * cvb);
     auto rawX = [&](int s) { return smem + s * kRawBytes; };
     auto Xhi = [&](int s) { return conv + s * cvb; };
     auto Xlo = [&](int s) { return conv + s * cvb + 8192; };
-    auto Whi = [&](int s) { return conv + s * cvb + 16384; };
-    auto Wlo = [&](int s) { return conv + s * cvb + 16384 + 64 * b; };
+    auto Whi = [&](int s) { return conv + s * cvb + (TSA ? 0 : 16384); };
+    auto Wlo = [&](int s) { return conv + s * cvb + (TSA ? 0 : 16384) + 64 * b; };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (n + 31) / 32;
@@ -1681,14 +1681,14 @@ size_t tbuild_smem(int b) {
            4;
 }
 
-int nraw_for(int b) {
-    const int cvb = 16384 + 128 * b;
+int nraw_for(int b, bool tsa = false) {
+    const int cvb = (tsa ? 0 : 16384) + 128 * b;
     const int r = (kSmemMax - 1024 - static_cast<int>(sizeof(Bars1)) - kStages1 * cvb) / kRawBytes;
     return std::max(2, std::min(kRaw1, r));
 }
-size_t smem1(int b) {
-    return static_cast<size_t>(nraw_for(b)) * kRawBytes +
-           static_cast<size_t>(kStages1) * (16384 + 128 * b) + sizeof(Bars1) + 1024;
+size_t smem1(int b, bool tsa = false) {
+    return static_cast<size_t>(nraw_for(b, tsa)) * kRawBytes +
+           static_cast<size_t>(kStages1) * ((tsa ? 0 : 16384) + 128 * b) + sizeof(Bars1) + 1024;
 }
 int nxs_for(int kv) {
     const int g = (kv / 32) * 16384;
@@ -2252,9 +2252,9 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         const bool tsa = ps.kw <= 128 && t_tsa;
         const CUtensorMap &mcur = tsa ? ((cur == X) ? mXb2 : mYb2) : ((cur == X) ? mX : mY);
         auto k5a = tsa ? wy_project_kernel<true> : wy_project_kernel<false>;
-        ++nlaunch, note(pdl_launch(k5a, q == 0 ? grid_first : grid_all, 480, smem1(ps.kw), stream,
+        ++nlaunch, note(pdl_launch(k5a, q == 0 ? grid_first : grid_all, 480, smem1(ps.kw, tsa), stream,
             mcur, *ps.mW, Gt, static_cast<int>(p.n), N, ps.kw, ps.wrow, static_cast<int>(R) + ps.wrow,
-            ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw), F(p.off_part),
+            ntiles, ps.dscale, ps.row0 / 32, nraw_for(ps.kw, tsa), F(p.off_part),
             reinterpret_cast<int *>(w + p.off_flag)));
         if (q == 0 && overlap) prep_rest(0);
         if (debug_stop_blocks >= 0) break;   // test hook: stop after the first projection
