@@ -89,3 +89,59 @@ def test_concurrent_streams_tensor_paths():
     for y, (i, d) in outs:
         assert torch.equal(y, ref_apply)
         assert torch.equal(i, ref_idx) and torch.equal(d, ref_d)
+
+
+def k1w_shapes(seed, count):
+    g = gi.rng(810, seed)
+    out = []
+    for _ in range(count):
+        n = int(g.integers(257, 1025)) * 4        # (1024, 4096]: multi-warp column groups
+        h = int(g.integers(1, 17))                 # the reflectors fit the TMEM columns
+        N = int(g.integers(1, 900))
+        out.append((n, h, N))
+    return out
+
+
+@pytest.mark.parametrize("n,h,N", k1w_shapes(1, 10))
+def test_fuzz_k1_tmem_blocked(n, h, N):
+    """K1t in blocks of four reflectors (K1w, forced) on random multi-warp shapes: both ops and
+    the symmetric form, ragged h (blocks shorter than four) and N."""
+    L = hh.hh.lib()
+    prev = (L.hh_debug_k1_stream(0), L.hh_debug_k1_tmem(1), L.hh_debug_k1_blocked(1))
+    try:
+        c = gi.make_case("sym", n, h, N, "f32", seed=n + h)
+        for op in (0, 1):
+            with hh.algo(hh.HH_ALGO_FUSED):
+                got = hh.hh_apply(op, dev(c.U), dev(c.X)).cpu().numpy()
+                assert hh.last_launch_info()["variant"].endswith("_kb4")
+            assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"fuzz K1w n{n} h{h} N{N} op{op}")
+        with hh.algo(hh.HH_ALGO_FUSED):
+            got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+        assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", 2 * h, f"fuzz K1w sym n{n} h{h}")
+    finally:
+        L.hh_debug_k1_blocked(prev[2])
+        L.hh_debug_k1_tmem(prev[1])
+        L.hh_debug_k1_stream(prev[0])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_shf_cost(seed):
+    """The SHF objective and its gradient (K8) on random shapes and both dtypes against the
+    oracle, per candidate (reading R21)."""
+    g = gi.rng(820, seed)
+    n, K = int(g.integers(1, 700)), int(g.integers(1, 150))
+    for dt, tol in ((np.float32, 1e-6), (np.float64, 1e-13)):
+        A = g.standard_normal((n, n))
+        B = g.standard_normal((n, n))
+        A, B = ((A + A.T) / 2).astype(dt), ((B + B.T) / 2).astype(dt)
+        U = g.standard_normal((K, n)).astype(dt)
+        cost, grad = hh.hh_shf_cost(dev(A), dev(B), dev(U))
+        c_ref, g_ref = oracle.shf_cost(A, B, U)
+        A64, B64, U64 = (x.astype(np.float64) for x in (A, B, U))
+        a, b = U64 @ A64, U64 @ B64
+        al, be = np.sum(U64 * a, 1), np.sum(U64 * b, 1)
+        na, nb = np.linalg.norm(a, axis=1), np.linalg.norm(b, axis=1)
+        t = tol * np.sqrt(n)
+        assert np.all(np.abs(cost.cpu().numpy() - c_ref) <= t * (2 * na * nb + 2 * np.abs(al * be)))
+        sg = 2 * (np.linalg.norm(A64) * nb + np.linalg.norm(B64) * na) + 4 * (np.abs(al) * nb + np.abs(be) * na)
+        assert np.all(np.linalg.norm(grad.cpu().numpy() - g_ref, axis=1) <= t * sg)
