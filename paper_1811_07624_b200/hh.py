@@ -93,16 +93,20 @@ def lib() -> ctypes.CDLL:
             L.hh_debug_k1_prefetch.restype = i32
             L.hh_debug_k1_tmem.argtypes = [i32]
             L.hh_debug_k1_tmem.restype = i32
-            L.hh_debug_k1_blocked.argtypes = [i32]
-            L.hh_debug_k1_blocked.restype = i32
-            L.hh_debug_mahal_fork.argtypes = [i32]
-            L.hh_debug_mahal_fork.restype = i32
+            if hasattr(L, "hh_debug_k1_blocked"):
+                L.hh_debug_k1_blocked.argtypes = [i32]
+                L.hh_debug_k1_blocked.restype = i32
+            if hasattr(L, "hh_debug_mahal_fork"):
+                L.hh_debug_mahal_fork.argtypes = [i32]
+                L.hh_debug_mahal_fork.restype = i32
             L.hh_debug_wy_pdl.argtypes = [i32]
             L.hh_debug_wy_pdl.restype = i32
-            L.hh_debug_wy_symfuse.argtypes = [i32]
-            L.hh_debug_wy_symfuse.restype = i32
-            L.hh_debug_wy_tsa.argtypes = [i32]
-            L.hh_debug_wy_tsa.restype = i32
+            if hasattr(L, "hh_debug_wy_symfuse"):
+                L.hh_debug_wy_symfuse.argtypes = [i32]
+                L.hh_debug_wy_symfuse.restype = i32
+            if hasattr(L, "hh_debug_wy_tsa"):
+                L.hh_debug_wy_tsa.argtypes = [i32]
+                L.hh_debug_wy_tsa.restype = i32
         if hasattr(L, "hh_debug_wy_timeline"):
             L.hh_debug_wy_timeline.argtypes = [p]
             L.hh_debug_wy_timeline.restype = i32
