@@ -768,6 +768,10 @@ __global__ void __launch_bounds__(480, 1)
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tbase = bars->tmem;
+    // TSA: blocks of b <= 128 keep two accumulators (0, 256) and put the A stages at 128; a
+    // 256-wide block has one accumulator (0..255) and the A stages at 256
+    const int nacc = (TSA && b > 128) ? 1 : 2;
+    const uint32_t abase = (TSA && b > 128) ? 256u : 128u;
     pdl_wait();   // the previous kernel's results (after this CTA's setup)
     pdl_trigger();
 
@@ -825,7 +829,7 @@ __global__ void __launch_bounds__(480, 1)
                 for (int kk = 0; kk < 2; ++kk) {
                     const uint64_t bh = tc::sdesc_sw64(wh + kk * 32), blo = tc::sdesc_sw64(wl + kk * 32);
                     if constexpr (TSA) {
-                        const uint32_t ta = tbase + 128u + static_cast<uint32_t>(s * 32 + kk * 8);
+                        const uint32_t ta = tbase + abase + static_cast<uint32_t>(s * 32 + kk * 8);
                         tc::mma_bf16_ts_w(d, ta, bh, idesc, (ks != klo || kk != 0) ? 1u : 0u);
                         tc::mma_bf16_ts_w(d, ta, blo, idesc, 1u);
                         tc::mma_bf16_ts_w(d, ta + 16u, bh, idesc, 1u);
@@ -843,7 +847,7 @@ __global__ void __launch_bounds__(480, 1)
                 }
             }
             tc::mma_commit_w(&bars->acc_full[a]);
-            if (++a == 2) {
+            if (++a == nacc) {
                 a = 0;
                 aph ^= 1u;
             }
@@ -885,7 +889,7 @@ __global__ void __launch_bounds__(480, 1)
                 for (int e = 0; e < 8; ++e) tc::split2(v[2 * e], v[2 * e + 1], H[e], L[e]);
                 mbar_wait(&bars->cempty[cs], cph ^ 1u);
                 tc::fence_after_sync();
-                const uint32_t ta = tl + 128u + static_cast<uint32_t>(cs * 32 + hf * 8);
+                const uint32_t ta = tl + abase + static_cast<uint32_t>(cs * 32 + hf * 8);
                 tc::tmem_st8(ta, make_uint4(H[0], H[1], H[2], H[3]), make_uint4(H[4], H[5], H[6], H[7]));
                 tc::tmem_st8(ta + 16u, make_uint4(L[0], L[1], L[2], L[3]), make_uint4(L[4], L[5], L[6], L[7]));
                 tc::tmem_wait_st();
@@ -1044,7 +1048,7 @@ __global__ void __launch_bounds__(480, 1)
             }
             tc::fence_before_sync();
             tc::mbar_arrive(&bars->acc_empty[a]);
-            if (++a == 2) {
+            if (++a == nacc) {
                 a = 0;
                 aph ^= 1u;
             }
@@ -2249,7 +2253,7 @@ cudaError_t launch_wy(const WyPlan &p, const float *U, const float *lam, const f
         const Pass &ps = prog[q];
         // K5a with X converted into TMEM (b <= 128) reads the raw tiles through the
         // SWIZZLE_128B map of the same box; the shared-memory form otherwise
-        const bool tsa = ps.kw <= 128 && t_tsa;
+        const bool tsa = (ps.kw <= 128 && (t_tsa & 1)) || (ps.kw == 256 && (t_tsa & 2));
         const CUtensorMap &mcur = tsa ? ((cur == X) ? mXb2 : mYb2) : ((cur == X) ? mX : mY);
         auto k5a = tsa ? wy_project_kernel<true> : wy_project_kernel<false>;
         ++nlaunch, note(pdl_launch(k5a, q == 0 ? grid_first : grid_all, 480, smem1(ps.kw, tsa), stream,
