@@ -391,3 +391,24 @@ def test_k1t_policy():
             L.hh_debug_k1_stream(prev)
         assert ("_tmem" in v) == want, (n, h, v)
         assert v.endswith("_kb4") == blk, (n, h, v)
+
+
+def test_mahalanobis_sort_beside_transform_matches_serial():
+    """hh_mahalanobis runs the pair sort on a second stream beside the transform (fork / join);
+    with the overlap off (hh_debug_mahal_fork 0) the result is bit-identical, and both match
+    the oracle.  Called twice per mode: the cached side stream is reused."""
+    m = gi.make_case("mahalanobis", 256, 7, 3000, "f32", seed=91, npairs=20000)
+    args = [dev(a) for a in (m.U, m.d, m.X, m.ia, m.ib)]
+    L = hh.hh.lib()
+    outs = {}
+    for f in (1, 0):
+        prev = L.hh_debug_mahal_fork(f)
+        try:
+            outs[f] = [hh.hh_mahalanobis(*args) for _ in range(2)]
+        finally:
+            L.hh_debug_mahal_fork(prev)
+    torch.cuda.synchronize()
+    for a in outs[1] + outs[0][1:]:
+        assert torch.equal(a, outs[0][0])
+    assert_parity(outs[1][0].cpu().numpy(), oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib), "f32", 7,
+                  "mahalanobis fork")
