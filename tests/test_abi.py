@@ -64,7 +64,8 @@ def test_workspace_query():
 
 @pytest.mark.parametrize("n,h,N,wy", [
     (1024, 10, 262144, False),                      # C2
-    (4096, 12, 65536, False), (4096, 13, 65536, True),   # C5 h=12 stays on K1
+    (4096, 12, 65536, False), (4096, 16, 65536, False), (4096, 17, 65536, True),   # K1w to h = 16
+    (2048, 18, 16384, False), (2048, 19, 16384, True),   # n = 2048, E = 2^25 band (r2 re-sweep)
     (2048, 16, 65536, False), (2048, 17, 65536, True),   # E = 2^27: large band
     (2048, 28, 131072, True),                       # the old n>=512, h>=32 rule kept K1 here
     (1024, 25, 32768, False), (1024, 26, 32768, True),   # E = 2^25: middle band
@@ -144,6 +145,9 @@ def test_product_does_not_touch_oracle():
 
 @pytest.mark.parametrize("n,h,N,wy", [
     (2048, 32, 131072, True),                       # C3
+    (2048, 11, 131072, False), (2048, 12, 131072, True),  # r2 re-sweep after K1w
+    (4096, 9, 65536, False), (4096, 10, 65536, True),
+    (4096, 11, 16384, False), (4096, 12, 16384, True),
     (1024, 10, 262144, False), (1024, 11, 262144, True),  # E = 2^28
     (1024, 18, 32768, False), (1024, 19, 32768, True),    # E = 2^25
     (2048, 31, 2048, False), (2048, 32, 2048, True),      # small problems
