@@ -96,8 +96,6 @@ __global__ void __launch_bounds__(NT) hh_stream_kernel(const FusedArgs a) {
         }
     }
     // one reflector (Eq. 2): alpha = u^T x (FFMA2 partial sums, xor butterfly over the group),
-    // x <- x - 2 alpha u
-    // one reflector (Eq. 2): alpha = u^T x (FFMA2 partial sums, xor butterfly over the group),
     // x <- x - 2 alpha u.  (Loading u_{i+1} during reflector i was measured 1.5x slower at
     // n = 1024: the extra registers cost a quarter of the resident warps.)
     auto reflect = [&](int i) {
@@ -268,6 +266,11 @@ bool stream_preferred(const FusedArgs &a) {
     const int64_t ub = a.h * a.n * 4;
     if (ub > (int64_t(128) << 10)) return false;
     if (a.n > 512 && a.h >= 9 && a.h <= 11) return false;
+    // n in (512, 1024], h in [12, 16]: K1 with the reflectors in TMEM (K1t) is ahead -- same box
+    // (tools/k1t_ab.py, profiles/r2/k1t_vs_k1s_r2.txt): n = 1024, h = 12 / 14 / 16: 341 / 402 /
+    // 435 us vs 455 / 533 / 566; n = 768, h = 16: 660 vs 689-709; symmetric n = 1024, h = 12:
+    // 620 vs 793
+    if (a.n > 512 && a.h >= 12 && a.h <= 16) return false;
     return true;
 }
 

@@ -412,3 +412,20 @@ def test_mahalanobis_sort_beside_transform_matches_serial():
         assert torch.equal(a, outs[0][0])
     assert_parity(outs[1][0].cpu().numpy(), oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib), "f32", 7,
                   "mahalanobis fork")
+
+
+def test_fused_path_policy_defaults():
+    """HH_ALGO_FUSED's default kernel per shape (all from same-box A/Bs): K1s for n <= 512 and
+    for n <= 1024 outside h = 9..16, the staged K1 at n = 1024, h = 10 (C2), K1t at n = 1024,
+    h = 12..16 (profiles/r2/k1t_vs_k1s_r2.txt), K1w for multi-warp groups from h = 12."""
+    g = torch.Generator().manual_seed(4)
+    for n, h, want in ((512, 12, "f32s_"), (1024, 8, "f32s_"), (1024, 10, "f32_tpc32_ch8_c2"),
+                       (1024, 12, "f32_tpc32_ch8_c2_tmem"), (1024, 16, "f32_tpc32_ch8_c2_tmem"),
+                       (1024, 20, "f32s_"), (4096, 12, "f32_tpc128_ch8_c2_tmem_kb4")):
+        U = torch.randn(h, n, generator=g, dtype=torch.float64)
+        U = (U / U.norm(dim=1, keepdim=True)).float().cuda()
+        X = torch.randn(300, n, generator=g).cuda()
+        with hh.algo(hh.HH_ALGO_FUSED):
+            hh.hh_apply(0, U, X)
+        v = hh.last_launch_info()["variant"]
+        assert v == want or (want == "f32s_" and v.startswith(want)), (n, h, v)
