@@ -38,8 +38,10 @@ int64_t wy_min_h(int64_t n, int64_t N) {
     // (n in (1024, 4096]: re-swept after K1t / K1w and the TMEM-A K5a, profiles/r2/xover_r2b.txt --
     // K1w stays ahead through h = 16, the most its TMEM holds: n = 4096 13 -> 17, n = 2048 mid
     // band 22 -> 19)
-    static const int big[7] = {24, 20, 18, 19, 17, 17, 7};    // E >= 2^27
-    static const int mid[7] = {28, 25, 23, 26, 19, 17, 16};   // 2^25 <= E < 2^27
+    // (n in (512, 1024] likewise after K1t took h = 12..16 from K1s, profiles/r2/xover_r2c.txt:
+    // 19 -> 17, middle band 26 -> 20)
+    static const int big[7] = {24, 20, 18, 17, 17, 17, 7};    // E >= 2^27
+    static const int mid[7] = {28, 25, 23, 20, 19, 17, 16};   // 2^25 <= E < 2^27
     const int64_t E = n * N;
     if (E >= (int64_t(1) << 27)) return big[i];
     if (E >= (int64_t(1) << 25)) return mid[i];
@@ -63,7 +65,7 @@ int64_t wy_min_h_sym(int64_t n, int64_t N) {
     // (n in (1024, 4096] re-swept in round 2, profiles/r2/xover_r2b.txt: 10 -> 12 and 8 -> 10 for
     // E >= 2^27, 15 -> 12 for n = 4096 in the middle band)
     static const int big[6] = {16, 13, 10, 11, 12, 10};      // E >= 2^27
-    static const int mid[6] = {24, 19, 18, 19, 18, 12};      // 2^25 <= E < 2^27
+    static const int mid[6] = {24, 19, 18, 15, 18, 12};      // 2^25 <= E < 2^27 (n <= 1024: 19 -> 15)
     const int64_t E = n * N;
     if (E >= (int64_t(1) << 27)) return big[i];
     if (E >= (int64_t(1) << 25)) return mid[i];

@@ -68,7 +68,8 @@ def test_workspace_query():
     (2048, 18, 16384, False), (2048, 19, 16384, True),   # n = 2048, E = 2^25 band (r2 re-sweep)
     (2048, 16, 65536, False), (2048, 17, 65536, True),   # E = 2^27: large band
     (2048, 28, 131072, True),                       # the old n>=512, h>=32 rule kept K1 here
-    (1024, 25, 32768, False), (1024, 26, 32768, True),   # E = 2^25: middle band
+    (1024, 19, 32768, False), (1024, 20, 32768, True),   # E = 2^25: middle band (r2 re-sweep)
+    (1024, 16, 262144, False), (1024, 17, 262144, True),  # K1t to h = 16, then K5 (r2)
     (1024, 31, 4096, False), (1024, 32, 4096, True),     # small problems: h >= 32
     (128, 23, 1 << 21, False), (128, 24, 1 << 21, True),   # n <= 512: against K1s (r2)
     (256, 19, 1 << 20, False), (256, 20, 1 << 20, True),
@@ -149,7 +150,7 @@ def test_product_does_not_touch_oracle():
     (4096, 9, 65536, False), (4096, 10, 65536, True),
     (4096, 11, 16384, False), (4096, 12, 16384, True),
     (1024, 10, 262144, False), (1024, 11, 262144, True),  # E = 2^28
-    (1024, 18, 32768, False), (1024, 19, 32768, True),    # E = 2^25
+    (1024, 14, 32768, False), (1024, 15, 32768, True),    # E = 2^25 (r2 re-sweep)
     (2048, 31, 2048, False), (2048, 32, 2048, True),      # small problems
     (128, 15, 1 << 21, False), (128, 16, 1 << 21, True),  # n <= 512: against K1s (r2)
     (256, 12, 1 << 20, False), (256, 13, 1 << 20, True),
