@@ -67,9 +67,12 @@ __device__ __forceinline__ void fadd2_rows(float &d0, float &d1, float b0, float
         : "f"(b0), "f"(b1));
 }
 
-template <int CH>
+// RW rows per warp pass (2 or 4): the rows' elements packed in pairs, so every FMA of the dot
+// and the update is one FFMA2 for two rows (u_k broadcast) and each u load serves RW rows.
+template <int CH, int RW = 2>
 __global__ void __launch_bounds__(256) row_apply_kernel(const float *__restrict__ A, float *__restrict__ B,
                                                         const float *__restrict__ U, int n, int h, int op) {
+    static_assert(RW == 2 || RW == 4, "rows per warp pass");
     extern __shared__ float S[];   // 32 rows x (n + 1)
     const int64_t base = static_cast<int64_t>(blockIdx.y) * n * n;
     const int r0 = blockIdx.x * 32;
@@ -81,52 +84,61 @@ __global__ void __launch_bounds__(256) row_apply_kernel(const float *__restrict_
     }
     __syncthreads();
     auto valid = [&](int k) { return lane + 32 * k < n; };
+    constexpr int NP = RW / 2;   // row pairs per pass
 #pragma unroll 1
-    for (int pr = 0; pr < 2; ++pr) {
-        const int i0 = warp * 4 + pr * 2;   // rows i0, i0 + 1 of the slab
-        // the two rows' elements packed as pairs: every FMA of the dot and the update is one
-        // FFMA2 for both rows (u_k broadcast), the butterfly one FADD2 per step
-        float x0[CH], x1[CH];
+    for (int pr = 0; pr < 4 / RW; ++pr) {
+        const int i0 = warp * 4 + pr * RW;   // rows i0 .. i0 + RW - 1 of the slab
+        float xa[NP][CH], xb[NP][CH];        // pair q: rows i0 + 2q, i0 + 2q + 1
 #pragma unroll
-        for (int k = 0; k < CH; ++k) {
-            x0[k] = valid(k) ? S[i0 * ld + lane + 32 * k] : 0.f;
-            x1[k] = valid(k) ? S[(i0 + 1) * ld + lane + 32 * k] : 0.f;
-        }
+        for (int q = 0; q < NP; ++q)
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                xa[q][k] = valid(k) ? S[(i0 + 2 * q) * ld + lane + 32 * k] : 0.f;
+                xb[q][k] = valid(k) ? S[(i0 + 2 * q + 1) * ld + lane + 32 * k] : 0.f;
+            }
         for (int t = 0; t < h; ++t) {
             const int i = op == 0 ? h - 1 - t : t;   // op N: u_h first; op T: u_1 first (R1)
             const float *u = U + static_cast<int64_t>(i) * n + lane;
             float uk[CH];
 #pragma unroll
             for (int k = 0; k < CH; ++k) uk[k] = valid(k) ? __ldg(u + 32 * k) : 0.f;
-            float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f;
+            float p0[NP], p1[NP];
 #pragma unroll
-            for (int k = 0; k < CH; k += 2) {
-                ffma2_rows(pa0, pa1, uk[k], uk[k], x0[k], x1[k]);
-                if (k + 1 < CH) ffma2_rows(pb0, pb1, uk[k + 1], uk[k + 1], x0[k + 1], x1[k + 1]);
+            for (int q = 0; q < NP; ++q) {
+                float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f;
+#pragma unroll
+                for (int k = 0; k < CH; k += 2) {
+                    ffma2_rows(pa0, pa1, uk[k], uk[k], xa[q][k], xb[q][k]);
+                    if (k + 1 < CH) ffma2_rows(pb0, pb1, uk[k + 1], uk[k + 1], xa[q][k + 1], xb[q][k + 1]);
+                }
+                p0[q] = pa0;
+                p1[q] = pa1;
+                fadd2_rows(p0[q], p1[q], pb0, pb1);
             }
-            float p0 = pa0, p1 = pa1;
-            fadd2_rows(p0, p1, pb0, pb1);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
-                const float t0 = __shfl_xor_sync(0xffffffffu, p0, off);
-                const float t1 = __shfl_xor_sync(0xffffffffu, p1, off);
-                fadd2_rows(p0, p1, t0, t1);
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    const float t0 = __shfl_xor_sync(0xffffffffu, p0[q], off);
+                    const float t1 = __shfl_xor_sync(0xffffffffu, p1[q], off);
+                    fadd2_rows(p0[q], p1[q], t0, t1);
+                }
             }
-            const float s0 = -(p0 + p0), s1 = -(p1 + p1);
 #pragma unroll
-            for (int k = 0; k < CH; ++k) ffma2_rows(x0[k], x1[k], s0, s1, uk[k], uk[k]);
-        }
-        float x[2][CH];
+            for (int q = 0; q < NP; ++q) {
+                const float s0 = -(p0[q] + p0[q]), s1 = -(p1[q] + p1[q]);
 #pragma unroll
-        for (int k = 0; k < CH; ++k) {
-            x[0][k] = x0[k];
-            x[1][k] = x1[k];
+                for (int k = 0; k < CH; ++k) ffma2_rows(xa[q][k], xb[q][k], s0, s1, uk[k], uk[k]);
+            }
         }
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int q = 0; q < NP; ++q)
 #pragma unroll
             for (int k = 0; k < CH; ++k)
-                if (valid(k)) S[(i0 + c) * ld + lane + 32 * k] = x[c][k];
+                if (valid(k)) {
+                    S[(i0 + 2 * q) * ld + lane + 32 * k] = xa[q][k];
+                    S[(i0 + 2 * q + 1) * ld + lane + 32 * k] = xb[q][k];
+                }
     }
     __syncthreads();
     for (int e = tid; e < 32 * n; e += 256) {
@@ -136,6 +148,16 @@ __global__ void __launch_bounds__(256) row_apply_kernel(const float *__restrict_
 }
 
 }  // namespace
+
+// hh_debug_k7_rows: rows per warp pass (2, or 4 for n <= 512; -1: policy).  Same box
+// (tools/k7_rows_ab.py, profiles/r2/k7_rows_ab_r2.txt, outputs bit-identical): 4 rows win at
+// n = 128 (39.8 vs 43.9 us), tie at 256, lose at 500 / 512 (75 / 157 vs 67 / 146 us)
+thread_local int t_k7_rw = -1;
+int k7_set_rows(int rw) {
+    const int prev = t_k7_rw;
+    t_k7_rw = (rw == 2 || rw == 4) ? rw : -1;
+    return prev;
+}
 
 bool row_apply_supported(int64_t n, int64_t h, int dtype) {
     return dtype == 0 && n >= 4 && n <= 1024 && n % 4 == 0 && h <= 256;
@@ -154,6 +176,11 @@ cudaError_t launch_row_apply(const void *A, void *B, const void *U, int64_t n, i
                                             static_cast<int>(h), op);
         return cudaGetLastError();
     };
+    if (t_k7_rw == 4 || (t_k7_rw < 0 && n <= 128)) {
+        if (n <= 128) return go(row_apply_kernel<4, 4>);
+        if (n <= 256) return go(row_apply_kernel<8, 4>);
+        if (n <= 512) return go(row_apply_kernel<16, 4>);
+    }
     if (n <= 128) return go(row_apply_kernel<4>);
     if (n <= 256) return go(row_apply_kernel<8>);
     if (n <= 512) return go(row_apply_kernel<16>);

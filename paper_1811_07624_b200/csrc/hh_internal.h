@@ -67,6 +67,7 @@ bool stream_preferred(const FusedArgs &a);   // the measured K1 / K1s policy
 cudaError_t launch_stream(const FusedArgs &a, cudaStream_t stream, LaunchInfo *info);
 int k1_set_prefetch(int dist);
 int k1_set_tmem(int on);      // A/B hook (hh_debug_k1_tmem): -1 policy, 0 never, 1 when eligible; previous
+int k7_set_rows(int rw);      // A/B hook (hh_debug_k7_rows): K7 rows per warp pass; previous
 int k1_set_blocked(int on);   // A/B hook (hh_debug_k1_blocked): K1w -1 policy, 0 never, 1 when K1t runs; previous
 int k1_set_stream(int on);   // A/B hook (hh_debug_k1_stream): -1 auto, 0 K1, 1 K1s; previous
 

@@ -96,6 +96,9 @@ def lib() -> ctypes.CDLL:
             if hasattr(L, "hh_debug_k1_blocked"):
                 L.hh_debug_k1_blocked.argtypes = [i32]
                 L.hh_debug_k1_blocked.restype = i32
+            if hasattr(L, "hh_debug_k7_rows"):
+                L.hh_debug_k7_rows.argtypes = [i32]
+                L.hh_debug_k7_rows.restype = i32
             if hasattr(L, "hh_debug_mahal_fork"):
                 L.hh_debug_mahal_fork.argtypes = [i32]
                 L.hh_debug_mahal_fork.restype = i32
