@@ -618,10 +618,14 @@ def run_hh(args):
             tpeak = float(pk.get("bf16_tflops", 1590.0)) if pk else 1590.0
             Mq = c.lam.shape[0]
             exe = 3 * 2 * ((c.n + 31) // 32 * 32) * c.N * Mq
+            # the distances run as bf16x3 products (three bf16 products per fp32-accurate one):
+            # the peak of that arithmetic is the bf16 peak / 3 (R18, as for K5)
             roof = {"bound": "tensor", "achieved": flops / (ms_step * 1e-3) / 1e12,
-                    "peak": tpeak, "unit": "TFLOP/s",
-                    "frac": flops / (ms_step * 1e-3) / 1e12 / tpeak, "traffic": traffic,
-                    "peak_source": "measured bf16 (MEASURED_PEAKS.json bf16_tflops)",
+                    "peak": tpeak / 3, "unit": "TFLOP/s",
+                    "frac": flops / (ms_step * 1e-3) / 1e12 / (tpeak / 3), "traffic": traffic,
+                    "frac_of_bf16_burst_algorithmic": flops / (ms_step * 1e-3) / 1e12 / tpeak,
+                    "peak_source": "measured bf16 burst (MEASURED_PEAKS.json bf16_tflops) / 3: the "
+                                   "fp32-accurate bf16x3 rate (DESIGN.md R18)",
                     "executed_tflops": exe / (ms_step * 1e-3) / 1e12,
                     "executed_frac": exe / (ms_step * 1e-3) / 1e12 / tpeak,
                     "pairs_per_s": c.N * Mq / (ms_step * 1e-3),
