@@ -32,10 +32,18 @@
  *   All floating-point arrays of one call share `dtype` (HH_F32 = float,
  *   HH_F64 = double).  Index arrays are int32.
  *
- * Alignment / size (v1 vector path; HH_ERR_UNSUPPORTED otherwise)
- *   - every float pointer 16-byte aligned, n * sizeof(dtype) % 16 == 0
- *     (n % 4 == 0 for f32, n % 2 == 0 for f64);
- *   - n <= 8192 (f32) / 4096 (f64).
+ * Alignment / size
+ *   - The fast kernels (fused K1 family, compact-WY tensor-core program) need every
+ *     float pointer 16-byte aligned, n * sizeof(dtype) % 16 == 0 (n % 4 == 0 for f32,
+ *     n % 2 == 0 for f64) and n <= 8192 (f32) / 4096 (f64).
+ *   - hh_apply, hh_apply_signed, hh_apply_qr, hh_sym_apply, hh_sym_apply_signed,
+ *     hh_mahalanobis and hh_apply_host take every other shape too (Eq. 1-2 hold for any
+ *     n): any n >= 1 whose column fits in shared memory (n <= ~57000 f32 / ~28000 f64)
+ *     and pointers aligned to the element run on a scalar-access kernel (K1g; correct,
+ *     not tuned; hh_mahalanobis then uses its per-pair form and ignores the workspace).
+ *   - HH_ERR_UNSUPPORTED: a pointer not aligned to its element, n beyond K1g's capacity,
+ *     HH_ALGO_WY forced on such a shape, or the other calls (hh_knn, hh_congruence) outside
+ *     the fast kernels' alignment / size.
  *
  * Semantics
  *   - Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream); no
@@ -82,7 +90,7 @@ typedef void *hh_stream_t;
 typedef enum {
     HH_OK = 0,
     HH_ERR_INVALID_VALUE = 1, /* bad size, NULL operand, bad op/dtype/call       */
-    HH_ERR_UNSUPPORTED = 2,   /* misaligned pointer, n*size % 16 != 0, n too big  */
+    HH_ERR_UNSUPPORTED = 2,   /* misaligned pointer, n too big, shape a path cannot run */
     HH_ERR_WORKSPACE = 3,     /* workspace_bytes below hh_workspace_bytes()       */
     HH_ERR_CUDA = 4           /* CUDA runtime error at launch / copy              */
 } hh_status;

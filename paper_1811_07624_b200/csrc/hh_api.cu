@@ -49,7 +49,7 @@ int64_t wy_min_h(int64_t n, int64_t N) {
 }
 
 bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
-    if (dtype != HH_F32 || !wy_supported(WY_APPLY_N, n, h, N)) return false;
+    if (dtype != HH_F32 || n > max_n(0) || !wy_supported(WY_APPLY_N, n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
     return h >= wy_min_h(n, N);
@@ -73,7 +73,7 @@ int64_t wy_min_h_sym(int64_t n, int64_t N) {
 }
 
 bool use_wy_sym(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
-    if (dtype != HH_F32 || !wy_supported(WY_SYM, n, h, N)) return false;
+    if (dtype != HH_F32 || n > max_n(0) || !wy_supported(WY_SYM, n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
     return h >= wy_min_h_sym(n, N);
@@ -83,7 +83,7 @@ bool use_wy_sym(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
 // kMaxPasses block passes, ...) is an error, never a silent switch to the SIMT kernel
 bool wy_forced_unsupported(int kind, hh_dtype dtype, int64_t n, int64_t h, int64_t N) {
     return t_algo == HH_ALGO_WY && h > 0 && N > 0 &&
-           (dtype != HH_F32 || !wy_supported(kind, n, h, N));
+           (dtype != HH_F32 || n > max_n(0) || !wy_supported(kind, n, h, N));
 }
 
 // the bucketed Mahalanobis path indexes pairs and points with int32
@@ -103,21 +103,39 @@ hh_status map_err(cudaError_t e) {
     return HH_ERR_CUDA;
 }
 
-// shape checks shared by the column calls; returns HH_OK or the error
+// The vector kernels (K1 / K1s / K1t, K5) move columns with 128-bit accesses: column stride a
+// multiple of 16 bytes and n within their variant tables.  Every other shape runs K1g
+// (hh_general.cu), which needs element alignment only.
+bool vector_shape(int64_t n, hh_dtype dtype) {
+    return (static_cast<size_t>(n) * elem(dtype)) % 16 == 0 && n <= max_n(dtype);
+}
+bool aligned_elem(const void *p, hh_dtype dtype) {
+    return reinterpret_cast<uintptr_t>(p) % elem(dtype) == 0;
+}
+
+// shape checks shared by the column calls; returns HH_OK or the error.  general_ok: the call
+// has the K1g path, so shapes / alignments outside the vector kernels' are accepted when K1g
+// takes them (the call itself then checks element alignment of its operands).
 hh_status check_common(int64_t n, int64_t h, const void *U, int64_t N, hh_dtype dtype,
-                       bool device_u = true) {
+                       bool device_u = true, bool general_ok = false) {
     if (!dtype_ok(dtype) || n < 1 || h < 0 || N < 0) return HH_ERR_INVALID_VALUE;
     if (h > 0 && !U) return HH_ERR_INVALID_VALUE;
-    if ((static_cast<size_t>(n) * elem(dtype)) % 16 != 0) return HH_ERR_UNSUPPORTED;
-    if (n > max_n(dtype)) return HH_ERR_UNSUPPORTED;
-    if (device_u && h > 0 && !aligned16(U)) return HH_ERR_UNSUPPORTED;
     if (h > (int64_t(1) << 30)) return HH_ERR_UNSUPPORTED;
+    if (general_ok) {
+        if (!vector_shape(n, dtype) && !general_supported(n, dtype == HH_F32 ? 0 : 1))
+            return HH_ERR_UNSUPPORTED;
+        if (device_u && h > 0 && !aligned_elem(U, dtype)) return HH_ERR_UNSUPPORTED;
+        return HH_OK;
+    }
+    if (!vector_shape(n, dtype)) return HH_ERR_UNSUPPORTED;
+    if (device_u && h > 0 && !aligned16(U)) return HH_ERR_UNSUPPORTED;
     return HH_OK;
 }
 
-hh_status run_fused(FusedArgs a, hh_dtype dtype, cudaStream_t stream) {
+hh_status run_fused(FusedArgs a, hh_dtype dtype, cudaStream_t stream, bool general = false) {
     LaunchInfo info;
-    cudaError_t e = launch_fused(a, dtype == HH_F32 ? 0 : 1, stream, &info);
+    cudaError_t e = general ? launch_general(a, dtype == HH_F32 ? 0 : 1, stream, &info)
+                            : launch_fused(a, dtype == HH_F32 ? 0 : 1, stream, &info);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (info.variant) {
         t_last = info;
@@ -341,15 +359,19 @@ static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const
                             size_t workspace_bytes, hh_stream_t stream, const void *dsign,
                             int dside, int qr = 0) {
     if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
-    hh_status st = check_common(n, h, U, N, dtype);
+    hh_status st = check_common(n, h, U, N, dtype, true, true);
     if (st != HH_OK) return st;
     if (N == 0) return HH_OK;
     if (!X || !Y) return HH_ERR_INVALID_VALUE;
-    if (!aligned16(X) || !aligned16(Y)) return HH_ERR_UNSUPPORTED;
     if (dside && !dsign) return HH_ERR_INVALID_VALUE;
-    if (dside && !aligned16(dsign)) return HH_ERR_UNSUPPORTED;
+    if (!aligned_elem(X, dtype) || !aligned_elem(Y, dtype) || (dside && !aligned_elem(dsign, dtype)))
+        return HH_ERR_UNSUPPORTED;
+    // K1g for the shapes and alignments the vector kernels do not take
+    const bool general = !vector_shape(n, dtype) || !aligned16(X) || !aligned16(Y) ||
+                         (h > 0 && !aligned16(U)) || (dside && !aligned16(dsign));
     if (wy_forced_unsupported(WY_APPLY_N, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
-    if (h > 0 && use_wy(dtype, n, h, N, t_algo)) {
+    if (general && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
+    if (!general && h > 0 && use_wy(dtype, n, h, N, t_algo)) {
         WyPlan p = wy_plan(op == HH_OP_T ? WY_APPLY_T : WY_APPLY_N, n, h, N);
         p.qr = qr;
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
@@ -380,7 +402,7 @@ static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const
     a.dsign = dsign;
     a.dside = dside;
     a.qr = qr;
-    return run_fused(a, dtype, stream);
+    return run_fused(a, dtype, stream, general);
 }
 
 hh_status hh_apply_qr(hh_op op, int64_t n, int64_t h, const void *U, const void *X, void *Y,
@@ -409,14 +431,19 @@ hh_status hh_apply_signed(hh_op op, hh_side side, int64_t n, int64_t h, const vo
 static hh_status sym_impl(int64_t n, int64_t h, const void *U, const void *lambda, const void *X,
                           void *Y, int64_t N, hh_dtype dtype, void *workspace,
                           size_t workspace_bytes, hh_stream_t stream, const void *dsign) {
-    hh_status st = check_common(n, h, U, N, dtype);
+    hh_status st = check_common(n, h, U, N, dtype, true, true);
     if (st != HH_OK) return st;
     if (N == 0) return HH_OK;
     if (!X || !Y || !lambda) return HH_ERR_INVALID_VALUE;
-    if (!aligned16(X) || !aligned16(Y) || !aligned16(lambda)) return HH_ERR_UNSUPPORTED;
-    if (dsign && !aligned16(dsign)) return HH_ERR_UNSUPPORTED;
+    if (!aligned_elem(X, dtype) || !aligned_elem(Y, dtype) || !aligned_elem(lambda, dtype) ||
+        (dsign && !aligned_elem(dsign, dtype)))
+        return HH_ERR_UNSUPPORTED;
+    const bool general = !vector_shape(n, dtype) || !aligned16(X) || !aligned16(Y) ||
+                         !aligned16(lambda) || (h > 0 && !aligned16(U)) ||
+                         (dsign && !aligned16(dsign));
     if (wy_forced_unsupported(WY_SYM, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
-    if (h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
+    if (general && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
+    if (!general && h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
         const WyPlan p = wy_plan(WY_SYM, n, h, N);
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
         if (workspace && !aligned16(workspace)) return HH_ERR_UNSUPPORTED;
@@ -446,7 +473,7 @@ static hh_status sym_impl(int64_t n, int64_t h, const void *U, const void *lambd
     a.mode = MODE_SYM;
     a.dsign = dsign;
     a.dside = dsign ? 3 : 0;
-    return run_fused(a, dtype, stream);
+    return run_fused(a, dtype, stream, general);
 }
 
 hh_status hh_sym_apply(int64_t n, int64_t h, const void *U, const void *lambda, const void *X,
@@ -471,15 +498,18 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
     if (npairs < 0 || M < 0) return HH_ERR_INVALID_VALUE;
     if (npairs > 0 && M < 1) return HH_ERR_INVALID_VALUE;
     if (npairs >= kMaxPairs || M >= kMaxPairs) return HH_ERR_UNSUPPORTED;
-    hh_status st = check_common(n, h, U, M, dtype);
+    hh_status st = check_common(n, h, U, M, dtype, true, true);
     if (st != HH_OK) return st;
     if (npairs == 0) return HH_OK;
     if (!d || !P || !ia || !ib || !dist) return HH_ERR_INVALID_VALUE;
-    if (!aligned16(d) || !aligned16(P)) return HH_ERR_UNSUPPORTED;
-    if (reinterpret_cast<uintptr_t>(dist) % elem(dtype) != 0) return HH_ERR_UNSUPPORTED;
+    if (!aligned_elem(d, dtype) || !aligned_elem(P, dtype) || !aligned_elem(dist, dtype))
+        return HH_ERR_UNSUPPORTED;
+    // shapes / alignments outside the vector kernels': the per-pair form on K1g (no scratch)
+    const bool general = !vector_shape(n, dtype) || !aligned16(d) || !aligned16(P) ||
+                         (h > 0 && !aligned16(U));
     size_t need = 0;
     hh_workspace_bytes(HH_CALL_MAHALANOBIS, n, h, M, npairs, dtype, &need);
-    if (workspace) {
+    if (workspace && !general) {
         if (workspace_bytes < need) return HH_ERR_WORKSPACE;
         if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
         // The counting sort of the pairs needs only ia: it runs on a second stream beside
@@ -548,7 +578,7 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
     a.h = h;
     a.N = npairs;
     a.mode = MODE_PAIR;
-    return run_fused(a, dtype, stream);
+    return run_fused(a, dtype, stream, general);
 }
 
 hh_status hh_shf_cost(int64_t n, const void *A, const void *B, const void *Uc, int64_t K,
@@ -647,7 +677,7 @@ hh_status hh_apply_host(hh_op op, int64_t n, int64_t h, const void *U_host, cons
                         void *Y_host, int64_t N, hh_dtype dtype, void *workspace,
                         size_t workspace_bytes, hh_stream_t stream) {
     if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
-    hh_status st = check_common(n, h, U_host, N, dtype, /*device_u=*/false);
+    hh_status st = check_common(n, h, U_host, N, dtype, /*device_u=*/false, /*general_ok=*/true);
     if (st != HH_OK) return st;
     if (N == 0) return HH_OK;
     if (!X_host || !Y_host || !workspace) return HH_ERR_INVALID_VALUE;

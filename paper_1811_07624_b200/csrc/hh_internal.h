@@ -79,6 +79,11 @@ cudaError_t launch_shf(int64_t n, const void *A, const void *B, const void *Uc, 
 // Largest n the vector kernels support for this dtype.
 int64_t max_n(int dtype);
 
+// K1g (hh_general.cu): the same modes for any n whose column fits in shared memory and
+// operands aligned to the element only (scalar accesses; the shapes K1 refuses).
+bool general_supported(int64_t n, int dtype);
+cudaError_t launch_general(const FusedArgs &a, int dtype, cudaStream_t stream, LaunchInfo *info);
+
 // Device attributes (cached per device, thread-safe).
 struct DevAttr {
     int sm_count = 0;

@@ -102,18 +102,22 @@ def test_validation_before_launch():
     assert _apply(0, 16, 1, A, A, A, -1, 0) == hh.HH_ERR_INVALID_VALUE          # N < 0
     assert _apply(0, 16, 1, None, A, A, 4, 0) == hh.HH_ERR_INVALID_VALUE        # U NULL
     assert _apply(0, 16, 1, A, A, A, 4, 5) == hh.HH_ERR_INVALID_VALUE           # bad dtype
-    # unsupported
-    assert _apply(0, 18, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED             # n*4 % 16
-    assert _apply(0, 9, 1, A, A, A, 4, 1) == hh.HH_ERR_UNSUPPORTED              # n*8 % 16
-    assert _apply(0, 16, 1, A + 4, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED         # U misaligned
-    assert _apply(0, 16, 1, A, A + 8, A, 4, 0) == hh.HH_ERR_UNSUPPORTED         # X misaligned
-    assert _apply(0, 8196, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED           # n > max
+    # unsupported: pointers not aligned to the element, n beyond K1g's shared memory
+    # (any n*size and 16-B misalignment run on K1g: tests/test_parity_gpu.py::test_general_*)
+    assert _apply(0, 16, 1, A + 2, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED         # U misaligned
+    assert _apply(0, 16, 1, A, A + 2, A, 4, 0) == hh.HH_ERR_UNSUPPORTED         # X misaligned
+    assert _apply(0, 16, 1, A, A, A + 4, 4, 1) == hh.HH_ERR_UNSUPPORTED         # Y misaligned (f64)
+    assert _apply(0, 60000, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED          # n > K1g capacity
+    assert _apply(0, 30000, 1, A, A, A, 4, 1) == hh.HH_ERR_UNSUPPORTED          # ... fp64
+    with hhpkg.algo(hh.HH_ALGO_WY):                                             # forced WY, K1g shape
+        assert _apply(0, 18, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED
+        assert _apply(0, 8196, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED
     # empty batches are successful no-ops (no launch), h = 0 needs no U
     assert _apply(0, 16, 1, A, None, None, 0, 0) == hh.HH_OK
     assert _apply(1, 16, 0, None, None, None, 0, 0) == hh.HH_OK
     # sym / Mahalanobis
     assert L.hh_sym_apply(16, 1, A, None, A, A, 4, 0, None, 0, None) == hh.HH_ERR_INVALID_VALUE
-    assert L.hh_sym_apply(16, 1, A, A + 4, A, A, 4, 0, None, 0, None) == hh.HH_ERR_UNSUPPORTED
+    assert L.hh_sym_apply(16, 1, A, A + 2, A, A, 4, 0, None, 0, None) == hh.HH_ERR_UNSUPPORTED
     assert L.hh_sym_apply(16, 1, A, A, A, A, 0, 0, None, 0, None) == hh.HH_OK
     assert L.hh_mahalanobis(16, 1, A, A, A, 0, A, A, 3, A, 0, None, 0, None) == \
         hh.HH_ERR_INVALID_VALUE                                                  # M = 0, pairs

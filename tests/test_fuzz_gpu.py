@@ -45,6 +45,39 @@ def test_fuzz_apply(n, h, N, algo):
         assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"fuzz apply n{n} h{h} N{N} {dt}")
 
 
+def any_shapes(seed, count):
+    """Arbitrary n (mostly not a multiple of 4: K1g), a few past the vector kernels' n."""
+    g = gi.rng(810, seed)
+    out = []
+    for _ in range(count):
+        n = int(g.integers(1, 3000)) if g.random() < 0.8 else int(g.integers(8193, 30000))
+        h = int(g.integers(0, 24))
+        N = int(g.integers(1, 200 if n < 3000 else 20))
+        out.append((n, h, N))
+    return out
+
+
+@pytest.mark.parametrize("n,h,N", any_shapes(1, 20))
+def test_fuzz_any_n(n, h, N):
+    """Every n: the apply (both ops), the symmetric form and the per-pair distance, fp32 and
+    fp64, whichever kernel the library picks (K1g unless the shape happens to fit K1)."""
+    for dt, tdt in (("f32", torch.float32), ("f64", torch.float64)):
+        if dt == "f64" and n > 25000:
+            continue
+        c = gi.make_case("sym", n, h, N, dt, seed=n + 3 * h)
+        U = dev(c.U) if h else torch.empty(0, n, device="cuda", dtype=tdt)
+        for op in (0, 1):
+            got = hh.hh_apply(op, U, dev(c.X)).cpu().numpy()
+            assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"any-n apply n{n} h{h} op{op} {dt}")
+        got = hh.hh_sym_apply(U, dev(c.lam), dev(c.X)).cpu().numpy()
+        assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), dt, h, f"any-n sym n{n} h{h} {dt}")
+        m = gi.make_case("mahalanobis", n, h, max(N, 2), dt, seed=n, npairs=3 * N + 5)
+        got = hh.hh_mahalanobis(dev(m.U) if h else torch.empty(0, n, device="cuda", dtype=tdt),
+                                dev(m.d), dev(m.X), dev(m.ia), dev(m.ib)).cpu().numpy()
+        assert_parity(got, oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib), dt, h,
+                      f"any-n pairs n{n} h{h} {dt}")
+
+
 @pytest.mark.parametrize("n,h,N", shapes(2, 12))
 def test_fuzz_sym_and_signed(n, h, N):
     h = max(h, 1)

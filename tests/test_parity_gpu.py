@@ -178,16 +178,16 @@ def test_errors_write_nothing():
     X = torch.randn(10, 1024, device="cuda")
     Y = torch.full_like(X, 7.0)
     U = torch.randn(3, 1024, device="cuda")
-    st = hh.hh.lib().hh_apply(0, 1024, 3, hh.hh._ptr(U), X.data_ptr() + 4, Y.data_ptr(), 2, 0,
-                              None, 0, None)       # misaligned X
+    st = hh.hh.lib().hh_apply(0, 1024, 3, hh.hh._ptr(U), X.data_ptr() + 2, Y.data_ptr(), 2, 0,
+                              None, 0, None)       # X not aligned to its element
     assert st == hh.hh.HH_ERR_UNSUPPORTED
     torch.cuda.synchronize()
     assert torch.all(Y == 7.0)
     with pytest.raises(ValueError):
         hh.hh_apply(0, U.cpu(), X.cpu())           # CPU tensors: no fallback
     Xo = torch.randn(10, 1022, device="cuda")
-    with pytest.raises(hh.HHError):
-        hh.hh_apply(0, torch.randn(1, 1022, device="cuda"), Xo)   # n*4 % 16 != 0
+    with pytest.raises(hh.HHError), hh.algo(hh.HH_ALGO_WY):
+        hh.hh_apply(0, torch.randn(40, 1022, device="cuda"), Xo)  # forced WY, n*4 % 16 != 0
     P = torch.randn(10, 64, device="cuda")
     ia = torch.zeros(5, dtype=torch.int32, device="cuda")
     # the binding re-allocates a too-small workspace, so call the ABI directly
@@ -429,3 +429,74 @@ def test_fused_path_policy_defaults():
             hh.hh_apply(0, U, X)
         v = hh.last_launch_info()["variant"]
         assert v == want or (want == "f32s_" and v.startswith(want)), (n, h, v)
+
+
+# ------------------------------------------------------------------ K1g: every other shape
+# n*size not a multiple of 16 bytes, n beyond the vector kernels' tables, n = 1; several
+# column groups per CTA and a ragged last group; fp32 and fp64
+GENERAL_SHAPES = [
+    (1, 3, 17, "f32"), (3, 2, 50, "f64"), (30, 5, 333, "f32"), (50, 7, 1001, "f32"),
+    (101, 9, 257, "f64"), (1023, 10, 700, "f32"), (1022, 4, 90, "f32"), (2049, 6, 130, "f64"),
+    (9000, 5, 41, "f32"), (20000, 3, 10, "f32"), (5001, 4, 23, "f64"), (40000, 2, 5, "f32"),
+]
+
+
+@pytest.mark.parametrize("n,h,N,dt", GENERAL_SHAPES)
+def test_general_apply(n, h, N, dt):
+    """Shapes the vector kernels refuse run on K1g: both ops, and in place (Y == X)."""
+    c = gi.make_case("apply", n, h, N, dt, seed=31)
+    for op in (0, 1):
+        got = run_apply(op, c.U, c.X)
+        assert hh.last_launch_info()["variant"].startswith(f"{dt}_general"), hh.last_launch_info()
+        assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"K1g n={n} op{op}")
+    X = dev(c.X)
+    out = hh.hh_apply(0, dev(c.U), X, X)
+    assert out.data_ptr() == X.data_ptr()
+    assert_parity(out.cpu().numpy(), oracle.apply(0, c.U, c.X), dt, h, f"K1g n={n} alias")
+
+
+@pytest.mark.parametrize("n,h,N,dt", [(30, 5, 333, "f32"), (101, 9, 257, "f64"),
+                                      (1023, 10, 300, "f32"), (9000, 5, 41, "f32")])
+def test_general_sym_signed_mahalanobis(n, h, N, dt):
+    c = gi.make_case("sym", n, h, N, dt, seed=32)
+    got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+    assert hh.last_launch_info()["variant"].startswith(f"{dt}_general")
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), dt, h, f"K1g sym n={n}")
+    g = gi.rng(33, n)
+    d = np.where(g.random(n) < 0.5, -1.0, 1.0).astype(c.X.dtype)
+    for op in (0, 1):
+        for side in (0, 1):
+            got = hh.hh_apply_signed(op, side, dev(c.U), dev(d), dev(c.X)).cpu().numpy()
+            assert_parity(got, oracle.apply_signed(op, side, c.U, d, c.X), dt, h,
+                          f"K1g signed n={n} op{op} side{side}")
+    got = hh.hh_sym_apply_signed(dev(c.U), dev(d), dev(c.lam), dev(c.X)).cpu().numpy()
+    assert_parity(got, oracle.sym_apply_signed(c.U, d, c.lam, c.X), dt, h, f"K1g sym signed n={n}")
+    m = gi.make_case("mahalanobis", n, h, 64, dt, seed=34, npairs=999)
+    m.ia[:8] = m.ib[:8]
+    dist = hh.hh_mahalanobis(dev(m.U), dev(m.d), dev(m.X), dev(m.ia), dev(m.ib)).cpu().numpy()
+    assert hh.last_launch_info()["variant"].startswith(f"{dt}_general")
+    assert_parity(dist, oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib), dt, h, f"K1g pairs n={n}")
+    assert np.all(dist[:8] == 0.0)
+
+
+def test_general_misaligned_pointers_and_edges():
+    """16-byte misaligned (but element-aligned) operands take K1g; h = 0 copies; N < group."""
+    c = gi.make_case("apply", 64, 6, 40, "f32", seed=35)
+    buf = torch.zeros(40 * 64 + 1, device="cuda")
+    Xo = buf[1:].view(40, 64)                      # data_ptr % 16 == 4
+    Xo.copy_(dev(c.X))
+    assert Xo.data_ptr() % 16 == 4
+    got = hh.hh_apply(0, dev(c.U), Xo).cpu().numpy()
+    assert hh.last_launch_info()["variant"].startswith("f32_general")
+    assert_parity(got, oracle.apply(0, c.U, c.X), "f32", 6, "K1g misaligned X")
+    e = gi.make_case("apply", 30, 0, 3, "f32", seed=36)
+    U0 = torch.empty(0, 30, device="cuda")
+    assert np.array_equal(hh.hh_apply(1, U0, dev(e.X)).cpu().numpy(), e.X)
+    z = gi.make_case("apply", 50, 4, 2, "f64", seed=37, zero_slots=(1,))
+    assert_parity(run_apply(0, z.U, z.X), oracle.apply(0, z.U, z.X), "f64", 4, "K1g u = 0 slot")
+
+
+def test_general_host_path():
+    c = gi.make_case("apply", 1022, 8, 500, "f32", seed=38)
+    out = hh.hh_apply_host(0, torch.from_numpy(c.U), torch.from_numpy(c.X)).numpy()
+    assert_parity(out, oracle.apply(0, c.U, c.X), "f32", 8, "K1g host")
