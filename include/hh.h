@@ -37,13 +37,13 @@
  *     float pointer 16-byte aligned, n * sizeof(dtype) % 16 == 0 (n % 4 == 0 for f32,
  *     n % 2 == 0 for f64) and n <= 8192 (f32) / 4096 (f64).
  *   - hh_apply, hh_apply_signed, hh_apply_qr, hh_sym_apply, hh_sym_apply_signed,
- *     hh_mahalanobis and hh_apply_host take every other shape too (Eq. 1-2 hold for any
- *     n): any n >= 1 whose column fits in shared memory (n <= ~57000 f32 / ~28000 f64)
- *     and pointers aligned to the element run on a scalar-access kernel (K1g; correct,
- *     not tuned; hh_mahalanobis then uses its per-pair form and ignores the workspace).
+ *     hh_mahalanobis, hh_congruence, hh_knn (n <= 256) and hh_apply_host take every other
+ *     shape too (Eq. 1-2 hold for any n): any n >= 1 whose column fits in shared memory
+ *     (n <= ~57000 f32 / ~28000 f64) and pointers aligned to the element run their
+ *     reflector passes on a scalar-access kernel (K1g; correct, not tuned;
+ *     hh_mahalanobis then uses its per-pair form and ignores the workspace).
  *   - HH_ERR_UNSUPPORTED: a pointer not aligned to its element, n beyond K1g's capacity,
- *     HH_ALGO_WY forced on such a shape, or the other calls (hh_knn, hh_congruence) outside
- *     the fast kernels' alignment / size.
+ *     or HH_ALGO_WY forced on such a shape.
  *
  * Semantics
  *   - Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream); no
@@ -278,7 +278,8 @@ hh_status hh_shf_cost(int64_t n, const void *A, const void *B, const void *Uc, i
  *   Each point is transformed once (fused kernel), then distances
  *   ||z_q||^2 + ||z_r||^2 - 2 z_q.z_r run on the tcgen05 tensor cores (bf16x3 split,
  *   fp32 accumulation) with a fused per-query top-k.
- *   v1 limits (HH_ERR_UNSUPPORTED otherwise): fp32, n % 4 == 0, n <= 256, 1 <= k <= 16.
+ *   v1 limits (HH_ERR_UNSUPPORTED otherwise): fp32, n <= 256, 1 <= k <= 16 (any such n:
+ *   the transform of points whose rows are not 16-byte strided runs on K1g).
  *   HH_ERR_INVALID_VALUE: M_ref < k, NULL operands.  workspace (DEVICE) >=
  *   hh_workspace_bytes(HH_CALL_KNN, n, h, M_ref, M_query, dtype).
  */

@@ -607,11 +607,15 @@ hh_status hh_congruence(hh_op op, int64_t n, int64_t h, const void *U, const voi
                         hh_stream_t stream) {
     if (op != HH_OP_N && op != HH_OP_T) return HH_ERR_INVALID_VALUE;
     if (count < 0) return HH_ERR_INVALID_VALUE;
-    hh_status st = check_common(n, h, U, n * count, dtype);
+    hh_status st = check_common(n, h, U, n * count, dtype, true, true);
     if (st != HH_OK) return st;
     if (count == 0) return HH_OK;
     if (!M || !Mout) return HH_ERR_INVALID_VALUE;
-    if (!aligned16(M) || !aligned16(Mout)) return HH_ERR_UNSUPPORTED;
+    // (shapes / alignments outside the vector kernels': the applies run on K1g around the
+    // transposes, which take any n)
+    if (!aligned_elem(M, dtype) || !aligned_elem(Mout, dtype)) return HH_ERR_UNSUPPORTED;
+    const bool general = !vector_shape(n, dtype) || !aligned16(M) || !aligned16(Mout) ||
+                         (h > 0 && !aligned16(U));
     size_t need = 0;
     hh_workspace_bytes(HH_CALL_CONGRUENCE, n, h, count, 0, dtype, &need);
     if (!workspace || workspace_bytes < need) return HH_ERR_WORKSPACE;
@@ -623,7 +627,7 @@ hh_status hh_congruence(hh_op op, int64_t n, int64_t h, const void *U, const voi
     const size_t awsb = need - 2 * mb;
     const int64_t NC = n * count;
     const int dt = dtype == HH_F32 ? 0 : 1;
-    if (h > 0 && row_apply_supported(n, h, dt)) {
+    if (!general && h > 0 && row_apply_supported(n, h, dt)) {
         // two passes: T1 = op(Q) M (columns), M_out = T1 op(Q)^T (rows, K7)
         st = apply_impl(op, n, h, U, M, T1, NC, dtype, awsb ? aws : nullptr, awsb, stream, nullptr, 0);
         if (st != HH_OK) return st;
@@ -656,8 +660,12 @@ hh_status hh_knn(int64_t n, int64_t h, const void *U, const void *d, const void 
     if ((h > 0 && !U) || !d || !P_ref || !P_query || !nn_idx || !nn_dist)
         return HH_ERR_INVALID_VALUE;
     if (dtype != HH_F32 || !knn_supported(n, M_ref, M_query, k)) return HH_ERR_UNSUPPORTED;
-    if (!aligned16(d) || !aligned16(P_ref) || !aligned16(P_query) || (h > 0 && !aligned16(U)))
+    if (!aligned_elem(d, dtype) || !aligned_elem(P_ref, dtype) || !aligned_elem(P_query, dtype) ||
+        (h > 0 && !aligned_elem(U, dtype)) || !aligned_elem(nn_dist, dtype))
         return HH_ERR_UNSUPPORTED;
+    // the transform runs on K1g when the points are not 16-byte strided / aligned
+    const bool general = !vector_shape(n, dtype) || !aligned16(d) || !aligned16(P_ref) ||
+                         !aligned16(P_query) || (h > 0 && !aligned16(U));
     const KnnPlan p = knn_plan(n, M_ref, M_query, k, device_attr().sm_count);
     if (!workspace || workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
     if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
@@ -665,7 +673,7 @@ hh_status hh_knn(int64_t n, int64_t h, const void *U, const void *d, const void 
     cudaError_t e = launch_knn(p, static_cast<const float *>(U), h, static_cast<const float *>(d),
                                static_cast<const float *>(P_ref),
                                static_cast<const float *>(P_query), nn_idx,
-                               static_cast<float *>(nn_dist), workspace, stream, &info);
+                               static_cast<float *>(nn_dist), workspace, stream, &info, general);
     if (info.variant) {
         t_last = info;
         t_has_last = true;

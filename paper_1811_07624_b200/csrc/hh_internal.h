@@ -147,7 +147,7 @@ KnnPlan knn_plan(int64_t n, int64_t Mr, int64_t Mq, int k, int sm_count);
 bool knn_supported(int64_t n, int64_t Mr, int64_t Mq, int k);
 cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float *d,
                        const float *Pr, const float *Pq, int32_t *nn_idx, float *nn_dist, void *ws,
-                       cudaStream_t stream, LaunchInfo *info);
+                       cudaStream_t stream, LaunchInfo *info, bool general = false);
 
 }  // namespace hh
 

@@ -471,14 +471,14 @@ KnnPlan knn_plan(int64_t n, int64_t Mr, int64_t Mq, int k, int sm_count) {
 }
 
 bool knn_supported(int64_t n, int64_t Mr, int64_t Mq, int k) {
-    return n >= 4 && n % 4 == 0 && n <= kKnnMaxN && k >= 1 &&
+    return n >= 1 && n <= kKnnMaxN && k >= 1 &&
            k <= kKnnMaxK && Mr >= k && Mq >= 1 && 2 * Mr < (int64_t(1) << 31) &&
            2 * Mq < (int64_t(1) << 31);
 }
 
 cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float *d,
                        const float *Pr, const float *Pq, int32_t *nn_idx, float *nn_dist, void *ws,
-                       cudaStream_t stream, LaunchInfo *info) {
+                       cudaStream_t stream, LaunchInfo *info, bool general) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kKnnMaxDev) return cudaErrorInvalidDevice;
     std::call_once(g_knn_attr_once[dev], [dev]() {
@@ -513,7 +513,9 @@ cudaError_t launch_knn(const KnnPlan &p, const float *U, int64_t h, const float 
         a.h = h;
         a.N = which ? p.Mq : p.Mr;
         a.mode = MODE_TRANSFORM;
-        cudaError_t e = launch_fused(a, 0, stream, nullptr);
+        // (K1g when n * 4 is not a multiple of 16 bytes or an operand is only element-aligned)
+        cudaError_t e = general ? launch_general(a, 0, stream, nullptr)
+                                : launch_fused(a, 0, stream, nullptr);
         if (e != cudaSuccess) return e;
     }
     // 2. bf16 hi/lo split + squared norms

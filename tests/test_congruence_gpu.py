@@ -19,7 +19,10 @@ def dev(a):
 
 @pytest.mark.parametrize("n,h,count,dt,path", [(64, 6, 5, "f64", "auto"), (1024, 10, 3, "f32", "auto"),
                                                (512, 40, 2, "f32", "wy"), (512, 40, 2, "f32", "fused"),
-                                               (100, 7, 4, "f32", "auto"), (2048, 33, 1, "f32", "auto")])
+                                               (100, 7, 4, "f32", "auto"), (2048, 33, 1, "f32", "auto"),
+                                               # n * size not a multiple of 16 bytes: K1g applies
+                                               (101, 7, 3, "f32", "auto"), (33, 5, 4, "f64", "auto"),
+                                               (9, 4, 6, "f32", "auto"), (1025, 6, 1, "f32", "auto")])
 def test_congruence(n, h, count, dt, path):
     g = gi.rng(600, n, h, count)
     U = gi.unit_reflectors(g, h, n, dt)

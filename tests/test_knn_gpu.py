@@ -45,7 +45,10 @@ def sq_norms(U, d, P):
 
 @pytest.mark.parametrize("n,h,Mr,Mq,k", [(40, 6, 2000, 300, 3), (100, 7, 1500, 200, 5),
                                          (200, 24, 1000, 130, 16), (64, 0, 700, 129, 1),
-                                         (256, 9, 513, 257, 8)])
+                                         (256, 9, 513, 257, 8),
+                                         # rows not 16-byte strided: the transform runs on K1g
+                                         (41, 6, 900, 150, 3), (30, 5, 600, 100, 4),
+                                         (255, 8, 400, 70, 2), (3, 2, 300, 40, 5)])
 def test_knn_parity(n, h, Mr, Mq, k):
     U, d, Pr, Pq = knn_case(n, h, Mr, Mq, seed=1)
     idx, dist = hh.hh_knn(dev(U) if h else torch.empty(0, n, device="cuda"), dev(d), dev(Pr),
