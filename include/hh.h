@@ -40,7 +40,7 @@
  *     hh_mahalanobis, hh_congruence, hh_knn (n <= 256) and hh_apply_host take every other
  *     shape too (Eq. 1-2 hold for any n): any n >= 1 whose column fits in shared memory
  *     (n <= ~57000 f32 / ~28000 f64) and pointers aligned to the element run their
- *     reflector passes on a scalar-access kernel (K1g; correct, not tuned;
+ *     reflector passes on scalar-access kernels (K1r / K1g; correct, 2-8x slower;
  *     hh_mahalanobis then uses its per-pair form and ignores the workspace).
  *   - HH_ERR_UNSUPPORTED: a pointer not aligned to its element, n beyond K1g's capacity,
  *     or HH_ALGO_WY forced on such a shape.

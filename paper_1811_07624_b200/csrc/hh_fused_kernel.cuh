@@ -134,6 +134,31 @@ __device__ __forceinline__ double vwsq(const double2 &x, const double2 &d) {
     return d.x * (x.x * x.x) + d.y * (x.y * x.y);
 }
 
+// ---- scalar "vectors" (E = 1): the SC form of the kernel, for columns whose stride or base is
+// not a multiple of 16 bytes (one element per access, lanes on consecutive elements)
+__device__ __forceinline__ void vzero(float &a) { a = 0.f; }
+__device__ __forceinline__ void vzero(double &a) { a = 0.0; }
+__device__ __forceinline__ void vfma(float &acc, float u, float x) { acc = fmaf(u, x, acc); }
+__device__ __forceinline__ void vfma(double &acc, double u, double x) { acc = fma(u, x, acc); }
+__device__ __forceinline__ float vsum(float a) { return a; }
+__device__ __forceinline__ double vsum(double a) { return a; }
+__device__ __forceinline__ void vaxpy(float &x, float s, float u) { x = fmaf(-s, u, x); }
+__device__ __forceinline__ void vaxpy(double &x, double s, double u) { x = fma(-s, u, x); }
+__device__ __forceinline__ void vmul(float &x, float l) { x *= l; }
+__device__ __forceinline__ void vmul(double &x, double l) { x *= l; }
+__device__ __forceinline__ void vmulsqrt(float &x, float d) { x *= sqrt_approx(d); }
+__device__ __forceinline__ void vmulsqrt(double &x, double d) { x *= sqrt(d); }
+__device__ __forceinline__ void vsub(float &a, float b) { a -= b; }
+__device__ __forceinline__ void vsub(double &a, double b) { a -= b; }
+__device__ __forceinline__ float vwsq(float x, float d) { return d * (x * x); }
+__device__ __forceinline__ double vwsq(double x, double d) { return d * (x * x); }
+__device__ __forceinline__ void st_global_hint(float *p, const float &v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_global_hint(double *p, const double &v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 template <typename V>
 __device__ __forceinline__ V ldg_v(const V *p) {
     return __ldg(p);
@@ -211,16 +236,23 @@ __device__ __forceinline__ void tmem_dealloc_n(uint32_t taddr, uint32_t ncols) {
 // per-reflector serial chain (dot -> reduction -> barrier -> update) becomes one per block, at
 // the price of a second TMEM read of each u.  The Gram G = U^T U (h x h, fp32) is formed once per
 // CTA from the TMEM-resident reflectors (fixed-order sums: identical in every CTA).
-template <typename T, int TPC, int CH, int C, int NT, bool FULL, bool UTM = false, int KB = 1>
+//
+// SC ("K1r"): scalar element ownership -- a thread owns the elements gt + TPC k (k < CH) of its
+// columns instead of 128-bit chunks, columns are loaded straight into registers with coalesced
+// one-element accesses, U is copied into shared memory by the CTA's threads (resident only).
+// Needs element alignment only: the shapes whose column stride or base is not a multiple of
+// 16 bytes (any n <= TPC CH).
+template <typename T, int TPC, int CH, int C, int NT, bool FULL, bool UTM = false, int KB = 1,
+          bool SC = false>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const FusedArgs a) {
-    static_assert(!UTM || (std::is_same<T, float>::value && 128 % TPC == 0 && TPC >= 32),
+    static_assert(!UTM || (!SC && std::is_same<T, float>::value && 128 % TPC == 0 && TPC >= 32),
                   "TMEM reflectors: fp32, TPC in {32, 64, 128}");
     static_assert(KB == 1 || (UTM && (KB * C == 4 || KB * C == 8 || KB * C == 16)),
                   "blocked reflectors: TMEM form, KB * C in {4, 8, 16}");
     constexpr int KV = KB > 1 ? KB * C : C;   // values per cross-lane reduction
     constexpr int UCOLS = 4 * CH;   // TMEM columns per reflector (UTM)
-    using V = typename VT<T>::V;
-    constexpr int E = VT<T>::E;
+    using V = typename std::conditional<SC, T, typename VT<T>::V>::type;
+    constexpr int E = SC ? 1 : VT<T>::E;
     constexpr int UT = TPC > 32 ? TPC : 32;  // threads per scheduling unit
     constexpr int GPU_ = UT / TPC;           // groups per unit
     constexpr int UC = GPU_ * C;             // columns per unit tile
@@ -250,6 +282,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     V *Us = reinterpret_cast<V *>(smem);
     V *Xs = Us + static_cast<size_t>(nbuf) * R * nv;
     T *red = reinterpret_cast<T *>(Xs + (stage ? static_cast<size_t>(NU) * UC * nv : 0));
+    if constexpr (SC)   // R nv elements need not end on a 16-byte boundary
+        red = reinterpret_cast<T *>((reinterpret_cast<uintptr_t>(red) + 15) & ~static_cast<uintptr_t>(15));
     uint64_t *bars = reinterpret_cast<uint64_t *>(red + (TPC > 32 ? 2 * NU * WPU * KV : 0));
     uint64_t *ubar = bars;      // [2]
     uint64_t *xbar = bars + 2;  // [NU]
@@ -389,6 +423,10 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     }
 
     // prologue: U (resident, or the first two chunk visits) and each unit's first tile
+    if constexpr (SC) {   // resident U copied by the CTA's threads (no 16-byte granularity)
+        for (int64_t i = tid; i < static_cast<int64_t>(h) * nv; i += NT) Us[i] = __ldg(Ug + i);
+        __syncthreads();
+    } else
     if (!UTM && tid == 0 && h > 0) {
         if (nc == 1) {
             issue_u(0, 0);
@@ -403,7 +441,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     uint32_t xphase = 0;
     int rpar = 0;       // reduction-buffer parity (TPC > 32)
     int64_t g = 0;      // chunk-visit counter (nc > 1)
-    bool u_ready = UTM || (h == 0) || (nc > 1);
+    bool u_ready = UTM || SC || (h == 0) || (nc > 1);
 
     auto valid_k = [&](int k) -> bool { return FULL || (gt + TPC * k < nv); };
 
@@ -413,7 +451,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         // multi-warp groups: keep the u chunk in registers across the cross-warp
         // reduction (a shared-memory store + barrier the compiler cannot see through),
         // so u is read from shared memory once per reflector, not twice
-        constexpr bool kKeepU = TPC > 32 || UTM;
+        constexpr bool kKeepU = (TPC > 32 || UTM) && !SC;
         V uk[kKeepU ? CH : 1];
         if constexpr (UTM) {
             uint32_t r[UCOLS];
@@ -439,8 +477,34 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         // packed FADD2 (two IEEE adds per instruction) -- fewer issue slots on the serial chain
         constexpr bool kPair = std::is_same<T, float>::value && C == 2 && TPC <= 32;
         // the packed partial sums and 2-alpha also serve the multi-warp two-column groups
-        constexpr bool kPairSum = std::is_same<T, float>::value && C == 2;
-        if constexpr (kPairSum) {
+        constexpr bool kPairSum = std::is_same<T, float>::value && C == 2 && !SC;
+        // SC, fp32, two columns: element k of both columns is one FFMA2 pair against (u, u);
+        // four accumulator pairs break the CH-long dependency chain
+        constexpr bool kScPair = SC && std::is_same<T, float>::value && C == 2;
+        if constexpr (kScPair) {
+            float q0[4] = {0.f, 0.f, 0.f, 0.f}, q1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                if (valid_k(k)) {
+                    const float uk0 = ub[gt + TPC * k];
+                    ffma2(q0[k & 3], q1[k & 3], uk0, uk0, x[0][k], x[1][k], q0[k & 3], q1[k & 3]);
+                }
+            }
+            float a0, a1, b0, b1;
+            fadd2(a0, a1, q0[0], q1[0], q0[1], q1[1]);
+            fadd2(b0, b1, q0[2], q1[2], q0[3], q1[3]);
+            fadd2(p[0], p[1], a0, a1, b0, b1);
+        } else if constexpr (SC) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                T q[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+                for (int k = 0; k < CH; ++k) {
+                    if (valid_k(k)) vfma(q[k & 3], ub[gt + TPC * k], x[c][k]);
+                }
+                p[c] = (q[0] + q[1]) + (q[2] + q[3]);
+            }
+        } else if constexpr (kPairSum) {
             V acc0, acc1;
             vzero(acc0);
             vzero(acc1);
@@ -520,7 +584,17 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             rpar ^= 1;
         }
         }
-        if constexpr (kPairSum) {
+        if constexpr (kScPair) {
+            float s0, s1;
+            fadd2(s0, s1, p[0], p[1], p[0], p[1]);
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                if (valid_k(k)) {
+                    const float uk0 = ub[gt + TPC * k];
+                    ffma2(x[0][k], x[1][k], -s0, -s1, uk0, uk0, x[0][k], x[1][k]);
+                }
+            }
+        } else if constexpr (kPairSum) {
             float s0, s1;
             fadd2(s0, s1, p[0], p[1], p[0], p[1]);   // 2 alpha for both columns at once
 #pragma unroll
@@ -649,7 +723,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     // (NEXT-f2: the fused kernel applies QR-structured reflectors in full -- it serves
     // small h, where the zero prefixes are a negligible share; K5 skips them.)
     auto run_range = [&](const V *base, int chunk_lo, int r0, int r1, bool desc) {
-        constexpr bool kPairLoop = std::is_same<T, float>::value && C == 2 && TPC <= 32;
+        constexpr bool kPairLoop = std::is_same<T, float>::value && C == 2 && TPC <= 32 && !SC;
         if constexpr (kPairLoop) {
             // two reflectors per loop trip: the loop bookkeeping is ~10 of the ~100 issue slots
             // of a reflector here, and this kernel is issue-bound (C2 0.358 -> 0.353 ms, A/B)
@@ -943,9 +1017,18 @@ struct FusedVariant {
             KB, NAME "_tmem_kb" #KB                                                        \
     }
 
+// the scalar-element form (K1r): ragged form only (n is never a multiple of 16 bytes there)
+#define HH_FUSED_VAR_SC(T, TPC, CH, C, NT, NAME)                                                   \
+    FusedVariant {                                                                                 \
+        nullptr,                                                                                   \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, false, 1, true>), \
+            nullptr, nullptr, TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME, NAME              \
+    }
+
 // tables (each defined in its own translation unit so the instantiations build in parallel)
 const FusedVariant *fused_table_f32(int *count);
 const FusedVariant *fused_table_f64(int *count);
 const FusedVariant *fused_alt_f32(int *count);   // A/B alternatives (hh_debug_k1)
+const FusedVariant *fused_table_scalar(int dtype, int *count);   // K1r (hh_fused_sc.cu)
 
 }  // namespace hh

@@ -202,7 +202,21 @@ bool general_supported(int64_t n, int dtype) {
                          static_cast<size_t>(device_attr().max_smem_optin);
 }
 
+namespace {
+thread_local int t_scalar = 1;
+}
+int general_set_scalar(int on) {
+    const int prev = t_scalar;
+    t_scalar = on;
+    return prev;
+}
+
 cudaError_t launch_general(const FusedArgs &a, int dtype, cudaStream_t stream, LaunchInfo *info) {
+    // K1r first: the register-resident persistent kernel with one-element accesses
+    if (t_scalar) {
+        const cudaError_t e = launch_fused_scalar(a, dtype, stream, info);
+        if (e != cudaErrorNotSupported) return e;
+    }
     const DevAttr &da = device_attr();
     const int s = dtype == 0 ? 4 : 8;
     const int nt = general_threads(a.n);

@@ -83,6 +83,11 @@ int64_t max_n(int dtype);
 // operands aligned to the element only (scalar accesses; the shapes K1 refuses).
 bool general_supported(int64_t n, int dtype);
 cudaError_t launch_general(const FusedArgs &a, int dtype, cudaStream_t stream, LaunchInfo *info);
+// K1r (hh_fused_sc.cu): the persistent fused kernel with one-element accesses, for the same
+// shapes while n is within the K1 tables and U fits in shared memory; cudaErrorNotSupported
+// otherwise (launch_general tries it first)
+cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info);
+int general_set_scalar(int on);   // A/B / test hook (hh_debug_general_scalar): 1 K1r first (default), 0 K1g only
 
 // Device attributes (cached per device, thread-safe).
 struct DevAttr {

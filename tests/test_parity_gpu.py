@@ -435,32 +435,68 @@ def test_fused_path_policy_defaults():
 # n*size not a multiple of 16 bytes, n beyond the vector kernels' tables, n = 1; several
 # column groups per CTA and a ragged last group; fp32 and fp64
 GENERAL_SHAPES = [
+    # one shape per K1r table row (ragged n inside each), several batches per unit
+    (63, 5, 3000, "f32"), (127, 6, 2500, "f32"), (250, 9, 2100, "f32"), (511, 12, 1900, "f32"),
+    (2047, 11, 1300, "f32"), (4095, 7, 700, "f32"), (8191, 3, 300, "f32"), (1021, 40, 900, "f32"),
+    (63, 5, 1500, "f64"), (127, 4, 1100, "f64"), (255, 8, 900, "f64"), (509, 10, 800, "f64"),
+    (1023, 9, 700, "f64"), (4095, 3, 200, "f64"),
     (1, 3, 17, "f32"), (3, 2, 50, "f64"), (30, 5, 333, "f32"), (50, 7, 1001, "f32"),
     (101, 9, 257, "f64"), (1023, 10, 700, "f32"), (1022, 4, 90, "f32"), (2049, 6, 130, "f64"),
     (9000, 5, 41, "f32"), (20000, 3, 10, "f32"), (5001, 4, 23, "f64"), (40000, 2, 5, "f32"),
 ]
 
 
+def is_general(dt):
+    """K1r (scalar-element persistent kernel, `f32r_...`) or K1g (`f32_general...`) ran."""
+    v = hh.last_launch_info()["variant"]
+    return v.startswith(f"{dt}r_") or v.startswith(f"{dt}_general")
+
+
+class k1g_only:
+    """Test hook: keep K1r off so that K1g also serves the shapes K1r would take."""
+
+    def __enter__(self):
+        self.prev = hh.hh.lib().hh_debug_general_scalar(0)
+
+    def __exit__(self, *exc):
+        hh.hh.lib().hh_debug_general_scalar(self.prev)
+
+
 @pytest.mark.parametrize("n,h,N,dt", GENERAL_SHAPES)
-def test_general_apply(n, h, N, dt):
-    """Shapes the vector kernels refuse run on K1g: both ops, and in place (Y == X)."""
+@pytest.mark.parametrize("k1r", [True, False])
+def test_general_apply(n, h, N, dt, k1r):
+    """Shapes the vector kernels refuse run on K1r / K1g: both ops, and in place (Y == X);
+    once as the library picks (K1r while n is inside its tables), once on K1g alone."""
+    import contextlib
     c = gi.make_case("apply", n, h, N, dt, seed=31)
-    for op in (0, 1):
-        got = run_apply(op, c.U, c.X)
-        assert hh.last_launch_info()["variant"].startswith(f"{dt}_general"), hh.last_launch_info()
-        assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"K1g n={n} op{op}")
-    X = dev(c.X)
-    out = hh.hh_apply(0, dev(c.U), X, X)
-    assert out.data_ptr() == X.data_ptr()
-    assert_parity(out.cpu().numpy(), oracle.apply(0, c.U, c.X), dt, h, f"K1g n={n} alias")
+    with (contextlib.nullcontext() if k1r else k1g_only()):
+        for op in (0, 1):
+            got = run_apply(op, c.U, c.X)
+            assert is_general(dt), hh.last_launch_info()
+            if not k1r or n > 8192:
+                assert hh.last_launch_info()["variant"].startswith(f"{dt}_general")
+            elif n <= 4096:
+                assert hh.last_launch_info()["variant"].startswith(f"{dt}r_")
+            assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"K1r/K1g n={n} op{op}")
+        X = dev(c.X)
+        out = hh.hh_apply(0, dev(c.U), X, X)
+        assert out.data_ptr() == X.data_ptr()
+        assert_parity(out.cpu().numpy(), oracle.apply(0, c.U, c.X), dt, h, f"K1r/K1g n={n} alias")
 
 
 @pytest.mark.parametrize("n,h,N,dt", [(30, 5, 333, "f32"), (101, 9, 257, "f64"),
                                       (1023, 10, 300, "f32"), (9000, 5, 41, "f32")])
-def test_general_sym_signed_mahalanobis(n, h, N, dt):
+@pytest.mark.parametrize("k1r", [True, False])
+def test_general_sym_signed_mahalanobis(n, h, N, dt, k1r):
+    import contextlib
+    with (contextlib.nullcontext() if k1r else k1g_only()):
+        _general_sym_signed_mahalanobis(n, h, N, dt)
+
+
+def _general_sym_signed_mahalanobis(n, h, N, dt):
     c = gi.make_case("sym", n, h, N, dt, seed=32)
     got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
-    assert hh.last_launch_info()["variant"].startswith(f"{dt}_general")
+    assert is_general(dt)
     assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), dt, h, f"K1g sym n={n}")
     g = gi.rng(33, n)
     d = np.where(g.random(n) < 0.5, -1.0, 1.0).astype(c.X.dtype)
@@ -474,7 +510,7 @@ def test_general_sym_signed_mahalanobis(n, h, N, dt):
     m = gi.make_case("mahalanobis", n, h, 64, dt, seed=34, npairs=999)
     m.ia[:8] = m.ib[:8]
     dist = hh.hh_mahalanobis(dev(m.U), dev(m.d), dev(m.X), dev(m.ia), dev(m.ib)).cpu().numpy()
-    assert hh.last_launch_info()["variant"].startswith(f"{dt}_general")
+    assert is_general(dt)
     assert_parity(dist, oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib), dt, h, f"K1g pairs n={n}")
     assert np.all(dist[:8] == 0.0)
 
@@ -487,7 +523,7 @@ def test_general_misaligned_pointers_and_edges():
     Xo.copy_(dev(c.X))
     assert Xo.data_ptr() % 16 == 4
     got = hh.hh_apply(0, dev(c.U), Xo).cpu().numpy()
-    assert hh.last_launch_info()["variant"].startswith("f32_general")
+    assert is_general("f32")
     assert_parity(got, oracle.apply(0, c.U, c.X), "f32", 6, "K1g misaligned X")
     e = gi.make_case("apply", 30, 0, 3, "f32", seed=36)
     U0 = torch.empty(0, 30, device="cuda")
