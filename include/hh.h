@@ -42,6 +42,8 @@
  *     (n <= ~57000 f32 / ~28000 f64) and pointers aligned to the element run their
  *     reflector passes on scalar-access kernels (K1r / K1g; correct, 2-8x slower;
  *     hh_mahalanobis then uses its per-pair form and ignores the workspace).
+ *     Aligned fp32 shapes with 8192 < n <= 65536 also have the tensor-core program (AUTO
+ *     takes it from h = 2 on large batches when a workspace is passed).
  *   - HH_ERR_UNSUPPORTED: a pointer not aligned to its element, n beyond K1g's capacity,
  *     or HH_ALGO_WY forced on such a shape.
  *

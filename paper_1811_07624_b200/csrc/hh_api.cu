@@ -32,6 +32,13 @@ thread_local int t_algo = HH_ALGO_AUTO;
 // (profiles/r1/crossover_r1.txt); E = 2^28 for the large band, 2^25 for the middle one.
 int64_t wy_min_h(int64_t n, int64_t N) {
     if (n < 128) return int64_t(1) << 30;
+    if (n > 8192) {
+        // beyond the K1 tables the alternative is K1g (U from L2 per column: ~0.45 ms per
+        // reflector at E = 2^28, against ~0.6 ms flat for one block of K5 --
+        // n = 16384, N = 16384: h = 4 1.78 ms on K1g, h = 8 / 64 0.60 / 0.63 ms on K5)
+        const int64_t E = n * N;
+        return E >= (int64_t(1) << 27) ? 2 : E >= (int64_t(1) << 25) ? 3 : 12;
+    }
     // bands follow K1's variant table (measured at the top n of each band)
     const int i = n <= 128 ? 0 : n <= 256 ? 1 : n <= 512 ? 2 : n <= 1024 ? 3 : n <= 2048 ? 4
                 : n <= 4096 ? 5 : 6;
@@ -48,8 +55,11 @@ int64_t wy_min_h(int64_t n, int64_t N) {
     return 32;   // small problems: K5's fixed cost dominates below h = 32
 }
 
+// the block program is measured and tested up to this n (its own limit is 2^20)
+constexpr int64_t kWyMaxN = 65536;
+
 bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
-    if (dtype != HH_F32 || n > max_n(0) || !wy_supported(WY_APPLY_N, n, h, N)) return false;
+    if (dtype != HH_F32 || n > kWyMaxN || !wy_supported(WY_APPLY_N, n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
     return h >= wy_min_h(n, N);
@@ -61,6 +71,10 @@ bool use_wy(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
 // the middle band raised by the same margin), n > 512 against K2 (profiles/r1/crossover_r1.txt).
 int64_t wy_min_h_sym(int64_t n, int64_t N) {
     if (n < 128) return int64_t(1) << 30;
+    if (n > 8192) {   // K1g runs 2h reflectors per column there (see wy_min_h)
+        const int64_t E = n * N;
+        return E >= (int64_t(1) << 27) ? 1 : E >= (int64_t(1) << 25) ? 2 : 6;
+    }
     const int i = n <= 128 ? 0 : n <= 256 ? 1 : n <= 512 ? 2 : n <= 1024 ? 3 : n <= 2048 ? 4 : 5;
     // (n in (1024, 4096] re-swept in round 2, profiles/r2/xover_r2b.txt: 10 -> 12 and 8 -> 10 for
     // E >= 2^27, 15 -> 12 for n = 4096 in the middle band)
@@ -73,7 +87,7 @@ int64_t wy_min_h_sym(int64_t n, int64_t N) {
 }
 
 bool use_wy_sym(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
-    if (dtype != HH_F32 || n > max_n(0) || !wy_supported(WY_SYM, n, h, N)) return false;
+    if (dtype != HH_F32 || n > kWyMaxN || !wy_supported(WY_SYM, n, h, N)) return false;
     if (algo == HH_ALGO_WY) return true;
     if (algo == HH_ALGO_FUSED) return false;
     return h >= wy_min_h_sym(n, N);
@@ -83,7 +97,7 @@ bool use_wy_sym(hh_dtype dtype, int64_t n, int64_t h, int64_t N, int algo) {
 // kMaxPasses block passes, ...) is an error, never a silent switch to the SIMT kernel
 bool wy_forced_unsupported(int kind, hh_dtype dtype, int64_t n, int64_t h, int64_t N) {
     return t_algo == HH_ALGO_WY && h > 0 && N > 0 &&
-           (dtype != HH_F32 || n > max_n(0) || !wy_supported(kind, n, h, N));
+           (dtype != HH_F32 || n > kWyMaxN || !wy_supported(kind, n, h, N));
 }
 
 // the bucketed Mahalanobis path indexes pairs and points with int32
@@ -122,7 +136,10 @@ hh_status check_common(int64_t n, int64_t h, const void *U, int64_t N, hh_dtype 
     if (h > 0 && !U) return HH_ERR_INVALID_VALUE;
     if (h > (int64_t(1) << 30)) return HH_ERR_UNSUPPORTED;
     if (general_ok) {
-        if (!vector_shape(n, dtype) && !general_supported(n, dtype == HH_F32 ? 0 : 1))
+        // (n past K1g's shared memory: only the block program can serve it -- fp32, 16-byte
+        // strides, past the crossover and with a workspace; otherwise the launch is refused)
+        if (!vector_shape(n, dtype) && !general_supported(n, dtype == HH_F32 ? 0 : 1) &&
+            !(dtype == HH_F32 && n % 4 == 0 && n <= kWyMaxN))
             return HH_ERR_UNSUPPORTED;
         if (device_u && h > 0 && !aligned_elem(U, dtype)) return HH_ERR_UNSUPPORTED;
         return HH_OK;
@@ -368,11 +385,12 @@ static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const
     if (!aligned_elem(X, dtype) || !aligned_elem(Y, dtype) || (dside && !aligned_elem(dsign, dtype)))
         return HH_ERR_UNSUPPORTED;
     // K1g for the shapes and alignments the vector kernels do not take
-    const bool general = !vector_shape(n, dtype) || !aligned16(X) || !aligned16(Y) ||
-                         (h > 0 && !aligned16(U)) || (dside && !aligned16(dsign));
+    const bool al16 = (static_cast<size_t>(n) * elem(dtype)) % 16 == 0 && aligned16(X) &&
+                      aligned16(Y) && (h == 0 || aligned16(U)) && (!dside || aligned16(dsign));
+    const bool general = !al16 || n > max_n(dtype);   // (the fused path then runs K1r / K1g)
     if (wy_forced_unsupported(WY_APPLY_N, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
-    if (general && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
-    if (!general && h > 0 && use_wy(dtype, n, h, N, t_algo)) {
+    if (!al16 && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
+    if (al16 && h > 0 && use_wy(dtype, n, h, N, t_algo)) {
         WyPlan p = wy_plan(op == HH_OP_T ? WY_APPLY_T : WY_APPLY_N, n, h, N);
         p.qr = qr;
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
@@ -439,12 +457,13 @@ static hh_status sym_impl(int64_t n, int64_t h, const void *U, const void *lambd
     if (!aligned_elem(X, dtype) || !aligned_elem(Y, dtype) || !aligned_elem(lambda, dtype) ||
         (dsign && !aligned_elem(dsign, dtype)))
         return HH_ERR_UNSUPPORTED;
-    const bool general = !vector_shape(n, dtype) || !aligned16(X) || !aligned16(Y) ||
-                         !aligned16(lambda) || (h > 0 && !aligned16(U)) ||
-                         (dsign && !aligned16(dsign));
+    const bool al16 = (static_cast<size_t>(n) * elem(dtype)) % 16 == 0 && aligned16(X) &&
+                      aligned16(Y) && aligned16(lambda) && (h == 0 || aligned16(U)) &&
+                      (!dsign || aligned16(dsign));
+    const bool general = !al16 || n > max_n(dtype);
     if (wy_forced_unsupported(WY_SYM, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
-    if (general && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
-    if (!general && h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
+    if (!al16 && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
+    if (al16 && h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
         const WyPlan p = wy_plan(WY_SYM, n, h, N);
         if (workspace && workspace_bytes < p.bytes) return HH_ERR_WORKSPACE;
         if (workspace && !aligned16(workspace)) return HH_ERR_UNSUPPORTED;

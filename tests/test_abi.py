@@ -78,6 +78,8 @@ def test_workspace_query():
     (64, 512, 1 << 22, False),                      # n < 128: always K1
     (8192, 6, 32768, False), (8192, 7, 32768, True),
     (8192, 15, 4096, False), (8192, 16, 4096, True),
+    (16384, 1, 16384, False), (16384, 2, 16384, True),   # n > 8192: against K1g
+    (16384, 11, 128, False), (16384, 12, 128, True),
 ])
 def test_auto_crossover(n, h, N, wy):
     """HH_ALGO_AUTO's K1/K5 choice (hh_api.cu wy_min_h; thresholds from the same-box sweep in
@@ -111,7 +113,8 @@ def test_validation_before_launch():
     assert _apply(0, 30000, 1, A, A, A, 4, 1) == hh.HH_ERR_UNSUPPORTED          # ... fp64
     with hhpkg.algo(hh.HH_ALGO_WY):                                             # forced WY, K1g shape
         assert _apply(0, 18, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED
-        assert _apply(0, 8196, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED
+        assert _apply(0, 70000, 1, A, A, A, 4, 0) == hh.HH_ERR_UNSUPPORTED      # beyond the block program
+        assert _apply(0, 8196, 1, A, A, A, 4, 0) == hh.HH_ERR_WORKSPACE         # n > 8192: WY, needs scratch
     # empty batches are successful no-ops (no launch), h = 0 needs no U
     assert _apply(0, 16, 1, A, None, None, 0, 0) == hh.HH_OK
     assert _apply(1, 16, 0, None, None, None, 0, 0) == hh.HH_OK

@@ -96,6 +96,24 @@ def test_wy_parity(n, h, N, op):
     assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"WY n{n} h{h} N{N} op{op}")
 
 
+@pytest.mark.parametrize("n,h,N", [(8196, 40, 300), (12288, 24, 260), (16384, 64, 300),
+                                   (32768, 300, 140), (65536, 33, 130)])
+def test_wy_large_n(n, h, N):
+    """n beyond the fused kernels' tables (8192): the block program takes aligned shapes up to
+    n = 65536 -- apply (both ops, AUTO picks it past the crossover) and the symmetric form."""
+    c = gi.make_case("sym", n, h, N, "f32", seed=29)
+    for op in (0, 1):
+        got = wy(op, c.U, c.X)
+        assert hh.last_launch_info()["variant"].startswith("wy_"), hh.last_launch_info()
+        assert_parity(got, oracle.apply(op, c.U, c.X), "f32", h, f"WY n{n} h{h} op{op}")
+    got = hh.hh_apply(0, dev(c.U), dev(c.X)).cpu().numpy()      # AUTO
+    assert_parity(got, oracle.apply(0, c.U, c.X), "f32", h, f"auto n{n} h{h}")
+    with hh.algo(hh.HH_ALGO_WY):
+        got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+    assert hh.last_launch_info()["variant"].startswith("wy_sym"), hh.last_launch_info()
+    assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), "f32", h, f"WY sym n{n} h{h}")
+
+
 def test_wy_alias_zero_slots_and_round_trip():
     c = gi.make_case("apply", 1024, 96, 400, "f32", seed=23, zero_slots=(0, 5, 95))
     U, X = dev(c.U), dev(c.X)
