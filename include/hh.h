@@ -42,6 +42,10 @@
  *     (n <= ~57000 f32 / ~28000 f64) and pointers aligned to the element run their
  *     reflector passes on scalar-access kernels (K1r / K1g; correct, 2-8x slower;
  *     hh_mahalanobis then uses its per-pair form and ignores the workspace).
+ *     With the workspace hh_workspace_bytes() reports for such a shape (non-zero from the
+ *     measured crossover in h), the call instead copies the operands to a 16-byte pitch,
+ *     runs the fast kernels on the copy and copies the result back (two extra passes
+ *     over X, flat in h).
  *     Aligned fp32 shapes with 8192 < n <= 65536 also have the tensor-core program (AUTO
  *     takes it from h = 2 on large batches when a workspace is passed).
  *   - HH_ERR_UNSUPPORTED: a pointer not aligned to its element, n beyond K1g's capacity,

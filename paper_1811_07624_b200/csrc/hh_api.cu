@@ -127,6 +127,55 @@ bool aligned_elem(const void *p, hh_dtype dtype) {
     return reinterpret_cast<uintptr_t>(p) % elem(dtype) == 0;
 }
 
+// ---- the padded detour for column strides that are not a multiple of 16 bytes
+// With a workspace, the columns (and U, lambda, D) are copied to a 16-byte pitch n4 (pads zero,
+// so every dot product and update is unchanged: Eq. 2 on the zero-extended vectors), the call
+// runs on the copy with the fast kernels (K1 family or the block program K5), and the result is
+// copied back: two extra passes over X against K1r's / K1g's cost per reflector (policy and
+// measurements in use_padded below).
+thread_local int t_pad = -1;   // test hook (hh_debug_general_pad): -1 policy, 0 never, 1 whenever possible
+bool stride_unaligned(int64_t n, hh_dtype dtype) {
+    return (static_cast<size_t>(n) * elem(dtype)) % 16 != 0;
+}
+int64_t padded_n(int64_t n, hh_dtype dtype) {
+    const int64_t q = 16 / static_cast<int64_t>(elem(dtype));
+    return (n + q - 1) / q * q;
+}
+bool k1r_capable(int64_t n, int64_t h, hh_dtype dtype) {
+    return n <= max_n(dtype) &&
+           static_cast<size_t>(h) * n * elem(dtype) + 1024 <= static_cast<size_t>(device_attr().max_smem_optin);
+}
+bool use_padded(int64_t n, int64_t h, hh_dtype dtype, bool sym) {
+    if (!stride_unaligned(n, dtype) || h < 1 || t_pad == 0) return false;
+    const int64_t n4 = padded_n(n, dtype);
+    if (n4 > max_n(dtype) && !(dtype == HH_F32 && n4 <= kWyMaxN)) return false;
+    if (t_pad == 1 || t_algo == HH_ALGO_WY) return true;   // (a forced K5 runs on the padded copy)
+    // same-box sweep at 1 GiB (tools/pad_time.py, profiles/r2/pad_time_r2.jsonl): the detour costs
+    // ~0.87 ms of copies + the aligned call; K1r grows by 0.05-0.06 ms per reflector --
+    // n = 1023: h = 16 1.20 (K1r) vs 1.35, h = 24 1.69 vs 1.48; n = 101: h = 8 0.54 vs 0.61,
+    // h = 12 0.74 vs 0.65; sym n = 1023: h = 8 1.28 vs 1.51, h = 12 1.77 vs 1.51; where only K1g
+    // would run (n = 9001): h = 2 0.95 vs 1.43, h = 4 1.56 vs 1.43, sym h = 2 1.69 vs 1.50
+    if (!k1r_capable(n, h, dtype)) return h >= (sym ? 2 : 4);
+    if (n <= 256) return h >= (sym ? 6 : 10);
+    return h >= (sym ? 10 : 19);
+}
+// scratch of the detour itself (U, X and up to two n-vectors at the padded pitch)
+struct PadPlan {
+    int64_t n4 = 0;
+    size_t off_u = 0, off_x = 0, off_v0 = 0, off_v1 = 0, off_inner = 0;
+};
+PadPlan pad_plan(int64_t n, int64_t h, int64_t N, hh_dtype dtype) {
+    PadPlan p;
+    p.n4 = padded_n(n, dtype);
+    const size_t s = elem(dtype);
+    p.off_u = 0;
+    p.off_x = round256(static_cast<size_t>(h) * p.n4 * s);
+    p.off_v0 = p.off_x + round256(static_cast<size_t>(N) * p.n4 * s);
+    p.off_v1 = p.off_v0 + round256(static_cast<size_t>(p.n4) * s);
+    p.off_inner = p.off_v1 + round256(static_cast<size_t>(p.n4) * s);
+    return p;
+}
+
 // shape checks shared by the column calls; returns HH_OK or the error.  general_ok: the call
 // has the K1g path, so shapes / alignments outside the vector kernels' are accepted when K1g
 // takes them (the call itself then checks element alignment of its operands).
@@ -270,6 +319,11 @@ int hh_debug_k1_tmem(int on) { return k1_set_tmem(on); }
 int hh_debug_k1_blocked(int on) { return k1_set_blocked(on); }
 int hh_debug_k7_rows(int rw) { return k7_set_rows(rw); }
 int hh_debug_general_scalar(int on) { return general_set_scalar(on); }
+int hh_debug_general_pad(int on) {
+    const int prev = t_pad;
+    t_pad = on;
+    return prev;
+}
 int hh_debug_mahal_fork(int on) {
     const int prev = t_mahal_fork;
     t_mahal_fork = on;
@@ -322,15 +376,36 @@ hh_status hh_workspace_bytes(hh_call call, int64_t n, int64_t h, int64_t N_or_M,
         return HH_ERR_INVALID_VALUE;
     switch (call) {
         case HH_CALL_APPLY:
-            *bytes = use_wy(dtype, n, h, N_or_M, t_algo) ? wy_plan(WY_APPLY_N, n, h, N_or_M).bytes
-                                                        : 0;
+        case HH_CALL_SYM: {
+            const bool sym = call == HH_CALL_SYM;
+            if (use_padded(n, h, dtype, sym)) {
+                // unaligned column stride: the padded copy + what the call needs on it
+                const PadPlan pp = pad_plan(n, h, N_or_M, dtype);
+                size_t inner = 0;
+                hh_workspace_bytes(call, pp.n4, h, N_or_M, 0, dtype, &inner);
+                *bytes = pp.off_inner + inner;
+                return HH_OK;
+            }
+            if (stride_unaligned(n, dtype)) {   // K1r / K1g: no scratch
+                *bytes = 0;
+                return HH_OK;
+            }
+            if (sym)
+                *bytes = use_wy_sym(dtype, n, h, N_or_M, t_algo) ? wy_plan(WY_SYM, n, h, N_or_M).bytes : 0;
+            else
+                *bytes = use_wy(dtype, n, h, N_or_M, t_algo) ? wy_plan(WY_APPLY_N, n, h, N_or_M).bytes : 0;
             return HH_OK;
-        case HH_CALL_SYM:
-            *bytes = use_wy_sym(dtype, n, h, N_or_M, t_algo) ? wy_plan(WY_SYM, n, h, N_or_M).bytes
-                                                            : 0;
-            return HH_OK;
+        }
         case HH_CALL_MAHALANOBIS:
             if (npairs >= kMaxPairs || N_or_M >= kMaxPairs) return HH_ERR_UNSUPPORTED;
+            if (stride_unaligned(n, dtype) && t_pad != 0 && padded_n(n, dtype) <= max_n(dtype)) {
+                // the padded copies of U, P, d, then the aligned call's scratch
+                const PadPlan pp = pad_plan(n, h, N_or_M, dtype);
+                *bytes = pp.off_inner +
+                         round256(static_cast<size_t>(pp.n4) * static_cast<size_t>(N_or_M) * elem(dtype)) +
+                         bucket_ws_bytes(N_or_M, npairs);
+                return HH_OK;
+            }
             *bytes = round256(static_cast<size_t>(n) * static_cast<size_t>(N_or_M) * elem(dtype)) +
                      bucket_ws_bytes(N_or_M, npairs);
             return HH_OK;
@@ -388,6 +463,27 @@ static hh_status apply_impl(hh_op op, int64_t n, int64_t h, const void *U, const
     const bool al16 = (static_cast<size_t>(n) * elem(dtype)) % 16 == 0 && aligned16(X) &&
                       aligned16(Y) && (h == 0 || aligned16(U)) && (!dside || aligned16(dsign));
     const bool general = !al16 || n > max_n(dtype);   // (the fused path then runs K1r / K1g)
+    if (workspace && use_padded(n, h, dtype, false)) {
+        if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+        const PadPlan pp = pad_plan(n, h, N, dtype);
+        size_t inner = 0;
+        hh_workspace_bytes(HH_CALL_APPLY, pp.n4, h, N, 0, dtype, &inner);
+        if (workspace_bytes < pp.off_inner + inner) return HH_ERR_WORKSPACE;
+        char *w = static_cast<char *>(workspace);
+        const int dt = dtype == HH_F32 ? 0 : 1;
+        cudaError_t e = launch_repitch(U, n, w + pp.off_u, pp.n4, h, n, pp.n4, 0.0, dt, stream);
+        if (e == cudaSuccess) e = launch_repitch(X, n, w + pp.off_x, pp.n4, N, n, pp.n4, 0.0, dt, stream);
+        if (e == cudaSuccess && dside)
+            e = launch_repitch(dsign, n, w + pp.off_v0, pp.n4, 1, n, pp.n4, 1.0, dt, stream);
+        if (e != cudaSuccess) return map_err(e);
+        st = apply_impl(op, pp.n4, h, w + pp.off_u, w + pp.off_x, w + pp.off_x, N, dtype,
+                        inner ? w + pp.off_inner : nullptr, inner, stream,
+                        dside ? w + pp.off_v0 : nullptr, dside, qr);
+        if (st != HH_OK) return st;
+        e = launch_repitch(w + pp.off_x, pp.n4, Y, n, N, n, n, 0.0, dt, stream);
+        if (t_has_last) t_last.launches += 3 + (dside ? 1 : 0);
+        return map_err(e);
+    }
     if (wy_forced_unsupported(WY_APPLY_N, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
     if (!al16 && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
     if (al16 && h > 0 && use_wy(dtype, n, h, N, t_algo)) {
@@ -461,6 +557,29 @@ static hh_status sym_impl(int64_t n, int64_t h, const void *U, const void *lambd
                       aligned16(Y) && aligned16(lambda) && (h == 0 || aligned16(U)) &&
                       (!dsign || aligned16(dsign));
     const bool general = !al16 || n > max_n(dtype);
+    if (workspace && use_padded(n, h, dtype, true)) {
+        if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+        const PadPlan pp = pad_plan(n, h, N, dtype);
+        size_t inner = 0;
+        hh_workspace_bytes(HH_CALL_SYM, pp.n4, h, N, 0, dtype, &inner);
+        if (workspace_bytes < pp.off_inner + inner) return HH_ERR_WORKSPACE;
+        char *w = static_cast<char *>(workspace);
+        const int dt = dtype == HH_F32 ? 0 : 1;
+        cudaError_t e = launch_repitch(U, n, w + pp.off_u, pp.n4, h, n, pp.n4, 0.0, dt, stream);
+        if (e == cudaSuccess) e = launch_repitch(X, n, w + pp.off_x, pp.n4, N, n, pp.n4, 0.0, dt, stream);
+        if (e == cudaSuccess)
+            e = launch_repitch(lambda, n, w + pp.off_v0, pp.n4, 1, n, pp.n4, 0.0, dt, stream);
+        if (e == cudaSuccess && dsign)
+            e = launch_repitch(dsign, n, w + pp.off_v1, pp.n4, 1, n, pp.n4, 1.0, dt, stream);
+        if (e != cudaSuccess) return map_err(e);
+        st = sym_impl(pp.n4, h, w + pp.off_u, w + pp.off_v0, w + pp.off_x, w + pp.off_x, N, dtype,
+                      inner ? w + pp.off_inner : nullptr, inner, stream,
+                      dsign ? w + pp.off_v1 : nullptr);
+        if (st != HH_OK) return st;
+        e = launch_repitch(w + pp.off_x, pp.n4, Y, n, N, n, n, 0.0, dt, stream);
+        if (t_has_last) t_last.launches += 4 + (dsign ? 1 : 0);
+        return map_err(e);
+    }
     if (wy_forced_unsupported(WY_SYM, dtype, n, h, N)) return HH_ERR_UNSUPPORTED;
     if (!al16 && t_algo == HH_ALGO_WY && h > 0) return HH_ERR_UNSUPPORTED;
     if (al16 && h > 0 && use_wy_sym(dtype, n, h, N, t_algo)) {
@@ -529,6 +648,24 @@ hh_status hh_mahalanobis(int64_t n, int64_t h, const void *U, const void *d, con
                          (h > 0 && !aligned16(U));
     size_t need = 0;
     hh_workspace_bytes(HH_CALL_MAHALANOBIS, n, h, M, npairs, dtype, &need);
+    if (workspace && stride_unaligned(n, dtype) && t_pad != 0 && padded_n(n, dtype) <= max_n(dtype)) {
+        // unaligned stride: transform-once on a copy of the points at a 16-byte pitch (pads
+        // zero: they stay zero through Q^T and add nothing to the distance)
+        if (workspace_bytes < need) return HH_ERR_WORKSPACE;
+        if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;
+        const PadPlan pp = pad_plan(n, h, M, dtype);
+        char *w = static_cast<char *>(workspace);
+        const int dt = dtype == HH_F32 ? 0 : 1;
+        cudaError_t e = cudaSuccess;
+        if (h > 0) e = launch_repitch(U, n, w + pp.off_u, pp.n4, h, n, pp.n4, 0.0, dt, stream);
+        if (e == cudaSuccess) e = launch_repitch(P, n, w + pp.off_x, pp.n4, M, n, pp.n4, 0.0, dt, stream);
+        if (e == cudaSuccess) e = launch_repitch(d, n, w + pp.off_v0, pp.n4, 1, n, pp.n4, 0.0, dt, stream);
+        if (e != cudaSuccess) return map_err(e);
+        st = hh_mahalanobis(pp.n4, h, h > 0 ? w + pp.off_u : nullptr, w + pp.off_v0, w + pp.off_x, M,
+                            ia, ib, npairs, dist, dtype, w + pp.off_inner, need - pp.off_inner, stream);
+        if (st == HH_OK && t_has_last) t_last.launches += 2 + (h > 0 ? 1 : 0);
+        return st;
+    }
     if (workspace && !general) {
         if (workspace_bytes < need) return HH_ERR_WORKSPACE;
         if (!aligned16(workspace)) return HH_ERR_UNSUPPORTED;

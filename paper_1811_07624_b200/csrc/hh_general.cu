@@ -188,6 +188,27 @@ cudaError_t launch_cg(const FusedArgs &a, int nt, size_t smem, int sm_count, int
     return e;
 }
 
+// Row re-pitch: dst[r][e] = e < ncopy ? src[r][e] : fill for e < nwrite (rows of ld_src / ld_dst
+// elements).  Pads the columns of an unaligned problem to a 16-byte pitch (and back), so that
+// the fast kernels can run on the padded copy.  A warp per row, lanes on consecutive elements
+// (coalesced on both sides).
+template <typename T>
+__global__ void __launch_bounds__(256) repitch_rows_kernel(const T *__restrict__ src, int64_t ld_src,
+                                                           T *__restrict__ dst, int64_t ld_dst,
+                                                           int64_t rows, int ncopy, int nwrite, T fill) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = w0; r < rows; r += nw) {
+        const T *s = src + r * ld_src;
+        T *d = dst + r * ld_dst;
+        int e = lane;
+#pragma unroll 4
+        for (; e < ncopy; e += 32) d[e] = __ldg(s + e);
+        for (; e < nwrite; e += 32) d[e] = fill;
+    }
+}
+
 size_t general_smem(int64_t n, int s, int cg, int nt) {
     return static_cast<size_t>(cg) * n * s + static_cast<size_t>(2) * (nt / 32) * cg * s;
 }
@@ -195,6 +216,23 @@ size_t general_smem(int64_t n, int s, int cg, int nt) {
 int general_threads(int64_t n) { return n <= 64 ? 32 : n <= 256 ? 64 : n <= 1024 ? 128 : 256; }
 
 }  // namespace
+
+cudaError_t launch_repitch(const void *src, int64_t ld_src, void *dst, int64_t ld_dst, int64_t rows,
+                           int64_t ncopy, int64_t nwrite, double fill, int dtype, cudaStream_t stream) {
+    if (rows <= 0) return cudaSuccess;
+    const int64_t want = (rows + 7) / 8;   // 8 warps per CTA
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(want, static_cast<int64_t>(device_attr().sm_count) * 16)));
+    if (dtype == 0)
+        repitch_rows_kernel<float><<<grid, 256, 0, stream>>>(
+            static_cast<const float *>(src), ld_src, static_cast<float *>(dst), ld_dst, rows,
+            static_cast<int>(ncopy), static_cast<int>(nwrite), static_cast<float>(fill));
+    else
+        repitch_rows_kernel<double><<<grid, 256, 0, stream>>>(
+            static_cast<const double *>(src), ld_src, static_cast<double *>(dst), ld_dst, rows,
+            static_cast<int>(ncopy), static_cast<int>(nwrite), fill);
+    return cudaGetLastError();
+}
 
 bool general_supported(int64_t n, int dtype) {
     const int s = dtype == 0 ? 4 : 8;

@@ -87,6 +87,10 @@ cudaError_t launch_general(const FusedArgs &a, int dtype, cudaStream_t stream, L
 // shapes while n is within the K1 tables and U fits in shared memory; cudaErrorNotSupported
 // otherwise (launch_general tries it first)
 cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info);
+// rows of ld_src elements -> rows of ld_dst elements: the first ncopy copied, then `fill` up to
+// nwrite (pads an unaligned problem to a 16-byte pitch, and strips the pad again)
+cudaError_t launch_repitch(const void *src, int64_t ld_src, void *dst, int64_t ld_dst, int64_t rows,
+                           int64_t ncopy, int64_t nwrite, double fill, int dtype, cudaStream_t stream);
 int general_set_scalar(int on);   // A/B / test hook (hh_debug_general_scalar): 1 K1r first (default), 0 K1g only
 
 // Device attributes (cached per device, thread-safe).

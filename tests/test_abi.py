@@ -90,6 +90,27 @@ def test_auto_crossover(n, h, N, wy):
         hhpkg.hh_workspace_bytes(hh.HH_CALL_APPLY, 0, 1, 1, 0, 0)
 
 
+def test_unaligned_stride_workspace_policy():
+    """Column strides that are not a multiple of 16 bytes: no scratch while K1r / K1g serve the
+    call, the padded copy (U, X, two n-vectors at the padded pitch) plus the aligned call's own
+    scratch from the measured crossover (hh_api.cu use_padded)."""
+    q = lambda call, n, h, N, dt=0: hhpkg.hh_workspace_bytes(call, n, h, N, 0, dt)
+    assert q(hh.HH_CALL_APPLY, 1023, 18, 262144) == 0
+    pad = q(hh.HH_CALL_APPLY, 1023, 19, 262144)
+    assert pad >= (262144 + 19 + 2) * 1024 * 4            # copies at pitch 1024
+    assert pad >= (262144 + 19 + 2) * 1024 * 4 + q(hh.HH_CALL_APPLY, 1024, 19, 262144)
+    assert q(hh.HH_CALL_APPLY, 101, 9, 1 << 20) == 0 and q(hh.HH_CALL_APPLY, 101, 10, 1 << 20) > 0
+    assert q(hh.HH_CALL_SYM, 1023, 9, 4096) == 0 and q(hh.HH_CALL_SYM, 1023, 10, 4096) > 0
+    assert q(hh.HH_CALL_APPLY, 9001, 3, 4096) == 0 and q(hh.HH_CALL_APPLY, 9001, 4, 4096) > 0
+    assert q(hh.HH_CALL_APPLY, 4095, 14, 4096) == 0 and q(hh.HH_CALL_APPLY, 4095, 15, 4096) > 0  # U past K1r
+    assert q(hh.HH_CALL_APPLY, 1023, 19, 4096, 1) > 0     # fp64: pitch of 2
+    assert q(hh.HH_CALL_APPLY, 1024, 10, 262144) == 0     # aligned shapes unchanged
+    # Mahalanobis: transform-once on the padded copy of the points
+    m_al = hhpkg.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, 512, 9, 65536, 1 << 21, 0)
+    m_un = hhpkg.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, 511, 9, 65536, 1 << 21, 0)
+    assert m_un >= m_al + 65536 * 512 * 4
+
+
 def _apply(op, n, h, U, X, Y, N, dt):
     return hh.lib().hh_apply(op, n, h, U, X, Y, N, dt, None, 0, None)
 

@@ -185,9 +185,9 @@ def test_errors_write_nothing():
     assert torch.all(Y == 7.0)
     with pytest.raises(ValueError):
         hh.hh_apply(0, U.cpu(), X.cpu())           # CPU tensors: no fallback
-    Xo = torch.randn(10, 1022, device="cuda")
+    Xo = torch.randn(10, 1023, device="cuda", dtype=torch.float64)
     with pytest.raises(hh.HHError), hh.algo(hh.HH_ALGO_WY):
-        hh.hh_apply(0, torch.randn(40, 1022, device="cuda"), Xo)  # forced WY, n*4 % 16 != 0
+        hh.hh_apply(0, torch.randn(40, 1023, device="cuda", dtype=torch.float64), Xo)  # forced WY, fp64
     P = torch.randn(10, 64, device="cuda")
     ia = torch.zeros(5, dtype=torch.int32, device="cuda")
     # the binding re-allocates a too-small workspace, so call the ABI directly
@@ -452,6 +452,21 @@ def is_general(dt):
     return v.startswith(f"{dt}r_") or v.startswith(f"{dt}_general")
 
 
+class padded:
+    """Test hook: 1 = take the padded detour whenever the stride is unaligned, 0 = never."""
+
+    def __init__(self, on):
+        self.on = on
+
+    def __enter__(self):
+        self.prev = hh.hh.lib().hh_debug_general_pad(self.on)
+        hh.hh.clear_workspace_cache()       # the knob sizes the workspace
+
+    def __exit__(self, *exc):
+        hh.hh.lib().hh_debug_general_pad(self.prev)
+        hh.hh.clear_workspace_cache()
+
+
 class k1g_only:
     """Test hook: keep K1r off so that K1g also serves the shapes K1r would take."""
 
@@ -469,7 +484,7 @@ def test_general_apply(n, h, N, dt, k1r):
     once as the library picks (K1r while n is inside its tables), once on K1g alone."""
     import contextlib
     c = gi.make_case("apply", n, h, N, dt, seed=31)
-    with (contextlib.nullcontext() if k1r else k1g_only()):
+    with (contextlib.nullcontext() if k1r else k1g_only()), padded(0):
         for op in (0, 1):
             got = run_apply(op, c.U, c.X)
             assert is_general(dt), hh.last_launch_info()
@@ -489,7 +504,7 @@ def test_general_apply(n, h, N, dt, k1r):
 @pytest.mark.parametrize("k1r", [True, False])
 def test_general_sym_signed_mahalanobis(n, h, N, dt, k1r):
     import contextlib
-    with (contextlib.nullcontext() if k1r else k1g_only()):
+    with (contextlib.nullcontext() if k1r else k1g_only()), padded(0):
         _general_sym_signed_mahalanobis(n, h, N, dt)
 
 
@@ -536,3 +551,56 @@ def test_general_host_path():
     c = gi.make_case("apply", 1022, 8, 500, "f32", seed=38)
     out = hh.hh_apply_host(0, torch.from_numpy(c.U), torch.from_numpy(c.X)).numpy()
     assert_parity(out, oracle.apply(0, c.U, c.X), "f32", 8, "K1g host")
+
+
+# ------------------------------------------------------------------ the padded detour
+@pytest.mark.parametrize("n,h,N,dt", [(30, 5, 333, "f32"), (101, 9, 257, "f64"), (1023, 10, 700, "f32"),
+                                      (1021, 40, 900, "f32"), (2047, 70, 300, "f32"),
+                                      (4095, 300, 140, "f32"), (9001, 20, 64, "f32"),
+                                      (509, 33, 500, "f64"), (8190, 12, 70, "f32")])
+def test_padded_detour(n, h, N, dt):
+    """Unaligned column strides through the padded copy (forced by the hook so that small h
+    takes it too): apply (both ops, alias), D on both sides, the symmetric forms -- and the
+    policy's own choice at these shapes."""
+    c = gi.make_case("sym", n, h, N, dt, seed=41)
+    d = np.where(gi.rng(42, n).random(n) < 0.5, -1.0, 1.0).astype(c.X.dtype)
+    for mode in (1, -1):
+        with padded(mode):
+            for op in (0, 1):
+                got = run_apply(op, c.U, c.X)
+                if mode == 1:
+                    assert not is_general(dt), hh.last_launch_info()
+                assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"padded n={n} op{op}")
+            got = hh.hh_sym_apply(dev(c.U), dev(c.lam), dev(c.X)).cpu().numpy()
+            assert_parity(got, oracle.sym_apply(c.U, c.lam, c.X), dt, h, f"padded sym n={n}")
+    with padded(1):
+        X = dev(c.X)
+        out = hh.hh_apply(1, dev(c.U), X, X)
+        assert_parity(out.cpu().numpy(), oracle.apply(1, c.U, c.X), dt, h, f"padded alias n={n}")
+        for side in (0, 1):
+            got = hh.hh_apply_signed(0, side, dev(c.U), dev(d), dev(c.X)).cpu().numpy()
+            assert_parity(got, oracle.apply_signed(0, side, c.U, d, c.X), dt, h, f"padded D n={n}")
+        got = hh.hh_sym_apply_signed(dev(c.U), dev(d), dev(c.lam), dev(c.X)).cpu().numpy()
+        assert_parity(got, oracle.sym_apply_signed(c.U, d, c.lam, c.X), dt, h, f"padded sym D n={n}")
+        if dt == "f32" and n >= 32:
+            with hh.algo(hh.HH_ALGO_WY):                 # a forced block program runs on the copy
+                got = run_apply(0, c.U, c.X)
+                assert hh.last_launch_info()["variant"].startswith("wy_"), hh.last_launch_info()
+            assert_parity(got, oracle.apply(0, c.U, c.X), dt, h, f"padded WY n={n}")
+
+
+@pytest.mark.parametrize("n,h,M,npairs,dt", [(30, 5, 64, 999, "f32"), (101, 9, 300, 5000, "f64"),
+                                             (511, 9, 2000, 30000, "f32"), (1023, 0, 100, 777, "f32")])
+def test_padded_mahalanobis(n, h, M, npairs, dt):
+    """Unaligned point stride with a workspace: transform-once + bucketed gather on the padded
+    copy (a = b stays exactly 0); without the detour the per-pair form on K1r / K1g."""
+    m = gi.make_case("mahalanobis", n, h, M, dt, seed=43, npairs=npairs)
+    m.ia[:8] = m.ib[:8]
+    ref = oracle.mahalanobis(m.U, m.d, m.X, m.ia, m.ib)
+    U = dev(m.U) if h else torch.empty(0, n, device="cuda", dtype=TDT[dt])
+    for mode in (-1, 0):
+        with padded(mode):
+            dist = hh.hh_mahalanobis(U, dev(m.d), dev(m.X), dev(m.ia), dev(m.ib)).cpu().numpy()
+            assert is_general(dt) == (mode == 0), hh.last_launch_info()
+            assert_parity(dist, ref, dt, h, f"padded pairs n={n} mode={mode}")
+            assert np.all(dist[:8] == 0.0)
