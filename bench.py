@@ -2,7 +2,7 @@
 """Benchmark of the Householder-product apply hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {hh,reference}]
-                    [--workload C2|C1|C3|C4|C5h12|C5h64|C5h256|C5h1024|KNN|CONG|QR4095|SHF] [--op N|T]
+                    [--workload C2|C1|C3|C4|C5h12|C5h64|C5h256|C5h1024|KNN|CONG|QR4095|SHF|U<n>H<h>] [--op N|T]
 
 Default workload = BASELINE.json configs[1] (the metric's config): Y = H1...Hh X,
 fp32, n=1024, h=10, N=262144 columns (1 GiB in, 1 GiB out; larger than the 126 MB
@@ -77,6 +77,9 @@ def workload_case(name: str, N_override=None):
         c.U = gi.qr_reflectors(gi.rng(5, h, 9), h, c.n, "f32")
         c.h, c.call, c.name = h, "apply_qr", f"QR{h}"
         return c
+    if name.startswith("U") and "H" in name:   # context: an unaligned column stride, e.g. U1023H10
+        n, h = (int(v) for v in name[1:].split("H"))   # 1 GiB of X; K1r / K1g / the padded detour
+        return gi.make_case("apply", n, h, N_override or (1 << 28) // n, "f32", seed=70)
     raise SystemExit(f"unknown workload {name}")
 
 
