@@ -319,6 +319,7 @@ int hh_debug_k1_tmem(int on) { return k1_set_tmem(on); }
 int hh_debug_k1_blocked(int on) { return k1_set_blocked(on); }
 int hh_debug_k7_rows(int rw) { return k7_set_rows(rw); }
 int hh_debug_general_scalar(int on) { return general_set_scalar(on); }
+int hh_debug_k1r_tmem(int on) { return k1r_set_tmem(on); }
 int hh_debug_general_pad(int on) {
     const int prev = t_pad;
     t_pad = on;

@@ -245,12 +245,13 @@ __device__ __forceinline__ void tmem_dealloc_n(uint32_t taddr, uint32_t ncols) {
 template <typename T, int TPC, int CH, int C, int NT, bool FULL, bool UTM = false, int KB = 1,
           bool SC = false>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const FusedArgs a) {
-    static_assert(!UTM || (!SC && std::is_same<T, float>::value && 128 % TPC == 0 && TPC >= 32),
+    static_assert(!UTM || (std::is_same<T, float>::value && 128 % TPC == 0 && TPC >= 32),
                   "TMEM reflectors: fp32, TPC in {32, 64, 128}");
+    static_assert(!(UTM && SC) || (CH % 8 == 0 && KB == 1), "scalar TMEM form: CH in {8, 16, 32}, unblocked");
     static_assert(KB == 1 || (UTM && (KB * C == 4 || KB * C == 8 || KB * C == 16)),
                   "blocked reflectors: TMEM form, KB * C in {4, 8, 16}");
     constexpr int KV = KB > 1 ? KB * C : C;   // values per cross-lane reduction
-    constexpr int UCOLS = 4 * CH;   // TMEM columns per reflector (UTM)
+    constexpr int UCOLS = SC ? CH : 4 * CH;   // TMEM columns per reflector (UTM)
     using V = typename std::conditional<SC, T, typename VT<T>::V>::type;
     constexpr int E = SC ? 1 : VT<T>::E;
     constexpr int UT = TPC > 32 ? TPC : 32;  // threads per scheduling unit
@@ -355,6 +356,23 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         if (warp < 4) {
             // warp q fills lane quarter q: lane 32 q + l holds the chunks of gt = (32 q + l) mod TPC
             const int g2 = (warp * 32 + lane) % TPC;
+            if constexpr (SC) {
+                // scalar ownership: column i CH + k of lane gt holds element gt + TPC k of u_i
+                const T *Us1 = reinterpret_cast<const T *>(a.U);
+                for (int i = 0; i < h; ++i) {
+#pragma unroll
+                    for (int k = 0; k < CH; k += 8) {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int64_t r = g2 + static_cast<int64_t>(TPC) * (k + e);
+                            w[e] = r < n ? __float_as_uint(__ldg(Us1 + static_cast<int64_t>(i) * n + r)) : 0u;
+                        }
+                        tc::tmem_st8(tlane + static_cast<uint32_t>(i * UCOLS + k),
+                                     make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]));
+                    }
+                }
+            } else
             for (int i = 0; i < h; ++i) {
 #pragma unroll
                 for (int k = 0; k < CH; k += 2) {
@@ -424,8 +442,10 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
 
     // prologue: U (resident, or the first two chunk visits) and each unit's first tile
     if constexpr (SC) {   // resident U copied by the CTA's threads (no 16-byte granularity)
-        for (int64_t i = tid; i < static_cast<int64_t>(h) * nv; i += NT) Us[i] = __ldg(Ug + i);
-        __syncthreads();
+        if constexpr (!UTM) {
+            for (int64_t i = tid; i < static_cast<int64_t>(h) * nv; i += NT) Us[i] = __ldg(Ug + i);
+            __syncthreads();
+        }
     } else
     if (!UTM && tid == 0 && h > 0) {
         if (nc == 1) {
@@ -451,16 +471,19 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         // multi-warp groups: keep the u chunk in registers across the cross-warp
         // reduction (a shared-memory store + barrier the compiler cannot see through),
         // so u is read from shared memory once per reflector, not twice
-        constexpr bool kKeepU = (TPC > 32 || UTM) && !SC;
+        constexpr bool kKeepU = UTM || (TPC > 32 && !SC);
         V uk[kKeepU ? CH : 1];
         if constexpr (UTM) {
             uint32_t r[UCOLS];
             tmem_ld_cols<UCOLS>(tlane + static_cast<uint32_t>(ui * UCOLS), r);
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if constexpr (std::is_same<T, float>::value)
+                if constexpr (SC) {
+                    if constexpr (std::is_same<T, float>::value) uk[k] = __uint_as_float(r[k]);
+                } else if constexpr (std::is_same<T, float>::value) {
                     uk[k] = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
                                         __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+                }
             }
         } else if constexpr (kKeepU) {
 #pragma unroll
@@ -486,7 +509,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
                 if (valid_k(k)) {
-                    const float uk0 = ub[gt + TPC * k];
+                    const float uk0 = uget(k);
                     ffma2(q0[k & 3], q1[k & 3], uk0, uk0, x[0][k], x[1][k], q0[k & 3], q1[k & 3]);
                 }
             }
@@ -500,7 +523,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 T q[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
                 for (int k = 0; k < CH; ++k) {
-                    if (valid_k(k)) vfma(q[k & 3], ub[gt + TPC * k], x[c][k]);
+                    if (valid_k(k)) vfma(q[k & 3], uget(k), x[c][k]);
                 }
                 p[c] = (q[0] + q[1]) + (q[2] + q[3]);
             }
@@ -590,7 +613,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
                 if (valid_k(k)) {
-                    const float uk0 = ub[gt + TPC * k];
+                    const float uk0 = uget(k);
                     ffma2(x[0][k], x[1][k], -s0, -s1, uk0, uk0, x[0][k], x[1][k]);
                 }
             }
@@ -1023,6 +1046,17 @@ struct FusedVariant {
         nullptr,                                                                                   \
             reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, false, 1, true>), \
             nullptr, nullptr, TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME, NAME              \
+    }
+
+// ... with the reflectors in TMEM (K1t's scalar form: one tcgen05.ld per reflector replaces the
+// CH one-element shared-memory reads of the dot and of the update)
+#define HH_FUSED_VAR_SC_TM(T, TPC, CH, C, NT, NAME)                                                \
+    FusedVariant {                                                                                 \
+        nullptr,                                                                                   \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, false, 1, true>), \
+            nullptr,                                                                               \
+            reinterpret_cast<const void *>(&hh_fused_kernel<T, TPC, CH, C, NT, false, true, 1, true>),  \
+            TPC, CH, C, NT, static_cast<int>(sizeof(T)), NAME, NAME "_tmem"                        \
     }
 
 // tables (each defined in its own translation unit so the instantiations build in parallel)

@@ -18,9 +18,9 @@ const FusedVariant kF32S[] = {
     HH_FUSED_VAR_SC(float, 8, 16, 1, 256, "f32r_tpc8_ch16_c1"),      // n <= 128
     HH_FUSED_VAR_SC(float, 16, 16, 1, 256, "f32r_tpc16_ch16_c1"),    // n <= 256
     HH_FUSED_VAR_SC(float, 32, 16, 2, 256, "f32r_tpc32_ch16_c2"),    // n <= 512
-    HH_FUSED_VAR_SC(float, 32, 32, 2, 512, "f32r_tpc32_ch32_c2"),    // n <= 1024
-    HH_FUSED_VAR_SC(float, 64, 32, 2, 512, "f32r_tpc64_ch32_c2"),    // n <= 2048
-    HH_FUSED_VAR_SC(float, 128, 32, 2, 512, "f32r_tpc128_ch32_c2"),  // n <= 4096
+    HH_FUSED_VAR_SC_TM(float, 32, 32, 2, 512, "f32r_tpc32_ch32_c2"),    // n <= 1024
+    HH_FUSED_VAR_SC_TM(float, 64, 32, 2, 512, "f32r_tpc64_ch32_c2"),    // n <= 2048
+    HH_FUSED_VAR_SC_TM(float, 128, 32, 2, 512, "f32r_tpc128_ch32_c2"),  // n <= 4096
     HH_FUSED_VAR_SC(float, 256, 32, 1, 512, "f32r_tpc256_ch32_c1"),  // n <= 8192
 };
 const FusedVariant kF64S[] = {
@@ -44,6 +44,15 @@ const FusedVariant *fused_table_scalar(int dtype, int *count) {
     return kF64S;
 }
 
+namespace {
+thread_local int t_sc_tmem = 1;   // A/B / test hook (hh_debug_k1r_tmem): 0 shared-memory U only, 1 policy, 2 TMEM whenever possible
+}
+int k1r_set_tmem(int on) {
+    const int prev = t_sc_tmem;
+    t_sc_tmem = on;
+    return prev;
+}
+
 // cudaErrorNotSupported when no variant holds n or U does not fit in shared memory (the
 // caller then runs K1g)
 cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, LaunchInfo *info) {
@@ -59,17 +68,27 @@ cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, Lau
     const int UC = (UT / v->tpc) * v->c;
     const int NU = v->nt / UT;
     const int WPU = UT / 32;
-    const size_t ub = static_cast<size_t>(a.h) * a.n * s;
+    // the reflectors in TMEM (CH columns each, 512 per CTA) when the variant has the form:
+    // one tcgen05.ld per reflector instead of 2 CH one-element shared-memory reads
+    int tcols = 32;
+    while (tcols < a.h * v->ch) tcols *= 2;
+    // Policy (same-box A/B, tools/k1g_time.py, profiles/r2/k1r_time_r2.jsonl): one-warp groups
+    // (n in (512, 1024]) -- n = 1023, h = 10 / 16: 0.827 / 1.192 -> 0.648 / 0.878 ms; multi-warp
+    // groups gain nothing (n = 2047 / 4095, h = 12: 1.024 / 1.073 vs 1.047 / 1.063 ms) and keep
+    // the shared-memory form unless the hook forces it (2)
+    const bool utm = t_sc_tmem != 0 && v->fn_tm_ragged != nullptr && a.mode != MODE_PAIR && a.h > 0 &&
+                     tcols <= 512 && (v->tpc == 32 || t_sc_tmem == 2);
+    const size_t ub = utm ? 0 : static_cast<size_t>(a.h) * a.n * s;
     const size_t red = v->tpc > 32 ? static_cast<size_t>(2) * NU * WPU * v->c * s : 0;
     const size_t bars = 8 * static_cast<size_t>(2 + NU) + 8;
     const size_t smem = ub + 16 + red + bars + 16;
     if (smem > static_cast<size_t>(da.max_smem_optin)) return cudaErrorNotSupported;
-    a.R = static_cast<int>(a.h);
     a.nchunks = 1;
     a.stage_x = 0;
     a.l2pf = 0;
-    a.tcols = 0;
-    const void *fn = v->fn_ragged;
+    a.tcols = utm ? tcols : 0;
+    a.R = utm ? 0 : static_cast<int>(a.h);   // (TMEM form: no U in shared memory)
+    const void *fn = utm ? v->fn_tm_ragged : v->fn_ragged;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          da.max_smem_optin);
     if (e != cudaSuccess) return e;
@@ -86,7 +105,7 @@ cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, Lau
     void *args[] = {&a};
     e = cudaLaunchKernel(fn, dim3(grid), dim3(v->nt), args, smem, stream);
     if (info) {
-        info->variant = v->name;
+        info->variant = utm ? v->name_tm : v->name;
         info->grid = grid;
         info->block = v->nt;
         info->smem = static_cast<int>(smem);

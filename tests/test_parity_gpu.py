@@ -467,6 +467,20 @@ class padded:
         hh.hh.clear_workspace_cache()
 
 
+class k1r_smem:
+    """Test hook: K1r with U in shared memory (0: its TMEM form off), or TMEM wherever the
+    variant has the form (2: also the multi-warp groups the policy leaves on shared memory)."""
+
+    def __init__(self, mode=0):
+        self.mode = mode
+
+    def __enter__(self):
+        self.prev = hh.hh.lib().hh_debug_k1r_tmem(self.mode)
+
+    def __exit__(self, *exc):
+        hh.hh.lib().hh_debug_k1r_tmem(self.prev)
+
+
 class k1g_only:
     """Test hook: keep K1r off so that K1g also serves the shapes K1r would take."""
 
@@ -478,20 +492,27 @@ class k1g_only:
 
 
 @pytest.mark.parametrize("n,h,N,dt", GENERAL_SHAPES)
-@pytest.mark.parametrize("k1r", [True, False])
+@pytest.mark.parametrize("k1r", [True, "smem", "tmem", False])
 def test_general_apply(n, h, N, dt, k1r):
     """Shapes the vector kernels refuse run on K1r / K1g: both ops, and in place (Y == X);
-    once as the library picks (K1r while n is inside its tables), once on K1g alone."""
+    once as the library picks (K1r while n is inside its tables, its TMEM form for fp32
+    n in (512, 4096], h <= 16), once with K1r's shared-memory form, once on K1g alone."""
     import contextlib
     c = gi.make_case("apply", n, h, N, dt, seed=31)
-    with (contextlib.nullcontext() if k1r else k1g_only()), padded(0):
+    ctx = contextlib.nullcontext() if k1r is True else k1r_smem(0) if k1r == "smem" else \
+        k1r_smem(2) if k1r == "tmem" else k1g_only()
+    with ctx, padded(0):
         for op in (0, 1):
             got = run_apply(op, c.U, c.X)
             assert is_general(dt), hh.last_launch_info()
+            v = hh.last_launch_info()["variant"]
             if not k1r or n > 8192:
-                assert hh.last_launch_info()["variant"].startswith(f"{dt}_general")
+                assert v.startswith(f"{dt}_general")
             elif n <= 4096:
-                assert hh.last_launch_info()["variant"].startswith(f"{dt}r_")
+                assert v.startswith(f"{dt}r_")
+                tm = dt == "f32" and 0 < h <= 16 and ((k1r is True and 512 < n <= 1024) or
+                                                      (k1r == "tmem" and 512 < n))
+                assert v.endswith("_tmem") == tm, v
             assert_parity(got, oracle.apply(op, c.U, c.X), dt, h, f"K1r/K1g n={n} op{op}")
         X = dev(c.X)
         out = hh.hh_apply(0, dev(c.U), X, X)

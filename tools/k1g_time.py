@@ -23,10 +23,17 @@ def t(fn, reps=10):
 
 
 for n, h, N in ((1024, 10, 262144), (1023, 10, 262144), (100, 7, 1 << 20), (101, 7, 1 << 20),
-                (4096, 12, 65536), (4097, 12, 65536), (16384, 8, 16384), (201, 16, 1 << 19)):
+                (4096, 12, 65536), (4095, 12, 65536), (4097, 12, 65536), (2047, 12, 131072), (1023, 16, 262144),
+                (16384, 8, 16384), (201, 16, 1 << 19)):
     U = torch.nn.functional.normalize(torch.randn(h, n, device="cuda"), dim=1)
     X = torch.randn(N, n, device="cuda")
     Y = torch.empty_like(X)
     ms = t(lambda: hh.hh_apply(0, U, X, Y))
-    print(json.dumps({"n": n, "h": h, "N": N, "ms": round(ms, 4), "GBps": round(2 * X.numel() * 4 / ms / 1e6, 1),
-                      "kernel": hh.last_launch_info()["variant"]}))
+    row = {"n": n, "h": h, "N": N, "ms": round(ms, 4), "GBps": round(2 * X.numel() * 4 / ms / 1e6, 1),
+           "kernel": hh.last_launch_info()["variant"]}
+    if "r_" in row["kernel"] and h <= 16 and 512 < n <= 4096:   # K1r: both forms
+        for mode, nm in ((0, "smem"), (2, "tmem")):
+            hh.hh.lib().hh_debug_k1r_tmem(mode)
+            row[nm + "_ms"] = round(t(lambda: hh.hh_apply(0, U, X, Y)), 4)
+        hh.hh.lib().hh_debug_k1r_tmem(1)
+    print(json.dumps(row))
