@@ -142,7 +142,7 @@ int64_t padded_n(int64_t n, hh_dtype dtype) {
     return (n + q - 1) / q * q;
 }
 bool k1r_capable(int64_t n, int64_t h, hh_dtype dtype) {
-    return n <= max_n(dtype) &&
+    return n <= max_n(dtype) / 2 &&   // K1r's tables: n <= 4096 (fp32) / 2048 (fp64)
            static_cast<size_t>(h) * n * elem(dtype) + 1024 <= static_cast<size_t>(device_attr().max_smem_optin);
 }
 bool use_padded(int64_t n, int64_t h, hh_dtype dtype, bool sym) {
@@ -320,6 +320,7 @@ int hh_debug_k1_blocked(int on) { return k1_set_blocked(on); }
 int hh_debug_k7_rows(int rw) { return k7_set_rows(rw); }
 int hh_debug_general_scalar(int on) { return general_set_scalar(on); }
 int hh_debug_k1r_tmem(int on) { return k1r_set_tmem(on); }
+int hh_debug_k1r_stage(int on) { return k1r_set_stage(on); }
 int hh_debug_general_pad(int on) {
     const int prev = t_pad;
     t_pad = on;

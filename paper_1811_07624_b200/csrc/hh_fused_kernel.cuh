@@ -283,8 +283,15 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     V *Us = reinterpret_cast<V *>(smem);
     V *Xs = Us + static_cast<size_t>(nbuf) * R * nv;
     T *red = reinterpret_cast<T *>(Xs + (stage ? static_cast<size_t>(NU) * UC * nv : 0));
-    if constexpr (SC)   // R nv elements need not end on a 16-byte boundary
-        red = reinterpret_cast<T *>((reinterpret_cast<uintptr_t>(red) + 15) & ~static_cast<uintptr_t>(15));
+    // SC: R nv elements need not end on a 16-byte boundary, and a staging slot holds the
+    // 16-byte-aligned superset of a tile (its first byte may sit up to 12 bytes into the slot,
+    // its last up to 12 bytes before the copy's end): byte pitch `spitch`
+    size_t spitch = 0;
+    if constexpr (SC) {
+        Xs = reinterpret_cast<V *>((reinterpret_cast<uintptr_t>(Xs) + 15) & ~static_cast<uintptr_t>(15));
+        spitch = (static_cast<size_t>(UC) * nv * sizeof(V) + 31) & ~static_cast<size_t>(15);
+        red = reinterpret_cast<T *>(reinterpret_cast<unsigned char *>(Xs) + (stage ? NU * spitch : 0));
+    }
     uint64_t *bars = reinterpret_cast<uint64_t *>(red + (TPC > 32 ? 2 * NU * WPU * KV : 0));
     uint64_t *ubar = bars;      // [2]
     uint64_t *xbar = bars + 2;  // [NU]
@@ -326,6 +333,26 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         const uint64_t pol = policy_evict_first();
         const char *src = reinterpret_cast<const char *>(Xg + c0 * nv);
         char *dst = reinterpret_cast<char *>(Xs + static_cast<size_t>(unit) * UC * nv);
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+            bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &xbar[unit], pol);
+    };
+    // SC: a tile is staged only if the 16-byte superset of its bytes stays inside X (all but,
+    // at most, the last tile); the others are loaded straight into registers
+    auto sc_stageable = [&](int64_t t) -> bool {
+        const int64_t c1 = min((t + 1) * UC, a.N);
+        const int64_t end = (c1 * nv * static_cast<int64_t>(sizeof(V)) + 15) & ~static_cast<int64_t>(15);
+        return end <= a.N * nv * static_cast<int64_t>(sizeof(V));
+    };
+    auto sc_issue_x = [&](int64_t t) {   // (X itself is 16-byte aligned when the launcher stages)
+        const int64_t c0 = t * UC;
+        const int64_t cols = min(static_cast<int64_t>(UC), a.N - c0);
+        const char *src = reinterpret_cast<const char *>(Xg + c0 * nv);
+        const uint32_t lead = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src) & 15u);
+        const uint32_t bytes = (static_cast<uint32_t>(cols * nv * sizeof(V)) + lead + 15u) & ~15u;
+        src -= lead;
+        mbar_arrive_expect_tx(&xbar[unit], bytes);
+        const uint64_t pol = policy_evict_first();
+        char *dst = reinterpret_cast<char *>(Xs) + static_cast<size_t>(unit) * spitch;
         for (uint32_t off = 0; off < bytes; off += 32768u)
             bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &xbar[unit], pol);
     };
@@ -455,7 +482,11 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 issue_u(chunk_of(static_cast<int>(g % L)), static_cast<int>(g & 1));
         }
     }
-    if (stage && ut == 0 && tile_of(0) < ntiles) issue_x(tile_of(0));
+    if constexpr (SC) {
+        if (stage && ut == 0 && tile_of(0) < ntiles && sc_stageable(tile_of(0))) sc_issue_x(tile_of(0));
+    } else {
+        if (stage && ut == 0 && tile_of(0) < ntiles) issue_x(tile_of(0));
+    }
 
     V x[C][CH];
     uint32_t xphase = 0;
@@ -816,7 +847,35 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                         }
                     }
                 }
-            } else if (stage) {
+            } else if (SC && stage && sc_stageable(t)) {
+                if constexpr (SC) {
+                    mbar_wait(&xbar[unit], xphase);
+                    xphase ^= 1u;
+                    // the tile starts `lead` bytes into the slot
+                    const unsigned char *slot = reinterpret_cast<const unsigned char *>(Xs) +
+                                                static_cast<size_t>(unit) * spitch +
+                                                (reinterpret_cast<uintptr_t>(Xg + t * UC * nv) & 15u);
+                    const V *xs = reinterpret_cast<const V *>(slot) + static_cast<size_t>(grp * C) * nv;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+#pragma unroll
+                        for (int k = 0; k < CH; ++k) {
+                            if (valid_k(k))
+                                x[c][k] = xs[static_cast<size_t>(c) * nv + gt + TPC * k];
+                            else
+                                vzero(x[c][k]);
+                        }
+                    }
+                    unit_sync();
+                    if (ut == 0) {
+                        const int64_t t1 = tile_of(b + 1);
+                        if (b + 1 < nb && t1 < ntiles && sc_stageable(t1)) {
+                            fence_proxy_async_smem();
+                            sc_issue_x(t1);
+                        }
+                    }
+                }
+            } else if (!SC && stage) {
                 mbar_wait(&xbar[unit], xphase);
                 xphase ^= 1u;
                 const V *xs = Xs + (static_cast<size_t>(unit) * UC + grp * C) * nv;

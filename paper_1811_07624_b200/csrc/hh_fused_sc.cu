@@ -21,7 +21,8 @@ const FusedVariant kF32S[] = {
     HH_FUSED_VAR_SC_TM(float, 32, 32, 2, 512, "f32r_tpc32_ch32_c2"),    // n <= 1024
     HH_FUSED_VAR_SC_TM(float, 64, 32, 2, 512, "f32r_tpc64_ch32_c2"),    // n <= 2048
     HH_FUSED_VAR_SC_TM(float, 128, 32, 2, 512, "f32r_tpc128_ch32_c2"),  // n <= 4096
-    HH_FUSED_VAR_SC(float, 256, 32, 1, 512, "f32r_tpc256_ch32_c1"),  // n <= 8192
+    // (a 256-thread one-column form for n <= 8192 measured slower than K1g -- n = 4097, h = 12:
+    // 4.0 vs 3.4 ms -- and was dropped: K1g or the padded detour serve n > 4096)
 };
 const FusedVariant kF64S[] = {
     HH_FUSED_VAR_SC(double, 8, 8, 1, 256, "f64r_tpc8_ch8_c1"),        // n <= 64
@@ -30,7 +31,6 @@ const FusedVariant kF64S[] = {
     HH_FUSED_VAR_SC(double, 32, 16, 1, 256, "f64r_tpc32_ch16_c1"),    // n <= 512
     HH_FUSED_VAR_SC(double, 64, 16, 1, 512, "f64r_tpc64_ch16_c1"),    // n <= 1024
     HH_FUSED_VAR_SC(double, 128, 16, 1, 512, "f64r_tpc128_ch16_c1"),  // n <= 2048
-    HH_FUSED_VAR_SC(double, 256, 16, 1, 512, "f64r_tpc256_ch16_c1"),  // n <= 4096
 };
 
 }  // namespace
@@ -45,7 +45,15 @@ const FusedVariant *fused_table_scalar(int dtype, int *count) {
 }
 
 namespace {
-thread_local int t_sc_tmem = 1;   // A/B / test hook (hh_debug_k1r_tmem): 0 shared-memory U only, 1 policy, 2 TMEM whenever possible
+thread_local int t_sc_tmem = 1;   // A/B / test hook (hh_debug_k1r_tmem): 0 = shared-memory U only
+}
+namespace {
+thread_local int t_sc_stage = 1;   // A/B / test hook (hh_debug_k1r_stage): 0 = columns straight into registers
+}
+int k1r_set_stage(int on) {
+    const int prev = t_sc_stage;
+    t_sc_stage = on;
+    return prev;
 }
 int k1r_set_tmem(int on) {
     const int prev = t_sc_tmem;
@@ -72,19 +80,25 @@ cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, Lau
     // one tcgen05.ld per reflector instead of 2 CH one-element shared-memory reads
     int tcols = 32;
     while (tcols < a.h * v->ch) tcols *= 2;
-    // Policy (same-box A/B, tools/k1g_time.py, profiles/r2/k1r_time_r2.jsonl): one-warp groups
-    // (n in (512, 1024]) -- n = 1023, h = 10 / 16: 0.827 / 1.192 -> 0.648 / 0.878 ms; multi-warp
-    // groups gain nothing (n = 2047 / 4095, h = 12: 1.024 / 1.073 vs 1.047 / 1.063 ms) and keep
-    // the shared-memory form unless the hook forces it (2)
+    // Same-box A/B (tools/k1g_time.py, profiles/r2/k1r_time_r2.jsonl), with staged tiles:
+    // n = 1023, h = 10 / 16: 0.75 / 1.11 -> 0.56 / 0.80 ms; n = 2047, h = 12: 1.00 -> 0.78;
+    // n = 4095, h = 12: 1.16 -> 1.04 (U in TMEM also leaves the shared memory to the slots)
     const bool utm = t_sc_tmem != 0 && v->fn_tm_ragged != nullptr && a.mode != MODE_PAIR && a.h > 0 &&
-                     tcols <= 512 && (v->tpc == 32 || t_sc_tmem == 2);
+                     tcols <= 512;
     const size_t ub = utm ? 0 : static_cast<size_t>(a.h) * a.n * s;
     const size_t red = v->tpc > 32 ? static_cast<size_t>(2) * NU * WPU * v->c * s : 0;
     const size_t bars = 8 * static_cast<size_t>(2 + NU) + 8;
-    const size_t smem = ub + 16 + red + bars + 16;
+    // staged column tiles (bulk copies of each tile's 16-byte superset, the next tile in flight
+    // while this one computes, as in K1) when X is 16-byte aligned and the slots fit
+    const size_t spitch = (static_cast<size_t>(UC) * a.n * s + 31) & ~static_cast<size_t>(15);
+    const size_t base = ub + 16 + red + bars + 16;
+    const bool stage = t_sc_stage != 0 && a.mode != MODE_PAIR && a.N > UC &&
+                       (reinterpret_cast<uintptr_t>(a.X) & 15u) == 0 &&
+                       base + NU * spitch <= static_cast<size_t>(da.max_smem_optin);
+    const size_t smem = base + (stage ? NU * spitch : 0);
     if (smem > static_cast<size_t>(da.max_smem_optin)) return cudaErrorNotSupported;
     a.nchunks = 1;
-    a.stage_x = 0;
+    a.stage_x = stage ? 1 : 0;
     a.l2pf = 0;
     a.tcols = utm ? tcols : 0;
     a.R = utm ? 0 : static_cast<int>(a.h);   // (TMEM form: no U in shared memory)

@@ -91,6 +91,7 @@ cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, Lau
 // nwrite (pads an unaligned problem to a 16-byte pitch, and strips the pad again)
 cudaError_t launch_repitch(const void *src, int64_t ld_src, void *dst, int64_t ld_dst, int64_t rows,
                            int64_t ncopy, int64_t nwrite, double fill, int dtype, cudaStream_t stream);
+int k1r_set_stage(int on);  // A/B / test hook (hh_debug_k1r_stage): K1r staged column tiles (default 1) or direct loads (0); previous
 int k1r_set_tmem(int on);   // A/B / test hook (hh_debug_k1r_tmem): K1r with U in TMEM (default 1) or shared memory (0); previous
 int general_set_scalar(int on);   // A/B / test hook (hh_debug_general_scalar): 1 K1r first (default), 0 K1g only
 

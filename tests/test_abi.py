@@ -102,6 +102,7 @@ def test_unaligned_stride_workspace_policy():
     assert q(hh.HH_CALL_APPLY, 101, 9, 1 << 20) == 0 and q(hh.HH_CALL_APPLY, 101, 10, 1 << 20) > 0
     assert q(hh.HH_CALL_SYM, 1023, 9, 4096) == 0 and q(hh.HH_CALL_SYM, 1023, 10, 4096) > 0
     assert q(hh.HH_CALL_APPLY, 9001, 3, 4096) == 0 and q(hh.HH_CALL_APPLY, 9001, 4, 4096) > 0
+    assert q(hh.HH_CALL_APPLY, 4097, 3, 4096) == 0 and q(hh.HH_CALL_APPLY, 4097, 4, 4096) > 0   # past K1r's tables
     assert q(hh.HH_CALL_APPLY, 4095, 14, 4096) == 0 and q(hh.HH_CALL_APPLY, 4095, 15, 4096) > 0  # U past K1r
     assert q(hh.HH_CALL_APPLY, 1023, 19, 4096, 1) > 0     # fp64: pitch of 2
     assert q(hh.HH_CALL_APPLY, 1024, 10, 262144) == 0     # aligned shapes unchanged

@@ -55,6 +55,27 @@ def test_graph_apply(algo, n, h, N, op):
             assert torch.equal(got, ref), (algo, rep)
 
 
+@pytest.mark.parametrize("n,h,N", [(1023, 10, 900), (101, 7, 3000), (1021, 40, 700), (9001, 5, 64)])
+def test_graph_unaligned_strides(n, h, N):
+    """Unaligned column strides under capture: K1r (TMEM and shared-memory forms), K1g, and the
+    padded detour (copies + the aligned call + the copy back are all stream-ordered kernels)."""
+    g0 = gi.rng(905, n, h)
+    U = dev(gi.unit_reflectors(g0, h, n, "f32"))
+    X = dev(gi.gaussian_columns(g0, N, n, "f32"))
+    Y = torch.empty_like(X)
+    wsb = hh.hh_workspace_bytes(hh.HH_CALL_APPLY, n, h, N, 0, torch.float32)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    graph, _ = capture(lambda: hh.hh_apply(0, U, X, Y, workspace=ws if wsb else None))
+    for rep in range(2):
+        X.copy_(dev(gi.gaussian_columns(gi.rng(906, rep), N, n, "f32")))
+        graph.replay()
+        torch.cuda.synchronize()
+        got = Y.clone()
+        ref = hh.hh_apply(0, U, X, workspace=ws if wsb else None)
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref), (n, h, rep)
+
+
 def test_graph_sym_and_mahalanobis_and_knn():
     n, h, N = 256, 32, 2000
     g0 = gi.rng(902)

@@ -31,9 +31,12 @@ for n, h, N in ((1024, 10, 262144), (1023, 10, 262144), (100, 7, 1 << 20), (101,
     ms = t(lambda: hh.hh_apply(0, U, X, Y))
     row = {"n": n, "h": h, "N": N, "ms": round(ms, 4), "GBps": round(2 * X.numel() * 4 / ms / 1e6, 1),
            "kernel": hh.last_launch_info()["variant"]}
+    if "r_" in row["kernel"]:   # K1r: columns straight into registers instead of staged tiles
+        hh.hh.lib().hh_debug_k1r_stage(0)
+        row["nostage_ms"] = round(t(lambda: hh.hh_apply(0, U, X, Y)), 4)
+        hh.hh.lib().hh_debug_k1r_stage(1)
     if "r_" in row["kernel"] and h <= 16 and 512 < n <= 4096:   # K1r: both forms
-        for mode, nm in ((0, "smem"), (2, "tmem")):
-            hh.hh.lib().hh_debug_k1r_tmem(mode)
-            row[nm + "_ms"] = round(t(lambda: hh.hh_apply(0, U, X, Y)), 4)
+        hh.hh.lib().hh_debug_k1r_tmem(0)
+        row["smem_ms"] = round(t(lambda: hh.hh_apply(0, U, X, Y)), 4)
         hh.hh.lib().hh_debug_k1r_tmem(1)
     print(json.dumps(row))
