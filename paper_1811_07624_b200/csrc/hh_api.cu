@@ -151,13 +151,16 @@ bool use_padded(int64_t n, int64_t h, hh_dtype dtype, bool sym) {
     if (n4 > max_n(dtype) && !(dtype == HH_F32 && n4 <= kWyMaxN)) return false;
     if (t_pad == 1 || t_algo == HH_ALGO_WY) return true;   // (a forced K5 runs on the padded copy)
     // same-box sweep at 1 GiB (tools/pad_time.py, profiles/r2/pad_time_r2.jsonl): the detour costs
-    // ~0.87 ms of copies + the aligned call; K1r grows by 0.05-0.06 ms per reflector --
-    // n = 1023: h = 16 1.20 (K1r) vs 1.35, h = 24 1.69 vs 1.48; n = 101: h = 8 0.54 vs 0.61,
-    // h = 12 0.74 vs 0.65; sym n = 1023: h = 8 1.28 vs 1.51, h = 12 1.77 vs 1.51; where only K1g
-    // would run (n = 9001): h = 2 0.95 vs 1.43, h = 4 1.56 vs 1.43, sym h = 2 1.69 vs 1.50
+    // ~0.87 ms of copies + the aligned call; K1r grows by 0.04-0.07 ms per reflector --
+    // n = 1023: h = 16 0.80 (K1r, U in TMEM) vs 1.36, h = 24 1.60 (U in shared memory) vs 1.49;
+    // sym h = 12 1.28 vs 1.53, h = 16 1.58 vs 1.53; n = 4095: h = 16 1.32 vs 1.51, sym h = 8
+    // 1.50 vs 1.54, h = 12 2.08 vs 1.59; n = 101: h = 8 0.55 vs 0.61, h = 12 0.74 vs 0.65, sym
+    // h = 4 0.57 vs 0.61, h = 8 0.97 vs 0.71; where only K1g would run (n = 9001): h = 2 0.95 vs
+    // 1.43, h = 4 1.57 vs 1.43, sym h = 2 1.69 vs 1.50
     if (!k1r_capable(n, h, dtype)) return h >= (sym ? 2 : 4);
-    if (n <= 256) return h >= (sym ? 6 : 10);
-    return h >= (sym ? 10 : 19);
+    if (n <= 256) return h >= (sym ? 5 : 10);
+    if (n <= 1024) return h >= (sym ? 16 : 21);
+    return h >= (sym ? 9 : 17);
 }
 // scratch of the detour itself (U, X and up to two n-vectors at the padded pitch)
 struct PadPlan {
