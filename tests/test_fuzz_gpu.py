@@ -78,6 +78,26 @@ def test_fuzz_any_n(n, h, N):
                       f"any-n pairs n{n} h{h} {dt}")
 
 
+def test_fuzz_unaligned_offsets():
+    """A seeded subset of tools/stress_unaligned.py: random n / h / N / dtype / op, operands at
+    random element offsets from a 16-byte boundary, in place or not, apply / sym / D, with each
+    of K1r's forms, K1g and the padded detour forced in turn -- all against the oracle."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                        "stress_unaligned.py")
+    spec = importlib.util.spec_from_file_location("stress_unaligned", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    g = gi.rng(990, 77)
+    fails = []
+    for i in range(120):
+        ok, msg = mod.one_case(g, i)
+        if not ok:
+            fails.append(msg)
+    assert not fails, fails
+
+
 @pytest.mark.parametrize("n,h,N", shapes(2, 12))
 def test_fuzz_sym_and_signed(n, h, N):
     h = max(h, 1)
