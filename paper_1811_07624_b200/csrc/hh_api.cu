@@ -142,8 +142,12 @@ int64_t padded_n(int64_t n, hh_dtype dtype) {
     return (n + q - 1) / q * q;
 }
 bool k1r_capable(int64_t n, int64_t h, hh_dtype dtype) {
-    return n <= max_n(dtype) / 2 &&   // K1r's tables: n <= 4096 (fp32) / 2048 (fp64)
-           static_cast<size_t>(h) * n * elem(dtype) + 1024 <= static_cast<size_t>(device_attr().max_smem_optin);
+    if (n > max_n(dtype) / 2) return false;   // K1r's tables: n <= 4096 (fp32) / 2048 (fp64)
+    if (dtype == HH_F32 && n > 512 && h <= 16) return true;   // U in TMEM
+    int64_t pitch = 64;                       // U in shared memory at its variant's row pitch
+    while (pitch < n) pitch *= 2;
+    return static_cast<size_t>(h) * pitch * elem(dtype) + 1024 <=
+           static_cast<size_t>(device_attr().max_smem_optin);
 }
 bool use_padded(int64_t n, int64_t h, hh_dtype dtype, bool sym) {
     if (!stride_unaligned(n, dtype) || h < 1 || t_pad == 0) return false;
@@ -151,16 +155,15 @@ bool use_padded(int64_t n, int64_t h, hh_dtype dtype, bool sym) {
     if (n4 > max_n(dtype) && !(dtype == HH_F32 && n4 <= kWyMaxN)) return false;
     if (t_pad == 1 || t_algo == HH_ALGO_WY) return true;   // (a forced K5 runs on the padded copy)
     // same-box sweep at 1 GiB (tools/pad_time.py, profiles/r2/pad_time_r2.jsonl): the detour costs
-    // ~0.87 ms of copies + the aligned call; K1r grows by 0.04-0.07 ms per reflector --
-    // n = 1023: h = 16 0.80 (K1r, U in TMEM) vs 1.36, h = 24 1.60 (U in shared memory) vs 1.49;
-    // sym h = 12 1.28 vs 1.53, h = 16 1.58 vs 1.53; n = 4095: h = 16 1.32 vs 1.51, sym h = 8
-    // 1.50 vs 1.54, h = 12 2.08 vs 1.59; n = 101: h = 8 0.55 vs 0.61, h = 12 0.74 vs 0.65, sym
-    // h = 4 0.57 vs 0.61, h = 8 0.97 vs 0.71; where only K1g would run (n = 9001): h = 2 0.95 vs
-    // 1.43, h = 4 1.57 vs 1.43, sym h = 2 1.69 vs 1.50
+    // ~0.87 ms of copies + the aligned call; K1r (no per-element predicates) grows by 0.02-0.03 ms
+    // per reflector -- n = 1023: h = 16 0.48 (U in TMEM) vs 1.36, h = 40 1.26 (U in shared
+    // memory) vs 1.53, h = 56 K1g 12.2 vs 1.52; sym h = 16 0.94 vs 1.53; n = 101: h = 40 1.01 vs
+    // 1.02, h = 56 1.36 vs 1.24, sym h = 16 0.85 vs 0.91; n = 4095: h = 16 0.67 vs 1.51, then
+    // only K1g: h = 20 4.8 vs 1.55; n = 9001 (K1g): h = 4 1.56 vs 1.42, sym h = 2 1.69 vs 1.50
     if (!k1r_capable(n, h, dtype)) return h >= (sym ? 2 : 4);
-    if (n <= 256) return h >= (sym ? 5 : 10);
-    if (n <= 1024) return h >= (sym ? 16 : 21);
-    return h >= (sym ? 9 : 17);
+    if (n <= 256) return h >= (sym ? 19 : 44);
+    if (n <= 1024) return h >= (sym ? 22 : 50);
+    return h >= (sym ? 17 : 40);
 }
 // scratch of the detour itself (U, X and up to two n-vectors at the padded pitch)
 struct PadPlan {

@@ -470,7 +470,12 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
     // prologue: U (resident, or the first two chunk visits) and each unit's first tile
     if constexpr (SC) {   // resident U copied by the CTA's threads (no 16-byte granularity)
         if constexpr (!UTM) {
-            for (int64_t i = tid; i < static_cast<int64_t>(h) * nv; i += NT) Us[i] = __ldg(Ug + i);
+            // rows at pitch TPC CH, zero past n: with x = 0 there too, the reflector loops need
+            // no per-element predicate (they cost more than the FMAs at CH = 32)
+            for (int i = tid; i < h * (TPC * CH); i += NT) {
+                const int row = i / (TPC * CH), r = i % (TPC * CH);
+                Us[i] = r < nv ? __ldg(Ug + static_cast<int64_t>(row) * nv + r) : T(0);
+            }
             __syncthreads();
         }
     } else
@@ -525,6 +530,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
         }
         auto uget = [&](int k) -> V {
             if constexpr (kKeepU) return uk[k];
+            else if constexpr (SC) return Us[static_cast<size_t>(ui) * (TPC * CH) + gt + TPC * k];
             else return ub[gt + TPC * k];
         };
         // fp32, two columns per single-warp group: the partial sums and the butterfly use
@@ -539,7 +545,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             float q0[4] = {0.f, 0.f, 0.f, 0.f}, q1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) {
+                // (positions past n hold u = 0 and x = 0 -- no per-element predicate)
+                {
                     const float uk0 = uget(k);
                     ffma2(q0[k & 3], q1[k & 3], uk0, uk0, x[0][k], x[1][k], q0[k & 3], q1[k & 3]);
                 }
@@ -554,7 +561,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 T q[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
                 for (int k = 0; k < CH; ++k) {
-                    if (valid_k(k)) vfma(q[k & 3], uget(k), x[c][k]);
+                    vfma(q[k & 3], uget(k), x[c][k]);
                 }
                 p[c] = (q[0] + q[1]) + (q[2] + q[3]);
             }
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             fadd2(s0, s1, p[0], p[1], p[0], p[1]);
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) {
+                {
                     const float uk0 = uget(k);
                     ffma2(x[0][k], x[1][k], -s0, -s1, uk0, uk0, x[0][k], x[1][k]);
                 }
@@ -658,6 +665,13 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                     vaxpy(x[0][k], s0, uk0);
                     vaxpy(x[1][k], s1, uk0);
                 }
+            }
+        } else if constexpr (SC) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const T s = p[c] + p[c];
+#pragma unroll
+                for (int k = 0; k < CH; ++k) vaxpy(x[c][k], s, uget(k));
             }
         } else {
 #pragma unroll

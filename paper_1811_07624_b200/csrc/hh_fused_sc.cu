@@ -85,7 +85,10 @@ cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, Lau
     // n = 4095, h = 12: 1.16 -> 1.04 (U in TMEM also leaves the shared memory to the slots)
     const bool utm = t_sc_tmem != 0 && v->fn_tm_ragged != nullptr && a.mode != MODE_PAIR && a.h > 0 &&
                      tcols <= 512;
-    const size_t ub = utm ? 0 : static_cast<size_t>(a.h) * a.n * s;
+    // (shared-memory U: rows at pitch TPC CH, zero padded -- see the kernel; the kernel places
+    // what follows U at R n elements, so R covers the padded rows)
+    const int64_t Rpad = utm ? 0 : (a.h * v->tpc * v->ch + a.n - 1) / a.n;
+    const size_t ub = static_cast<size_t>(Rpad) * a.n * s;
     const size_t red = v->tpc > 32 ? static_cast<size_t>(2) * NU * WPU * v->c * s : 0;
     const size_t bars = 8 * static_cast<size_t>(2 + NU) + 8;
     // staged column tiles (bulk copies of each tile's 16-byte superset, the next tile in flight
@@ -101,7 +104,7 @@ cudaError_t launch_fused_scalar(FusedArgs a, int dtype, cudaStream_t stream, Lau
     a.stage_x = stage ? 1 : 0;
     a.l2pf = 0;
     a.tcols = utm ? tcols : 0;
-    a.R = utm ? 0 : static_cast<int>(a.h);   // (TMEM form: no U in shared memory)
+    a.R = static_cast<int>(Rpad);   // (TMEM form: no U in shared memory)
     const void *fn = utm ? v->fn_tm_ragged : v->fn_ragged;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          da.max_smem_optin);

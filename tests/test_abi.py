@@ -95,18 +95,18 @@ def test_unaligned_stride_workspace_policy():
     call, the padded copy (U, X, two n-vectors at the padded pitch) plus the aligned call's own
     scratch from the measured crossover (hh_api.cu use_padded)."""
     q = lambda call, n, h, N, dt=0: hhpkg.hh_workspace_bytes(call, n, h, N, 0, dt)
-    assert q(hh.HH_CALL_APPLY, 1023, 20, 262144) == 0
-    pad = q(hh.HH_CALL_APPLY, 1023, 21, 262144)
-    assert pad >= (262144 + 21 + 2) * 1024 * 4            # copies at pitch 1024
-    assert pad >= (262144 + 21 + 2) * 1024 * 4 + q(hh.HH_CALL_APPLY, 1024, 21, 262144)
-    assert q(hh.HH_CALL_APPLY, 101, 9, 1 << 20) == 0 and q(hh.HH_CALL_APPLY, 101, 10, 1 << 20) > 0
-    assert q(hh.HH_CALL_SYM, 1023, 15, 4096) == 0 and q(hh.HH_CALL_SYM, 1023, 16, 4096) > 0
-    assert q(hh.HH_CALL_SYM, 2047, 8, 4096) == 0 and q(hh.HH_CALL_SYM, 2047, 9, 4096) > 0
-    assert q(hh.HH_CALL_SYM, 101, 4, 4096) == 0 and q(hh.HH_CALL_SYM, 101, 5, 4096) > 0
+    assert q(hh.HH_CALL_APPLY, 1023, 49, 262144) == 0
+    pad = q(hh.HH_CALL_APPLY, 1023, 50, 262144)
+    assert pad >= (262144 + 50 + 2) * 1024 * 4            # copies at pitch 1024
+    assert pad >= (262144 + 50 + 2) * 1024 * 4 + q(hh.HH_CALL_APPLY, 1024, 50, 262144)
+    assert q(hh.HH_CALL_APPLY, 101, 43, 1 << 20) == 0 and q(hh.HH_CALL_APPLY, 101, 44, 1 << 20) > 0
+    assert q(hh.HH_CALL_SYM, 1023, 21, 4096) == 0 and q(hh.HH_CALL_SYM, 1023, 22, 4096) > 0
+    assert q(hh.HH_CALL_SYM, 2047, 16, 4096) == 0 and q(hh.HH_CALL_SYM, 2047, 17, 4096) > 0
+    assert q(hh.HH_CALL_SYM, 101, 18, 4096) == 0 and q(hh.HH_CALL_SYM, 101, 19, 4096) > 0
     assert q(hh.HH_CALL_APPLY, 9001, 3, 4096) == 0 and q(hh.HH_CALL_APPLY, 9001, 4, 4096) > 0
     assert q(hh.HH_CALL_APPLY, 4097, 3, 4096) == 0 and q(hh.HH_CALL_APPLY, 4097, 4, 4096) > 0   # past K1r's tables
-    assert q(hh.HH_CALL_APPLY, 4095, 14, 4096) == 0 and q(hh.HH_CALL_APPLY, 4095, 15, 4096) > 0  # U past K1r
-    assert q(hh.HH_CALL_APPLY, 1023, 21, 4096, 1) > 0     # fp64: pitch of 2
+    assert q(hh.HH_CALL_APPLY, 4095, 16, 4096) == 0 and q(hh.HH_CALL_APPLY, 4095, 17, 4096) > 0  # U past K1r (TMEM holds 16)
+    assert q(hh.HH_CALL_APPLY, 1023, 60, 4096, 1) > 0     # fp64: pitch of 2 (U past K1r's shared memory)
     assert q(hh.HH_CALL_APPLY, 1024, 10, 262144) == 0     # aligned shapes unchanged
     # Mahalanobis: transform-once on the padded copy of the points
     m_al = hhpkg.hh_workspace_bytes(hh.HH_CALL_MAHALANOBIS, 512, 9, 65536, 1 << 21, 0)

@@ -24,7 +24,7 @@ def t(fn, reps=5):
 
 L = hh.hh.lib()
 for n, N in ((1023, 262144), (101, 1 << 20), (4095, 65536), (9001, 29824)):
-    for h in (2, 4, 8, 12, 16, 24, 40):
+    for h in (4, 8, 12, 16, 20, 24, 32, 40, 56):
         U = torch.nn.functional.normalize(torch.randn(h, n, device="cuda"), dim=1)
         X = torch.randn(N, n, device="cuda")
         Y = torch.empty_like(X)
