@@ -40,8 +40,10 @@
  *     hh_mahalanobis, hh_congruence, hh_knn (n <= 256) and hh_apply_host take every other
  *     shape too (Eq. 1-2 hold for any n): any n >= 1 whose column fits in shared memory
  *     (n <= ~57000 f32 / ~28000 f64) and pointers aligned to the element run their
- *     reflector passes on scalar-access kernels (K1r / K1g; correct, 2-8x slower;
- *     hh_mahalanobis then uses its per-pair form and ignores the workspace).
+ *     reflector passes on scalar-access kernels (K1r, close to the aligned kernels'
+ *     speed for n <= 4096 while U fits on chip; K1g for the rest, several times slower;
+ *     hh_mahalanobis then uses its per-pair form, or with a workspace transform-once on
+ *     a copy of the points at a 16-byte pitch).
  *     With the workspace hh_workspace_bytes() reports for such a shape (non-zero from the
  *     measured crossover in h), the call instead copies the operands to a 16-byte pitch,
  *     runs the fast kernels on the copy and copies the result back (two extra passes
