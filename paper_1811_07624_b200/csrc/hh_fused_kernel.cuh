@@ -528,6 +528,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                 else vzero(uk[k]);
             }
         }
+        // (U in TMEM: positions past n hold u = 0 -- zero-filled at the TMEM fill -- and x = 0, so
+        // the reflector loops below skip the ragged-tail predicate: `UTM || valid_k(k)`)
         auto uget = [&](int k) -> V {
             if constexpr (kKeepU) return uk[k];
             else if constexpr (SC) return Us[static_cast<size_t>(ui) * (TPC * CH) + gt + TPC * k];
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             vzero(acc1);
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) {
+                if (UTM || valid_k(k)) {
                     const V uk0 = uget(k);
                     vfma(acc0, uk0, x[0][k]);
                     vfma(acc1, uk0, x[1][k]);
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             vzero(acc);
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) vfma(acc, uget(k), x[c][k]);
+                if (UTM || valid_k(k)) vfma(acc, uget(k), x[c][k]);
             }
             p[c] = vsum(acc);
         }
@@ -660,7 +662,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             fadd2(s0, s1, p[0], p[1], p[0], p[1]);   // 2 alpha for both columns at once
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) {
+                if (UTM || valid_k(k)) {
                     const V uk0 = uget(k);
                     vaxpy(x[0][k], s0, uk0);
                     vaxpy(x[1][k], s1, uk0);
@@ -679,7 +681,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
             const T s = p[c] + p[c];
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
-                if (valid_k(k)) vaxpy(x[c][k], s, uget(k));
+                if (UTM || valid_k(k)) vaxpy(x[c][k], s, uget(k));
             }
         }
         }
@@ -705,7 +707,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                         for (int c = 0; c < C; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                         for (int k = 0; k < CH; ++k) {
-                            if (valid_k(k)) {
+                            if (UTM || valid_k(k)) {
                                 const float4 uk0 = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
                                                                __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
 #pragma unroll
@@ -775,7 +777,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) hh_fused_kernel(const F
                         tmem_ld_cols<UCOLS>(tlane + static_cast<uint32_t>(idx[t] * UCOLS), r);
 #pragma unroll
                         for (int k = 0; k < CH; ++k) {
-                            if (valid_k(k)) {
+                            if (UTM || valid_k(k)) {
                                 const float4 uk0 = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
                                                                __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
 #pragma unroll
